@@ -1,0 +1,142 @@
+/*
+ * pipefusion_b200.h -- C ABI of the B200-native PipeFusion executor.
+ *
+ * Drop-in boundary for the reference's numerical emulator
+ * (`ditsim`, /root/reference/proj/include/ditsim/execute.hpp). Each entry
+ * point names the reference interface it replaces. Plain pointers and sizes
+ * only: no C++ or torch types cross this boundary.
+ *
+ * Matrices are fp64 (the reference's Eigen::MatrixXd element type) in either
+ * row-major or column-major order (Eigen's default is column-major, numpy's
+ * row-major) selected by a `layout` argument.
+ *
+ * Errors: every function returns a pf_status. PF_VALIDATION corresponds to
+ * the reference's ditsim::ValidationError (CLI exit 2), PF_NUMERIC to
+ * ditsim::NumericError (CLI exit 1) -- model.hpp:27-36, ditsim.cpp:430-439.
+ * The message of the most recent failure is available through
+ * pf_last_error() and keeps the reference's wording ("divisible",
+ * "non-finite activation at timestep T, layer L", "staleness bound violated").
+ *
+ * Thread safety: a context may be used by one host thread at a time; distinct
+ * contexts are independent. One host thread drives all stages of a context
+ * (one CUDA stream per stage; stages may live on distinct GPUs).
+ */
+#ifndef PIPEFUSION_B200_H_
+#define PIPEFUSION_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PF_OK = 0,
+  PF_NUMERIC = 1,     /* ditsim::NumericError */
+  PF_VALIDATION = 2,  /* ditsim::ValidationError */
+  PF_CUDA = 3,        /* CUDA runtime / driver failure (no reference analogue) */
+} pf_status;
+
+typedef enum { PF_ROW_MAJOR = 0, PF_COL_MAJOR = 1 } pf_layout;
+
+/* Model shape: ToyDiT (execute.hpp:31-45). mlp_hidden = lround(mlp_ratio*hs)
+ * as in build_toy_model (toy_model.cpp:56). seq_len is the K/V buffer height
+ * p (WorkloadSpec::seq_len, model.hpp:204). */
+typedef struct {
+  int layers;
+  int hidden_size;
+  int heads;
+  int mlp_hidden;
+  int64_t seq_len;
+} pf_model_desc;
+
+/* Staleness accounting of one run: ditsim::StalenessStats (execute.hpp:108-114).
+ * fresh_fraction, when non-NULL, receives n_stages x (patches*(steps-warmup))
+ * values, stage-major: the buffer fresh fraction after each steady patch
+ * completion of that stage, in completion order. */
+typedef struct {
+  int64_t fresh_patch_reads;
+  int64_t stale_patch_reads;
+  double* fresh_fraction;
+  int64_t fresh_fraction_capacity; /* number of doubles available */
+} pf_stats;
+
+typedef struct pf_ctx pf_ctx;
+
+/* Create an executor whose model weights are generated from `seed` exactly as
+ * ditsim::build_toy_model(seed, layers, hidden_size, heads, mlp_ratio) does
+ * (toy_model.cpp:44-82: one mt19937_64 stream, layers in order
+ * W_q, W_k, W_v, W_o, W_mlp_in, W_mlp_out, then condition_bias), without
+ * materialising the fp64 model on the host. Layers are split into
+ * n_stages contiguous stages, stage d on CUDA device devices[d]
+ * (devices may repeat: several stages on one GPU, each with its own stream).
+ * Replaces: build_toy_model (execute.hpp:52-53) + the per-worker StageBuffers
+ * allocation of run_pipefusion (execute.cpp:38-49). */
+pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
+                        const int* devices, int n_stages, pf_ctx** out);
+
+/* Create an executor from caller-owned fp64 weights: 6 matrices per layer in
+ * ToyDiTLayer order (w_q, w_k, w_v, w_o [hs x hs], w_mlp_in [hs x mlp],
+ * w_mlp_out [mlp x hs]), i.e. weights[6*l + i], plus condition_bias [hs].
+ * Replaces: passing `const ToyDiT&` to run_pipefusion (execute.hpp:124). */
+pf_status pf_create(const pf_model_desc* desc, const double* const* weights,
+                    const double* condition_bias, pf_layout layout,
+                    const int* devices, int n_stages, pf_ctx** out);
+
+void pf_destroy(pf_ctx* ctx);
+
+/* Message of the last failure on this context (or of the last failed
+ * pf_create*, when ctx is NULL). Never NULL. */
+const char* pf_last_error(const pf_ctx* ctx);
+
+/* ditsim::run_pipefusion(toy, x_init, steps, workers=n_stages, patches,
+ * warmup, eta) -- execute.hpp:124-127, execute.cpp:689-698.
+ * x_init / x_out: host [seq_len x hidden_size] fp64 in `layout`. The call is
+ * synchronous. stats may be NULL. */
+pf_status pf_run_pipefusion(pf_ctx* ctx, const double* x_init, pf_layout layout,
+                            int steps, int patches, int warmup, double eta,
+                            double* x_out, pf_stats* stats);
+
+/* Same schedule on a device-resident fp32 latent (row-major, on stage 0's
+ * device), updated in place; enqueued on `stream` (a cudaStream_t of stage
+ * 0's device, 0 = legacy default) and returns without synchronising. Used to
+ * time the path with inputs already resident in HBM. Staleness stats are
+ * computed on the host while enqueueing. */
+pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
+                                   int patches, int warmup, double eta,
+                                   void* stream, pf_stats* stats);
+
+/* Wait for work enqueued by pf_run_pipefusion_device and report deferred
+ * numeric errors (non-finite activations). */
+pf_status pf_synchronize(pf_ctx* ctx, void* stream);
+
+/* ditsim::serial_reference(toy, x_init, steps, eta) -- execute.hpp:102-104,
+ * toy_model.cpp:201-214: full-sequence forward each step, no staleness. */
+pf_status pf_serial_reference(pf_ctx* ctx, const double* x_init,
+                              pf_layout layout, int steps, double eta,
+                              double* x_out);
+
+/* ditsim::toy_layer_forward(layer, heads, h, k_buf, v_buf, row0) --
+ * execute.hpp:75-77, toy_model.cpp:169-177, for unit parity: rows
+ * [row0, row0+rows) of h pass through global layer `layer` against the given
+ * full [seq_len x hs] K/V buffers (updated in place with this block's fresh
+ * rows, as the reference does). */
+pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
+                           int64_t row0, double* k_buf, double* v_buf,
+                           pf_layout layout);
+
+/* Introspection for tests and benchmarks. */
+int pf_stage_count(const pf_ctx* ctx);
+int pf_stage_first_layer(const pf_ctx* ctx, int stage);
+int pf_stage_layer_count(const pf_ctx* ctx, int stage);
+/* Number of kernels the last run enqueued (sum over stages). */
+int64_t pf_last_launch_count(const pf_ctx* ctx);
+/* Version string of the library build. */
+const char* pf_version(void);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* PIPEFUSION_B200_H_ */

@@ -1,0 +1,37 @@
+/*
+ * pipefusion_b200_debug.h -- kernel-level test entry points (device pointers).
+ *
+ * Not part of the drop-in boundary: these exist so the unit tests can check a
+ * single sm_100a kernel against a plain fp32 computation of the same op.
+ *   pf_debug_gemm       <- ditsim::matmul_rows      (toy_model.cpp:93-102)
+ *   pf_debug_attention  <- ditsim::attention_rows   (toy_model.cpp:104-143)
+ */
+#ifndef PIPEFUSION_B200_DEBUG_H_
+#define PIPEFUSION_B200_DEBUG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C[r, n] = sum_k A[row0 + r, k] * B[n, k] for r < rows, n < N.
+ * A: bf16 [total_rows x K] row-major, B: bf16 [N x K] row-major,
+ * C: fp32 [rows x N] (row r of the block at C + r*N).
+ * Returns 0 on success, else a cudaError_t value. */
+int pf_debug_gemm(const void* A, const void* B, float* C, int rows, int row0,
+                  int total_rows, int N, int K, void* stream);
+
+/* Attention of query rows [row0, row0+rows) of q against all P rows of k/v.
+ * q, k, v: bf16 [P x hs] row-major (head h = columns [h*dh, (h+1)*dh)).
+ * out: bf16 [P x hs] (rows [row0, row0+rows) written).
+ * Returns 0 on success, else a cudaError_t value. */
+int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
+                       int P, int rows, int row0, int heads, int hs,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,284 @@
+"""B200-native PipeFusion executor (host-side Python mirror of the C ABI).
+
+The product is the sm_100a shared library `libpipefusion_b200.so` (C ABI in
+include/pipefusion_b200.h). This module binds it with ctypes and mirrors the
+reference's executor interface (/root/reference/proj/include/ditsim/execute.hpp)
+so tests read like the reference's own:
+
+    ctx = ToyDiTCuda(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers)
+    res = ctx.run_pipefusion(x_init, steps, patches, warmup, eta)
+    res.final_x, res.stats.fresh_patch_reads, ...
+
+There is no CPU fallback: importing works without a GPU, but every compute
+call goes through the CUDA library and raises if it is missing or fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "LIB_PATH", "load_library", "ValidationError", "NumericError", "CudaError",
+    "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
+    "mlp_hidden_of",
+]
+
+LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
+
+# Every symbol declared in include/pipefusion_b200.h and pipefusion_b200_debug.h.
+EXPORTED_SYMBOLS = [
+    "pf_create_toy", "pf_create", "pf_destroy", "pf_last_error",
+    "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
+    "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
+    "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
+    "pf_version", "pf_debug_gemm", "pf_debug_attention",
+]
+
+PF_OK, PF_NUMERIC, PF_VALIDATION, PF_CUDA = 0, 1, 2, 3
+PF_ROW_MAJOR, PF_COL_MAJOR = 0, 1
+
+
+class ValidationError(ValueError):
+    """ditsim::ValidationError (model.hpp:27-30); CLI exit code 2."""
+
+
+class NumericError(ArithmeticError):
+    """ditsim::NumericError (model.hpp:32-36); CLI exit code 1."""
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure inside the library."""
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("layers", ctypes.c_int), ("hidden_size", ctypes.c_int),
+                ("heads", ctypes.c_int), ("mlp_hidden", ctypes.c_int),
+                ("seq_len", ctypes.c_int64)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("fresh_patch_reads", ctypes.c_int64),
+                ("stale_patch_reads", ctypes.c_int64),
+                ("fresh_fraction", ctypes.POINTER(ctypes.c_double)),
+                ("fresh_fraction_capacity", ctypes.c_int64)]
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
+    """Load (once) and type the C ABI. Raises if the library is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise CudaError(f"{p} not built: run `python __graft_entry__.py build` "
+                        "(or paper_2405_14430_b200/_build.py)")
+    lib = ctypes.CDLL(str(p))
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    dptr = ctypes.POINTER(ctypes.c_double)
+    lib.pf_create_toy.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc),
+                                  ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(dptr), dptr, i32,
+                              ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_destroy.argtypes = [vp]
+    lib.pf_destroy.restype = None
+    lib.pf_last_error.argtypes = [vp]
+    lib.pf_last_error.restype = ctypes.c_char_p
+    lib.pf_run_pipefusion.argtypes = [vp, dptr, i32, i32, i32, i32, dbl, dptr,
+                                      ctypes.POINTER(_Stats)]
+    lib.pf_run_pipefusion_device.argtypes = [vp, vp, i32, i32, i32, dbl, vp,
+                                             ctypes.POINTER(_Stats)]
+    lib.pf_synchronize.argtypes = [vp, vp]
+    lib.pf_serial_reference.argtypes = [vp, dptr, i32, i32, dbl, dptr]
+    lib.pf_layer_forward.argtypes = [vp, i32, dptr, i64, i64, dptr, dptr, i32]
+    for name in ("pf_stage_count",):
+        getattr(lib, name).argtypes = [vp]
+    lib.pf_stage_first_layer.argtypes = [vp, i32]
+    lib.pf_stage_layer_count.argtypes = [vp, i32]
+    lib.pf_last_launch_count.argtypes = [vp]
+    lib.pf_last_launch_count.restype = i64
+    lib.pf_version.restype = ctypes.c_char_p
+    lib.pf_debug_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
+    lib.pf_debug_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _raise(status: int, msg: str) -> None:
+    if status == PF_OK:
+        return
+    if status == PF_VALIDATION:
+        raise ValidationError(msg)
+    if status == PF_NUMERIC:
+        raise NumericError(msg)
+    raise CudaError(msg)
+
+
+def mlp_hidden_of(hidden_size: int, mlp_ratio: float) -> int:
+    """int(std::lround(mlp_ratio * hidden_size)) as in toy_model.cpp:56."""
+    v = mlp_ratio * hidden_size
+    return int(math.floor(v + 0.5)) if v >= 0 else -int(math.floor(-v + 0.5))
+
+
+@dataclass
+class StalenessStats:
+    """ditsim::StalenessStats (execute.hpp:108-114)."""
+    fresh_patch_reads: int = 0
+    stale_patch_reads: int = 0
+    per_worker_fresh_fraction: List[List[float]] = field(default_factory=list)
+
+
+@dataclass
+class ParallelRunResult:
+    """ditsim::ParallelRunResult (execute.hpp:116-119); final timestep is -1."""
+    final_x: np.ndarray
+    stats: StalenessStats
+    timestep: int = -1
+
+
+def _f64c(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class ToyDiTCuda:
+    """A toy DiT resident on B200 stage devices, split into `workers` stages.
+
+    Weights come from `seed` exactly as build_toy_model does
+    (toy_model.cpp:44-82), or from explicit fp64 matrices via `from_weights`.
+    """
+
+    def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
+                 mlp_ratio: float, seq_len: int, workers: int = 1,
+                 devices: Optional[Sequence[int]] = None, _weights=None):
+        self._lib = load_library()
+        self._ctx = ctypes.c_void_p()
+        self.layers, self.hidden_size, self.heads = layers, hidden_size, heads
+        self.mlp_hidden = mlp_hidden_of(hidden_size, mlp_ratio)
+        self.seq_len, self.workers = seq_len, workers
+        desc = _Desc(layers, hidden_size, heads, self.mlp_hidden, seq_len)
+        devs = list(devices) if devices is not None else [0] * workers
+        if len(devs) != workers:
+            raise ValidationError("devices must list one CUDA device per worker")
+        dev_arr = (ctypes.c_int * max(1, workers))(*devs)
+        if _weights is None:
+            st = self._lib.pf_create_toy(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                         dev_arr, workers, ctypes.byref(self._ctx))
+        else:
+            mats, cb = _weights
+            keep = [_f64c(m) for m in mats]
+            ptrs = (ctypes.POINTER(ctypes.c_double) * len(keep))(*[_dptr(m) for m in keep])
+            cbc = _f64c(cb)
+            st = self._lib.pf_create(ctypes.byref(desc), ptrs, _dptr(cbc), PF_ROW_MAJOR,
+                                     dev_arr, workers, ctypes.byref(self._ctx))
+        if st != PF_OK:
+            _raise(st, self._lib.pf_last_error(None).decode())
+
+    @classmethod
+    def from_weights(cls, layer_mats, condition_bias, heads: int, seq_len: int,
+                     workers: int = 1, devices=None) -> "ToyDiTCuda":
+        """layer_mats: per layer (w_q, w_k, w_v, w_o, w_mlp_in, w_mlp_out) fp64."""
+        flat = [m for layer in layer_mats for m in layer]
+        hs = int(np.asarray(flat[0]).shape[0])
+        mlp = int(np.asarray(flat[4]).shape[1])
+        obj = cls.__new__(cls)
+        cls.__init__(obj, 0, len(layer_mats), hs, heads, mlp / hs, seq_len, workers,
+                     devices, _weights=(flat, condition_bias))
+        return obj
+
+    # ---------------------------------------------------------------- lifecycle
+    def close(self) -> None:
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._lib.pf_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _err(self) -> str:
+        return self._lib.pf_last_error(self._ctx).decode()
+
+    # ---------------------------------------------------------------- stages
+    def stage_layers(self) -> List[range]:
+        n = self._lib.pf_stage_count(self._ctx)
+        out = []
+        for d in range(n):
+            f = self._lib.pf_stage_first_layer(self._ctx, d)
+            c = self._lib.pf_stage_layer_count(self._ctx, d)
+            out.append(range(f, f + c))
+        return out
+
+    def last_launch_count(self) -> int:
+        return int(self._lib.pf_last_launch_count(self._ctx))
+
+    # ---------------------------------------------------------------- runs
+    def run_pipefusion(self, x_init, steps: int, patches: int, warmup: int,
+                       eta: float) -> ParallelRunResult:
+        """ditsim::run_pipefusion (execute.hpp:124-127) on the GPU stages."""
+        x = _f64c(x_init)
+        if x.shape != (self.seq_len, self.hidden_size):
+            raise ValidationError("latent width does not match the model hidden size")
+        out = np.empty_like(x)
+        per = max(0, patches * (steps - warmup))
+        cap = self.workers * per
+        ff = (ctypes.c_double * max(1, cap))()
+        st = _Stats(0, 0, ff, cap)
+        status = self._lib.pf_run_pipefusion(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
+                                             patches, warmup, ctypes.c_double(eta),
+                                             _dptr(out), ctypes.byref(st))
+        _raise(status, self._err())
+        fr = [list(ff[d * per:(d + 1) * per]) for d in range(self.workers)]
+        return ParallelRunResult(out, StalenessStats(st.fresh_patch_reads,
+                                                     st.stale_patch_reads, fr))
+
+    def serial_reference(self, x_init, steps: int, eta: float) -> np.ndarray:
+        """ditsim::serial_reference (execute.hpp:102-104) on the GPU."""
+        x = _f64c(x_init)
+        out = np.empty_like(x)
+        status = self._lib.pf_serial_reference(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
+                                               ctypes.c_double(eta), _dptr(out))
+        _raise(status, self._err())
+        return out
+
+    def layer_forward(self, layer: int, h, k_buf, v_buf, row0: int):
+        """ditsim::toy_layer_forward (execute.hpp:75-77); returns (h, k, v)."""
+        h = _f64c(h).copy()
+        k = _f64c(k_buf).copy()
+        v = _f64c(v_buf).copy()
+        status = self._lib.pf_layer_forward(self._ctx, layer, _dptr(h), h.shape[0], row0,
+                                            _dptr(k), _dptr(v), PF_ROW_MAJOR)
+        _raise(status, self._err())
+        return h, k, v
+
+    def run_pipefusion_device(self, x_dev_ptr: int, steps: int, patches: int,
+                              warmup: int, eta: float, stream_ptr: int = 0) -> StalenessStats:
+        """Enqueue a run on a device fp32 latent (in place); asynchronous."""
+        st = _Stats(0, 0, None, 0)
+        status = self._lib.pf_run_pipefusion_device(
+            self._ctx, ctypes.c_void_p(x_dev_ptr), steps, patches, warmup,
+            ctypes.c_double(eta), ctypes.c_void_p(stream_ptr), ctypes.byref(st))
+        _raise(status, self._err())
+        return StalenessStats(st.fresh_patch_reads, st.stale_patch_reads, [])
+
+    def synchronize(self, stream_ptr: int = 0) -> None:
+        _raise(self._lib.pf_synchronize(self._ctx, ctypes.c_void_p(stream_ptr)), self._err())

@@ -1,0 +1,288 @@
+// C ABI (include/pipefusion_b200.h) over the PipeFusion runtime.
+#include "pipefusion_b200.h"
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "runtime.h"
+
+struct pf_ctx {
+  std::unique_ptr<pf::Engine> engine;
+  std::string last_error;
+  float* x_scratch = nullptr;  // device latent for the host-buffer entry points
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+template <class F>
+pf_status guarded(std::string* err, F&& f) {
+  try {
+    f();
+    if (err) err->clear();
+    return PF_OK;
+  } catch (const pf::ValidationError& e) {
+    if (err) *err = e.what();
+    return PF_VALIDATION;
+  } catch (const pf::NumericError& e) {
+    if (err) *err = e.what();
+    return PF_NUMERIC;
+  } catch (const pf::CudaError& e) {
+    if (err) *err = e.what();
+    return PF_CUDA;
+  } catch (const std::bad_alloc&) {
+    if (err) *err = "host allocation failed";
+    return PF_CUDA;
+  } catch (const std::exception& e) {
+    if (err) *err = e.what();
+    return PF_CUDA;
+  }
+}
+
+pf::ModelShape shape_of(const pf_model_desc* d) {
+  if (!d) throw pf::ValidationError("model description is NULL");
+  pf::ModelShape s;
+  s.layers = d->layers;
+  s.hs = d->hidden_size;
+  s.heads = d->heads;
+  s.mlp = d->mlp_hidden;
+  s.P = d->seq_len;
+  return s;
+}
+
+std::vector<int> device_list(const int* devices, int n) {
+  if (n < 1) throw pf::ValidationError("workers and patches must be >= 1");
+  std::vector<int> v(static_cast<size_t>(n), 0);
+  if (devices)
+    for (int i = 0; i < n; ++i) v[size_t(i)] = devices[i];
+  return v;
+}
+
+// Uniform in [-1, 1) from the top 53 bits of mt19937_64, matrix filled
+// row-major -- the reference's next_uniform / fill_matrix
+// (toy_model.cpp:28-40).
+double next_uniform(std::mt19937_64& rng) {
+  return double(rng() >> 11) * 0x1.0p-52 - 1.0;
+}
+
+void fill(std::mt19937_64& rng, std::vector<double>& m, int rows, int cols,
+          double scale) {
+  m.resize(size_t(rows) * cols);
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) m[size_t(r) * cols + c] = next_uniform(rng) * scale;
+}
+
+void upload_x(pf_ctx* ctx, const double* x, pf_layout layout) {
+  const pf::ModelShape& m = ctx->engine->shape();
+  const int64_t P = m.P;
+  const int hs = m.hs;
+  std::vector<float> xf(size_t(P) * hs);
+  for (int64_t r = 0; r < P; ++r)
+    for (int c = 0; c < hs; ++c)
+      xf[size_t(r) * hs + c] = float(layout == PF_COL_MAJOR ? x[size_t(c) * P + r]
+                                                            : x[size_t(r) * hs + c]);
+  const pf::Stage& s0 = ctx->engine->stage(0);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s0.device);
+  if (!ctx->x_scratch) {
+    if (cudaMalloc(&ctx->x_scratch, xf.size() * 4) != cudaSuccess)
+      throw pf::CudaError("cudaMalloc latent failed");
+  }
+  cudaError_t e = cudaMemcpy(ctx->x_scratch, xf.data(), xf.size() * 4, cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) throw pf::CudaError(std::string("latent upload: ") + cudaGetErrorString(e));
+}
+
+void download_x(pf_ctx* ctx, double* x, pf_layout layout) {
+  const pf::ModelShape& m = ctx->engine->shape();
+  const int64_t P = m.P;
+  const int hs = m.hs;
+  std::vector<float> xf(size_t(P) * hs);
+  const pf::Stage& s0 = ctx->engine->stage(0);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s0.device);
+  cudaError_t e = cudaMemcpy(xf.data(), ctx->x_scratch, xf.size() * 4, cudaMemcpyDeviceToHost);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) throw pf::CudaError(std::string("latent download: ") + cudaGetErrorString(e));
+  for (int64_t r = 0; r < P; ++r)
+    for (int c = 0; c < hs; ++c) {
+      const double v = double(xf[size_t(r) * hs + c]);
+      if (layout == PF_COL_MAJOR) x[size_t(c) * P + r] = v;
+      else x[size_t(r) * hs + c] = v;
+    }
+}
+
+void export_stats(const pf::RunStats& rs, pf_stats* out) {
+  if (!out) return;
+  out->fresh_patch_reads = rs.fresh;
+  out->stale_patch_reads = rs.stale;
+  if (out->fresh_fraction) {
+    int64_t k = 0;
+    for (const auto& v : rs.fresh_fraction)
+      for (double f : v)
+        if (k < out->fresh_fraction_capacity) out->fresh_fraction[k++] = f;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
+                        const int* devices, int n_stages, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    // build_toy_model (toy_model.cpp:44-82), streamed layer by layer.
+    std::mt19937_64 rng(seed);
+    const double scale = 1.0 / std::sqrt(double(s.hs));
+    std::vector<double> w[6];
+    for (int l = 0; l < s.layers; ++l) {
+      fill(rng, w[0], s.hs, s.hs, scale);
+      fill(rng, w[1], s.hs, s.hs, scale);
+      fill(rng, w[2], s.hs, s.hs, scale);
+      fill(rng, w[3], s.hs, s.hs, scale);
+      fill(rng, w[4], s.hs, s.mlp, scale);
+      fill(rng, w[5], s.mlp, s.hs, scale);
+      pf::HostMatrix hm[6] = {
+          {w[0].data(), s.hs, s.hs, false},  {w[1].data(), s.hs, s.hs, false},
+          {w[2].data(), s.hs, s.hs, false},  {w[3].data(), s.hs, s.hs, false},
+          {w[4].data(), s.hs, s.mlp, false}, {w[5].data(), s.mlp, s.hs, false}};
+      ctx->engine->load_layer(l, hm);
+    }
+    std::vector<double> cb;
+    fill(rng, cb, 1, s.hs, 1.0);
+    ctx->engine->load_condition_bias(cb.data());
+    *out = ctx.release();
+  });
+}
+
+pf_status pf_create(const pf_model_desc* desc, const double* const* weights,
+                    const double* condition_bias, pf_layout layout,
+                    const int* devices, int n_stages, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out || !weights || !condition_bias)
+      throw pf::ValidationError("NULL weights / bias / output pointer");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    const bool cm = layout == PF_COL_MAJOR;
+    for (int l = 0; l < s.layers; ++l) {
+      const double* const* w = weights + 6 * l;
+      for (int i = 0; i < 6; ++i)
+        if (!w[i]) throw pf::ValidationError("NULL weight matrix");
+      pf::HostMatrix hm[6] = {{w[0], s.hs, s.hs, cm},  {w[1], s.hs, s.hs, cm},
+                              {w[2], s.hs, s.hs, cm},  {w[3], s.hs, s.hs, cm},
+                              {w[4], s.hs, s.mlp, cm}, {w[5], s.mlp, s.hs, cm}};
+      ctx->engine->load_layer(l, hm);
+    }
+    ctx->engine->load_condition_bias(condition_bias);
+    *out = ctx.release();
+  });
+}
+
+void pf_destroy(pf_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->x_scratch) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->engine->stage(0).device);
+    cudaFree(ctx->x_scratch);
+    cudaSetDevice(prev);
+  }
+  delete ctx;
+}
+
+const char* pf_last_error(const pf_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : g_create_error.c_str();
+}
+
+pf_status pf_run_pipefusion(pf_ctx* ctx, const double* x_init, pf_layout layout,
+                            int steps, int patches, int warmup, double eta,
+                            double* x_out, pf_stats* stats) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!x_init || !x_out) throw pf::ValidationError("NULL latent pointer");
+    upload_x(ctx, x_init, layout);
+    pf::RunStats rs;
+    const pf::Stage& s0 = ctx->engine->stage(0);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s0.device);
+    struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
+    ctx->engine->enqueue_run(ctx->x_scratch, steps, patches, warmup, float(eta),
+                             s0.stream, &rs);
+    ctx->engine->finish(s0.stream);
+    download_x(ctx, x_out, layout);
+    export_stats(rs, stats);
+  });
+}
+
+pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
+                                   int patches, int warmup, double eta,
+                                   void* stream, pf_stats* stats) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!x_dev) throw pf::ValidationError("NULL latent pointer");
+    pf::RunStats rs;
+    ctx->engine->enqueue_run(x_dev, steps, patches, warmup, float(eta),
+                             static_cast<cudaStream_t>(stream), &rs);
+    export_stats(rs, stats);
+  });
+}
+
+pf_status pf_synchronize(pf_ctx* ctx, void* stream) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error,
+                 [&] { ctx->engine->finish(static_cast<cudaStream_t>(stream)); });
+}
+
+pf_status pf_serial_reference(pf_ctx* ctx, const double* x_init, pf_layout layout,
+                              int steps, double eta, double* x_out) {
+  if (!ctx) return PF_VALIDATION;
+  if (steps < 1) {
+    ctx->last_error = "serial_reference needs steps >= 1";
+    return PF_VALIDATION;
+  }
+  // W = S with one patch: every step is a full-sequence synchronous forward
+  // with freshly written K/V, which is serial_reference (toy_model.cpp:201-214).
+  return pf_run_pipefusion(ctx, x_init, layout, steps, 1, steps, eta, x_out, nullptr);
+}
+
+pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
+                           int64_t row0, double* k_buf, double* v_buf,
+                           pf_layout layout) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!h || !k_buf || !v_buf) throw pf::ValidationError("NULL buffer pointer");
+    ctx->engine->layer_forward_host(layer, h, rows, row0, k_buf, v_buf,
+                                    layout == PF_COL_MAJOR);
+  });
+}
+
+int pf_stage_count(const pf_ctx* ctx) { return ctx ? ctx->engine->stage_count() : 0; }
+int pf_stage_first_layer(const pf_ctx* ctx, int stage) {
+  if (!ctx || stage < 0 || stage >= ctx->engine->stage_count()) return -1;
+  return ctx->engine->stage(stage).first_layer;
+}
+int pf_stage_layer_count(const pf_ctx* ctx, int stage) {
+  if (!ctx || stage < 0 || stage >= ctx->engine->stage_count()) return -1;
+  return ctx->engine->stage(stage).layer_count;
+}
+int64_t pf_last_launch_count(const pf_ctx* ctx) {
+  return ctx ? ctx->engine->last_launch_count() : 0;
+}
+const char* pf_version(void) { return "pipefusion_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

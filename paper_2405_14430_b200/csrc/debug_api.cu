@@ -1,0 +1,95 @@
+// Kernel-level test entry points (include/pipefusion_b200_debug.h).
+#include <cmath>
+#include <vector>
+
+#include "kernels.h"
+#include "pipefusion_b200_debug.h"
+
+namespace {
+
+// Repack [P x hs] row-major bf16 into the attention layouts
+// (Q/K: [heads][P][dhp], V^T: [heads][dhp][P]), zero padded.
+__global__ void pack_heads_kernel(const pf::bf16* __restrict__ src, pf::bf16* __restrict__ qk,
+                                  pf::bf16* __restrict__ vt, int P, int hs, int heads, int dh,
+                                  int dhp) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P * hs) return;
+  const int r = idx / hs, c = idx % hs;
+  const int h = c / dh, d = c % dh;
+  if (qk) qk[(size_t(h) * P + r) * dhp + d] = src[idx];
+  if (vt) vt[(size_t(h) * dhp + d) * P + r] = src[idx];
+}
+
+}  // namespace
+
+extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
+                             int row0, int total_rows, int N, int K, void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CUtensorMap ta, tb;
+  if (!pf::encode_tmap_bf16_2d(&ta, A, uint64_t(K), uint64_t(total_rows), uint64_t(K) * 2,
+                               64, 128, 128))
+    return int(cudaErrorInvalidValue);
+  if (!pf::encode_tmap_bf16_2d(&tb, B, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
+                               uint32_t(pf::gemm_bn(N)), 128))
+    return int(cudaErrorInvalidValue);
+  pf::EpiParams ep;
+  ep.out_f32 = C - size_t(row0) * N;  // epilogue indexes by global row
+  ep.ld = N;
+  return int(pf::gemm(ta, tb, rows, row0, N, K, pf::Epi::StoreF32, ep,
+                      pf::device_sm_count(dev), static_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
+                                  int P, int rows, int row0, int heads, int hs,
+                                  void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int dh = hs / heads;
+  const int dhp = (dh + 15) / 16 * 16;
+  pf::bf16 *qp = nullptr, *kp = nullptr, *vp = nullptr;
+  float* work = nullptr;
+  const size_t n = size_t(heads) * P * dhp;
+  cudaMallocAsync(reinterpret_cast<void**>(&qp), n * 2, s);
+  cudaMallocAsync(reinterpret_cast<void**>(&kp), n * 2, s);
+  cudaMallocAsync(reinterpret_cast<void**>(&vp), n * 2, s);
+  cudaMemsetAsync(qp, 0, n * 2, s);
+  cudaMemsetAsync(kp, 0, n * 2, s);
+  cudaMemsetAsync(vp, 0, n * 2, s);
+  const int total = P * hs;
+  pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(q), qp,
+                                                         nullptr, P, hs, heads, dh, dhp);
+  pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(k), kp,
+                                                         nullptr, P, hs, heads, dh, dhp);
+  pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(v),
+                                                         nullptr, vp, P, hs, heads, dh, dhp);
+  CUtensorMap tq, tk, tv;
+  bool ok = pf::encode_tmap_bf16_2d(&tq, qp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
+                                    128, 32) &&
+            pf::encode_tmap_bf16_2d(&tk, kp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
+                                    128, 32) &&
+            pf::encode_tmap_bf16_2d(&tv, vp, uint64_t(P), uint64_t(heads) * dhp,
+                                    uint64_t(P) * 2, 64, uint32_t(dhp), 128);
+  int err = ok ? 0 : int(cudaErrorInvalidValue);
+  if (ok) {
+    pf::AttnLaunch a{dhp, P, rows, row0, heads, dh, hs, float(1.0 / std::sqrt(double(dh))),
+                     static_cast<pf::bf16*>(out), nullptr, 0};
+    const int sms = pf::device_sm_count(dev);
+    const int splits = pf::attn_splits(a, sms);
+    if (splits > 1) {
+      a.work_floats = pf::attn_work_floats(dhp, heads, rows, splits);
+      cudaMallocAsync(reinterpret_cast<void**>(&work), a.work_floats * 4, s);
+      a.work = work;
+    }
+    err = int(pf::attention(tq, tk, tv, a, sms, s));
+  }
+  cudaStreamSynchronize(s);
+  cudaFreeAsync(qp, s);
+  cudaFreeAsync(kp, s);
+  cudaFreeAsync(vp, s);
+  if (work) cudaFreeAsync(work, s);
+  cudaStreamSynchronize(s);
+  if (!err) err = int(cudaGetLastError());
+  return err;
+}

@@ -1,0 +1,178 @@
+// Persistent warp-specialised tcgen05 GEMM for the toy DiT block:
+//   D[rows x N] = A[rows x K] . B[N x K]^T      (bf16 operands, fp32 in TMEM)
+// followed by a fused epilogue functor (K/V scatter, residual add, tanh).
+//
+// This is the sm_100a replacement of the reference's `matmul_rows`
+// (/root/reference/proj/src/toy_model.cpp:93-102): out = x . w with w stored
+// here pre-transposed (N x K, K-major) so both operands are K-major.
+//
+// Roles (256 threads):
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      tcgen05.mma issuer (one elected lane)
+//   warp 2      TMEM allocator / deallocator
+//   warps 4..7  epilogue: TMEM -> registers -> functor (warp w reads lanes
+//               32*(w%4) .. +31, i.e. one accumulator row per thread)
+// Pipelines: STAGES-deep smem ring (TMA <-> MMA) and a 2-deep TMEM
+// accumulator ring (MMA <-> epilogue) so a tile's epilogue overlaps the next
+// tile's main loop.
+#pragma once
+
+#include "sm100_ptx.cuh"
+
+namespace pf {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBK = 64;  // 64 bf16 = 128 B = one SW128 atom row
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr uint32_t kBBytes = BN * kGemmBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
+  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;  // + align slack
+  static constexpr uint32_t kTmemCols = (2 * BN <= 32)    ? 32
+                                        : (2 * BN <= 64)  ? 64
+                                        : (2 * BN <= 128) ? 128
+                                        : (2 * BN <= 256) ? 256
+                                                          : 512;
+};
+
+template <int BN, int STAGES, class Epi>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tma_a,
+                        const __grid_constant__ CUtensorMap tma_b, int rows,
+                        int row0, int N, int K, Epi epi) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = ptx::lane_id();
+  const int m_tiles = (rows + kGemmBM - 1) / kGemmBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tma_a);
+    ptx::prefetch_tmap(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          ptx::mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK,
+                           row0 + mt * kGemmBM);
+          ptx::tma_load_2d(sb, &tma_b, &full[stage], kb * kGemmBK, nt * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b_base = a_base + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k) {
+            ptx::umma_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
+                              ptx::desc_kmajor_sw128(b_base + k * 32), idesc,
+                              (kb | k) != 0);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mt = tile % m_tiles;
+      const int nt = tile / m_tiles;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const int local_row = mt * kGemmBM + 32 * q + int(lane);
+      const bool row_ok = local_row < rows;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = nt * BN + 32 * c;
+        if (col0 >= N) break;
+        uint32_t r[32];
+        ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, r);
+        ptx::tmem_wait_ld();
+        if (row_ok) {
+          const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+          epi(row0 + local_row, col0, v, nvalid);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace pf

@@ -1,0 +1,429 @@
+// Kernel instantiations and host launchers: tcgen05 GEMM with the toy-DiT
+// epilogues, tcgen05 attention, and the bandwidth-bound sampler kernels.
+#include <climits>
+#include <cstdio>
+#include <mutex>
+
+#include "attn_sm100.cuh"
+#include "gemm_sm100.cuh"
+#include "kernels.h"
+
+namespace pf {
+
+// ============================================================== tensor maps
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
+                              void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<EncodeFn>(p);
+    }
+  });
+  return fn;
+}
+
+}  // namespace
+
+bool encode_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner,
+                         uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
+                         uint32_t box_outer, int swizzle_bytes) {
+  EncodeFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+  if (swizzle_bytes == 32) sw = CU_TENSOR_MAP_SWIZZLE_32B;
+  if (swizzle_bytes == 64) sw = CU_TENSOR_MAP_SWIZZLE_64B;
+  if (swizzle_bytes == 128) sw = CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int device_sm_count(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 1;
+}
+
+// ============================================================== epilogues
+namespace {
+
+// The dynamic shared-memory opt-in is per (kernel, device); remember which
+// devices have been configured for each kernel instantiation.
+template <auto kern>
+cudaError_t ensure_smem_attr(uint32_t bytes) {
+  static std::mutex mu;
+  static uint64_t done_mask = 0;  // one static per instantiation of Kern
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && (done_mask >> dev) & 1) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess && dev < 64) done_mask |= uint64_t(1) << dev;
+  return e;
+}
+
+struct EpiStoreF32 {
+  float* out;
+  int ld;
+  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+    float* o = out + size_t(row) * ld + col0;
+    if (nvalid == 32) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4)
+        *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < nvalid) o[e] = v[e];
+    }
+  }
+};
+
+// h (fp32 residual stream) += acc; refresh the bf16 operand copy; flag
+// non-finite values (the reference's require_finite, execute.cpp:75-83).
+struct EpiResidual {
+  float* h;
+  bf16* hb;
+  int ld;
+  int* flag;
+  int code;
+  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+    float* hr = h + size_t(row) * ld + col0;
+    bf16* br = hb + size_t(row) * ld + col0;
+    bool bad = false;
+    if (nvalid == 32) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        float4 a = *reinterpret_cast<const float4*>(hr + e);
+        float4 b = *reinterpret_cast<const float4*>(hr + e + 4);
+        a.x += v[e + 0]; a.y += v[e + 1]; a.z += v[e + 2]; a.w += v[e + 3];
+        b.x += v[e + 4]; b.y += v[e + 5]; b.z += v[e + 6]; b.w += v[e + 7];
+        *reinterpret_cast<float4*>(hr + e) = a;
+        *reinterpret_cast<float4*>(hr + e + 4) = b;
+        uint4 pk;
+        pk.x = ptx::pack_bf16x2(a.x, a.y);
+        pk.y = ptx::pack_bf16x2(a.z, a.w);
+        pk.z = ptx::pack_bf16x2(b.x, b.y);
+        pk.w = ptx::pack_bf16x2(b.z, b.w);
+        *reinterpret_cast<uint4*>(br + e) = pk;
+        bad |= !(isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) &&
+                 isfinite(b.x) && isfinite(b.y) && isfinite(b.z) && isfinite(b.w));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        if (e < nvalid) {
+          const float x = hr[e] + v[e];
+          hr[e] = x;
+          br[e] = __float2bfloat16_rn(x);
+          bad |= !isfinite(x);
+        }
+      }
+    }
+    if (bad && flag) atomicMin(flag, code);
+  }
+};
+
+struct EpiTanh {
+  bf16* z;
+  int ld;
+  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+    bf16* o = z + size_t(row) * ld + col0;
+    if (nvalid == 32) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        uint4 pk;
+        pk.x = ptx::pack_bf16x2(ptx::tanh_approx(v[e + 0]), ptx::tanh_approx(v[e + 1]));
+        pk.y = ptx::pack_bf16x2(ptx::tanh_approx(v[e + 2]), ptx::tanh_approx(v[e + 3]));
+        pk.z = ptx::pack_bf16x2(ptx::tanh_approx(v[e + 4]), ptx::tanh_approx(v[e + 5]));
+        pk.w = ptx::pack_bf16x2(ptx::tanh_approx(v[e + 6]), ptx::tanh_approx(v[e + 7]));
+        *reinterpret_cast<uint4*>(o + e) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < nvalid) o[e] = __float2bfloat16_rn(ptx::tanh_approx(v[e]));
+    }
+  }
+};
+
+// Fused QKV projection epilogue: Q and K rows go to the head-major padded
+// buffers at their sequence row (K overwrites the stale rows of this patch in
+// place, toy_model.cpp:174-175); V is stored transposed per head so it is the
+// K-major B operand of the P.V product.
+struct EpiQKV {
+  bf16* q;
+  bf16* k;
+  bf16* vt;
+  int hs, dh, dhp, P;
+  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      if (e >= nvalid) break;
+      const int n = col0 + e;
+      const int which = n / hs;
+      const int nn = n - which * hs;
+      const int head = nn / dh;
+      const int d = nn - head * dh;
+      const bf16 val = __float2bfloat16_rn(v[e]);
+      if (which == 0) {
+        q[(size_t(head) * P + row) * dhp + d] = val;
+      } else if (which == 1) {
+        k[(size_t(head) * P + row) * dhp + d] = val;
+      } else {
+        vt[(size_t(head) * dhp + d) * P + row] = val;
+      }
+    }
+  }
+};
+
+template <int BN, int STAGES, class E>
+cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int rows,
+                        int row0, int N, int K, const E& epi, int sm_count,
+                        cudaStream_t stream) {
+  using L = GemmSmem<BN, STAGES>;
+  constexpr auto kern = gemm_bf16_tn_kernel<BN, STAGES, E>;
+  cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((rows + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
+  const int grid = tiles < sm_count ? tiles : sm_count;
+  kern<<<grid, 256, L::kTotal, stream>>>(a, b, rows, row0, N, K, epi);
+  return cudaGetLastError();
+}
+
+template <int BN, int STAGES>
+cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
+                          int row0, int N, int K, Epi kind, const EpiParams& ep,
+                          int sm_count, cudaStream_t stream) {
+  switch (kind) {
+    case Epi::StoreF32:
+      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K,
+                                     EpiStoreF32{ep.out_f32, ep.ld}, sm_count, stream);
+    case Epi::Residual:
+      return launch_gemm<BN, STAGES>(
+          a, b, rows, row0, N, K,
+          EpiResidual{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code}, sm_count,
+          stream);
+    case Epi::Tanh:
+      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K,
+                                     EpiTanh{ep.out_bf16, ep.ld}, sm_count, stream);
+    case Epi::QKV:
+      return launch_gemm<BN, STAGES>(
+          a, b, rows, row0, N, K,
+          EpiQKV{ep.q, ep.k, ep.vt, ep.hs, ep.dh, ep.dhp, ep.P}, sm_count, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int gemm_bn(int N) { return N <= 64 ? 64 : 128; }
+
+cudaError_t gemm(const CUtensorMap& a, const CUtensorMap& b, int rows, int row0,
+                 int N, int K, Epi kind, const EpiParams& ep, int sm_count,
+                 cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (gemm_bn(N) == 64)
+    return gemm_dispatch<64, 8>(a, b, rows, row0, N, K, kind, ep, sm_count, stream);
+  return gemm_dispatch<128, 6>(a, b, rows, row0, N, K, kind, ep, sm_count, stream);
+}
+
+// ============================================================== attention
+int attn_splits(const AttnLaunch& a, int sm_count) {
+  const int q_tiles = (a.rows + kAttnBM - 1) / kAttnBM;
+  const int ctas = q_tiles * a.heads;
+  const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  if (ctas >= sm_count || blocks < 2) return 1;
+  int splits = (sm_count + ctas - 1) / ctas;
+  if (splits > blocks) splits = blocks;
+  if (splits > 16) splits = 16;
+  const int per = (blocks + splits - 1) / splits;
+  return (blocks + per - 1) / per;
+}
+
+size_t attn_work_floats(int dhp, int heads, int rows, int splits) {
+  if (splits <= 1) return 0;
+  const size_t rows_pad = size_t((rows + kAttnBM - 1) / kAttnBM) * kAttnBM;
+  return size_t(splits) * heads * rows_pad * (dhp + 2);
+}
+
+namespace {
+template <int DHP>
+cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
+                        const CUtensorMap& vt, const AttnLaunch& a, int sm_count,
+                        cudaStream_t stream) {
+  using L = AttnSmem<DHP>;
+  {
+    cudaError_t e = ensure_smem_attr<attn_fwd_kernel<DHP>>(L::kTotal);
+    if (e != cudaSuccess) return e;
+  }
+  const int q_tiles = (a.rows + kAttnBM - 1) / kAttnBM;
+  const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  const int splits = attn_splits(a, sm_count);
+  AttnParams prm;
+  prm.P = a.P;
+  prm.rows = a.rows;
+  prm.row0 = a.row0;
+  prm.heads = a.heads;
+  prm.dh = a.dh;
+  prm.hs = a.hs;
+  prm.scale_log2 = a.scale * 1.4426950408889634f;
+  prm.kv_splits = splits;
+  prm.blocks_per_split = (blocks + splits - 1) / splits;
+  prm.out = a.out;
+  prm.rows_pad = q_tiles * kAttnBM;
+  prm.part_o = nullptr;
+  prm.part_ml = nullptr;
+  if (splits > 1) {
+    const size_t need = attn_work_floats(DHP, a.heads, a.rows, splits);
+    if (!a.work || a.work_floats < need) return cudaErrorInvalidValue;
+    prm.part_o = a.work;
+    prm.part_ml = a.work + size_t(splits) * a.heads * prm.rows_pad * DHP;
+  }
+  dim3 grid(q_tiles, a.heads, splits);
+  attn_fwd_kernel<DHP><<<grid, 256, L::kTotal, stream>>>(q, k, vt, prm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || splits == 1) return e;
+  const int total = a.rows * a.heads * (DHP / 16);
+  attn_combine_kernel<DHP><<<(total + 255) / 256, 256, 0, stream>>>(prm);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
+                      const CUtensorMap& vt, const AttnLaunch& a, int sm_count,
+                      cudaStream_t stream) {
+  if (a.rows <= 0) return cudaSuccess;
+  switch (a.dhp) {
+    case 16: return launch_attn<16>(q, k, vt, a, sm_count, stream);
+    case 32: return launch_attn<32>(q, k, vt, a, sm_count, stream);
+    case 48: return launch_attn<48>(q, k, vt, a, sm_count, stream);
+    case 64: return launch_attn<64>(q, k, vt, a, sm_count, stream);
+    case 80: return launch_attn<80>(q, k, vt, a, sm_count, stream);
+    case 96: return launch_attn<96>(q, k, vt, a, sm_count, stream);
+    case 112: return launch_attn<112>(q, k, vt, a, sm_count, stream);
+    case 128: return launch_attn<128>(q, k, vt, a, sm_count, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ============================================================== sampler
+namespace {
+
+// Patch split + deferred sampler update (execute.cpp:198-203):
+//   x_j -= eta * eps_j (when update);  h_j = x_j + cb;  hb_j = bf16(h_j)
+// 4 consecutive columns per thread (hs % 8 == 0 keeps float4 alignment).
+__global__ void patch_prepare_kernel(float* __restrict__ x,
+                                     const float* __restrict__ eps,
+                                     const float* __restrict__ cb,
+                                     float* __restrict__ h32, bf16* __restrict__ hb,
+                                     size_t base, size_t n4, int hs4, float eta,
+                                     int update) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const size_t off = base + 4 * i;
+    float4 xv = *reinterpret_cast<const float4*>(x + off);
+    if (update) {
+      const float4 ev = *reinterpret_cast<const float4*>(eps + off);
+      xv.x -= eta * ev.x;
+      xv.y -= eta * ev.y;
+      xv.z -= eta * ev.z;
+      xv.w -= eta * ev.w;
+      *reinterpret_cast<float4*>(x + off) = xv;
+    }
+    const int c4 = int(i % size_t(hs4));
+    const float4 bv = *reinterpret_cast<const float4*>(cb + 4 * c4);
+    float4 hv = make_float4(xv.x + bv.x, xv.y + bv.y, xv.z + bv.z, xv.w + bv.w);
+    *reinterpret_cast<float4*>(h32 + off) = hv;
+    uint2 pk;
+    pk.x = ptx::pack_bf16x2(hv.x, hv.y);
+    pk.y = ptx::pack_bf16x2(hv.z, hv.w);
+    *reinterpret_cast<uint2*>(hb + off) = pk;
+  }
+}
+
+__global__ void latent_update_kernel(float* __restrict__ x,
+                                     const float* __restrict__ src, float eta,
+                                     size_t n4) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+       i += size_t(gridDim.x) * blockDim.x) {
+    float4 xv = reinterpret_cast<float4*>(x)[i];
+    const float4 sv = reinterpret_cast<const float4*>(src)[i];
+    xv.x -= eta * sv.x;
+    xv.y -= eta * sv.y;
+    xv.z -= eta * sv.z;
+    xv.w -= eta * sv.w;
+    reinterpret_cast<float4*>(x)[i] = xv;
+  }
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ h, bf16* __restrict__ hb,
+                               size_t n4) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(h)[i];
+    uint2 pk;
+    pk.x = ptx::pack_bf16x2(v.x, v.y);
+    pk.y = ptx::pack_bf16x2(v.z, v.w);
+    reinterpret_cast<uint2*>(hb)[i] = pk;
+  }
+}
+
+__global__ void reset_flag_kernel(int* flag) { *flag = INT_MAX; }
+
+int ew_grid(size_t n4) {
+  size_t g = (n4 + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t patch_prepare(float* x, const float* eps, const float* cb, float* h32,
+                          bf16* hb, int row0, int rows, int hs, float eta,
+                          bool update, cudaStream_t stream) {
+  const size_t base = size_t(row0) * hs;
+  const size_t n4 = size_t(rows) * hs / 4;
+  patch_prepare_kernel<<<ew_grid(n4), 256, 0, stream>>>(
+      x, eps, cb, h32, hb, base, n4, hs / 4, eta, update ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t latent_update(float* x, const float* src, float eta, size_t n,
+                          cudaStream_t stream) {
+  latent_update_kernel<<<ew_grid(n / 4), 256, 0, stream>>>(x, src, eta, n / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream) {
+  to_bf16_kernel<<<ew_grid(n / 4), 256, 0, stream>>>(h32, hb, n / 4);
+  return cudaGetLastError();
+}
+
+cudaError_t reset_flag(int* flag, cudaStream_t stream) {
+  reset_flag_kernel<<<1, 1, 0, stream>>>(flag);
+  return cudaGetLastError();
+}
+
+}  // namespace pf

@@ -1,0 +1,151 @@
+// PipeFusion runtime on B200: per-stage device state, the patch-pipeline
+// scheduler and the staleness bookkeeping. Host C++; the hot arithmetic is in
+// kernels.cu.
+//
+// Mirrors the reference executor (/root/reference/proj/src/execute.cpp):
+//   StageBuffers            execute.cpp:38-49    -> Stage (+ StageLayer K/V)
+//   check_staleness_and_count :51-65             -> Engine::check_staleness
+//   stage_forward_full      :134-147             -> Engine::stage_full
+//   stage_forward_patch     :150-165             -> Engine::stage_patch
+//   run_pipefusion_inline   :167-223             -> Engine::enqueue_run
+//   Channel<PatchMsg> sends :239-244, 275-281    -> Engine::send_rows (stream
+//                                                   ordered copy + event)
+// The worker threads of the reference's Threads backend become CUDA streams:
+// the host enqueues the inline order once and stage streams overlap on the
+// device exactly where the reference's threads would run concurrently.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace pf {
+
+class ValidationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class NumericError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+struct ModelShape {
+  int layers = 0;
+  int hs = 0;
+  int heads = 0;
+  int mlp = 0;
+  int64_t P = 0;  // sequence length = K/V buffer rows
+  int dh = 0;
+  int dhp = 0;    // dh rounded up to a multiple of 16
+};
+
+// Host fp64 source of one layer's weights, in the reference's orientation
+// (x . W). `at(r, c)` reads element (r, c).
+struct HostMatrix {
+  const double* data = nullptr;
+  int rows = 0, cols = 0;
+  bool col_major = false;
+  double at(int r, int c) const {
+    return col_major ? data[size_t(c) * rows + r] : data[size_t(r) * cols + c];
+  }
+};
+
+struct StageLayer {
+  bf16* wqkv = nullptr;  // [3hs x hs]  (N x K)
+  bf16* wo = nullptr;    // [hs x hs]
+  bf16* win = nullptr;   // [mlp x hs]
+  bf16* wout = nullptr;  // [hs x mlp]
+  bf16* k = nullptr;     // [heads][P][dhp]
+  bf16* vt = nullptr;    // [heads][dhp][P]
+  CUtensorMap tm_wqkv, tm_wo, tm_win, tm_wout, tm_k, tm_vt;
+};
+
+struct Stage {
+  int device = 0;
+  int first_layer = 0;
+  int layer_count = 0;
+  int sm_count = 1;
+  cudaStream_t stream = nullptr;
+  std::vector<StageLayer> layers;
+  float* h32 = nullptr;   // [P x hs] residual stream (landing buffer)
+  bf16* hb = nullptr;     // [P x hs] bf16 operand copy of h32
+  bf16* q = nullptr;      // [heads][P][dhp]
+  bf16* attn = nullptr;   // [P x hs]
+  bf16* z = nullptr;      // [P x mlp]
+  float* attn_work = nullptr;
+  size_t attn_work_floats = 0;
+  int* flag = nullptr;    // first non-finite (ordinal), INT_MAX if none
+  CUtensorMap tm_hb, tm_attn, tm_z, tm_q;
+  cudaEvent_t ev_fwd = nullptr;  // "rows sent to stage d+1"
+  // stage 0 only
+  float* x = nullptr;    // [P x hs] latent
+  float* eps = nullptr;  // [P x hs] noise landing buffer (== last stage h32 when N == 1)
+  float* cb = nullptr;   // [hs] condition bias
+  std::vector<cudaEvent_t> ev_eps;  // per patch, recorded by the last stage
+};
+
+struct RunStats {
+  int64_t fresh = 0;
+  int64_t stale = 0;
+  std::vector<std::vector<double>> fresh_fraction;  // per stage
+};
+
+class Engine {
+ public:
+  // weights: per layer 6 HostMatrix (w_q, w_k, w_v, w_o, w_mlp_in, w_mlp_out);
+  // generated on the fly by `fill_layer` to avoid materialising fp64 models.
+  using LayerSource = void (*)(void* user, int layer, std::vector<double>* mats /*6*/);
+
+  Engine(const ModelShape& shape, const std::vector<int>& devices);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // Upload one layer (fp64 host matrices in the reference orientation).
+  void load_layer(int layer, const HostMatrix (&w)[6]);
+  void load_condition_bias(const double* cb);
+
+  const ModelShape& shape() const { return shape_; }
+  int stage_count() const { return int(stages_.size()); }
+  const Stage& stage(int d) const { return stages_[size_t(d)]; }
+  int64_t last_launch_count() const { return launches_; }
+
+  // Enqueue a full PipeFusion run on a device latent (stage 0's device).
+  void enqueue_run(float* x_dev, int steps, int patches, int warmup, float eta,
+                   cudaStream_t caller, RunStats* stats);
+  // Synchronise every stage and raise deferred numeric errors.
+  void finish(cudaStream_t caller);
+
+  // Single layer (unit parity), on stage owning `layer`.
+  void layer_forward_host(int layer, double* h, int64_t rows, int64_t row0,
+                          double* k_buf, double* v_buf, bool col_major);
+
+  float* stage0_x() { return stages_[0].x; }
+
+ private:
+  void alloc_stage(Stage& s, int first, int count, bool is_first);
+  void free_stage(Stage& s);
+  void layer_forward(Stage& s, int lf, int rows, int row0, int code);
+  void send_rows(int from, int row0, int rows);
+  int stage_of_layer(int layer) const;
+
+  ModelShape shape_;
+  std::vector<Stage> stages_;
+  int64_t launches_ = 0;
+  // ordinal -> (timestep, global layer) for non-finite reporting
+  std::vector<std::pair<int, int>> codes_;
+};
+
+void validate_shape(const ModelShape& s);
+
+}  // namespace pf

@@ -1,0 +1,94 @@
+"""Kernel-level parity of the sm_100a kernels against plain fp32 torch.
+
+GEMM  <- ditsim::matmul_rows   (toy_model.cpp:93-102)
+Attn  <- ditsim::attention_rows (toy_model.cpp:104-143)
+Inputs are bf16 (the kernels' operand type); the reference computation is
+fp32 on the same bf16 values, so the only differences are accumulation order
+(GEMM) and bf16 rounding of P plus exp2 approximation (attention).
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2405_14430_b200 import load_library  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B, rows, row0):
+    lib = load_library()
+    N, K = B.shape
+    C = torch.empty(rows, N, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    err = lib.pf_debug_gemm(A.data_ptr(), B.data_ptr(), C.data_ptr(), rows, row0,
+                            A.shape[0], N, K, s)
+    torch.cuda.synchronize()
+    assert err == 0, f"cuda error {err}"
+    return C
+
+
+@pytest.mark.parametrize("total,rows,row0,N,K", [
+    (128, 128, 0, 128, 64),
+    (256, 256, 0, 128, 128),
+    (64, 64, 0, 32, 32),        # reference config hs=32
+    (64, 16, 48, 96, 32),       # patch block, fused QKV width
+    (32, 32, 0, 16, 16),        # hs=16 (K < BK, N < BN)
+    (300, 170, 100, 200, 72),   # ragged everything
+    (4096, 512, 1536, 3456, 1152),  # PixArt patch QKV
+    (4096, 4096, 0, 1152, 4608),    # PixArt MLP-out full sequence
+])
+def test_gemm_matches_fp32(total, rows, row0, N, K):
+    g = torch.Generator(device="cuda").manual_seed(total + N + K)
+    A = (torch.rand(total, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    C = _gemm(A, B, rows, row0)
+    ref = A[row0:row0 + rows].float() @ B.float().T
+    err = (C - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 1e-4 * max(1.0, scale) + 1e-3, (err, scale)
+
+
+def _attn(q, k, v, heads, rows, row0):
+    lib = load_library()
+    P, hs = q.shape
+    out = torch.zeros(P, hs, dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    err = lib.pf_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                 P, rows, row0, heads, hs, s)
+    torch.cuda.synchronize()
+    assert err == 0, f"cuda error {err}"
+    return out
+
+
+def _attn_ref(q, k, v, heads, rows, row0):
+    P, hs = q.shape
+    dh = hs // heads
+    qf = q[row0:row0 + rows].float().view(rows, heads, dh).transpose(0, 1)
+    kf = k.float().view(P, heads, dh).transpose(0, 1)
+    vf = v.float().view(P, heads, dh).transpose(0, 1)
+    s = qf @ kf.transpose(1, 2) / dh ** 0.5
+    p = torch.softmax(s, dim=-1)
+    return (p @ vf).transpose(0, 1).reshape(rows, hs)
+
+
+@pytest.mark.parametrize("P,heads,hs,rows,row0,scale", [
+    (64, 4, 32, 64, 0, 1.0),        # reference config, dh = 8
+    (64, 4, 32, 16, 32, 1.0),       # one patch of four
+    (32, 4, 16, 32, 0, 1.0),        # dh = 4
+    (256, 4, 128, 64, 128, 3.0),    # tiny config patch, dh = 32
+    (256, 4, 128, 256, 0, 3.0),
+    (1024, 8, 512, 1024, 0, 4.0),   # dh = 64
+    (4096, 16, 1152, 512, 1024, 3.0),  # PixArt patch, dh = 72, split-KV
+    (4096, 16, 1152, 4096, 0, 3.0),    # PixArt full sequence
+    (520, 2, 256, 136, 384, 2.0),   # ragged P / rows, dh = 128
+])
+def test_attention_matches_fp32(P, heads, hs, rows, row0, scale):
+    g = torch.Generator(device="cuda").manual_seed(P + hs + rows)
+    mk = lambda: ((torch.rand(P, hs, device="cuda", generator=g) * 2 - 1) * scale).to(torch.bfloat16)
+    q, k, v = mk(), mk(), mk()
+    out = _attn(q, k, v, heads, rows, row0)[row0:row0 + rows].float()
+    ref = _attn_ref(q, k, v, heads, rows, row0)
+    err = (out - ref).abs().max().item()
+    assert err < 2e-2, err
+    rel = ((out - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
