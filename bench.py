@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark: seconds per image of PipeFusion DiT inference on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c3|c1|cref] [--patches M]
+
+Metric (BASELINE.json): "sec/image DiT latency at 1/2/4/8 B200 (PipeFusion
+N,M); % of BF16 TC peak". One bench "step" = one image: the full 20-step
+PipeFusion denoising loop (1 synchronous warmup step + 19 pipelined steps) of
+the PixArt-alpha-shaped toy DiT (28 layers, hidden 1152, 16 heads, 4096
+tokens = 1024 px), random-init weights from the reference's own RNG stream
+(build_toy_model, seed 0) and the reference's synthetic latent.
+
+* value  - device time per image with the latent already resident in HBM
+           (CUDA events on the caller stream, which joins every stage stream).
+* e2e    - the same through the C ABI the reference would bind
+           (pf_run_pipefusion): fp64 host latent in, host->device copy, run,
+           device->host copy, fp64 host latent out; wall clock per call.
+* roofline - dominant kernel from a CUDA-event profile of one extra run
+           (every kernel bracketed by events on its own stream), algorithmic
+           FLOPs per SURVEY 8(d): QKV 6*r*hs^2, attention 4*r*p*hs, out-proj
+           2*r*hs^2, MLP 2*2*r*hs*mlp per (patch, layer).
+* cpu_baseline / --impl reference - the reference's own CPU code
+           (oracle/_ref, compiled from /root/reference) timed on this host on
+           sampled toy_layer_forward units at the true shape, extrapolated to
+           a full image (a full C2 image is ~1e14 FLOP on an fp64 scalar loop).
+
+Under torchrun with N > 1 ranks, rank 0 drives all N GPUs of the node (one
+stage per GPU, one CUDA stream per stage); the other ranks join the barriers
+and the max-over-ranks timing reduction.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "sec/image DiT latency at 1/2/4/8 B200 (PipeFusion N,M); % of BF16 TC peak"
+UNIT = "s/image"
+
+CONFIGS = {
+    # name: (layers, hidden, heads, seq_len, diffusion steps, warmup steps)
+    "c2": dict(name="PixArt-alpha-shaped DiT 1024px (28 layers, hidden 1152, 16 heads, "
+                    "4096 tokens), 20 steps, 1 warmup",
+               L=28, hs=1152, heads=16, p=4096, S=20, W=1),
+    "c3": dict(name="PixArt-alpha-shaped DiT 2048px (28 layers, hidden 1152, 16 heads, "
+                    "16384 tokens), 20 steps, 1 warmup",
+               L=28, hs=1152, heads=16, p=16384, S=20, W=1),
+    "c1": dict(name="tiny DiT (4 layers, hidden 128, 4 heads, 256 tokens), 5 steps, 1 warmup",
+               L=4, hs=128, heads=4, p=256, S=5, W=1),
+    "cref": dict(name="reference_execute.cfg (4 layers, hidden 32, 4 heads, 64 tokens), 20 "
+                      "steps, 1 warmup", L=4, hs=32, heads=4, p=64, S=20, W=1),
+}
+
+
+def flops_per_image(c, mlp):
+    """The reference's ComputeModel (simulate.cpp:30-44) for mlp_ratio 4:
+    S * L * (24 p hs^2 + 4 p^2 hs); generalised to mlp = 4 hs."""
+    p, hs = c["p"], c["hs"]
+    return c["S"] * c["L"] * (8 * p * hs * hs + 4 * p * hs * mlp + 4 * p * p * hs)
+
+
+def load_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", ",".join(str(g) for g in self.gpus)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
+    """Time the reference's own toy_layer_forward (oracle/_ref, built from
+    /root/reference) at the true shape on `sample_rows` query rows against a
+    full p-row K/V buffer, one sample per host core in parallel, and
+    extrapolate to one image: S * L * (p / sample_rows) samples."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import loader
+    if not loader.REFERENCE_LIB.exists():
+        loader.build(reference=True)
+    ref = loader.Reference()
+    model = ref.build_toy_model(0, 1, c["hs"], c["heads"], 4.0)
+    cores = min(os.cpu_count() or 1, 64)
+    rng = np.random.default_rng(0)
+    k = rng.uniform(-1, 1, (c["p"], c["hs"]))
+    v = rng.uniform(-1, 1, (c["p"], c["hs"]))
+
+    def one(i):
+        h = np.random.default_rng(i).uniform(-1, 1, (sample_rows, c["hs"]))
+        row0 = (i * sample_rows) % c["p"]
+        model.layer_forward(0, h, k, v, row0)
+        return 1
+
+    done, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        while True:
+            done += sum(ex.map(one, range(done, done + cores)))
+            if time.perf_counter() - t0 > budget_s * 0.5 or done >= 8 * cores:
+                break
+    wall = time.perf_counter() - t0
+    per_sample = wall / done  # throughput-equivalent seconds per sample
+    samples_per_image = c["S"] * c["L"] * (c["p"] / sample_rows)
+    return {
+        "value": per_sample * samples_per_image, "unit": UNIT, "cores": cores,
+        "kind": "reference",
+        "sample": (f"{done} toy_layer_forward units of {sample_rows} query rows x "
+                   f"{c['p']}-row K/V at hs={c['hs']} heads={c['heads']} (reference "
+                   f"toy_model.cpp, fp64, {cores} threads in {wall:.1f}s); extrapolated "
+                   f"x{samples_per_image:.0f} units/image (linear in rows)"),
+    }
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, c, world, rank):
+    import torch
+    import paper_2405_14430_b200 as pf
+
+    n = args.gpus
+    M = args.patches or n
+    peaks, peak_kind = load_peaks()
+    result = None
+    if rank == 0:
+        torch.cuda.set_device(0)
+        devices = list(range(n))
+        t_build = time.perf_counter()
+        model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
+        t_build = time.perf_counter() - t_build
+        mlp = model.mlp_hidden
+        x0 = pf.make_initial_latent(0, c["p"], c["hs"])
+        x0_dev = torch.from_numpy(x0.astype(np.float32)).cuda()
+        x_dev = torch.empty_like(x0_dev)
+        stream = torch.cuda.Stream()
+        sp = stream.cuda_stream
+
+        def one_image():
+            x_dev.copy_(x0_dev)
+            model.run_pipefusion_device(x_dev.data_ptr(), c["S"], M, c["W"], 0.1, sp)
+
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                one_image()
+            model.synchronize(sp)
+            launches = model.last_launch_count()
+    barrier(world)
+    if rank == 0:
+        torch.cuda.synchronize()
+        with ClockSampler(list(range(n))) as clocks:
+            with torch.cuda.stream(stream):
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record(stream)
+                for _ in range(args.steps):
+                    one_image()
+                ev1.record(stream)
+                model.synchronize(sp)
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
+        clock_info = clocks.summary()
+    else:
+        ms = 0.0
+    ms = max_over_ranks(ms, world)
+    barrier(world)
+    if rank != 0:
+        return None
+
+    sec_per_image = ms / 1e3 / args.steps
+    # ---- e2e through the C ABI with host buffers
+    e2e_times = []
+    out = None
+    for i in range(max(2, args.steps) + 1):
+        t0 = time.perf_counter()
+        out = model.run_pipefusion(x0, c["S"], M, c["W"], 0.1)
+        dt = time.perf_counter() - t0
+        if i > 0:
+            e2e_times.append(dt)
+    e2e = statistics.mean(e2e_times)
+    finite = bool(np.isfinite(out.final_x).all())
+    # ---- per-kernel CUDA-event profile of one extra image
+    model.set_profiling(True)
+    with torch.cuda.stream(stream):
+        one_image()
+        model.synchronize(sp)
+    prof = model.kernel_profile()
+    model.set_profiling(False)
+    gemm_kinds = ["gemm_qkv", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out"]
+    dom = max((k for k in prof if k != "sampler"), key=lambda k: prof[k]["ms"])
+    peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    kernels = {}
+    for k, d in prof.items():
+        if d["launches"] == 0:
+            continue
+        e = {"ms_per_image": d["ms"], "launches": d["launches"],
+             "avg_us": 1e3 * d["ms"] / d["launches"]}
+        if d["flops"]:
+            e["tflops"] = d["flops"] / (d["ms"] * 1e-3) / 1e12
+            e["frac_bf16"] = e["tflops"] / peak_tf
+        if d["bytes"]:
+            e["gbs"] = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+            e["frac_hbm"] = e["gbs"] / peaks["hbm_gbs"]
+        kernels[k] = e
+    gemm_ms = sum(prof[k]["ms"] for k in gemm_kinds)
+    gemm_fl = sum(prof[k]["flops"] for k in gemm_kinds)
+    d = prof[dom]
+    achieved = d["flops"] / d["launches"] / (d["ms"] / d["launches"] * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom)
+        except Exception:
+            traffic = None
+    total_flops = flops_per_image(c, mlp)
+    line = {
+        "metric": METRIC, "value": sec_per_image, "unit": UNIT, "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (reference RNG: build_toy_model seed 0, "
+                                  "make_initial_latent seed 0)",
+        "config": {"workload": c["name"], "layers": c["L"], "hidden_size": c["hs"],
+                   "heads": c["heads"], "seq_len": c["p"], "diffusion_steps": c["S"],
+                   "warmup_steps": c["W"], "patches": M, "stages": n,
+                   "parallelism": f"pipefusion N={n} M={M}",
+                   "l2": "working set > L2 (0.9 GB bf16 weights + 0.6 GB K/V per image "
+                         "pass), no explicit flush"},
+        "tc_frac_image": total_flops / sec_per_image / 1e12 / peak_tf,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": c["p"] * c["hs"] * 4,
+                "d2h_bytes_per_step": c["p"] * c["hs"] * 4,
+                "api": "pf_run_pipefusion (C ABI, fp64 host latent in/out)"},
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved,
+                     "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,
+                     "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
+                     "gemm_all_frac": (gemm_fl / (gemm_ms * 1e-3) / 1e12) / peak_tf},
+        "kernels": kernels,
+        "gpu_launches": launches * args.steps,
+        "clocks": clock_info,
+        "finite": finite,
+        "model_build_s": t_build,
+    }
+    return line
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--patches", type=int, default=0, help="M (default: N)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    c = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank == 0:
+            base = cpu_reference_baseline(c, budget_s=args.cpu_budget)
+            line = {"metric": METRIC, "value": base["value"], "unit": UNIT,
+                    "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                    "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                    "dtype": "f64", "data": "synthetic", "impl": "reference",
+                    "config": {"workload": c["name"], "patches": args.patches or args.gpus},
+                    "cpu_baseline": base,
+                    "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    line = run_ours(args, c, world, rank)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_reference_baseline(c, budget_s=args.cpu_budget)
+            except Exception as e:  # the checker must not sink the GPU number
+                line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

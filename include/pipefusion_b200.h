@@ -126,6 +126,21 @@ pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
                            int64_t row0, double* k_buf, double* v_buf,
                            pf_layout layout);
 
+/* ditsim::make_initial_latent(seed, seq_len, hidden_size) -- execute.hpp:56-57,
+ * toy_model.cpp:84-91 (host, bit-exact mt19937_64 stream). out: row-major
+ * [seq_len x hidden_size]. */
+pf_status pf_make_initial_latent(uint64_t seed, int64_t seq_len, int hidden_size,
+                                 double* out);
+
+/* Per-kernel CUDA-event profile (no reference analogue). When enabled, every
+ * kernel of subsequent runs is bracketed by events on its stage stream;
+ * pf_kernel_profile() resolves the last run (call after it completed).
+ * kind: 0 QKV GEMM, 1 attention, 2 out-proj GEMM, 3 MLP-in GEMM,
+ * 4 MLP-out GEMM, 5 sampler/patch kernels. flops/bytes are algorithmic. */
+pf_status pf_set_profiling(pf_ctx* ctx, int enabled);
+pf_status pf_kernel_profile(pf_ctx* ctx, int kind, double* total_ms,
+                            int64_t* launches, double* flops, double* bytes);
+
 /* Introspection for tests and benchmarks. */
 int pf_stage_count(const pf_ctx* ctx);
 int pf_stage_first_layer(const pf_ctx* ctx, int stage);

@@ -25,7 +25,7 @@ import numpy as np
 __all__ = [
     "LIB_PATH", "load_library", "ValidationError", "NumericError", "CudaError",
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
-    "mlp_hidden_of",
+    "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
@@ -36,8 +36,12 @@ EXPORTED_SYMBOLS = [
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
-    "pf_version", "pf_debug_gemm", "pf_debug_attention",
+    "pf_version", "pf_make_initial_latent", "pf_set_profiling", "pf_kernel_profile",
+    "pf_debug_gemm", "pf_debug_attention",
 ]
+
+KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
+                "sampler"]
 
 PF_OK, PF_NUMERIC, PF_VALIDATION, PF_CUDA = 0, 1, 2, 3
 PF_ROW_MAJOR, PF_COL_MAJOR = 0, 1
@@ -105,6 +109,9 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_last_launch_count.argtypes = [vp]
     lib.pf_last_launch_count.restype = i64
     lib.pf_version.restype = ctypes.c_char_p
+    lib.pf_make_initial_latent.argtypes = [ctypes.c_uint64, i64, i32, dptr]
+    lib.pf_set_profiling.argtypes = [vp, i32]
+    lib.pf_kernel_profile.argtypes = [vp, i32, dptr, ctypes.POINTER(i64), dptr, dptr]
     lib.pf_debug_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     lib.pf_debug_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
     if path is None:
@@ -126,6 +133,15 @@ def mlp_hidden_of(hidden_size: int, mlp_ratio: float) -> int:
     """int(std::lround(mlp_ratio * hidden_size)) as in toy_model.cpp:56."""
     v = mlp_ratio * hidden_size
     return int(math.floor(v + 0.5)) if v >= 0 else -int(math.floor(-v + 0.5))
+
+
+def make_initial_latent(seed: int, seq_len: int, hidden_size: int) -> np.ndarray:
+    """ditsim::make_initial_latent (execute.hpp:56-57), host, bit-exact."""
+    lib = load_library()
+    out = np.empty((seq_len, hidden_size), dtype=np.float64)
+    _raise(lib.pf_make_initial_latent(ctypes.c_uint64(seed), seq_len, hidden_size,
+                                      _dptr(out)), lib.pf_last_error(None).decode())
+    return out
 
 
 @dataclass
@@ -279,6 +295,21 @@ class ToyDiTCuda:
             ctypes.c_double(eta), ctypes.c_void_p(stream_ptr), ctypes.byref(st))
         _raise(status, self._err())
         return StalenessStats(st.fresh_patch_reads, st.stale_patch_reads, [])
+
+    def set_profiling(self, enabled: bool) -> None:
+        self._lib.pf_set_profiling(self._ctx, 1 if enabled else 0)
+
+    def kernel_profile(self) -> dict:
+        """Per kernel kind of the last profiled run: ms, launches, flops, bytes."""
+        out = {}
+        for kind, name in enumerate(KERNEL_KINDS):
+            ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+            n = ctypes.c_int64()
+            _raise(self._lib.pf_kernel_profile(self._ctx, kind, ctypes.byref(ms),
+                                               ctypes.byref(n), ctypes.byref(fl),
+                                               ctypes.byref(by)), self._err())
+            out[name] = dict(ms=ms.value, launches=n.value, flops=fl.value, bytes=by.value)
+        return out
 
     def synchronize(self, stream_ptr: int = 0) -> None:
         _raise(self._lib.pf_synchronize(self._ctx, ctypes.c_void_p(stream_ptr)), self._err())

@@ -271,6 +271,36 @@ pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
   });
 }
 
+pf_status pf_make_initial_latent(uint64_t seed, int64_t seq_len, int hidden_size,
+                                 double* out) {
+  return guarded(&g_create_error, [&] {
+    if (seq_len < 1 || hidden_size < 1)
+      throw pf::ValidationError("latent needs seq_len >= 1 and hidden_size >= 1");
+    if (!out) throw pf::ValidationError("NULL output pointer");
+    std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ULL);
+    for (int64_t i = 0; i < seq_len * hidden_size; ++i) out[i] = next_uniform(rng);
+  });
+}
+
+pf_status pf_set_profiling(pf_ctx* ctx, int enabled) {
+  if (!ctx) return PF_VALIDATION;
+  ctx->engine->set_profiling(enabled != 0);
+  return PF_OK;
+}
+
+pf_status pf_kernel_profile(pf_ctx* ctx, int kind, double* total_ms, int64_t* launches,
+                            double* flops, double* bytes) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (kind < 0 || kind >= pf::kKindCount) throw pf::ValidationError("kernel kind out of range");
+    pf::KernelProfile p = ctx->engine->collect_profile();
+    if (total_ms) *total_ms = p.ms[kind];
+    if (launches) *launches = p.launches[kind];
+    if (flops) *flops = p.flops[kind];
+    if (bytes) *bytes = p.bytes[kind];
+  });
+}
+
 int pf_stage_count(const pf_ctx* ctx) { return ctx ? ctx->engine->stage_count() : 0; }
 int pf_stage_first_layer(const pf_ctx* ctx, int stage) {
   if (!ctx || stage < 0 || stage >= ctx->engine->stage_count()) return -1;

@@ -146,6 +146,10 @@ Engine::Engine(const ModelShape& shape_in, const std::vector<int>& devices)
 }
 
 Engine::~Engine() {
+  for (size_t d = 0; d < prof_pool_.size() && d < stages_.size(); ++d) {
+    DeviceGuard g(stages_[d].device);
+    for (cudaEvent_t e : prof_pool_[d]) cudaEventDestroy(e);
+  }
   for (Stage& s : stages_) free_stage(s);
 }
 
@@ -274,6 +278,7 @@ void Engine::load_condition_bias(const double* cb) {
 void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
   const ModelShape& m = shape_;
   StageLayer& L = s.layers[size_t(lf)];
+  const double r = rows, hs = m.hs, mlp = m.mlp, P = double(m.P);
   EpiParams qkv;
   qkv.q = s.q;
   qkv.k = L.k;
@@ -282,29 +287,80 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
   qkv.dh = m.dh;
   qkv.dhp = m.dhp;
   qkv.P = int(m.P);
+  prof_begin(s, kGemmQKV, 2 * r * hs * 3 * hs, 0);
   check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * m.hs, m.hs, Epi::QKV, qkv,
              s.sm_count, s.stream), "gemm qkv");
+  prof_end(s);
   AttnLaunch a{m.dhp, int(m.P), rows, row0, m.heads, m.dh, m.hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
+  prof_begin(s, kAttention, 4 * r * P * hs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_vt, a, s.sm_count, s.stream), "attention");
+  prof_end(s);
   EpiParams res;
   res.out_f32 = s.h32;
   res.out_bf16 = s.hb;
   res.ld = m.hs;
   res.flag = s.flag;
   res.code = code;
+  prof_begin(s, kGemmOut, 2 * r * hs * hs, 0);
   check(gemm(s.tm_attn, L.tm_wo, rows, row0, m.hs, m.hs, Epi::Residual, res,
              s.sm_count, s.stream), "gemm out-proj");
+  prof_end(s);
   EpiParams th;
   th.out_bf16 = s.z;
   th.ld = m.mlp;
+  prof_begin(s, kGemmMlpIn, 2 * r * hs * mlp, 0);
   check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, m.hs, Epi::Tanh, th,
              s.sm_count, s.stream), "gemm mlp-in");
+  prof_end(s);
+  prof_begin(s, kGemmMlpOut, 2 * r * hs * mlp, 0);
   check(gemm(s.tm_z, L.tm_wout, rows, row0, m.hs, m.mlp, Epi::Residual, res,
              s.sm_count, s.stream), "gemm mlp-out");
+  prof_end(s);
   const int splits = attn_splits(a, s.sm_count);
   launches_ += 5 + (splits > 1 ? 1 : 0);
+}
+
+cudaEvent_t Engine::prof_event(int stage) {
+  if (prof_pool_.size() < stages_.size()) prof_pool_.resize(stages_.size());
+  if (prof_used_.size() < stages_.size()) prof_used_.resize(stages_.size(), 0);
+  auto& pool = prof_pool_[size_t(stage)];
+  size_t& used = prof_used_[size_t(stage)];
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    PF_CUDA_CHECK(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void Engine::prof_begin(Stage& s, int kind, double flops, double bytes) {
+  if (!profiling_) return;
+  const int d = int(&s - stages_.data());
+  ProfRec r{kind, d, prof_event(d), prof_event(d), flops, bytes};
+  PF_CUDA_CHECK(cudaEventRecord(r.a, s.stream));
+  prof_.push_back(r);
+}
+
+void Engine::prof_end(Stage& s) {
+  if (!profiling_) return;
+  PF_CUDA_CHECK(cudaEventRecord(prof_.back().b, s.stream));
+}
+
+KernelProfile Engine::collect_profile() {
+  KernelProfile out;
+  for (const ProfRec& r : prof_) {
+    DeviceGuard g(stages_[size_t(r.stage)].device);
+    PF_CUDA_CHECK(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    PF_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    out.ms[r.kind] += ms;
+    out.launches[r.kind] += 1;
+    out.flops[r.kind] += r.flops;
+    out.bytes[r.kind] += r.bytes;
+  }
+  return out;
 }
 
 // Stage-boundary transfer of rows [row0, row0+rows) of the residual stream:
@@ -381,6 +437,8 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
                           std::vector<int>(size_t(patches), steps));
   codes_.clear();
   launches_ = 0;
+  prof_.clear();
+  prof_used_.assign(stages_.size(), 0);
 
   // Fork: every stage stream waits for the caller's prior work.
   cudaEvent_t ev_start;
@@ -394,6 +452,16 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start, 0));
     check(reset_flag(s.flag, s.stream), "reset_flag");
     ++launches_;
+    // StageBuffers are zero-initialised per run (execute.cpp:42-48). Without
+    // warmup the zero rows are read as stale context, so clear them; with
+    // warmup every row is rewritten before it is read.
+    if (warmup == 0) {
+      const size_t kv = size_t(m.heads) * size_t(m.P) * size_t(m.dhp) * sizeof(bf16);
+      for (StageLayer& L : s.layers) {
+        PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
+        PF_CUDA_CHECK(cudaMemsetAsync(L.vt, 0, kv, s.stream));
+      }
+    }
   }
   {
     DeviceGuard g(s0.device);
@@ -410,8 +478,10 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     const int t = steps - 1 - w;
     {
       DeviceGuard g(s0.device);
+      prof_begin(s0, kSampler, 0, double(m.P) * m.hs * (4 + 4 + 2));
       check(patch_prepare(x_dev, nullptr, s0.cb, s0.h32, s0.hb, 0, int(m.P), m.hs,
                           0.f, false, s0.stream), "patch_prepare");
+      prof_end(s0);
       ++launches_;
     }
     for (int d = 0; d < n; ++d) {
@@ -433,7 +503,9 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[0], 0));
     }
     DeviceGuard g(s0.device);
+    prof_begin(s0, kSampler, 0, double(m.P) * m.hs * 12);
     check(latent_update(x_dev, s0.eps, eta, size_t(m.P) * m.hs, s0.stream), "latent_update");
+    prof_end(s0);
     ++launches_;
   }
 
@@ -447,8 +519,10 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         DeviceGuard g(s0.device);
         if (q > 0 && n > 1)
           PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[size_t(j)], 0));
+        prof_begin(s0, kSampler, 0, double(r) * m.hs * (q > 0 ? 4 + 4 + 4 + 4 + 2 : 4 + 4 + 2));
         check(patch_prepare(x_dev, s0.eps, s0.cb, s0.h32, s0.hb, row0, r, m.hs, eta,
                             q > 0, s0.stream), "patch_prepare");
+        prof_end(s0);
         ++launches_;
       }
       for (int d = 0; d < n; ++d) {
@@ -490,7 +564,9 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     if (n > 1)
       for (int j = 0; j < patches; ++j)
         PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[size_t(j)], 0));
+    prof_begin(s0, kSampler, 0, double(m.P) * m.hs * 12);
     check(latent_update(x_dev, s0.eps, eta, size_t(m.P) * m.hs, s0.stream), "latent_update");
+    prof_end(s0);
     ++launches_;
   }
 

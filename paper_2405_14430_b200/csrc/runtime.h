@@ -4,9 +4,10 @@
 //
 // Mirrors the reference executor (/root/reference/proj/src/execute.cpp):
 //   StageBuffers            execute.cpp:38-49    -> Stage (+ StageLayer K/V)
-//   check_staleness_and_count :51-65             -> Engine::check_staleness
-//   stage_forward_full      :134-147             -> Engine::stage_full
-//   stage_forward_patch     :150-165             -> Engine::stage_patch
+//   check_staleness_and_count :51-65             -> Engine::enqueue_run (host)
+//   stage_forward_full      :134-147             -> enqueue_run warmup loop
+//   stage_forward_patch     :150-165             -> enqueue_run steady loop
+//   toy_layer_forward       toy_model.cpp:169-177 -> Engine::layer_forward
 //   run_pipefusion_inline   :167-223             -> Engine::enqueue_run
 //   Channel<PatchMsg> sends :239-244, 275-281    -> Engine::send_rows (stream
 //                                                   ordered copy + event)
@@ -94,6 +95,19 @@ struct Stage {
   std::vector<cudaEvent_t> ev_eps;  // per patch, recorded by the last stage
 };
 
+// Kernel kinds for the optional per-launch CUDA-event profile.
+enum KernelKind : int {
+  kGemmQKV = 0, kAttention = 1, kGemmOut = 2, kGemmMlpIn = 3, kGemmMlpOut = 4,
+  kSampler = 5, kKindCount = 6
+};
+
+struct KernelProfile {
+  double ms[kKindCount] = {0};        // summed device time (CUDA events)
+  int64_t launches[kKindCount] = {0};
+  double flops[kKindCount] = {0};     // algorithmic FLOPs (SURVEY 8d model)
+  double bytes[kKindCount] = {0};     // algorithmic HBM bytes (sampler)
+};
+
 struct RunStats {
   int64_t fresh = 0;
   int64_t stale = 0;
@@ -102,10 +116,6 @@ struct RunStats {
 
 class Engine {
  public:
-  // weights: per layer 6 HostMatrix (w_q, w_k, w_v, w_o, w_mlp_in, w_mlp_out);
-  // generated on the fly by `fill_layer` to avoid materialising fp64 models.
-  using LayerSource = void (*)(void* user, int layer, std::vector<double>* mats /*6*/);
-
   Engine(const ModelShape& shape, const std::vector<int>& devices);
   ~Engine();
   Engine(const Engine&) = delete;
@@ -132,12 +142,32 @@ class Engine {
 
   float* stage0_x() { return stages_[0].x; }
 
+  // Bracket every kernel of the next runs with CUDA events (stage streams).
+  void set_profiling(bool on) { profiling_ = on; }
+  // Resolve the events of the last profiled run (after finish()).
+  KernelProfile collect_profile();
+
  private:
   void alloc_stage(Stage& s, int first, int count, bool is_first);
   void free_stage(Stage& s);
   void layer_forward(Stage& s, int lf, int rows, int row0, int code);
   void send_rows(int from, int row0, int rows);
   int stage_of_layer(int layer) const;
+
+  struct ProfRec {
+    int kind;
+    int stage;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  void prof_begin(Stage& s, int kind, double flops, double bytes);
+  void prof_end(Stage& s);
+  cudaEvent_t prof_event(int stage);
+
+  bool profiling_ = false;
+  std::vector<ProfRec> prof_;
+  std::vector<std::vector<cudaEvent_t>> prof_pool_;  // per stage
+  std::vector<size_t> prof_used_;
 
   ModelShape shape_;
   std::vector<Stage> stages_;
