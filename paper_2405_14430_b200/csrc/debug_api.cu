@@ -8,7 +8,7 @@
 namespace {
 
 // Repack [P x hs] row-major bf16 into the attention layouts
-// (Q/K: [heads][P][dhp], V^T: [heads][dhp][P]), zero padded.
+// (Q/K/V: [heads][P][dhp]), zero padded.
 __global__ void pack_heads_kernel(const pf::bf16* __restrict__ src, pf::bf16* __restrict__ qk,
                                   pf::bf16* __restrict__ vt, int P, int hs, int heads, int dh,
                                   int dhp) {
@@ -62,15 +62,15 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
                                                          nullptr, P, hs, heads, dh, dhp);
   pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(k), kp,
                                                          nullptr, P, hs, heads, dh, dhp);
-  pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(v),
-                                                         nullptr, vp, P, hs, heads, dh, dhp);
+  pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(v), vp,
+                                                         nullptr, P, hs, heads, dh, dhp);
   CUtensorMap tq, tk, tv;
   bool ok = pf::encode_tmap_bf16_2d(&tq, qp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
                                     128, 32) &&
             pf::encode_tmap_bf16_2d(&tk, kp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
                                     128, 32) &&
-            pf::encode_tmap_bf16_2d(&tv, vp, uint64_t(P), uint64_t(heads) * dhp,
-                                    uint64_t(P) * 2, 64, uint32_t(dhp), 128);
+            pf::encode_tmap_bf16_2d(&tv, vp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
+                                    128, 32);
   int err = ok ? 0 : int(cudaErrorInvalidValue);
   if (ok) {
     pf::AttnLaunch a{dhp, P, rows, row0, heads, dh, hs, float(1.0 / std::sqrt(double(dh))),

@@ -168,16 +168,36 @@ struct EpiTanh {
   }
 };
 
-// Fused QKV projection epilogue: Q and K rows go to the head-major padded
-// buffers at their sequence row (K overwrites the stale rows of this patch in
-// place, toy_model.cpp:174-175); V is stored transposed per head so it is the
-// K-major B operand of the P.V product.
+// Fused QKV projection epilogue: Q, K and V rows go to the head-major padded
+// buffers [heads][P][dhp] at their sequence row -- K and V overwrite the
+// stale rows of this patch in place (toy_model.cpp:174-175). With hs and dh
+// multiples of 8, each 8-column group lies in one (q|k|v, head) and is stored
+// as one 16-byte vector.
 struct EpiQKV {
   bf16* q;
   bf16* k;
-  bf16* vt;
+  bf16* v;
   int hs, dh, dhp, P;
-  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+  __device__ void operator()(int row, int col0, const float (&acc)[32], int nvalid) const {
+    if ((hs & 7) == 0 && (dh & 7) == 0) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (8 * g >= nvalid) break;
+        const int n = col0 + 8 * g;
+        const int which = n / hs;
+        const int nn = n - which * hs;
+        const int head = nn / dh;
+        const int d = nn - head * dh;
+        bf16* base = which == 0 ? q : (which == 1 ? k : v);
+        uint4 pk;
+        pk.x = ptx::pack_bf16x2(acc[8 * g + 0], acc[8 * g + 1]);
+        pk.y = ptx::pack_bf16x2(acc[8 * g + 2], acc[8 * g + 3]);
+        pk.z = ptx::pack_bf16x2(acc[8 * g + 4], acc[8 * g + 5]);
+        pk.w = ptx::pack_bf16x2(acc[8 * g + 6], acc[8 * g + 7]);
+        *reinterpret_cast<uint4*>(base + (size_t(head) * P + row) * dhp + d) = pk;
+      }
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       if (e >= nvalid) break;
@@ -186,14 +206,8 @@ struct EpiQKV {
       const int nn = n - which * hs;
       const int head = nn / dh;
       const int d = nn - head * dh;
-      const bf16 val = __float2bfloat16_rn(v[e]);
-      if (which == 0) {
-        q[(size_t(head) * P + row) * dhp + d] = val;
-      } else if (which == 1) {
-        k[(size_t(head) * P + row) * dhp + d] = val;
-      } else {
-        vt[(size_t(head) * dhp + d) * P + row] = val;
-      }
+      bf16* base = which == 0 ? q : (which == 1 ? k : v);
+      base[(size_t(head) * P + row) * dhp + d] = __float2bfloat16_rn(acc[e]);
     }
   }
 };
@@ -231,7 +245,7 @@ cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
     case Epi::QKV:
       return launch_gemm<BN, STAGES>(
           a, b, rows, row0, N, K,
-          EpiQKV{ep.q, ep.k, ep.vt, ep.hs, ep.dh, ep.dhp, ep.P}, sm_count, stream);
+          EpiQKV{ep.q, ep.k, ep.v, ep.hs, ep.dh, ep.dhp, ep.P}, sm_count, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -271,7 +285,7 @@ size_t attn_work_floats(int dhp, int heads, int rows, int splits) {
 namespace {
 template <int DHP>
 cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
-                        const CUtensorMap& vt, const AttnLaunch& a, int sm_count,
+                        const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                         cudaStream_t stream) {
   using L = AttnSmem<DHP>;
   {
@@ -302,7 +316,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.part_ml = a.work + size_t(splits) * a.heads * prm.rows_pad * DHP;
   }
   dim3 grid(q_tiles, a.heads, splits);
-  attn_fwd_kernel<DHP><<<grid, 256, L::kTotal, stream>>>(q, k, vt, prm);
+  attn_fwd_kernel<DHP><<<grid, 256, L::kTotal, stream>>>(q, k, v, prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || splits == 1) return e;
   const int total = a.rows * a.heads * (DHP / 16);
@@ -312,18 +326,18 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
 }  // namespace
 
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
-                      const CUtensorMap& vt, const AttnLaunch& a, int sm_count,
+                      const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                       cudaStream_t stream) {
   if (a.rows <= 0) return cudaSuccess;
   switch (a.dhp) {
-    case 16: return launch_attn<16>(q, k, vt, a, sm_count, stream);
-    case 32: return launch_attn<32>(q, k, vt, a, sm_count, stream);
-    case 48: return launch_attn<48>(q, k, vt, a, sm_count, stream);
-    case 64: return launch_attn<64>(q, k, vt, a, sm_count, stream);
-    case 80: return launch_attn<80>(q, k, vt, a, sm_count, stream);
-    case 96: return launch_attn<96>(q, k, vt, a, sm_count, stream);
-    case 112: return launch_attn<112>(q, k, vt, a, sm_count, stream);
-    case 128: return launch_attn<128>(q, k, vt, a, sm_count, stream);
+    case 16: return launch_attn<16>(q, k, v, a, sm_count, stream);
+    case 32: return launch_attn<32>(q, k, v, a, sm_count, stream);
+    case 48: return launch_attn<48>(q, k, v, a, sm_count, stream);
+    case 64: return launch_attn<64>(q, k, v, a, sm_count, stream);
+    case 80: return launch_attn<80>(q, k, v, a, sm_count, stream);
+    case 96: return launch_attn<96>(q, k, v, a, sm_count, stream);
+    case 112: return launch_attn<112>(q, k, v, a, sm_count, stream);
+    case 128: return launch_attn<128>(q, k, v, a, sm_count, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -29,13 +29,13 @@ struct EpiParams {
   // Residual: h = out_f32[row*ld + n] + acc; out_f32 = h; out_bf16 = bf16(h);
   //           non-finite h -> atomicMin(flag, code)
   // Tanh:     out_bf16[row*ld + n] = bf16(tanh(acc))
-  // QKV:      n in [0,hs): q, [hs,2hs): k, [2hs,3hs): v^T (per-head padded)
+  // QKV:      n in [0,hs): q, [hs,2hs): k, [2hs,3hs): v, each [heads][P][dhp]
   float* out_f32 = nullptr;
   bf16* out_bf16 = nullptr;
   int ld = 0;
   bf16* q = nullptr;
   bf16* k = nullptr;
-  bf16* vt = nullptr;
+  bf16* v = nullptr;
   int hs = 0, dh = 0, dhp = 0, P = 0;
   int* flag = nullptr;
   int code = 0;
@@ -60,7 +60,7 @@ struct AttnLaunch {
 int attn_splits(const AttnLaunch& a, int sm_count);
 size_t attn_work_floats(int dhp, int heads, int rows, int splits);
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
-                      const CUtensorMap& vt, const AttnLaunch& a, int sm_count,
+                      const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                       cudaStream_t stream);
 
 // Sampler / patch split-merge (HBM-bound, vectorised).

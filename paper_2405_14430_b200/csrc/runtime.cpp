@@ -196,13 +196,13 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
     L.win = dalloc<bf16>(mlp * hs);
     L.wout = dalloc<bf16>(hs * mlp);
     L.k = dalloc<bf16>(heads * P * dhp);
-    L.vt = dalloc<bf16>(heads * dhp * P);
+    L.v = dalloc<bf16>(heads * P * dhp);
     L.tm_wqkv = tmap(L.wqkv, hs, 3 * hs, hs * 2, 64, uint32_t(gemm_bn(int(3 * hs))), 128);
     L.tm_wo = tmap(L.wo, hs, hs, hs * 2, 64, uint32_t(gemm_bn(int(hs))), 128);
     L.tm_win = tmap(L.win, hs, mlp, hs * 2, 64, uint32_t(gemm_bn(int(mlp))), 128);
     L.tm_wout = tmap(L.wout, mlp, hs, mlp * 2, 64, uint32_t(gemm_bn(int(hs))), 128);
     L.tm_k = tmap(L.k, dhp, heads * P, dhp * 2, 16, 128, 32);
-    L.tm_vt = tmap(L.vt, P, heads * dhp, P * 2, 64, uint32_t(dhp), 128);
+    L.tm_v = tmap(L.v, dhp, heads * P, dhp * 2, 16, 128, 32);
   }
   if (is_first) {
     s.x = dalloc<float>(P * hs);
@@ -216,7 +216,7 @@ void Engine::free_stage(Stage& s) {
   if (s.stream) cudaStreamSynchronize(s.stream);
   for (StageLayer& L : s.layers) {
     dfree(L.wqkv); dfree(L.wo); dfree(L.win); dfree(L.wout);
-    dfree(L.k); dfree(L.vt);
+    dfree(L.k); dfree(L.v);
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
@@ -282,7 +282,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
   EpiParams qkv;
   qkv.q = s.q;
   qkv.k = L.k;
-  qkv.vt = L.vt;
+  qkv.v = L.v;
   qkv.hs = m.hs;
   qkv.dh = m.dh;
   qkv.dhp = m.dhp;
@@ -295,7 +295,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
   prof_begin(s, kAttention, 4 * r * P * hs, 0);
-  check(attention(s.tm_q, L.tm_k, L.tm_vt, a, s.sm_count, s.stream), "attention");
+  check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
   prof_end(s);
   EpiParams res;
   res.out_f32 = s.h32;
@@ -459,7 +459,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       const size_t kv = size_t(m.heads) * size_t(m.P) * size_t(m.dhp) * sizeof(bf16);
       for (StageLayer& L : s.layers) {
         PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
-        PF_CUDA_CHECK(cudaMemsetAsync(L.vt, 0, kv, s.stream));
+        PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kv, s.stream));
       }
     }
   }
@@ -624,12 +624,12 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
       hb[size_t(r) * hs + c] = __float2bfloat16_rn(v);
     }
   std::vector<bf16> kd(size_t(m.heads) * P * m.dhp, __float2bfloat16_rn(0.f));
-  std::vector<bf16> vd(size_t(m.heads) * m.dhp * P, __float2bfloat16_rn(0.f));
+  std::vector<bf16> vd(size_t(m.heads) * P * m.dhp, __float2bfloat16_rn(0.f));
   for (int64_t r = 0; r < P; ++r)
     for (int c = 0; c < hs; ++c) {
       const int head = c / m.dh, dd = c % m.dh;
       kd[(size_t(head) * P + r) * m.dhp + dd] = __float2bfloat16_rn(float(k_buf[idx(r, c, P)]));
-      vd[(size_t(head) * m.dhp + dd) * P + r] = __float2bfloat16_rn(float(v_buf[idx(r, c, P)]));
+      vd[(size_t(head) * P + r) * m.dhp + dd] = __float2bfloat16_rn(float(v_buf[idx(r, c, P)]));
     }
   DeviceGuard g(s.device);
   PF_CUDA_CHECK(cudaMemcpyAsync(s.h32 + row0 * hs, h32.data(), h32.size() * 4,
@@ -637,7 +637,7 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
   PF_CUDA_CHECK(cudaMemcpyAsync(s.hb + row0 * hs, hb.data(), hb.size() * 2,
                                 cudaMemcpyHostToDevice, s.stream));
   PF_CUDA_CHECK(cudaMemcpyAsync(L.k, kd.data(), kd.size() * 2, cudaMemcpyHostToDevice, s.stream));
-  PF_CUDA_CHECK(cudaMemcpyAsync(L.vt, vd.data(), vd.size() * 2, cudaMemcpyHostToDevice, s.stream));
+  PF_CUDA_CHECK(cudaMemcpyAsync(L.v, vd.data(), vd.size() * 2, cudaMemcpyHostToDevice, s.stream));
   check(reset_flag(s.flag, s.stream), "reset_flag");
   codes_.assign(1, {0, layer});
   launches_ = 1;
@@ -645,7 +645,7 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
   PF_CUDA_CHECK(cudaMemcpyAsync(h32.data(), s.h32 + row0 * hs, h32.size() * 4,
                                 cudaMemcpyDeviceToHost, s.stream));
   PF_CUDA_CHECK(cudaMemcpyAsync(kd.data(), L.k, kd.size() * 2, cudaMemcpyDeviceToHost, s.stream));
-  PF_CUDA_CHECK(cudaMemcpyAsync(vd.data(), L.vt, vd.size() * 2, cudaMemcpyDeviceToHost, s.stream));
+  PF_CUDA_CHECK(cudaMemcpyAsync(vd.data(), L.v, vd.size() * 2, cudaMemcpyDeviceToHost, s.stream));
   PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
   for (int64_t r = 0; r < rows; ++r)
     for (int c = 0; c < hs; ++c) h[idx(r, c, rows)] = double(h32[size_t(r) * hs + c]);
@@ -653,7 +653,7 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
     for (int c = 0; c < hs; ++c) {
       const int head = c / m.dh, dd = c % m.dh;
       k_buf[idx(r, c, P)] = double(__bfloat162float(kd[(size_t(head) * P + r) * m.dhp + dd]));
-      v_buf[idx(r, c, P)] = double(__bfloat162float(vd[(size_t(head) * m.dhp + dd) * P + r]));
+      v_buf[idx(r, c, P)] = double(__bfloat162float(vd[(size_t(head) * P + r) * m.dhp + dd]));
     }
   int f = INT_MAX;
   PF_CUDA_CHECK(cudaMemcpy(&f, s.flag, sizeof(int), cudaMemcpyDeviceToHost));

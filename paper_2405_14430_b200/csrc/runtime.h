@@ -67,8 +67,8 @@ struct StageLayer {
   bf16* win = nullptr;   // [mlp x hs]
   bf16* wout = nullptr;  // [hs x mlp]
   bf16* k = nullptr;     // [heads][P][dhp]
-  bf16* vt = nullptr;    // [heads][dhp][P]
-  CUtensorMap tm_wqkv, tm_wo, tm_win, tm_wout, tm_k, tm_vt;
+  bf16* v = nullptr;     // [heads][P][dhp]
+  CUtensorMap tm_wqkv, tm_wo, tm_win, tm_wout, tm_k, tm_v;
 };
 
 struct Stage {

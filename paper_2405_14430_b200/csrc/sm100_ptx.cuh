@@ -145,11 +145,26 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw32(uint32_t saddr) {
          (static_cast<uint64_t>(6) << 61);                  // SWIZZLE_32B
 }
 
-// Instruction descriptor: bf16 x bf16 -> f32, both operands K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
+// MN-major operand, 32-byte swizzle: atoms of 8 K-rows x 32 B (16 bf16 along
+// MN). SBO = byte stride between 8-row K groups, LBO = byte stride between
+// 16-element MN blocks (cute/arch/mma_sm100_desc.hpp, make_umma_desc<MN>).
+__device__ __forceinline__ uint64_t desc_mnmajor_sw32(uint32_t saddr, uint32_t lbo,
+                                                      uint32_t sbo) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) |
+         (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(6) << 61);                  // SWIZZLE_32B
+}
+
+// Instruction descriptor: bf16 x bf16 -> f32; A K-major, B K-major unless
+// b_mn_major (bit 16).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N,
+                                                      bool b_mn_major = false) {
   return (1u << 4)            // D format f32
          | (1u << 7)          // A bf16
          | (1u << 10)         // B bf16
+         | ((b_mn_major ? 1u : 0u) << 16)
          | ((N >> 3) << 17)   // N
          | ((M >> 4) << 24);  // M
 }
