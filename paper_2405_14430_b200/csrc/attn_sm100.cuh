@@ -15,16 +15,20 @@
 // (SWIZZLE_32B atoms), which serve both as K-major (Q, K) and MN-major (V)
 // UMMA operands.
 //
-// One CTA = 128 query rows x one head x one kv split. Roles (256 threads):
-//   warp 0      TMA producer: Q once, then K_i and V_i in separate rings
-//   warp 1      MMA issuer: S_i = Q K_i^T into TMEM (double-buffered), then
-//               O += P_{i-1} V_{i-1} (TMEM accumulator); K slots are released
-//               as soon as S_i completes, V slots after PV_i
-//   warp 2      TMEM allocator
-//   warps 4..7  softmax: one query row per thread; online softmax in fp32 with
-//               lazy rescaling (O and l are rescaled only when the running max
-//               grows by more than 2^8), P written as bf16 into a
-//               double-buffered 128B-swizzled smem tile.
+// One CTA = NT query tiles of 128 rows (NT = 2 for dh <= 96, sharing every
+// K/V tile, which halves the L2->SM operand traffic per FLOP) x one head x
+// one kv split. Roles (128 + 128 NT threads):
+//   warp 0        TMA producer: Q tiles once, then K_i and V_i in two rings
+//   warp 1        MMA issuer: S_{t,i} = Q_t K_i^T into TMEM (one buffer per
+//                 tile), then O_t += P_{t,i-1} V_{i-1} (TMEM accumulators);
+//                 K slots are released as soon as the S MMAs complete, V
+//                 slots after the PV MMAs
+//   warp 2        TMEM allocator (S_t at column 128 t, O_t at 256 + 128 t)
+//   warps 4..     one softmax warpgroup per tile: one query row per thread;
+//                 online softmax in fp32 with lazy rescaling (O and l are
+//                 rescaled only when the running max grows by more than 2^8);
+//                 P is computed into registers while PV_{t,i-1} drains, then
+//                 stored as bf16 into the tile's 128B-swizzled smem P buffer.
 // With kv_splits > 1 each split writes an unnormalised partial (O, m, l) in
 // fp32 and `attn_combine_kernel` merges the splits in a fixed order.
 #pragma once
@@ -33,23 +37,34 @@
 
 namespace pf {
 
-constexpr int kAttnBM = 128;   // query rows per CTA
+constexpr int kAttnBM = 128;   // query rows per tile
 constexpr int kAttnBN = 128;   // kv rows per block
 
-template <int DHP>
+// NT query tiles (of 128 rows) per CTA share every K/V tile.
+template <int DHP, int NT>
 struct AttnSmem {
-  static constexpr int kStages = DHP <= 80 ? 3 : 2;
   static constexpr uint32_t kTileBytes = kAttnBM * DHP * 2;  // Q, K or V tile
+  static constexpr uint32_t kTileAlloc = (kTileBytes + 1023) & ~1023u;
   static constexpr uint32_t kPBytes = kAttnBM * kAttnBN * 2;  // 32 KB
+  static constexpr uint32_t kBudget = 232448 - 1024 - 512;
+  static constexpr int kStagesMax =
+      int((kBudget - NT * (kTileAlloc + kPBytes)) / (2 * kTileAlloc));
+  static constexpr int kStages = kStagesMax > 4 ? 4 : kStagesMax;
   static constexpr uint32_t kQOff = 0;
-  static constexpr uint32_t kKOff = (kTileBytes + 1023) & ~1023u;
-  static constexpr uint32_t kVOff = kKOff + kStages * kKOff;
-  static constexpr uint32_t kPOff = kVOff + kStages * kKOff;
-  static constexpr uint32_t kBarOff = kPOff + 2 * kPBytes;
+  static constexpr uint32_t kKOff = NT * kTileAlloc;
+  static constexpr uint32_t kVOff = kKOff + kStages * kTileAlloc;
+  static constexpr uint32_t kPOff = kVOff + kStages * kTileAlloc;
+  static constexpr uint32_t kBarOff = kPOff + NT * kPBytes;
   static constexpr uint32_t kTotal = kBarOff + 512 + 1024;
+  static constexpr int kThreads = 128 + 128 * NT;
   static_assert(DHP % 16 == 0 && DHP <= 128, "head dim padding");
+  static_assert(kStages >= 2, "attention smem budget");
   static_assert(kTotal <= 232448, "attention smem budget");
 };
+
+// Tiles per CTA for a padded head dim: two while the smem budget allows a
+// >= 2-deep K/V ring next to two Q tiles and two P tiles.
+__host__ __device__ constexpr int attn_tiles_per_cta(int dhp) { return dhp <= 96 ? 2 : 1; }
 
 struct AttnParams {
   int P;            // kv rows in the buffer (= sequence length)
@@ -62,15 +77,15 @@ struct AttnParams {
   __nv_bfloat16* out;  // [P][hs]   (used when kv_splits == 1)
   float* part_o;       // [splits][heads][rows_pad][DHP] (kv_splits > 1)
   float* part_ml;      // [splits][heads][rows_pad][2]
-  int rows_pad;        // q_tiles * 128
+  int rows_pad;        // ctas_along_q * NT * 128
 };
 
-template <int DHP>
-__global__ void __launch_bounds__(256, 1)
+template <int DHP, int NT>
+__global__ void __launch_bounds__(128 + 128 * NT, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, AttnParams prm) {
-  using L = AttnSmem<DHP>;
+  using L = AttnSmem<DHP, NT>;
   constexpr int S = L::kStages;
   constexpr int kChunks = DHP / 16;
   extern __shared__ uint8_t smem_raw[];
@@ -86,15 +101,15 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* k_empty = k_full + S;    // [S]
   uint64_t* v_full = k_empty + S;    // [S]
   uint64_t* v_empty = v_full + S;    // [S]
-  uint64_t* s_full = v_empty + S;    // [2]
-  uint64_t* s_empty = s_full + 2;    // [2]
-  uint64_t* p_full = s_empty + 2;    // [2]
-  uint64_t* pv_done = p_full + 2;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* s_full = v_empty + S;    // [NT]
+  uint64_t* s_empty = s_full + NT;   // [NT]
+  uint64_t* p_full = s_empty + NT;   // [NT]
+  uint64_t* pv_done = p_full + NT;   // [NT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NT);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = ptx::lane_id();
-  const int qt = blockIdx.x;
+  const int qt = blockIdx.x;  // group of NT query tiles
   const int head = blockIdx.y;
   const int split = blockIdx.z;
   const int total_blocks = (prm.P + kAttnBN - 1) / kAttnBN;
@@ -114,28 +129,34 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&v_full[s], 1);
       ptx::mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&s_full[b], 1);
-      ptx::mbar_init(&s_empty[b], 128);
-      ptx::mbar_init(&p_full[b], 128);
-      ptx::mbar_init(&pv_done[b], 1);
+    for (int t = 0; t < NT; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&s_empty[t], 128);
+      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&pv_done[t], 1);
     }
     ptx::fence_barrier_init();
   }
+  // TMEM: S_t at column 128 t, O_t at 256 + 128 t.
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tmem_o = tmem_base + 256;
-
+  // With NT = 2 (384 threads) registers move from the producer warpgroup
+  // (TMA, MMA, allocator) to the two softmax warpgroups (S row + packed P).
+  if (warp < 4) {
+    if constexpr (NT == 2) ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
     if (lane == 0) {
-      const int qrow = head * prm.P + prm.row0 + qt * kAttnBM;
-      ptx::mbar_arrive_expect_tx(q_full, L::kTileBytes);
+      const int qrow = head * prm.P + prm.row0 + qt * (NT * kAttnBM);
+      ptx::mbar_arrive_expect_tx(q_full, NT * L::kTileBytes);
 #pragma unroll
-      for (int c = 0; c < kChunks; ++c)
-        ptx::tma_load_2d(sQ + c * (kAttnBM * 32), &tm_q, q_full, c * 16, qrow);
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c)
+          ptx::tma_load_2d(sQ + t * L::kTileAlloc + c * (kAttnBM * 32), &tm_q, q_full,
+                           c * 16, qrow + t * kAttnBM);
       for (int i = 0; i < nblk; ++i) {
         const int s = i % S;
         const uint32_t ph = ((i / S) & 1) ^ 1;
@@ -144,13 +165,13 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_arrive_expect_tx(&k_full[s], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sK + s * L::kKOff + c * (kAttnBN * 32), &tm_k, &k_full[s],
+          ptx::tma_load_2d(sK + s * L::kTileAlloc + c * (kAttnBN * 32), &tm_k, &k_full[s],
                            c * 16, kvrow);
         ptx::mbar_wait(&v_empty[s], ph);
         ptx::mbar_arrive_expect_tx(&v_full[s], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sV + s * L::kKOff + c * (kAttnBN * 32), &tm_v, &v_full[s],
+          ptx::tma_load_2d(sV + s * L::kTileAlloc + c * (kAttnBN * 32), &tm_v, &v_full[s],
                            c * 16, kvrow);
       }
     }
@@ -165,68 +186,77 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_wait(q_full, 0);
 
       auto issue_pv = [&](int j) {
-        const int b = j & 1;
         const int s = j % S;
         ptx::mbar_wait(&v_full[s], (j / S) & 1);
-        ptx::mbar_wait(&p_full[b], (j >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t pb = p_base + b * L::kPBytes;
-        const uint32_t vb = v_base + s * L::kKOff;
+        const uint32_t vb = v_base + s * L::kTileAlloc;
 #pragma unroll
-        for (int k = 0; k < kAttnBN / 16; ++k) {
-          // A: P rows x 16 kv (SW128 K-major, 64 kv per atom column)
-          // B: V 16 kv rows x DHP (SW32 MN-major: LBO = next 16-col chunk,
-          //    SBO = next 8 kv rows)
-          ptx::umma_bf16_ss(tmem_o,
-                            ptx::desc_kmajor_sw128(pb + (k >> 2) * (kAttnBM * 128) + (k & 3) * 32),
-                            ptx::desc_mnmajor_sw32(vb + k * 16 * 32, kAttnBN * 32, 256),
-                            idesc_o, (j | k) != 0);
+        for (int t = 0; t < NT; ++t) {
+          ptx::mbar_wait(&p_full[t], j & 1);
+          ptx::tc_fence_after();
+          const uint32_t pb = p_base + t * L::kPBytes;
+#pragma unroll
+          for (int k = 0; k < kAttnBN / 16; ++k) {
+            // A: P rows x 16 kv (SW128 K-major, 64 kv per atom column)
+            // B: V 16 kv rows x DHP (SW32 MN-major: LBO = next 16-col chunk,
+            //    SBO = next 8 kv rows)
+            ptx::umma_bf16_ss(tmem_base + 256 + 128 * t,
+                              ptx::desc_kmajor_sw128(pb + (k >> 2) * (kAttnBM * 128) + (k & 3) * 32),
+                              ptx::desc_mnmajor_sw32(vb + k * 16 * 32, kAttnBN * 32, 256),
+                              idesc_o, (j | k) != 0);
+          }
+          ptx::umma_commit(&pv_done[t]);
         }
-        ptx::umma_commit(&pv_done[b]);
         ptx::umma_commit(&v_empty[s]);
       };
 
       for (int i = 0; i < nblk; ++i) {
         const int s = i % S;
-        const int b = i & 1;
         ptx::mbar_wait(&k_full[s], (i / S) & 1);
-        if (i >= 2) ptx::mbar_wait(&s_empty[b], ((i >> 1) - 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t kb = k_base + s * L::kKOff;
+        const uint32_t kb = k_base + s * L::kTileAlloc;
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c) {
-          ptx::umma_bf16_ss(tmem_base + b * kAttnBN,
-                            ptx::desc_kmajor_sw32(q_base + c * (kAttnBM * 32)),
-                            ptx::desc_kmajor_sw32(kb + c * (kAttnBN * 32)),
-                            idesc_s, c != 0);
+        for (int t = 0; t < NT; ++t) {
+          if (i >= 1) ptx::mbar_wait(&s_empty[t], (i - 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t qb = q_base + t * L::kTileAlloc;
+#pragma unroll
+          for (int c = 0; c < kChunks; ++c) {
+            ptx::umma_bf16_ss(tmem_base + 128 * t,
+                              ptx::desc_kmajor_sw32(qb + c * (kAttnBM * 32)),
+                              ptx::desc_kmajor_sw32(kb + c * (kAttnBN * 32)),
+                              idesc_s, c != 0);
+          }
+          ptx::umma_commit(&s_full[t]);
         }
-        ptx::umma_commit(&s_full[b]);
         ptx::umma_commit(&k_empty[s]);
         if (i >= 1) issue_pv(i - 1);
       }
       issue_pv(nblk - 1);
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    if constexpr (NT == 2) ptx::setmaxnreg_inc<224>();
+    const int t = (warp - 4) >> 2;        // query tile of this warpgroup
     const int q = warp & 3;
     const int trow = 32 * q + int(lane);  // row within the tile == TMEM lane
     const uint32_t lane_off = uint32_t(32 * q) << 16;
+    const uint32_t tmem_s = tmem_base + 128 * t + lane_off;
+    const uint32_t tmem_o = tmem_base + 256 + 128 * t + lane_off;
+    uint8_t* pbuf = sP + t * L::kPBytes;
     const float sc = prm.scale_log2;
     float m_ref = -INFINITY;  // running (lazy) max, scaled log2 domain
     float l_sum = 0.f;
     for (int i = 0; i < nblk; ++i) {
-      const int b = i & 1;
       const int kv0 = (blk_begin + i) * kAttnBN;
-      ptx::mbar_wait(&s_full[b], (i >> 1) & 1);
+      ptx::mbar_wait(&s_full[t], i & 1);
       ptx::tc_fence_after();
       uint32_t sr[kAttnBN];
 #pragma unroll
       for (int c = 0; c < kAttnBN / 32; ++c)
-        ptx::tmem_ld32(tmem_base + lane_off + b * kAttnBN + 32 * c,
-                       *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        ptx::tmem_ld32(tmem_s + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
       ptx::tmem_wait_ld();
-      // S buffer b may be overwritten by S_{i+2} now.
+      // S_t may be overwritten by S_{t,i+1} now.
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&s_empty[b]);
+      ptx::mbar_arrive(&s_empty[t]);
 
       float* s = reinterpret_cast<float*>(sr);
       if (kv0 + kAttnBN > prm.P) {  // kv rows past the buffer end are masked
@@ -245,66 +275,68 @@ __global__ void __launch_bounds__(256, 1)
       const bool need = bm > m_ref + 8.0f;
       const float m_new = need ? bm : m_ref;
       const float alpha = need ? ptx::ex2_approx(m_ref - m_new) : 1.0f;  // 0 on first block
-      if (__any_sync(0xffffffffu, need) && i > 0) {
-        // O accumulated through PV_{i-1}: wait for it, then rescale in TMEM.
-        ptx::mbar_wait(&pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < kChunks; ++c) {
-          uint32_t r[16];
-          ptx::tmem_ld16(tmem_o + lane_off + 16 * c, r);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          ptx::tmem_st16(tmem_o + lane_off + 16 * c, r);
-        }
-        ptx::tmem_wait_st();
-      }
-      l_sum *= alpha;
-      m_ref = m_new;
 
-      // P_{i-2} (same smem buffer) must have been consumed by PV_{i-2}.
-      if (i >= 2) ptx::mbar_wait(&pv_done[b], ((i - 2) >> 1) & 1);
-      uint8_t* pbuf = sP + b * L::kPBytes;
+      // P in registers (bf16 pairs) while PV_{t,i-1} may still read P smem.
+      uint32_t pk[kAttnBN / 2];
       float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int e = 0; e < kAttnBN; e += 4) {
+        const float p0 = ptx::ex2_approx(fmaf(s[e], sc, -m_new));
+        const float p1 = ptx::ex2_approx(fmaf(s[e + 1], sc, -m_new));
+        const float p2 = ptx::ex2_approx(fmaf(s[e + 2], sc, -m_new));
+        const float p3 = ptx::ex2_approx(fmaf(s[e + 3], sc, -m_new));
+        ls0 += p0 + p1;
+        ls1 += p2 + p3;
+        pk[e / 2] = ptx::pack_bf16x2(p0, p1);
+        pk[e / 2 + 1] = ptx::pack_bf16x2(p2, p3);
+      }
+      if (i >= 1) {
+        // PV_{t,i-1} has consumed P_t (and finished accumulating into O_t).
+        ptx::mbar_wait(&pv_done[t], (i - 1) & 1);
+        ptx::tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int e0 = 64 * h + 8 * c;
-          float p[8];
+          for (int c = 0; c < kChunks; ++c) {
+            uint32_t r[16];
+            ptx::tmem_ld16(tmem_o + 16 * c, r);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 8; ++e) p[e] = ptx::ex2_approx(fmaf(s[e0 + e], sc, -m_new));
-          ls0 += (p[0] + p[1]) + (p[2] + p[3]);
-          ls1 += (p[4] + p[5]) + (p[6] + p[7]);
-          uint4 v;
-          v.x = ptx::pack_bf16x2(p[0], p[1]);
-          v.y = ptx::pack_bf16x2(p[2], p[3]);
-          v.z = ptx::pack_bf16x2(p[4], p[5]);
-          v.w = ptx::pack_bf16x2(p[6], p[7]);
-          const int chunk = c ^ (trow & 7);
-          *reinterpret_cast<uint4*>(pbuf + h * (kAttnBM * 128) + trow * 128 + chunk * 16) = v;
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            ptx::tmem_st16(tmem_o + 16 * c, r);
+          }
+          ptx::tmem_wait_st();
         }
       }
-      l_sum += ls0 + ls1;
+      l_sum = l_sum * alpha + (ls0 + ls1);
+      m_ref = m_new;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int w0 = 32 * h + 4 * c;
+          const int chunk = c ^ (trow & 7);
+          *reinterpret_cast<uint4*>(pbuf + h * (kAttnBM * 128) + trow * 128 + chunk * 16) =
+              make_uint4(pk[w0], pk[w0 + 1], pk[w0 + 2], pk[w0 + 3]);
+        }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&p_full[b]);
+      ptx::mbar_arrive(&p_full[t]);
     }
 
     // Epilogue: wait for the last PV, read O, normalise, store.
-    ptx::mbar_wait(&pv_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+    ptx::mbar_wait(&pv_done[t], (nblk - 1) & 1);
     ptx::tc_fence_after();
-    const bool row_ok = qt * kAttnBM + trow < prm.rows;
-    const int grow = prm.row0 + qt * kAttnBM + trow;  // global query row
+    const int lrow = qt * (NT * kAttnBM) + t * kAttnBM + trow;  // row within the launch
+    const bool row_ok = lrow < prm.rows;
     if (prm.kv_splits == 1) {
       const float inv_l = 1.0f / l_sum;
-      __nv_bfloat16* orow = prm.out + size_t(grow) * prm.hs + size_t(head) * prm.dh;
+      __nv_bfloat16* orow =
+          prm.out + size_t(prm.row0 + lrow) * prm.hs + size_t(head) * prm.dh;
       const bool vec = (prm.dh % 8 == 0) && (prm.hs % 8 == 0);
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
         uint32_t r[16];
-        ptx::tmem_ld16(tmem_o + lane_off + 16 * c, r);
+        ptx::tmem_ld16(tmem_o + 16 * c, r);
         ptx::tmem_wait_ld();
         if (row_ok) {
           if (vec) {
@@ -330,12 +362,12 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     } else {
-      const size_t prow = (size_t(split) * prm.heads + head) * prm.rows_pad + qt * kAttnBM + trow;
+      const size_t prow = (size_t(split) * prm.heads + head) * prm.rows_pad + lrow;
       float* po = prm.part_o + prow * DHP;
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
         uint32_t r[16];
-        ptx::tmem_ld16(tmem_o + lane_off + 16 * c, r);
+        ptx::tmem_ld16(tmem_o + 16 * c, r);
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 16; e += 4)
@@ -360,6 +392,7 @@ __global__ void __launch_bounds__(256, 1)
 // One thread per (query row, head, 16-column chunk).
 template <int DHP>
 __global__ void attn_combine_kernel(AttnParams prm) {
+  // prm.rows_pad rows per (split, head) block of the partial buffers
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int chunks = DHP / 16;
   const int total = prm.rows * prm.heads * chunks;

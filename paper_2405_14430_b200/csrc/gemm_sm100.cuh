@@ -141,11 +141,23 @@ __global__ void __launch_bounds__(256, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int mt = tile % m_tiles;
       const int nt = tile / m_tiles;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
       const int local_row = mt * kGemmBM + 32 * q + int(lane);
       const bool row_ok = local_row < rows;
-#pragma unroll 1
+      // Epilogues that read an existing output (the residual stream) issue
+      // those loads before waiting for the accumulator, so they overlap the
+      // tile's main loop instead of sitting on the critical path.
+      float pre[Epi::kPreload ? BN / 32 : 1][32];
+      if constexpr (Epi::kPreload) {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + 32 * c;
+          if (row_ok && col0 < N)
+            epi.preload(row0 + local_row, col0, pre[c], (N - col0) < 32 ? (N - col0) : 32);
+        }
+      }
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+#pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         const int col0 = nt * BN + 32 * c;
         if (col0 >= N) break;
@@ -157,7 +169,11 @@ __global__ void __launch_bounds__(256, 1)
           float v[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-          epi(row0 + local_row, col0, v, nvalid);
+          if constexpr (Epi::kPreload) {
+            epi.apply(row0 + local_row, col0, v, pre[c], nvalid);
+          } else {
+            epi(row0 + local_row, col0, v, nvalid);
+          }
         }
       }
       ptx::tc_fence_before();

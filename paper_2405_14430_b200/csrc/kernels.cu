@@ -84,6 +84,7 @@ cudaError_t ensure_smem_attr(uint32_t bytes) {
 }
 
 struct EpiStoreF32 {
+  static constexpr bool kPreload = false;
   float* out;
   int ld;
   __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
@@ -102,23 +103,40 @@ struct EpiStoreF32 {
 
 // h (fp32 residual stream) += acc; refresh the bf16 operand copy; flag
 // non-finite values (the reference's require_finite, execute.cpp:75-83).
+// The residual rows are preloaded before the accumulator is ready.
 struct EpiResidual {
+  static constexpr bool kPreload = true;
   float* h;
   bf16* hb;
   int ld;
   int* flag;
   int code;
-  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+  __device__ void preload(int row, int col0, float (&pre)[32], int nvalid) const {
+    const float* hr = h + size_t(row) * ld + col0;
+    if (nvalid == 32) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(hr + e);
+        pre[e] = a.x; pre[e + 1] = a.y; pre[e + 2] = a.z; pre[e + 3] = a.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) pre[e] = e < nvalid ? hr[e] : 0.f;
+    }
+  }
+  __device__ void apply(int row, int col0, const float (&v)[32], const float (&pre)[32],
+                        int nvalid) const {
     float* hr = h + size_t(row) * ld + col0;
     bf16* br = hb + size_t(row) * ld + col0;
     bool bad = false;
     if (nvalid == 32) {
 #pragma unroll
       for (int e = 0; e < 32; e += 8) {
-        float4 a = *reinterpret_cast<const float4*>(hr + e);
-        float4 b = *reinterpret_cast<const float4*>(hr + e + 4);
-        a.x += v[e + 0]; a.y += v[e + 1]; a.z += v[e + 2]; a.w += v[e + 3];
-        b.x += v[e + 4]; b.y += v[e + 5]; b.z += v[e + 6]; b.w += v[e + 7];
+        float4 a, b;
+        a.x = pre[e + 0] + v[e + 0]; a.y = pre[e + 1] + v[e + 1];
+        a.z = pre[e + 2] + v[e + 2]; a.w = pre[e + 3] + v[e + 3];
+        b.x = pre[e + 4] + v[e + 4]; b.y = pre[e + 5] + v[e + 5];
+        b.z = pre[e + 6] + v[e + 6]; b.w = pre[e + 7] + v[e + 7];
         *reinterpret_cast<float4*>(hr + e) = a;
         *reinterpret_cast<float4*>(hr + e + 4) = b;
         uint4 pk;
@@ -134,7 +152,7 @@ struct EpiResidual {
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
         if (e < nvalid) {
-          const float x = hr[e] + v[e];
+          const float x = pre[e] + v[e];
           hr[e] = x;
           br[e] = __float2bfloat16_rn(x);
           bad |= !isfinite(x);
@@ -146,6 +164,7 @@ struct EpiResidual {
 };
 
 struct EpiTanh {
+  static constexpr bool kPreload = false;
   bf16* z;
   int ld;
   __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
@@ -174,6 +193,7 @@ struct EpiTanh {
 // multiples of 8, each 8-column group lies in one (q|k|v, head) and is stored
 // as one 16-byte vector.
 struct EpiQKV {
+  static constexpr bool kPreload = false;
   bf16* q;
   bf16* k;
   bf16* v;
@@ -265,8 +285,8 @@ cudaError_t gemm(const CUtensorMap& a, const CUtensorMap& b, int rows, int row0,
 
 // ============================================================== attention
 int attn_splits(const AttnLaunch& a, int sm_count) {
-  const int q_tiles = (a.rows + kAttnBM - 1) / kAttnBM;
-  const int ctas = q_tiles * a.heads;
+  const int rows_per_cta = attn_tiles_per_cta(a.dhp) * kAttnBM;
+  const int ctas = ((a.rows + rows_per_cta - 1) / rows_per_cta) * a.heads;
   const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
   if (ctas >= sm_count || blocks < 2) return 1;
   int splits = (sm_count + ctas - 1) / ctas;
@@ -278,7 +298,8 @@ int attn_splits(const AttnLaunch& a, int sm_count) {
 
 size_t attn_work_floats(int dhp, int heads, int rows, int splits) {
   if (splits <= 1) return 0;
-  const size_t rows_pad = size_t((rows + kAttnBM - 1) / kAttnBM) * kAttnBM;
+  const int rows_per_cta = attn_tiles_per_cta(dhp) * kAttnBM;
+  const size_t rows_pad = size_t((rows + rows_per_cta - 1) / rows_per_cta) * rows_per_cta;
   return size_t(splits) * heads * rows_pad * (dhp + 2);
 }
 
@@ -287,12 +308,13 @@ template <int DHP>
 cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
                         const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                         cudaStream_t stream) {
-  using L = AttnSmem<DHP>;
+  constexpr int NT = attn_tiles_per_cta(DHP);
+  using L = AttnSmem<DHP, NT>;
   {
-    cudaError_t e = ensure_smem_attr<attn_fwd_kernel<DHP>>(L::kTotal);
+    cudaError_t e = ensure_smem_attr<attn_fwd_kernel<DHP, NT>>(L::kTotal);
     if (e != cudaSuccess) return e;
   }
-  const int q_tiles = (a.rows + kAttnBM - 1) / kAttnBM;
+  const int q_ctas = (a.rows + NT * kAttnBM - 1) / (NT * kAttnBM);
   const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
   const int splits = attn_splits(a, sm_count);
   AttnParams prm;
@@ -306,7 +328,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   prm.kv_splits = splits;
   prm.blocks_per_split = (blocks + splits - 1) / splits;
   prm.out = a.out;
-  prm.rows_pad = q_tiles * kAttnBM;
+  prm.rows_pad = q_ctas * NT * kAttnBM;
   prm.part_o = nullptr;
   prm.part_ml = nullptr;
   if (splits > 1) {
@@ -315,8 +337,8 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.part_o = a.work;
     prm.part_ml = a.work + size_t(splits) * a.heads * prm.rows_pad * DHP;
   }
-  dim3 grid(q_tiles, a.heads, splits);
-  attn_fwd_kernel<DHP><<<grid, 256, L::kTotal, stream>>>(q, k, v, prm);
+  dim3 grid(q_ctas, a.heads, splits);
+  attn_fwd_kernel<DHP, NT><<<grid, L::kThreads, L::kTotal, stream>>>(q, k, v, prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || splits == 1) return e;
   const int total = a.rows * a.heads * (DHP / 16);
