@@ -30,6 +30,12 @@ int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
                        int P, int rows, int row0, int heads, int hs,
                        void* stream);
 
+/* Debug timeline: enable=1 allocates a device trace buffer that subsequent
+ * pf_debug_attention launches fill with clock64 stamps of CTA (0,0,0);
+ * host (8192 uint64, may be NULL) receives the current contents; enable=0
+ * frees it. */
+int pf_debug_attention_trace(int enable, unsigned long long* host);
+
 #ifdef __cplusplus
 }
 #endif

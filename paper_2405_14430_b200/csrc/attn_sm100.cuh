@@ -15,20 +15,21 @@
 // (SWIZZLE_32B atoms), which serve both as K-major (Q, K) and MN-major (V)
 // UMMA operands.
 //
-// One CTA = NT query tiles of 128 rows (NT = 2 for dh <= 96, sharing every
-// K/V tile, which halves the L2->SM operand traffic per FLOP) x one head x
-// one kv split. Roles (128 + 128 NT threads):
+// One CTA = NT = 2 query tiles of 128 rows (sharing every K/V tile, which
+// halves the L2->SM operand traffic per FLOP) x one head x one kv split.
+// Roles (384 threads):
 //   warp 0        TMA producer: Q tiles once, then K_i and V_i in two rings
-//   warp 1        MMA issuer: S_{t,i} = Q_t K_i^T into TMEM (one buffer per
-//                 tile), then O_t += P_{t,i-1} V_{i-1} (TMEM accumulators);
-//                 K slots are released as soon as the S MMAs complete, V
-//                 slots after the PV MMAs
-//   warp 2        TMEM allocator (S_t at column 128 t, O_t at 256 + 128 t)
-//   warps 4..     one softmax warpgroup per tile: one query row per thread;
+//   warp 1        MMA issuer: S_{t,i} = Q_t K_i^T (SS: both operands in smem)
+//                 into TMEM, O_t += P_{t,i} V_i (TS: P read from TMEM)
+//   warp 2        TMEM allocator (S_t at column 128 t, P_t = S_t + 64,
+//                 O_t at 256 + 128 t)
+//   warps 4..11   one softmax warpgroup per tile: one query row per thread;
 //                 online softmax in fp32 with lazy rescaling (O and l are
 //                 rescaled only when the running max grows by more than 2^8);
-//                 P is computed into registers while PV_{t,i-1} drains, then
-//                 stored as bf16 into the tile's 128B-swizzled smem P buffer.
+//                 P is packed to bf16 and stored into TMEM over the consumed
+//                 scores, so P never touches shared memory (the SS-mode MMAs
+//                 and TMA already use most of the smem bandwidth). exp2 is
+//                 split 3:1 between MUFU.EX2 and an FMA-pipe polynomial.
 // With kv_splits > 1 each split writes an unnormalised partial (O, m, l) in
 // fp32 and `attn_combine_kernel` merges the splits in a fixed order.
 #pragma once
@@ -45,16 +46,13 @@ template <int DHP, int NT>
 struct AttnSmem {
   static constexpr uint32_t kTileBytes = kAttnBM * DHP * 2;  // Q, K or V tile
   static constexpr uint32_t kTileAlloc = (kTileBytes + 1023) & ~1023u;
-  static constexpr uint32_t kPBytes = kAttnBM * kAttnBN * 2;  // 32 KB
   static constexpr uint32_t kBudget = 232448 - 1024 - 512;
-  static constexpr int kStagesMax =
-      int((kBudget - NT * (kTileAlloc + kPBytes)) / (2 * kTileAlloc));
+  static constexpr int kStagesMax = int((kBudget - NT * kTileAlloc) / (2 * kTileAlloc));
   static constexpr int kStages = kStagesMax > 4 ? 4 : kStagesMax;
   static constexpr uint32_t kQOff = 0;
   static constexpr uint32_t kKOff = NT * kTileAlloc;
   static constexpr uint32_t kVOff = kKOff + kStages * kTileAlloc;
-  static constexpr uint32_t kPOff = kVOff + kStages * kTileAlloc;
-  static constexpr uint32_t kBarOff = kPOff + NT * kPBytes;
+  static constexpr uint32_t kBarOff = kVOff + kStages * kTileAlloc;
   static constexpr uint32_t kTotal = kBarOff + 512 + 1024;
   static constexpr int kThreads = 128 + 128 * NT;
   static_assert(DHP % 16 == 0 && DHP <= 128, "head dim padding");
@@ -62,9 +60,9 @@ struct AttnSmem {
   static_assert(kTotal <= 232448, "attention smem budget");
 };
 
-// Tiles per CTA for a padded head dim: two while the smem budget allows a
-// >= 2-deep K/V ring next to two Q tiles and two P tiles.
-__host__ __device__ constexpr int attn_tiles_per_cta(int dhp) { return dhp <= 96 ? 2 : 1; }
+// Two query tiles per CTA for every supported head dim: with P kept in
+// tensor memory the smem holds only Q and the K/V rings.
+__host__ __device__ constexpr int attn_tiles_per_cta(int /*dhp*/) { return 2; }
 
 struct AttnParams {
   int P;            // kv rows in the buffer (= sequence length)
@@ -78,7 +76,17 @@ struct AttnParams {
   float* part_o;       // [splits][heads][rows_pad][DHP] (kv_splits > 1)
   float* part_ml;      // [splits][heads][rows_pad][2]
   int rows_pad;        // ctas_along_q * NT * 128
+  // Debug timeline (clock64) of CTA (0,0,0); null in production. Slots:
+  // [0, 4096) softmax t: 2048 t + 8 i + event; [4096, 6144) MMA: 8 i + event;
+  // [6144, 8192) TMA: 8 i + event.
+  unsigned long long* trace;
 };
+
+__device__ __forceinline__ void attn_trace(const AttnParams& prm, int slot) {
+  if (prm.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+      (threadIdx.x & 31) == 0)
+    prm.trace[slot] = clock64();
+}
 
 template <int DHP, int NT>
 __global__ void __launch_bounds__(128 + 128 * NT, 1)
@@ -94,18 +102,16 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
   uint8_t* sQ = smem + L::kQOff;
   uint8_t* sK = smem + L::kKOff;
   uint8_t* sV = smem + L::kVOff;
-  uint8_t* sP = smem + L::kPOff;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;       // [S]
   uint64_t* k_empty = k_full + S;    // [S]
   uint64_t* v_full = k_empty + S;    // [S]
   uint64_t* v_empty = v_full + S;    // [S]
-  uint64_t* s_full = v_empty + S;    // [NT]
-  uint64_t* s_empty = s_full + NT;   // [NT]
-  uint64_t* p_full = s_empty + NT;   // [NT]
-  uint64_t* pv_done = p_full + NT;   // [NT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NT);
+  uint64_t* s_full = v_empty + S;    // [NT]  S_t ready (and PV_{t,i-1} done)
+  uint64_t* p_full = s_full + NT;    // [NT]  P_t written to TMEM, S_t consumed
+  uint64_t* o_done = p_full + NT;    // [NT]  last PV_t complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NT);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = ptx::lane_id();
@@ -131,24 +137,25 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     }
     for (int t = 0; t < NT; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&s_empty[t], 128);
       ptx::mbar_init(&p_full[t], 128);
-      ptx::mbar_init(&pv_done[t], 1);
+      ptx::mbar_init(&o_done[t], 1);
     }
     ptx::fence_barrier_init();
   }
-  // TMEM: S_t at column 128 t, O_t at 256 + 128 t.
+  // TMEM columns: S_t = [128 t, 128 t + 128) fp32, P_t = S_t + 64 (64 columns
+  // of packed bf16 pairs, written over consumed scores), O_t = 256 + 128 t.
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
   // With NT = 2 (384 threads) registers move from the producer warpgroup
-  // (TMA, MMA, allocator) to the two softmax warpgroups (S row + packed P).
+  // (TMA, MMA, allocator) to the two softmax warpgroups.
   if (warp < 4) {
     if constexpr (NT == 2) ptx::setmaxnreg_dec<56>();
-  if (warp == 0) {
-    if (lane == 0) {
+    if (warp == 0 && lane == 0) {
+      // ------------------------------------------------------------ TMA
       const int qrow = head * prm.P + prm.row0 + qt * (NT * kAttnBM);
       ptx::mbar_arrive_expect_tx(q_full, NT * L::kTileBytes);
 #pragma unroll
@@ -161,102 +168,117 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
         const int s = i % S;
         const uint32_t ph = ((i / S) & 1) ^ 1;
         const int kvrow = head * prm.P + (blk_begin + i) * kAttnBN;
+        attn_trace(prm, 6144 + 8 * i + 0);
         ptx::mbar_wait(&k_empty[s], ph);
+        attn_trace(prm, 6144 + 8 * i + 1);
         ptx::mbar_arrive_expect_tx(&k_full[s], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
           ptx::tma_load_2d(sK + s * L::kTileAlloc + c * (kAttnBN * 32), &tm_k, &k_full[s],
                            c * 16, kvrow);
         ptx::mbar_wait(&v_empty[s], ph);
+        attn_trace(prm, 6144 + 8 * i + 2);
         ptx::mbar_arrive_expect_tx(&v_full[s], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
           ptx::tma_load_2d(sV + s * L::kTileAlloc + c * (kAttnBN * 32), &tm_v, &v_full[s],
                            c * 16, kvrow);
       }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
+    } else if (warp == 1 && lane == 0) {
+      // ------------------------------------------------------------ MMA
+      // Issue order: S_{0,0} S_{1,0} | PV_{0,0} S_{0,1} PV_{1,0} S_{1,1} | ...
+      // PV_{t,i} reads P_t from the S_t columns and S_{t,i+1} overwrites them
+      // afterwards: tcgen05.mma from one thread execute in issue order.
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(kAttnBM, kAttnBN);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(kAttnBM, DHP, /*b_mn_major=*/true);
       const uint32_t q_base = ptx::smem_u32(sQ);
       const uint32_t k_base = ptx::smem_u32(sK);
       const uint32_t v_base = ptx::smem_u32(sV);
-      const uint32_t p_base = ptx::smem_u32(sP);
       ptx::mbar_wait(q_full, 0);
 
-      auto issue_pv = [&](int j) {
-        const int s = j % S;
-        ptx::mbar_wait(&v_full[s], (j / S) & 1);
-        const uint32_t vb = v_base + s * L::kTileAlloc;
+      auto issue_s = [&](int t, int i) {
+        const uint32_t kb = k_base + (i % S) * L::kTileAlloc;
+        const uint32_t qb = q_base + t * L::kTileAlloc;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          ptx::mbar_wait(&p_full[t], j & 1);
-          ptx::tc_fence_after();
-          const uint32_t pb = p_base + t * L::kPBytes;
+        for (int c = 0; c < kChunks; ++c)
+          ptx::umma_bf16_ss(tmem_base + 128 * t, ptx::desc_kmajor_sw32(qb + c * (kAttnBM * 32)),
+                            ptx::desc_kmajor_sw32(kb + c * (kAttnBN * 32)), idesc_s, c != 0);
+        ptx::umma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int i) {
+        const uint32_t vb = v_base + (i % S) * L::kTileAlloc;
+        const uint32_t pt = tmem_base + 128 * t + 64;
 #pragma unroll
-          for (int k = 0; k < kAttnBN / 16; ++k) {
-            // A: P rows x 16 kv (SW128 K-major, 64 kv per atom column)
-            // B: V 16 kv rows x DHP (SW32 MN-major: LBO = next 16-col chunk,
-            //    SBO = next 8 kv rows)
-            ptx::umma_bf16_ss(tmem_base + 256 + 128 * t,
-                              ptx::desc_kmajor_sw128(pb + (k >> 2) * (kAttnBM * 128) + (k & 3) * 32),
-                              ptx::desc_mnmajor_sw32(vb + k * 16 * 32, kAttnBN * 32, 256),
-                              idesc_o, (j | k) != 0);
-          }
-          ptx::umma_commit(&pv_done[t]);
-        }
-        ptx::umma_commit(&v_empty[s]);
+        for (int k = 0; k < kAttnBN / 16; ++k)
+          // A: P_t columns (8 per 16 kv); B: V 16 kv rows x DHP (SW32
+          // MN-major: LBO = next 16-column chunk, SBO = next 8 kv rows)
+          ptx::umma_bf16_ts(tmem_base + 256 + 128 * t, pt + 8 * k,
+                            ptx::desc_mnmajor_sw32(vb + k * 16 * 32, kAttnBN * 32, 256),
+                            idesc_o, (i | k) != 0);
       };
 
+      ptx::mbar_wait(&k_full[0], 0);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int t = 0; t < NT; ++t) issue_s(t, 0);
+      ptx::umma_commit(&k_empty[0]);
       for (int i = 0; i < nblk; ++i) {
         const int s = i % S;
-        ptx::mbar_wait(&k_full[s], (i / S) & 1);
-        const uint32_t kb = k_base + s * L::kTileAlloc;
+        const bool more = i + 1 < nblk;
+        attn_trace(prm, 4096 + 8 * i + 0);
+        ptx::mbar_wait(&v_full[s], (i / S) & 1);
+        attn_trace(prm, 4096 + 8 * i + 1);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          if (i >= 1) ptx::mbar_wait(&s_empty[t], (i - 1) & 1);
+          ptx::mbar_wait(&p_full[t], i & 1);
+          attn_trace(prm, 4096 + 8 * i + 2 + 2 * t);
           ptx::tc_fence_after();
-          const uint32_t qb = q_base + t * L::kTileAlloc;
-#pragma unroll
-          for (int c = 0; c < kChunks; ++c) {
-            ptx::umma_bf16_ss(tmem_base + 128 * t,
-                              ptx::desc_kmajor_sw32(qb + c * (kAttnBM * 32)),
-                              ptx::desc_kmajor_sw32(kb + c * (kAttnBN * 32)),
-                              idesc_s, c != 0);
+          issue_pv(t, i);
+          if (more) {
+            if (t == 0) {
+              ptx::mbar_wait(&k_full[(i + 1) % S], ((i + 1) / S) & 1);
+              ptx::tc_fence_after();
+            }
+            issue_s(t, i + 1);
+            attn_trace(prm, 4096 + 8 * i + 3 + 2 * t);
+          } else {
+            ptx::umma_commit(&o_done[t]);
           }
-          ptx::umma_commit(&s_full[t]);
         }
-        ptx::umma_commit(&k_empty[s]);
-        if (i >= 1) issue_pv(i - 1);
+        ptx::umma_commit(&v_empty[s]);
+        if (more) ptx::umma_commit(&k_empty[(i + 1) % S]);
       }
-      issue_pv(nblk - 1);
     }
-  }
   } else {
     if constexpr (NT == 2) ptx::setmaxnreg_inc<224>();
+    // -------------------------------------------------------------- softmax
     const int t = (warp - 4) >> 2;        // query tile of this warpgroup
     const int q = warp & 3;
     const int trow = 32 * q + int(lane);  // row within the tile == TMEM lane
     const uint32_t lane_off = uint32_t(32 * q) << 16;
     const uint32_t tmem_s = tmem_base + 128 * t + lane_off;
+    const uint32_t tmem_p = tmem_s + 64;
     const uint32_t tmem_o = tmem_base + 256 + 128 * t + lane_off;
-    uint8_t* pbuf = sP + t * L::kPBytes;
     const float sc = prm.scale_log2;
     float m_ref = -INFINITY;  // running (lazy) max, scaled log2 domain
     float l_sum = 0.f;
+    // Warpgroup 0 takes the first exp turn.
+    if constexpr (NT == 2) {
+      if (t == 1) ptx::named_bar_arrive(1, 256);
+    }
     for (int i = 0; i < nblk; ++i) {
       const int kv0 = (blk_begin + i) * kAttnBN;
+      // S_{t,i} complete; so is PV_{t,i-1} (issued before it), hence O_t is
+      // stable until P_{t,i} is published.
+      attn_trace(prm, 2048 * t + 8 * i + 0);
       ptx::mbar_wait(&s_full[t], i & 1);
+      attn_trace(prm, 2048 * t + 8 * i + 1);
       ptx::tc_fence_after();
       uint32_t sr[kAttnBN];
 #pragma unroll
       for (int c = 0; c < kAttnBN / 32; ++c)
         ptx::tmem_ld32(tmem_s + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
       ptx::tmem_wait_ld();
-      // S_t may be overwritten by S_{t,i+1} now.
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&s_empty[t]);
 
       float* s = reinterpret_cast<float*>(sr);
       if (kv0 + kAttnBN > prm.P) {  // kv rows past the buffer end are masked
@@ -265,66 +287,91 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
         for (int e = 0; e < kAttnBN; ++e)
           if (e >= valid) s[e] = -INFINITY;
       }
-      float bm0 = s[0], bm1 = s[1];
+      float bm[8];
 #pragma unroll
-      for (int e = 2; e < kAttnBN; e += 2) {
-        bm0 = fmaxf(bm0, s[e]);
-        bm1 = fmaxf(bm1, s[e + 1]);
-      }
-      const float bm = fmaxf(bm0, bm1) * sc;
-      const bool need = bm > m_ref + 8.0f;
-      const float m_new = need ? bm : m_ref;
+      for (int a = 0; a < 8; ++a) bm[a] = s[a];
+#pragma unroll
+      for (int e = 8; e < kAttnBN; e += 8)
+#pragma unroll
+        for (int a = 0; a < 8; ++a) bm[a] = fmaxf(bm[a], s[e + a]);
+      const float bmax =
+          fmaxf(fmaxf(fmaxf(bm[0], bm[1]), fmaxf(bm[2], bm[3])),
+                fmaxf(fmaxf(bm[4], bm[5]), fmaxf(bm[6], bm[7]))) * sc;
+      const bool need = bmax > m_ref + 8.0f;
+      const float m_new = need ? bmax : m_ref;
       const float alpha = need ? ptx::ex2_approx(m_ref - m_new) : 1.0f;  // 0 on first block
-
-      // P in registers (bf16 pairs) while PV_{t,i-1} may still read P smem.
-      uint32_t pk[kAttnBN / 2];
-      float ls0 = 0.f, ls1 = 0.f;
+      // Ping-pong the exp-heavy section between the two softmax warpgroups
+      // (named barriers 1/2): while one warpgroup exponentiates, the tensor
+      // pipe runs the other tile's PV and next S, and the MUFU is not shared.
+      attn_trace(prm, 2048 * t + 8 * i + 2);
+      if constexpr (NT == 2) ptx::named_bar_sync(1 + t, 256);
+      attn_trace(prm, 2048 * t + 8 * i + 3);
+      if (i > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
-      for (int e = 0; e < kAttnBN; e += 4) {
-        const float p0 = ptx::ex2_approx(fmaf(s[e], sc, -m_new));
-        const float p1 = ptx::ex2_approx(fmaf(s[e + 1], sc, -m_new));
-        const float p2 = ptx::ex2_approx(fmaf(s[e + 2], sc, -m_new));
-        const float p3 = ptx::ex2_approx(fmaf(s[e + 3], sc, -m_new));
-        ls0 += p0 + p1;
-        ls1 += p2 + p3;
-        pk[e / 2] = ptx::pack_bf16x2(p0, p1);
-        pk[e / 2 + 1] = ptx::pack_bf16x2(p2, p3);
+        for (int c = 0; c < kChunks; ++c) {
+          uint32_t r[16];
+          ptx::tmem_ld16(tmem_o + 16 * c, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          ptx::tmem_st16(tmem_o + 16 * c, r);
+        }
       }
-      if (i >= 1) {
-        // PV_{t,i-1} has consumed P_t (and finished accumulating into O_t).
-        ptx::mbar_wait(&pv_done[t], (i - 1) & 1);
-        ptx::tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
+      // P = exp2(s * sc - m): packed fp32x2 FMAs; 1 of every 4 pairs of
+      // pairs goes through the FMA-pipe polynomial, the rest through
+      // MUFU.EX2; P is packed to bf16 pairs and stored into TMEM over S.
+      const float2 sc2 = make_float2(sc, sc);
+      const float2 nm2 = make_float2(-m_new, -m_new);
 #pragma unroll
-          for (int c = 0; c < kChunks; ++c) {
-            uint32_t r[16];
-            ptx::tmem_ld16(tmem_o + 16 * c, r);
-            ptx::tmem_wait_ld();
+      for (int h = 0; h < 2; ++h) {
+        uint32_t pk[32];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-            ptx::tmem_st16(tmem_o + 16 * c, r);
+        for (int g = 0; g < 16; ++g) {
+          const int e = 64 * h + 4 * g;
+          const float2 x0 = ptx::ffma2(make_float2(s[e], s[e + 1]), sc2, nm2);
+          const float2 x1 = ptx::ffma2(make_float2(s[e + 2], s[e + 3]), sc2, nm2);
+          float2 p0, p1;
+          if ((g & 3) == 3) {
+            p0 = ptx::ex2_poly2(x0);
+            p1 = ptx::ex2_poly2(x1);
+          } else {
+            p0 = make_float2(ptx::ex2_approx(x0.x), ptx::ex2_approx(x0.y));
+            p1 = make_float2(ptx::ex2_approx(x1.x), ptx::ex2_approx(x1.y));
           }
-          ptx::tmem_wait_st();
+          s[e] = p0.x; s[e + 1] = p0.y; s[e + 2] = p1.x; s[e + 3] = p1.y;
+          pk[2 * g] = ptx::pack_bf16x2(p0.x, p0.y);
+          pk[2 * g + 1] = ptx::pack_bf16x2(p1.x, p1.y);
         }
+        if (h == 1) {
+          if constexpr (NT == 2) ptx::named_bar_arrive(2 - t, 256);  // hand the turn over
+        }
+        ptx::tmem_st32(tmem_p + 32 * h, pk);
       }
-      l_sum = l_sum * alpha + (ls0 + ls1);
-      m_ref = m_new;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int w0 = 32 * h + 4 * c;
-          const int chunk = c ^ (trow & 7);
-          *reinterpret_cast<uint4*>(pbuf + h * (kAttnBM * 128) + trow * 128 + chunk * 16) =
-              make_uint4(pk[w0], pk[w0 + 1], pk[w0 + 2], pk[w0 + 3]);
-        }
-      ptx::fence_proxy_async_smem();
+      ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[t]);
+      attn_trace(prm, 2048 * t + 8 * i + 4);
+      // Row sum off the critical path (the PV MMA is already running).
+      float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+      for (int e = 0; e < kAttnBN; e += 8) {
+        a0 = ptx::fadd2(a0, make_float2(s[e], s[e + 1]));
+        a1 = ptx::fadd2(a1, make_float2(s[e + 2], s[e + 3]));
+        a2 = ptx::fadd2(a2, make_float2(s[e + 4], s[e + 5]));
+        a3 = ptx::fadd2(a3, make_float2(s[e + 6], s[e + 7]));
+      }
+      a0 = ptx::fadd2(ptx::fadd2(a0, a1), ptx::fadd2(a2, a3));
+      l_sum = l_sum * alpha + (a0.x + a0.y);
+      m_ref = m_new;
+      attn_trace(prm, 2048 * t + 8 * i + 5);
+    }
+    // Balance the ping-pong: warpgroup 0 consumes warpgroup 1's last hand-off.
+    if constexpr (NT == 2) {
+      if (t == 0) ptx::named_bar_sync(1, 256);
     }
 
     // Epilogue: wait for the last PV, read O, normalise, store.
-    ptx::mbar_wait(&pv_done[t], (nblk - 1) & 1);
+    ptx::mbar_wait(&o_done[t], 0);
     ptx::tc_fence_after();
     const int lrow = qt * (NT * kAttnBM) + t * kAttnBM + trow;  // row within the launch
     const bool row_ok = lrow < prm.rows;

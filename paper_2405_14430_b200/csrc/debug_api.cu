@@ -40,6 +40,26 @@ extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
                       pf::device_sm_count(dev), static_cast<cudaStream_t>(stream)));
 }
 
+namespace {
+unsigned long long* g_attn_trace = nullptr;  // device buffer, 8192 slots
+}
+
+// Debug-only: record the clock64 timeline of CTA (0,0,0) of the next
+// pf_debug_attention launches into `host` (8192 slots) when enabled.
+extern "C" int pf_debug_attention_trace(int enable, unsigned long long* host) {
+  if (enable && !g_attn_trace) {
+    cudaMalloc(reinterpret_cast<void**>(&g_attn_trace), 8192 * 8);
+    cudaMemset(g_attn_trace, 0, 8192 * 8);
+  }
+  if (host && g_attn_trace)
+    cudaMemcpy(host, g_attn_trace, 8192 * 8, cudaMemcpyDeviceToHost);
+  if (!enable && g_attn_trace) {
+    cudaFree(g_attn_trace);
+    g_attn_trace = nullptr;
+  }
+  return int(cudaGetLastError());
+}
+
 extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
                                   int P, int rows, int row0, int heads, int hs,
                                   void* stream) {
@@ -74,7 +94,7 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
   int err = ok ? 0 : int(cudaErrorInvalidValue);
   if (ok) {
     pf::AttnLaunch a{dhp, P, rows, row0, heads, dh, hs, float(1.0 / std::sqrt(double(dh))),
-                     static_cast<pf::bf16*>(out), nullptr, 0};
+                     static_cast<pf::bf16*>(out), nullptr, 0, g_attn_trace};
     const int sms = pf::device_sm_count(dev);
     const int splits = pf::attn_splits(a, sms);
     if (splits > 1) {

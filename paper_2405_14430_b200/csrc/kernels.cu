@@ -331,6 +331,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   prm.rows_pad = q_ctas * NT * kAttnBM;
   prm.part_o = nullptr;
   prm.part_ml = nullptr;
+  prm.trace = a.trace;
   if (splits > 1) {
     const size_t need = attn_work_floats(DHP, a.heads, a.rows, splits);
     if (!a.work || a.work_floats < need) return cudaErrorInvalidValue;

@@ -56,6 +56,7 @@ struct AttnLaunch {
   bf16* out;             // [P][hs]
   float* work;           // split-KV partials (may be null if splits == 1)
   size_t work_floats;    // capacity of `work`
+  unsigned long long* trace = nullptr;  // debug timeline (see AttnParams)
 };
 int attn_splits(const AttnLaunch& a, int sm_count);
 size_t attn_work_floats(int dhp, int heads, int rows, int splits);

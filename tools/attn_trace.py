@@ -1,0 +1,52 @@
+"""Time the attention kernel alone at a given shape and dump the clock64
+timeline of CTA (0,0,0) (debug instrumentation; not a bench)."""
+import ctypes
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2405_14430_b200 as pf  # noqa: E402
+
+P, heads, hs, rows, row0 = [int(x) for x in (sys.argv[1:6] if len(sys.argv) > 5 else (4096, 16, 1152, 4096, 0))]
+lib = pf.load_library()
+g = torch.Generator(device="cuda").manual_seed(0)
+mk = lambda: ((torch.rand(P, hs, device="cuda", generator=g) * 2 - 1) * 2).to(torch.bfloat16)
+q, k, v = mk(), mk(), mk()
+out = torch.zeros(P, hs, dtype=torch.bfloat16, device="cuda")
+s = torch.cuda.current_stream().cuda_stream
+run = lambda: lib.pf_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                     P, rows, row0, heads, hs, s)
+for _ in range(3):
+    run()
+torch.cuda.synchronize()
+# pf_debug_attention includes repacking kernels; time the whole call and note it
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    run()
+e1.record()
+torch.cuda.synchronize()
+print("debug_attention call (incl. repack) us:", e0.elapsed_time(e1) / 10 * 1e3)
+buf = (ctypes.c_ulonglong * 8192)()
+lib.pf_debug_attention_trace(1, None)
+run()
+torch.cuda.synchronize()
+lib.pf_debug_attention_trace(1, buf)
+lib.pf_debug_attention_trace(0, None)
+a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+base = a[a > 0].min()
+t = np.where(a > 0, a - base, -1)
+nblk = (P + 127) // 128
+res = {"softmax0": t[0:8 * nblk].reshape(nblk, 8)[:, :6].tolist(),
+       "softmax1": t[2048:2048 + 8 * nblk].reshape(nblk, 8)[:, :6].tolist(),
+       "mma": t[4096:4096 + 8 * nblk].reshape(nblk, 8)[:, :6].tolist(),
+       "tma": t[6144:6144 + 8 * nblk].reshape(nblk, 8)[:, :3].tolist()}
+Path("gpurun_out").mkdir(exist_ok=True)
+Path("gpurun_out/attn_trace.json").write_text(json.dumps(res))
+for i in range(min(nblk, 12)):
+    print(i, "sm0", res["softmax0"][i], "sm1", res["softmax1"][i], "mma", res["mma"][i][:6], "tma", res["tma"][i])
+print("last", res["softmax0"][-1], res["softmax1"][-1])
