@@ -26,12 +26,12 @@ extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
                              int row0, int total_rows, int N, int K, void* stream) {
   int dev = 0;
   cudaGetDevice(&dev);
-  CUtensorMap ta, tb;
+  CUtensorMap ta;
+  pf::WeightMaps tb;
   if (!pf::encode_tmap_bf16_2d(&ta, A, uint64_t(K), uint64_t(total_rows), uint64_t(K) * 2,
                                64, 128, 128))
     return int(cudaErrorInvalidValue);
-  if (!pf::encode_tmap_bf16_2d(&tb, B, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
-                               uint32_t(pf::gemm_bn(N)), 128))
+  if (!pf::make_weight_maps(&tb, static_cast<const pf::bf16*>(B), N, K))
     return int(cudaErrorInvalidValue);
   pf::EpiParams ep;
   ep.out_f32 = C - size_t(row0) * N;  // epilogue indexes by global row

@@ -191,4 +191,182 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 2-SM variant (cluster of 2 CTAs on one TPC, tcgen05.mma.cta_group::2):
+// one 256 x BN output tile per CTA pair. CTA r TMA-loads A rows
+// [m0 + 128 r, +128) and B rows [n0 + BN/2 r, +BN/2); the even CTA issues
+// the M = 256 MMAs, whose B operand is read half from each CTA. Per SM this
+// halves the shared-memory operand traffic of the 1-SM 128 x BN kernel
+// (SS-mode MMA + TMA writes otherwise exceed the 128 B/clk smem bandwidth).
+template <int BN, int STAGES>
+struct Gemm2SmSmem {
+  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;        // 16 KB
+  static constexpr uint32_t kBBytes = (BN / 2) * kGemmBK * 2;       // half of B
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
+  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;
+  static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static_assert(BN % 32 == 0 && BN <= 256, "2-SM tile N");
+  static_assert(((BN / 2) * 128) % 1024 == 0, "B half must keep 1024-B aligned stages");
+};
+
+template <int BN, int STAGES, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm2sm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tma_a,
+                           const __grid_constant__ CUtensorMap tma_b, int rows, int row0,
+                           int N, int K, Epi epi) {
+  using L = Gemm2SmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int m_tiles = (rows + 2 * kGemmBM - 1) / (2 * kGemmBM);
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tma_a);
+    ptx::prefetch_tmap(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2);  // one elected arrival per CTA of the pair
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm<L::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
+          ptx::tma_load_2d_2sm(sa, &tma_a, &full[stage], kb * kGemmBK,
+                               row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM);
+          ptx::tma_load_2d_2sm(sb, &tma_b, &full[stage], kb * kGemmBK,
+                               nt * BN + int(rank) * (BN / 2));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b_base = a_base + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k)
+            ptx::umma2_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
+                               ptx::desc_kmajor_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+          ptx::umma2_commit_mc(&empty[stage], 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma2_commit_mc(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      const int mt = tile % m_tiles;
+      const int nt = tile / m_tiles;
+      const int local_row = mt * 2 * kGemmBM + int(rank) * kGemmBM + 32 * q + int(lane);
+      const bool row_ok = local_row < rows;
+      float pre[Epi::kPreload ? BN / 32 : 1][32];
+      if constexpr (Epi::kPreload) {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + 32 * c;
+          if (row_ok && col0 < N)
+            epi.preload(row0 + local_row, col0, pre[c], (N - col0) < 32 ? (N - col0) : 32);
+        }
+      }
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = nt * BN + 32 * c;
+        if (col0 >= N) break;
+        uint32_t r[32];
+        ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, r);
+        ptx::tmem_wait_ld();
+        if (row_ok) {
+          const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+          if constexpr (Epi::kPreload) {
+            epi.apply(row0 + local_row, col0, v, pre[c], nvalid);
+          } else {
+            epi(row0 + local_row, col0, v, nvalid);
+          }
+        }
+      }
+      // All four epilogue warps of this CTA have drained accumulator `acc`:
+      // one elected thread tells the pair's MMA issuer (in the even CTA).
+      ptx::tc_fence_before();
+      ptx::named_bar_sync(1, 128);
+      if (warp == 4 && lane == 0)
+        ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<L::kTmemCols>(tmem_base);
+  }
+}
+
 }  // namespace pf

@@ -246,41 +246,79 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int rows,
   return cudaGetLastError();
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, class E>
+cudaError_t launch_gemm2sm(const CUtensorMap& a, const CUtensorMap& b, int rows,
+                           int row0, int N, int K, const E& epi, int sm_count,
+                           cudaStream_t stream) {
+  using L = Gemm2SmSmem<BN, STAGES>;
+  constexpr auto kern = gemm2sm_bf16_tn_kernel<BN, STAGES, E>;
+  cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
+  if (e != cudaSuccess) return e;
+  const int tiles = ((rows + 2 * kGemmBM - 1) / (2 * kGemmBM)) * ((N + BN - 1) / BN);
+  const int pairs = sm_count / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, 256, L::kTotal, stream>>>(a, b, rows, row0, N, K, epi);
+  return cudaGetLastError();
+}
+
+template <bool kTwoSm, int BN, int STAGES>
 cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
                           int row0, int N, int K, Epi kind, const EpiParams& ep,
                           int sm_count, cudaStream_t stream) {
+  auto go = [&](const auto& epi) {
+    if constexpr (kTwoSm)
+      return launch_gemm2sm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream);
+    else
+      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream);
+  };
   switch (kind) {
     case Epi::StoreF32:
-      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K,
-                                     EpiStoreF32{ep.out_f32, ep.ld}, sm_count, stream);
+      return go(EpiStoreF32{ep.out_f32, ep.ld});
     case Epi::Residual:
-      return launch_gemm<BN, STAGES>(
-          a, b, rows, row0, N, K,
-          EpiResidual{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code}, sm_count,
-          stream);
+      return go(EpiResidual{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code});
     case Epi::Tanh:
-      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K,
-                                     EpiTanh{ep.out_bf16, ep.ld}, sm_count, stream);
+      return go(EpiTanh{ep.out_bf16, ep.ld});
     case Epi::QKV:
-      return launch_gemm<BN, STAGES>(
-          a, b, rows, row0, N, K,
-          EpiQKV{ep.q, ep.k, ep.v, ep.hs, ep.dh, ep.dhp, ep.P}, sm_count, stream);
+      return go(EpiQKV{ep.q, ep.k, ep.v, ep.hs, ep.dh, ep.dhp, ep.P});
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
-int gemm_bn(int N) { return N <= 64 ? 64 : 128; }
+int gemm_bn_1sm(int N) { return N <= 64 ? 64 : 128; }
 
-cudaError_t gemm(const CUtensorMap& a, const CUtensorMap& b, int rows, int row0,
+int gemm_bn_2sm(int N) {
+  if (N % 256 == 0) return 256;
+  if (N % 192 == 0) return 192;
+  return 128;
+}
+
+bool make_weight_maps(WeightMaps* maps, const bf16* w, int N, int K) {
+  return encode_tmap_bf16_2d(&maps->one_sm, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
+                             uint32_t(gemm_bn_1sm(N)), 128) &&
+         encode_tmap_bf16_2d(&maps->two_sm, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
+                             uint32_t(gemm_bn_2sm(N) / 2), 128);
+}
+
+cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  int N, int K, Epi kind, const EpiParams& ep, int sm_count,
                  cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
-  if (gemm_bn(N) == 64)
-    return gemm_dispatch<64, 8>(a, b, rows, row0, N, K, kind, ep, sm_count, stream);
-  return gemm_dispatch<128, 6>(a, b, rows, row0, N, K, kind, ep, sm_count, stream);
+  // The CTA-pair kernel wins where its 256 x 256 tiles apply (the MLP-in
+  // projection, 78 % of peak vs 60 % for 1-SM 128 x 128 tiles); for narrower
+  // N the row-per-thread epilogue, not the MMA, bounds the kernel and the
+  // 1-SM tiling keeps more CTAs in flight (measured: profiles/).
+  if (rows >= 2 * kGemmBM && sm_count >= 2 && gemm_bn_2sm(N) == 256) {
+    switch (gemm_bn_2sm(N)) {
+      case 256: return gemm_dispatch<true, 256, 6>(a, b.two_sm, rows, row0, N, K, kind, ep, sm_count, stream);
+      case 192: return gemm_dispatch<true, 192, 7>(a, b.two_sm, rows, row0, N, K, kind, ep, sm_count, stream);
+      default: return gemm_dispatch<true, 128, 8>(a, b.two_sm, rows, row0, N, K, kind, ep, sm_count, stream);
+    }
+  }
+  if (gemm_bn_1sm(N) == 64)
+    return gemm_dispatch<false, 64, 8>(a, b.one_sm, rows, row0, N, K, kind, ep, sm_count, stream);
+  return gemm_dispatch<false, 128, 6>(a, b.one_sm, rows, row0, N, K, kind, ep, sm_count, stream);
 }
 
 // ============================================================== attention

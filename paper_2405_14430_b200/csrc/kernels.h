@@ -41,11 +41,21 @@ struct EpiParams {
   int code = 0;
 };
 
+// Tensor maps over a weight B [N x K] (K-major bf16) for both GEMM paths:
+// one_sm: box 64 x gemm_bn_1sm(N); two_sm: box 64 x gemm_bn_2sm(N)/2.
+struct WeightMaps {
+  CUtensorMap one_sm;
+  CUtensorMap two_sm;
+};
+int gemm_bn_1sm(int N);
+int gemm_bn_2sm(int N);
+bool make_weight_maps(WeightMaps* maps, const bf16* w, int N, int K);
+
 // D[rows x N] = A[row0 .. row0+rows, 0..K) . B[N x K]^T, epilogue `kind`.
-// `a` is a tensor map over the whole A buffer (box 64 x 128, SW128);
-// `b` over B (box 64 x bn, SW128) where bn = gemm_bn(N).
-int gemm_bn(int N);
-cudaError_t gemm(const CUtensorMap& a, const CUtensorMap& b, int rows, int row0,
+// `a` is a tensor map over the whole A buffer (box 64 x 128, SW128). Row
+// blocks of >= 256 rows use the 2-SM (CTA pair) kernel, smaller ones the
+// 1-SM kernel.
+cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  int N, int K, Epi kind, const EpiParams& ep, int sm_count,
                  cudaStream_t stream);
 

@@ -197,10 +197,11 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
     L.wout = dalloc<bf16>(hs * mlp);
     L.k = dalloc<bf16>(heads * P * dhp);
     L.v = dalloc<bf16>(heads * P * dhp);
-    L.tm_wqkv = tmap(L.wqkv, hs, 3 * hs, hs * 2, 64, uint32_t(gemm_bn(int(3 * hs))), 128);
-    L.tm_wo = tmap(L.wo, hs, hs, hs * 2, 64, uint32_t(gemm_bn(int(hs))), 128);
-    L.tm_win = tmap(L.win, hs, mlp, hs * 2, 64, uint32_t(gemm_bn(int(mlp))), 128);
-    L.tm_wout = tmap(L.wout, mlp, hs, mlp * 2, 64, uint32_t(gemm_bn(int(hs))), 128);
+    if (!make_weight_maps(&L.tm_wqkv, L.wqkv, int(3 * hs), int(hs)) ||
+        !make_weight_maps(&L.tm_wo, L.wo, int(hs), int(hs)) ||
+        !make_weight_maps(&L.tm_win, L.win, int(mlp), int(hs)) ||
+        !make_weight_maps(&L.tm_wout, L.wout, int(hs), int(mlp)))
+      throw CudaError("cuTensorMapEncodeTiled failed for a weight matrix");
     L.tm_k = tmap(L.k, dhp, heads * P, dhp * 2, 16, 128, 32);
     L.tm_v = tmap(L.v, dhp, heads * P, dhp * 2, 16, 128, 32);
   }

@@ -68,7 +68,8 @@ struct StageLayer {
   bf16* wout = nullptr;  // [hs x mlp]
   bf16* k = nullptr;     // [heads][P][dhp]
   bf16* v = nullptr;     // [heads][P][dhp]
-  CUtensorMap tm_wqkv, tm_wo, tm_win, tm_wout, tm_k, tm_v;
+  WeightMaps tm_wqkv, tm_wo, tm_win, tm_wout;
+  CUtensorMap tm_k, tm_v;
 };
 
 struct Stage {

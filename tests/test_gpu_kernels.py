@@ -35,7 +35,11 @@ def _gemm(A, B, rows, row0):
     (32, 32, 0, 16, 16),        # hs=16 (K < BK, N < BN)
     (300, 170, 100, 200, 72),   # ragged everything
     (4096, 512, 1536, 3456, 1152),  # PixArt patch QKV
-    (4096, 4096, 0, 1152, 4608),    # PixArt MLP-out full sequence
+    (4096, 4096, 0, 1152, 4608),    # PixArt MLP-out full sequence (2-SM, BN 128)
+    (4096, 4096, 0, 4608, 1152),    # PixArt MLP-in (2-SM, BN 256)
+    (1024, 1000, 24, 4608, 1152),   # 2-SM with a ragged last row tile
+    (512, 300, 100, 96, 64),        # 2-SM with N < BN (B half partly out of range)
+    (2048, 256, 1792, 3456, 1152),  # one 2-SM row tile, BN 192
 ])
 def test_gemm_matches_fp32(total, rows, row0, N, K):
     g = torch.Generator(device="cuda").manual_seed(total + N + K)
