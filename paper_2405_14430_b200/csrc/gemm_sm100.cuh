@@ -369,4 +369,214 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Residual-stream GEMM with a TMA epilogue (1 SM, 128 x 128 tiles):
+//   h32[rows, N] += A . B^T;  hb = bf16(h32);  non-finite -> flag
+// The producer warp TMA-loads the fp32 residual tile into a 128B-swizzled
+// smem buffer once the tile's k-loop is issued; the epilogue warps add the
+// TMEM accumulator in smem, write the bf16 copy next to it, and one thread
+// TMA-stores both tiles. Global traffic is bulk and coalesced instead of
+// one row per thread. Requires rows % 128 == 0 (whole row tiles: stores must
+// not touch rows of other patches) and N % 32 == 0.
+struct ResidTmaArgs {
+  float* h;        // for the finite check only
+  int* flag;
+  int code;
+};
+
+template <int STAGES>
+struct GemmResSmem {
+  static constexpr int BN = 128;
+  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr uint32_t kBBytes = BN * kGemmBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kCOff = STAGES * kStageBytes;       // fp32 tile: 4 x 16 KB
+  static constexpr uint32_t kDOff = kCOff + 4 * 16384;          // bf16 tile: 2 x 16 KB
+  static constexpr uint32_t kBarOffset = kDOff + 2 * 16384;
+  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;
+  static_assert(kTotal <= 232448, "residual GEMM smem budget");
+};
+
+template <int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    gemm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
+                          const __grid_constant__ CUtensorMap tma_b,
+                          const __grid_constant__ CUtensorMap tma_h32,
+                          const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
+                          int N, int K, ResidTmaArgs args) {
+  using L = GemmResSmem<STAGES>;
+  constexpr int BN = L::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sC = smem + L::kCOff;
+  uint8_t* sD = smem + L::kDOff;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* c_full = tempty + 2;
+  uint64_t* c_empty = c_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_empty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = ptx::lane_id();
+  const int m_tiles = rows / kGemmBM;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tma_a);
+    ptx::prefetch_tmap(&tma_b);
+    ptx::prefetch_tmap(&tma_h32);
+    ptx::prefetch_tmap(&tma_hb);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::mbar_init(c_full, 1);
+    ptx::mbar_init(c_empty, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<256>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t c_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          ptx::mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK, row0 + mt * kGemmBM);
+          ptx::tma_load_2d(sb, &tma_b, &full[stage], kb * kGemmBK, nt * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        // residual tile (previous tile's stores must have drained the buffer)
+        ptx::mbar_wait(c_empty, c_phase ^ 1);
+        ptx::mbar_arrive_expect_tx(c_full, 4 * 16384);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          ptx::tma_load_2d(sC + c * 16384, &tma_h32, c_full, nt * BN + 32 * c,
+                           row0 + mt * kGemmBM);
+        c_phase ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b_base = a_base + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k)
+            ptx::umma_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
+                              ptx::desc_kmajor_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = 32 * q + int(lane);  // row within the tile == TMEM lane
+    const uint32_t sw = uint32_t(r & 7);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    uint32_t c_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mt = tile % m_tiles;
+      const int nt = tile / m_tiles;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::mbar_wait(c_full, c_phase);
+      ptx::tc_fence_after();
+      bool bad = false;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, v);
+        ptx::tmem_wait_ld();
+        uint8_t* crow = sC + c * 16384 + r * 128;
+        uint8_t* drow = sD + (c >> 1) * 16384 + r * 128;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {  // 16-byte piece g of the 32 fp32 columns
+          float4* pc = reinterpret_cast<float4*>(crow + ((uint32_t(g) ^ sw) << 4));
+          float4 x = *pc;
+          x.x += __uint_as_float(v[4 * g + 0]);
+          x.y += __uint_as_float(v[4 * g + 1]);
+          x.z += __uint_as_float(v[4 * g + 2]);
+          x.w += __uint_as_float(v[4 * g + 3]);
+          *pc = x;
+          bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+          // bf16 copy: columns 32c + 4g .. +3 -> byte 64 (c&1) + 8 g of the row
+          const uint32_t byte = uint32_t(64 * (c & 1) + 8 * g);
+          uint2* pd = reinterpret_cast<uint2*>(drow + ((((byte >> 4) ^ sw) << 4) | (byte & 15)));
+          *pd = make_uint2(ptx::pack_bf16x2(x.x, x.y), ptx::pack_bf16x2(x.z, x.w));
+        }
+      }
+      if (bad && args.flag) atomicMin(args.flag, args.code);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (warp == 4 && lane == 0) {
+        const int gr = row0 + mt * kGemmBM;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tma_store_2d(&tma_h32, sC + c * 16384, nt * BN + 32 * c, gr);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) ptx::tma_store_2d(&tma_hb, sD + c * 16384, nt * BN + 64 * c, gr);
+        ptx::tma_store_commit();
+        ptx::tma_store_wait_read();
+        ptx::mbar_arrive(c_empty);
+      }
+      c_phase ^= 1;
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    // outstanding stores must complete before the CTA exits
+    if (warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<256>(tmem_base);
+  }
+}
+
 }  // namespace pf

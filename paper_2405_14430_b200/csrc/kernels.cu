@@ -37,9 +37,27 @@ EncodeFn get_encode_fn() {
 
 }  // namespace
 
+static bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base,
+                          uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                          uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
 bool encode_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner,
                          uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
                          uint32_t box_outer, int swizzle_bytes) {
+  return encode_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, inner, outer, row_bytes,
+                        box_inner, box_outer, swizzle_bytes);
+}
+
+bool encode_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                        int swizzle_bytes) {
+  return encode_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, inner, outer, row_bytes,
+                        box_inner, box_outer, swizzle_bytes);
+}
+
+static bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base,
+                          uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                          uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
   EncodeFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -50,7 +68,7 @@ bool encode_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner,
   if (swizzle_bytes == 32) sw = CU_TENSOR_MAP_SWIZZLE_32B;
   if (swizzle_bytes == 64) sw = CU_TENSOR_MAP_SWIZZLE_64B;
   if (swizzle_bytes == 128) sw = CU_TENSOR_MAP_SWIZZLE_128B;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  CUresult r = fn(map, dt, 2,
                   const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -305,6 +323,19 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  int N, int K, Epi kind, const EpiParams& ep, int sm_count,
                  cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
+  if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % kGemmBM == 0 && N % 32 == 0 &&
+      gemm_bn_1sm(N) == 128) {
+    constexpr int kStages = 4;
+    using L = GemmResSmem<kStages>;
+    constexpr auto kern = gemm_resid_tma_kernel<kStages>;
+    cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
+    if (e != cudaSuccess) return e;
+    const int tiles = (rows / kGemmBM) * ((N + L::BN - 1) / L::BN);
+    const int grid = tiles < sm_count ? tiles : sm_count;
+    kern<<<grid, 256, L::kTotal, stream>>>(a, b.one_sm, *ep.tm_h32, *ep.tm_hb, rows, row0, N, K,
+                                           ResidTmaArgs{ep.out_f32, ep.flag, ep.code});
+    return cudaGetLastError();
+  }
   // The CTA-pair kernel wins where its 256 x 256 tiles apply (the MLP-in
   // projection, 78 % of peak vs 60 % for 1-SM 128 x 128 tiles); for narrower
   // N the row-per-thread epilogue, not the MMA, bounds the kernel and the

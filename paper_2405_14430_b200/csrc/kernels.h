@@ -20,6 +20,10 @@ bool encode_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner,
                          uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
                          uint32_t box_outer, int swizzle_bytes);
 
+bool encode_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t inner,
+                        uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
+                        uint32_t box_outer, int swizzle_bytes);
+
 int device_sm_count(int device);
 
 enum class Epi : int { StoreF32 = 0, QKV = 1, Residual = 2, Tanh = 3 };
@@ -39,6 +43,10 @@ struct EpiParams {
   int hs = 0, dh = 0, dhp = 0, P = 0;
   int* flag = nullptr;
   int code = 0;
+  // Residual only: tensor maps over out_f32 (fp32, box 32 x 128, SW128) and
+  // out_bf16 (bf16, box 64 x 128, SW128) enable the TMA epilogue.
+  const CUtensorMap* tm_h32 = nullptr;
+  const CUtensorMap* tm_hb = nullptr;
 };
 
 // Tensor maps over a weight B [N x K] (K-major bf16) for both GEMM paths:

@@ -186,6 +186,8 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
     s.attn_work = need ? dalloc<float>(need) : nullptr;
   }
   s.tm_hb = tmap(s.hb, hs, P, hs * 2, 64, 128, 128);
+  if (!encode_tmap_f32_2d(&s.tm_h32, s.h32, hs, P, hs * 4, 32, 128, 128))
+    throw CudaError("cuTensorMapEncodeTiled failed for the residual stream");
   s.tm_attn = tmap(s.attn, hs, P, hs * 2, 64, 128, 128);
   s.tm_z = tmap(s.z, mlp, P, mlp * 2, 64, 128, 128);
   s.tm_q = tmap(s.q, dhp, heads * P, dhp * 2, 16, 128, 32);
@@ -304,6 +306,10 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
   res.ld = m.hs;
   res.flag = s.flag;
   res.code = code;
+  if (m.hs % 32 == 0) {
+    res.tm_h32 = &s.tm_h32;
+    res.tm_hb = &s.tm_hb;
+  }
   prof_begin(s, kGemmOut, 2 * r * hs * hs, 0);
   check(gemm(s.tm_attn, L.tm_wo, rows, row0, m.hs, m.hs, Epi::Residual, res,
              s.sm_count, s.stream), "gemm out-proj");

@@ -88,6 +88,7 @@ struct Stage {
   size_t attn_work_floats = 0;
   int* flag = nullptr;    // first non-finite (ordinal), INT_MAX if none
   CUtensorMap tm_hb, tm_attn, tm_z, tm_q;
+  CUtensorMap tm_h32;  // fp32 residual stream, box 32 x 128 (TMA epilogue)
   cudaEvent_t ev_fwd = nullptr;  // "rows sent to stage d+1"
   // stage 0 only
   float* x = nullptr;    // [P x hs] latent
