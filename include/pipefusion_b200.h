@@ -132,6 +132,12 @@ pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
 pf_status pf_make_initial_latent(uint64_t seed, int64_t seq_len, int hidden_size,
                                  double* out);
 
+/* CUDA graphs (default on): the first run of a given (latent buffer,
+ * steps, patches, warmup, eta, stream) is captured into a CUDA graph and
+ * later runs replay it -- one graph launch per image. Disabled automatically
+ * while profiling, on the legacy default stream, and across several devices. */
+pf_status pf_set_graphs(pf_ctx* ctx, int enabled);
+
 /* Per-kernel CUDA-event profile (no reference analogue). When enabled, every
  * kernel of subsequent runs is bracketed by events on its stage stream;
  * pf_kernel_profile() resolves the last run (call after it completed).

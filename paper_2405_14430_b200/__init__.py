@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
-    "pf_version", "pf_make_initial_latent", "pf_set_profiling", "pf_kernel_profile",
+    "pf_version", "pf_make_initial_latent", "pf_set_graphs", "pf_set_profiling", "pf_kernel_profile",
     "pf_debug_gemm", "pf_debug_attention", "pf_debug_attention_trace",
 ]
 
@@ -111,6 +111,7 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_version.restype = ctypes.c_char_p
     lib.pf_make_initial_latent.argtypes = [ctypes.c_uint64, i64, i32, dptr]
     lib.pf_set_profiling.argtypes = [vp, i32]
+    lib.pf_set_graphs.argtypes = [vp, i32]
     lib.pf_kernel_profile.argtypes = [vp, i32, dptr, ctypes.POINTER(i64), dptr, dptr]
     lib.pf_debug_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     lib.pf_debug_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
@@ -296,6 +297,9 @@ class ToyDiTCuda:
             ctypes.c_double(eta), ctypes.c_void_p(stream_ptr), ctypes.byref(st))
         _raise(status, self._err())
         return StalenessStats(st.fresh_patch_reads, st.stale_patch_reads, [])
+
+    def set_graphs(self, enabled: bool) -> None:
+        self._lib.pf_set_graphs(self._ctx, 1 if enabled else 0)
 
     def set_profiling(self, enabled: bool) -> None:
         self._lib.pf_set_profiling(self._ctx, 1 if enabled else 0)

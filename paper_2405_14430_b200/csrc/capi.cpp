@@ -221,8 +221,7 @@ pf_status pf_run_pipefusion(pf_ctx* ctx, const double* x_init, pf_layout layout,
     cudaGetDevice(&prev);
     cudaSetDevice(s0.device);
     struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
-    ctx->engine->enqueue_run(ctx->x_scratch, steps, patches, warmup, float(eta),
-                             s0.stream, &rs);
+    ctx->engine->run(ctx->x_scratch, steps, patches, warmup, float(eta), s0.stream, &rs);
     ctx->engine->finish(s0.stream);
     download_x(ctx, x_out, layout);
     export_stats(rs, stats);
@@ -236,8 +235,8 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
   return guarded(&ctx->last_error, [&] {
     if (!x_dev) throw pf::ValidationError("NULL latent pointer");
     pf::RunStats rs;
-    ctx->engine->enqueue_run(x_dev, steps, patches, warmup, float(eta),
-                             static_cast<cudaStream_t>(stream), &rs);
+    ctx->engine->run(x_dev, steps, patches, warmup, float(eta),
+                     static_cast<cudaStream_t>(stream), &rs);
     export_stats(rs, stats);
   });
 }
@@ -280,6 +279,12 @@ pf_status pf_make_initial_latent(uint64_t seed, int64_t seq_len, int hidden_size
     std::mt19937_64 rng(seed ^ 0x9e3779b97f4a7c15ULL);
     for (int64_t i = 0; i < seq_len * hidden_size; ++i) out[i] = next_uniform(rng);
   });
+}
+
+pf_status pf_set_graphs(pf_ctx* ctx, int enabled) {
+  if (!ctx) return PF_VALIDATION;
+  ctx->engine->set_graphs(enabled != 0);
+  return PF_OK;
 }
 
 pf_status pf_set_profiling(pf_ctx* ctx, int enabled) {

@@ -579,4 +579,206 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair residual GEMM with the TMA epilogue (256 x 128 pair tiles): the
+// 2-SM main loop of gemm2sm_bf16_tn_kernel and the smem residual epilogue of
+// gemm_resid_tma_kernel, each CTA handling its own 128 rows.
+template <int STAGES>
+struct Gemm2SmResSmem {
+  static constexpr int BN = 128;
+  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr uint32_t kBBytes = (BN / 2) * kGemmBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kCOff = STAGES * kStageBytes;
+  static constexpr uint32_t kDOff = kCOff + 4 * 16384;
+  static constexpr uint32_t kBarOffset = kDOff + 2 * 16384;
+  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;
+  static_assert(kTotal <= 232448, "2-SM residual GEMM smem budget");
+};
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm2sm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
+                             const __grid_constant__ CUtensorMap tma_b,
+                             const __grid_constant__ CUtensorMap tma_h32,
+                             const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
+                             int N, int K, ResidTmaArgs args) {
+  using L = Gemm2SmResSmem<STAGES>;
+  constexpr int BN = L::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sC = smem + L::kCOff;
+  uint8_t* sD = smem + L::kDOff;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* c_full = tempty + 2;
+  uint64_t* c_empty = c_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_empty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int m_tiles = rows / (2 * kGemmBM);
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tma_a);
+    ptx::prefetch_tmap(&tma_b);
+    ptx::prefetch_tmap(&tma_h32);
+    ptx::prefetch_tmap(&tma_hb);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2);
+    }
+    ptx::mbar_init(c_full, 1);
+    ptx::mbar_init(c_empty, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm<256>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t c_phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        const int my_row = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
+          ptx::tma_load_2d_2sm(sa, &tma_a, &full[stage], kb * kGemmBK, my_row);
+          ptx::tma_load_2d_2sm(sb, &tma_b, &full[stage], kb * kGemmBK,
+                               nt * BN + int(rank) * (BN / 2));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mbar_wait(c_empty, c_phase ^ 1);
+        ptx::mbar_arrive_expect_tx(c_full, 4 * 16384);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          ptx::tma_load_2d(sC + c * 16384, &tma_h32, c_full, nt * BN + 32 * c, my_row);
+        c_phase ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b_base = a_base + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k)
+            ptx::umma2_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
+                               ptx::desc_kmajor_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+          ptx::umma2_commit_mc(&empty[stage], 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma2_commit_mc(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = 32 * q + int(lane);
+    const uint32_t sw = uint32_t(r & 7);
+    const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    uint32_t c_phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      const int mt = tile % m_tiles;
+      const int nt = tile / m_tiles;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::mbar_wait(c_full, c_phase);
+      ptx::tc_fence_after();
+      bool bad = false;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, v);
+        ptx::tmem_wait_ld();
+        uint8_t* crow = sC + c * 16384 + r * 128;
+        uint8_t* drow = sD + (c >> 1) * 16384 + r * 128;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float4* pc = reinterpret_cast<float4*>(crow + ((uint32_t(g) ^ sw) << 4));
+          float4 x = *pc;
+          x.x += __uint_as_float(v[4 * g + 0]);
+          x.y += __uint_as_float(v[4 * g + 1]);
+          x.z += __uint_as_float(v[4 * g + 2]);
+          x.w += __uint_as_float(v[4 * g + 3]);
+          *pc = x;
+          bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+          const uint32_t byte = uint32_t(64 * (c & 1) + 8 * g);
+          uint2* pd = reinterpret_cast<uint2*>(drow + ((((byte >> 4) ^ sw) << 4) | (byte & 15)));
+          *pd = make_uint2(ptx::pack_bf16x2(x.x, x.y), ptx::pack_bf16x2(x.z, x.w));
+        }
+      }
+      if (bad && args.flag) atomicMin(args.flag, args.code);
+      ptx::tc_fence_before();
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (warp == 4 && lane == 0) {
+        ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        const int gr = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tma_store_2d(&tma_h32, sC + c * 16384, nt * BN + 32 * c, gr);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) ptx::tma_store_2d(&tma_hb, sD + c * 16384, nt * BN + 64 * c, gr);
+        ptx::tma_store_commit();
+        ptx::tma_store_wait_read();
+        ptx::mbar_arrive(c_empty);
+      }
+      c_phase ^= 1;
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<256>(tmem_base);
+  }
+}
+
 }  // namespace pf

@@ -316,13 +316,31 @@ bool make_weight_maps(WeightMaps* maps, const bf16* w, int N, int K) {
   return encode_tmap_bf16_2d(&maps->one_sm, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
                              uint32_t(gemm_bn_1sm(N)), 128) &&
          encode_tmap_bf16_2d(&maps->two_sm, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
-                             uint32_t(gemm_bn_2sm(N) / 2), 128);
+                             uint32_t(gemm_bn_2sm(N) / 2), 128) &&
+         encode_tmap_bf16_2d(&maps->two_sm_128, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
+                             64, 128);
 }
 
 cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  int N, int K, Epi kind, const EpiParams& ep, int sm_count,
                  cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
+  if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % (2 * kGemmBM) == 0 &&
+      N % 32 == 0 && sm_count >= 2 && K >= 2048) {
+    // long-K residual GEMM (MLP-out): CTA pairs halve the per-SM smem
+    // operand traffic of the main loop
+    constexpr int kStages = 5;
+    using L = Gemm2SmResSmem<kStages>;
+    constexpr auto kern = gemm2sm_resid_tma_kernel<kStages>;
+    cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
+    if (e != cudaSuccess) return e;
+    const int tiles = (rows / (2 * kGemmBM)) * ((N + L::BN - 1) / L::BN);
+    const int pairs = sm_count / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    kern<<<grid, 256, L::kTotal, stream>>>(a, b.two_sm_128, *ep.tm_h32, *ep.tm_hb, rows, row0, N, K,
+                                           ResidTmaArgs{ep.out_f32, ep.flag, ep.code});
+    return cudaGetLastError();
+  }
   if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % kGemmBM == 0 && N % 32 == 0 &&
       gemm_bn_1sm(N) == 128) {
     constexpr int kStages = 4;

@@ -54,6 +54,7 @@ struct EpiParams {
 struct WeightMaps {
   CUtensorMap one_sm;
   CUtensorMap two_sm;
+  CUtensorMap two_sm_128;  // box 64 x 64: CTA-pair tiles of N = 128 (residual GEMMs)
 };
 int gemm_bn_1sm(int N);
 int gemm_bn_2sm(int N);

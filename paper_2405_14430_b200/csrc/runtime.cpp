@@ -146,6 +146,12 @@ Engine::Engine(const ModelShape& shape_in, const std::vector<int>& devices)
 }
 
 Engine::~Engine() {
+  if (ev_start_) {
+    DeviceGuard g(stages_[0].device);
+    cudaEventDestroy(ev_start_);
+  }
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   for (size_t d = 0; d < prof_pool_.size() && d < stages_.size(); ++d) {
     DeviceGuard g(stages_[d].device);
     for (cudaEvent_t e : prof_pool_[d]) cudaEventDestroy(e);
@@ -418,19 +424,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     throw ValidationError(os.str());
   }
   Stage& s0 = stages_[0];
-  if (n > 1 && !s0.eps) {
-    DeviceGuard g(s0.device);
-    s0.eps = dalloc<float>(size_t(m.P) * m.hs);
-  }
-  if (n == 1) s0.eps = s0.h32;
-  if (int(s0.ev_eps.size()) < patches) {
-    DeviceGuard g(stages_[size_t(n - 1)].device);
-    while (int(s0.ev_eps.size()) < patches) {
-      cudaEvent_t e;
-      PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      s0.ev_eps.push_back(e);
-    }
-  }
+  prepare_run(patches);
 
   // Host bookkeeping: StageBuffers::src (execute.cpp:38-49), sentinel = steps.
   std::vector<std::vector<std::vector<int>>> src(static_cast<size_t>(n));
@@ -448,10 +442,9 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
   prof_used_.assign(stages_.size(), 0);
 
   // Fork: every stage stream waits for the caller's prior work.
-  cudaEvent_t ev_start;
+  cudaEvent_t ev_start = ev_start_;
   {
     DeviceGuard g(s0.device);
-    PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
     PF_CUDA_CHECK(cudaEventRecord(ev_start, caller));
   }
   for (Stage& s : stages_) {
@@ -470,11 +463,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       }
     }
   }
-  {
-    DeviceGuard g(s0.device);
-    cudaEventDestroy(ev_start);
-  }
-
   auto next_code = [&](int t, int layer) {
     codes_.emplace_back(t, layer);
     return int(codes_.size()) - 1;
@@ -584,6 +572,69 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     DeviceGuard g0(s0.device);
     PF_CUDA_CHECK(cudaStreamWaitEvent(caller, s.ev_fwd, 0));
   }
+}
+
+// Allocations and events a run needs, created outside any stream capture.
+void Engine::prepare_run(int patches) {
+  const int n = stage_count();
+  Stage& s0 = stages_[0];
+  if (!ev_start_) {
+    DeviceGuard g(s0.device);
+    PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+  }
+  if (n > 1 && !s0.eps) {
+    DeviceGuard g(s0.device);
+    s0.eps = dalloc<float>(size_t(shape_.P) * shape_.hs);
+  }
+  if (n == 1) s0.eps = s0.h32;
+  if (int(s0.ev_eps.size()) < patches) {
+    DeviceGuard g(stages_[size_t(n - 1)].device);
+    while (int(s0.ev_eps.size()) < patches) {
+      cudaEvent_t e;
+      PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s0.ev_eps.push_back(e);
+    }
+  }
+}
+
+void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
+                 cudaStream_t caller, RunStats* stats) {
+  if (patches >= 1) prepare_run(patches);
+  bool single_device = true;
+  for (const Stage& s : stages_) single_device &= s.device == stages_[0].device;
+  if (!graphs_enabled_ || profiling_ || caller == nullptr || !single_device) {
+    enqueue_run(x_dev, steps, patches, warmup, eta, caller, stats);
+    return;
+  }
+  uint32_t eta_bits;
+  std::memcpy(&eta_bits, &eta, sizeof(eta_bits));
+  const GraphKey key{x_dev, steps, patches, warmup, eta_bits, caller};
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
+    GraphEntry e;
+    DeviceGuard g(stages_[0].device);
+    PF_CUDA_CHECK(cudaStreamBeginCapture(caller, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t graph = nullptr;
+    try {
+      enqueue_run(x_dev, steps, patches, warmup, eta, caller, &e.stats);
+    } catch (...) {
+      cudaStreamEndCapture(caller, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    PF_CUDA_CHECK(cudaStreamEndCapture(caller, &graph));
+    cudaError_t err = cudaGraphInstantiate(&e.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    PF_CUDA_CHECK(err);
+    e.launches = launches_;
+    e.codes = codes_;
+    it = graphs_.emplace(key, std::move(e)).first;
+  }
+  DeviceGuard g(stages_[0].device);
+  PF_CUDA_CHECK(cudaGraphLaunch(it->second.exec, caller));
+  launches_ = it->second.launches;
+  codes_ = it->second.codes;
+  if (stats) *stats = it->second.stats;
 }
 
 void Engine::finish(cudaStream_t caller) {

@@ -19,7 +19,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <stdexcept>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -135,6 +137,13 @@ class Engine {
   // Enqueue a full PipeFusion run on a device latent (stage 0's device).
   void enqueue_run(float* x_dev, int steps, int patches, int warmup, float eta,
                    cudaStream_t caller, RunStats* stats);
+  // Same as enqueue_run, replayed from a CUDA graph captured on first use
+  // for this (latent, schedule, stream): one launch per image instead of
+  // thousands. Falls back to enqueue_run when profiling, on the legacy
+  // default stream, or when stages span several devices.
+  void run(float* x_dev, int steps, int patches, int warmup, float eta,
+           cudaStream_t caller, RunStats* stats);
+  void set_graphs(bool on) { graphs_enabled_ = on; }
   // Synchronise every stage and raise deferred numeric errors.
   void finish(cudaStream_t caller);
 
@@ -154,6 +163,8 @@ class Engine {
   void free_stage(Stage& s);
   void layer_forward(Stage& s, int lf, int rows, int row0, int code);
   void send_rows(int from, int row0, int rows);
+  void prepare_run(int patches);
+  cudaEvent_t ev_start_ = nullptr;
   int stage_of_layer(int layer) const;
 
   struct ProfRec {
@@ -165,6 +176,16 @@ class Engine {
   void prof_begin(Stage& s, int kind, double flops, double bytes);
   void prof_end(Stage& s);
   cudaEvent_t prof_event(int stage);
+
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    RunStats stats;
+    int64_t launches = 0;
+    std::vector<std::pair<int, int>> codes;
+  };
+  using GraphKey = std::tuple<float*, int, int, int, uint32_t, cudaStream_t>;
+  std::map<GraphKey, GraphEntry> graphs_;
+  bool graphs_enabled_ = true;
 
   bool profiling_ = false;
   std::vector<ProfRec> prof_;
