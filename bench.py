@@ -57,6 +57,13 @@ CONFIGS = {
     "c3": dict(name="PixArt-alpha-shaped DiT 2048px (28 layers, hidden 1152, 16 heads, "
                     "16384 tokens), 20 steps, 1 warmup",
                L=28, hs=1152, heads=16, p=16384, S=20, W=1),
+    "c2px": dict(name="PixArt-alpha DiT block variant 1024px (28 layers, hidden 1152, 16 heads, "
+                      "4096 tokens, 120 text tokens; adaLN-single + LayerNorm, cross-attention, "
+                      "GELU MLP), 20 steps, 1 warmup",
+                 L=28, hs=1152, heads=16, p=4096, S=20, W=1, block="pixart", T=120),
+    "c3px": dict(name="PixArt-alpha DiT block variant 2048px (28 layers, hidden 1152, 16 heads, "
+                      "16384 tokens, 120 text tokens), 20 steps, 1 warmup",
+                 L=28, hs=1152, heads=16, p=16384, S=20, W=1, block="pixart", T=120),
     "c1": dict(name="tiny DiT (4 layers, hidden 128, 4 heads, 256 tokens), 5 steps, 1 warmup",
                L=4, hs=128, heads=4, p=256, S=5, W=1),
     "cref": dict(name="reference_execute.cfg (4 layers, hidden 32, 4 heads, 64 tokens), 20 "
@@ -68,6 +75,12 @@ def flops_per_image(c, mlp):
     """The reference's ComputeModel (simulate.cpp:30-44) for mlp_ratio 4:
     S * L * (24 p hs^2 + 4 p^2 hs); generalised to mlp = 4 hs."""
     p, hs = c["p"], c["hs"]
+    if c.get("block") == "pixart":
+        # QKV 6, out 2, cross-q 2, cross-out 2 (x p hs^2), MLP 4 p hs mlp, self- and
+        # cross-attention 4 p (p + T) hs per step and layer; text K/V once per image
+        T = c["T"]
+        return (c["S"] * c["L"] * (12 * p * hs * hs + 4 * p * hs * mlp + 4 * p * (p + T) * hs)
+                + c["L"] * 4 * T * hs * hs)
     return c["S"] * c["L"] * (8 * p * hs * hs + 4 * p * hs * mlp + 4 * p * p * hs)
 
 
@@ -140,11 +153,47 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline
+def cpu_port_baseline_pixart(c, budget_s=20.0, sample_rows=32):
+    """PixArt block: the reference has no such block, so the CPU baseline is
+    the fp64 oracle port (oracle/px_oracle.c, scalar, one layer unit per host
+    thread) on sampled 32-row units at the true shape, extrapolated."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import loader
+    if not loader.RESTATEMENT_LIB.exists():
+        loader.build(reference=False)
+    o = loader.PixArtOracle(0, 1, c["hs"], c["heads"], 4.0, c["T"])
+    cores = min(os.cpu_count() or 1, 64)
+    rng = np.random.default_rng(0)
+    k = rng.uniform(-1, 1, (c["p"], c["hs"]))
+    v = rng.uniform(-1, 1, (c["p"], c["hs"]))
+
+    def one(i):
+        h = np.random.default_rng(i).uniform(-1, 1, (sample_rows, c["hs"]))
+        o.layer_forward(0, i % c["S"], c["S"], h, k, v, (i * sample_rows) % c["p"])
+        return 1
+
+    done, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        while True:
+            done += sum(ex.map(one, range(done, done + cores)))
+            if time.perf_counter() - t0 > budget_s * 0.5 or done >= 4 * cores:
+                break
+    wall = time.perf_counter() - t0
+    samples_per_image = c["S"] * c["L"] * (c["p"] / sample_rows)
+    return {"value": wall / done * samples_per_image, "unit": UNIT, "cores": cores,
+            "kind": "port",
+            "sample": (f"{done} PixArt-block layer units of {sample_rows} query rows x "
+                       f"{c['p']}-row K/V (oracle/px_oracle.c fp64, {cores} threads in "
+                       f"{wall:.1f}s); extrapolated x{samples_per_image:.0f} units/image")}
+
+
 def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
     """Time the reference's own toy_layer_forward (oracle/_ref, built from
     /root/reference) at the true shape on `sample_rows` query rows against a
     full p-row K/V buffer, one sample per host core in parallel, and
     extrapolate to one image: S * L * (p / sample_rows) samples."""
+    if c.get("block") == "pixart":
+        return cpu_port_baseline_pixart(c, budget_s, sample_rows)
     from concurrent.futures import ThreadPoolExecutor
     from oracle import loader
     if not loader.REFERENCE_LIB.exists():
@@ -194,7 +243,10 @@ def run_ours(args, c, world, rank):
         torch.cuda.set_device(0)
         devices = list(range(n))
         t_build = time.perf_counter()
-        model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
+        if c.get("block") == "pixart":
+            model = pf.PixArtCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n, devices)
+        else:
+            model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
         t_build = time.perf_counter() - t_build
         mlp = model.mlp_hidden
         x0 = pf.make_initial_latent(0, c["p"], c["hs"])
@@ -253,8 +305,10 @@ def run_ours(args, c, world, rank):
         model.synchronize(sp)
     prof = model.kernel_profile()
     model.set_profiling(False)
-    gemm_kinds = ["gemm_qkv", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out"]
-    dom = max((k for k in prof if k != "sampler"), key=lambda k: prof[k]["ms"])
+    gemm_kinds = ["gemm_qkv", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out", "gemm_cross_q",
+                  "gemm_cross_out"]
+    dom = max((k for k in prof if k not in ("sampler", "conditioning")),
+              key=lambda k: prof[k]["ms"])
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     kernels = {}
     for k, d in prof.items():
@@ -294,6 +348,7 @@ def run_ours(args, c, world, rank):
                    "l2": "working set > L2 (0.9 GB bf16 weights + 0.6 GB K/V per image "
                          "pass), no explicit flush"},
         "tc_frac_image": total_flops / sec_per_image / 1e12 / peak_tf,
+        "block": c.get("block", "toy"),
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": c["p"] * c["hs"] * 4,
                 "d2h_bytes_per_step": c["p"] * c["hs"] * 4,
                 "api": "pf_run_pipefusion (C ABI, fp64 host latent in/out)"},

@@ -84,6 +84,22 @@ pf_status pf_create(const pf_model_desc* desc, const double* const* weights,
                     const double* condition_bias, pf_layout layout,
                     const int* devices, int n_stages, pf_ctx** out);
 
+/* PixArt-alpha block variant (no reference analogue:
+ * the reference's only block is the toy block of toy_model.cpp:145-177).
+ * Same executor and schedule as pf_create_toy (run_pipefusion's loop,
+ * execute.cpp:167-223) with the block replaced by adaLN-single modulate +
+ * LayerNorm, self-attention over the stale/fresh K/V buffer, cross-attention
+ * over `text_tokens` text tokens, and a GELU(tanh) MLP. Parameters and text
+ * tokens are generated from `seed` as oracle/px_oracle.c (pxo_build) states. */
+pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                           const int* devices, int n_stages, pf_ctx** out);
+
+/* Replace the text tokens y [tokens x hidden_size] of a PixArt model. */
+pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout layout);
+
+/* 0 = toy block, 1 = PixArt block, -1 = NULL context. */
+int pf_block_kind(const pf_ctx* ctx);
+
 void pf_destroy(pf_ctx* ctx);
 
 /* Message of the last failure on this context (or of the last failed
@@ -126,6 +142,13 @@ pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
                            int64_t row0, double* k_buf, double* v_buf,
                            pf_layout layout);
 
+/* pf_layer_forward with the block conditioned on timestep index `timestep`
+ * of a `steps`-step run (PixArt block; for the toy block it equals
+ * pf_layer_forward). */
+pf_status pf_layer_forward_t(pf_ctx* ctx, int layer, int timestep, int steps, double* h,
+                             int64_t rows, int64_t row0, double* k_buf, double* v_buf,
+                             pf_layout layout);
+
 /* ditsim::make_initial_latent(seed, seq_len, hidden_size) -- execute.hpp:56-57,
  * toy_model.cpp:84-91 (host, bit-exact mt19937_64 stream). out: row-major
  * [seq_len x hidden_size]. */
@@ -142,7 +165,10 @@ pf_status pf_set_graphs(pf_ctx* ctx, int enabled);
  * kernel of subsequent runs is bracketed by events on its stage stream;
  * pf_kernel_profile() resolves the last run (call after it completed).
  * kind: 0 QKV GEMM, 1 attention, 2 out-proj GEMM, 3 MLP-in GEMM,
- * 4 MLP-out GEMM, 5 sampler/patch kernels. flops/bytes are algorithmic. */
+ * 4 MLP-out GEMM, 5 sampler/patch kernels; PixArt block only: 6 cross-attention
+ * query GEMM, 7 cross-attention, 8 cross-attention out-proj GEMM,
+ * 9 conditioning (timestep embedding, adaLN, LayerNorm fold, text K/V).
+ * flops/bytes are algorithmic. */
 pf_status pf_set_profiling(pf_ctx* ctx, int enabled);
 pf_status pf_kernel_profile(pf_ctx* ctx, int kind, double* total_ms,
                             int64_t* launches, double* flops, double* bytes);

@@ -269,3 +269,103 @@ class Reference(_Impl):
         if rc:
             raise OracleError(rc, err.value.decode())
         return out
+
+
+# ---------------------------------------------------------------- PixArt block
+PXO_PARAMS = ["wqkv", "bqkv", "wo", "bo", "wqc", "bqc", "wkc", "bkc", "wvc", "bvc", "woc",
+              "boc", "w1", "b1", "w2", "b2", "sst"]
+PXO_GLOBALS = ["wt1", "bt1", "wt2", "bt2", "wt0", "bt0", "cb", "y"]
+
+
+class PixArtOracle:
+    """fp64 PixArt-alpha block variant under the reference schedule
+    (oracle/px_oracle.c). Row-major float64 numpy in and out."""
+
+    def __init__(self, seed, layers, hs, heads, mlp_ratio, text_tokens,
+                 path: Optional[Path] = None):
+        p = path or RESTATEMENT_LIB
+        if not p.exists():
+            raise FileNotFoundError(f"{p} missing: run `make -C oracle`")
+        self.lib = lib = ctypes.CDLL(str(p))
+        lib.pxo_build.restype = ctypes.c_void_p
+        lib.pxo_build.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_double, ctypes.c_int]
+        lib.pxo_free.argtypes = [ctypes.c_void_p]
+        lib.pxo_mlp_hidden.argtypes = [ctypes.c_void_p]
+        lib.pxo_param.restype = _d
+        lib.pxo_param.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        lib.pxo_global.restype = _d
+        lib.pxo_global.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.pxo_set_text.argtypes = [ctypes.c_void_p, _d]
+        lib.pxo_tvec.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _d]
+        lib.pxo_layer_forward.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, _d, ctypes.c_int64, _d, _d,
+                                          ctypes.c_int64, ctypes.c_int64]
+        lib.pxo_serial.argtypes = [ctypes.c_void_p, _d, ctypes.c_int64, ctypes.c_int,
+                                   ctypes.c_double, _d, ctypes.c_char_p, ctypes.c_int]
+        lib.pxo_pipefusion.argtypes = [ctypes.c_void_p, _d, ctypes.c_int64, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                       _d, _i64p, _i64p, ctypes.c_char_p, ctypes.c_int]
+        self.h = lib.pxo_build(seed, layers, hs, heads, mlp_ratio, text_tokens)
+        if not self.h:
+            raise OracleError(2, "invalid PixArt model shape")
+        self.layers, self.hs, self.heads, self.T = layers, hs, heads, text_tokens
+        self.mlp = lib.pxo_mlp_hidden(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.pxo_free(self.h)
+            self.h = None
+
+    def _shape(self, name):
+        hs, mlp, T = self.hs, self.mlp, self.T
+        return {"wqkv": (hs, 3 * hs), "bqkv": (3 * hs,), "w1": (hs, mlp), "b1": (mlp,),
+                "w2": (mlp, hs), "sst": (6, hs), "wt1": (256, hs), "wt2": (hs, hs),
+                "wt0": (hs, 6 * hs), "bt0": (6 * hs,), "y": (T, hs)}.get(
+                    name, (hs, hs) if name.startswith("w") else (hs,))
+
+    def param(self, layer: int, name: str) -> np.ndarray:
+        shp = self._shape(name)
+        ptr = self.lib.pxo_param(self.h, layer, PXO_PARAMS.index(name))
+        return np.ctypeslib.as_array(ptr, shape=shp).copy()
+
+    def glob(self, name: str) -> np.ndarray:
+        shp = self._shape(name)
+        ptr = self.lib.pxo_global(self.h, PXO_GLOBALS.index(name))
+        return np.ctypeslib.as_array(ptr, shape=shp).copy()
+
+    def set_text(self, y):
+        y = _c(y)
+        self.lib.pxo_set_text(self.h, _p(y))
+
+    def tvec(self, t: int, steps: int) -> np.ndarray:
+        out = np.empty(6 * self.hs)
+        self.lib.pxo_tvec(self.h, t, steps, _p(out))
+        return out
+
+    def layer_forward(self, layer, t, steps, h, k, v, row0):
+        h, k, v = _c(h).copy(), _c(k).copy(), _c(v).copy()
+        self.lib.pxo_layer_forward(self.h, layer, t, steps, _p(h), h.shape[0], _p(k), _p(v),
+                                   k.shape[0], row0)
+        return h, k, v
+
+    def serial_reference(self, x, steps, eta):
+        x = _c(x)
+        out = np.empty_like(x)
+        err = ctypes.create_string_buffer(256)
+        rc = self.lib.pxo_serial(self.h, _p(x), x.shape[0], steps, eta, _p(out), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out
+
+    def run_pipefusion(self, x, steps, workers, patches, warmup, eta):
+        x = _c(x)
+        out = np.empty_like(x)
+        fresh, stale = ctypes.c_int64(), ctypes.c_int64()
+        err = ctypes.create_string_buffer(256)
+        rc = self.lib.pxo_pipefusion(self.h, _p(x), x.shape[0], steps, workers, patches,
+                                     warmup, eta, _p(out), ctypes.byref(fresh),
+                                     ctypes.byref(stale), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return out, (fresh.value, stale.value)

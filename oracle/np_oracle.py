@@ -89,3 +89,86 @@ def random_model(rng, L, hs, mlp):
     layers = [(u(hs, hs) * s, u(hs, hs) * s, u(hs, hs) * s, u(hs, hs) * s,
                u(hs, mlp) * s, u(mlp, hs) * s) for _ in range(L)]
     return layers, u(hs)
+
+
+# ---------------------------------------------------------------- PixArt block
+# Independent numpy restatement of oracle/px_oracle.c (same spec, vectorised),
+# used to cross-check the C oracle before it is trusted as the GPU checker.
+def px_tvec(g, t, steps, hs):
+    tau = 1000.0 * t / steps
+    f = np.exp(-np.log(10000.0) * np.arange(128) / 128.0)
+    sin_ = np.concatenate([np.cos(tau * f), np.sin(tau * f)])
+    silu = lambda a: a / (1.0 + np.exp(-a))  # noqa: E731
+    e1 = silu(sin_ @ g["wt1"] + g["bt1"])
+    temb = e1 @ g["wt2"] + g["bt2"]
+    return silu(temb) @ g["wt0"] + g["bt0"]
+
+
+def _ln_mod(h, shift, scale):
+    mu = h.mean(axis=1, keepdims=True)
+    var = ((h - mu) ** 2).mean(axis=1, keepdims=True)
+    return (h - mu) / np.sqrt(var + 1e-6) * (1.0 + scale) + shift
+
+
+def _gelu_tanh(x):
+    return 0.5 * x * (1.0 + np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def px_layer_forward(p, heads, mod, h, k_buf, v_buf, row0, y):
+    """p: dict of one layer's parameters; mod = sst + tv [6 hs]; y text tokens."""
+    hs = h.shape[1]
+    sh1, sc1, g1, sh2, sc2, g2 = (mod[i * hs:(i + 1) * hs] for i in range(6))
+    r = h.shape[0]
+    a = _ln_mod(h, sh1, sc1)
+    qkv = a @ p["wqkv"] + p["bqkv"]
+    k_buf[row0:row0 + r] = qkv[:, hs:2 * hs]
+    v_buf[row0:row0 + r] = qkv[:, 2 * hs:]
+    h = h + g1 * (attention_rows(qkv[:, :hs], k_buf, v_buf, heads) @ p["wo"] + p["bo"])
+    kc = y @ p["wkc"] + p["bkc"]
+    vc = y @ p["wvc"] + p["bvc"]
+    qc = h @ p["wqc"] + p["bqc"]
+    h = h + attention_rows(qc, kc, vc, heads) @ p["woc"] + p["boc"]
+    z = _gelu_tanh(_ln_mod(h, sh2, sc2) @ p["w1"] + p["b1"])
+    return h + g2 * (z @ p["w2"] + p["b2"])
+
+
+def px_pipefusion(o, x, steps, patches, warmup, eta):
+    """Vectorised mirror of px_oracle.c pxo_pipefusion for an oracle model `o`
+    (loader.PixArtOracle): same loop, numpy matmuls (not bit-exact with C)."""
+    L, hs, heads = o.layers, o.hs, o.heads
+    g = {n: o.glob(n) for n in ("wt1", "bt1", "wt2", "bt2", "wt0", "bt0", "cb", "y")}
+    prm = [{n: o.param(l, n) for n in ("wqkv", "bqkv", "wo", "bo", "wqc", "bqc", "wkc", "bkc",
+                                       "wvc", "bvc", "woc", "boc", "w1", "b1", "w2", "b2",
+                                       "sst")} for l in range(L)]
+    p = x.shape[0]
+    r = p // patches
+    x = np.array(x, dtype=np.float64)
+    kb = [np.zeros((p, hs)) for _ in range(L)]
+    vb = [np.zeros((p, hs)) for _ in range(L)]
+    for w in range(warmup):
+        t = steps - 1 - w
+        tv = px_tvec(g, t, steps, hs)
+        h = x + g["cb"]
+        for l in range(L):
+            h = px_layer_forward(prm[l], heads, prm[l]["sst"].reshape(-1) + tv, h, kb[l], vb[l],
+                                 0, g["y"])
+        x = x - eta * h
+    steady = steps - warmup
+    pending = np.zeros_like(x)
+    eps = np.zeros_like(x)
+    for q in range(steady):
+        t = steady - 1 - q
+        tv = px_tvec(g, t, steps, hs)
+        for j in range(patches):
+            sl = slice(j * r, (j + 1) * r)
+            if q > 0:
+                x[sl] = x[sl] - eta * pending[sl]
+            h = x[sl] + g["cb"]
+            for l in range(L):
+                h = px_layer_forward(prm[l], heads, prm[l]["sst"].reshape(-1) + tv, h, kb[l],
+                                     vb[l], j * r, g["y"])
+            eps[sl] = h
+        pending = eps.copy()
+    if steady > 0:
+        x = x - eta * pending
+    return x

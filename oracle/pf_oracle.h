@@ -71,6 +71,31 @@ int pfo_schedule(int n, int m, int steps, int warmup, int* patch, int* timestep,
 /* fresh_area_series, freshness.cpp:64-75 */
 int pfo_fresh_series(int n, int m, int steps, int warmup, double* out, int cap);
 
+
+/* ---- PixArt-alpha block variant (px_oracle.c) ---- */
+typedef struct pxo_model pxo_model;
+/* Parameter ids per layer (x.W orientation, [in x out] row-major). */
+enum {
+  PXO_WQKV = 0, PXO_BQKV, PXO_WO, PXO_BO, PXO_WQC, PXO_BQC, PXO_WKC, PXO_BKC, PXO_WVC,
+  PXO_BVC, PXO_WOC, PXO_BOC, PXO_W1, PXO_B1, PXO_W2, PXO_B2, PXO_SST
+};
+pxo_model* pxo_build(uint64_t seed, int layers, int hs, int heads, double mlp_ratio, int T);
+void pxo_free(pxo_model* m);
+int pxo_mlp_hidden(const pxo_model* m);
+const double* pxo_param(const pxo_model* m, int layer, int id);
+/* 0 wt1 [256 x hs], 1 bt1, 2 wt2 [hs x hs], 3 bt2, 4 wt0 [hs x 6hs], 5 bt0,
+ * 6 condition_bias [hs], 7 text tokens y [T x hs] */
+const double* pxo_global(const pxo_model* m, int id);
+void pxo_set_text(pxo_model* m, const double* y);
+void pxo_tvec(const pxo_model* m, int t, int steps, double* tv);
+void pxo_layer_forward(const pxo_model* m, int layer, int t, int steps, double* h,
+                       int64_t rows, double* kbuf, double* vbuf, int64_t p, int64_t row0);
+int pxo_serial(const pxo_model* m, const double* x, int64_t p, int steps, double eta,
+               double* out, char* err, int cap);
+int pxo_pipefusion(const pxo_model* m, const double* x, int64_t p, int steps, int workers,
+                   int patches, int warmup, double eta, double* out, int64_t* fresh,
+                   int64_t* stale, char* err, int cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,14 +25,15 @@ import numpy as np
 __all__ = [
     "LIB_PATH", "load_library", "ValidationError", "NumericError", "CudaError",
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
-    "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS",
+    "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
 
 # Every symbol declared in include/pipefusion_b200.h and pipefusion_b200_debug.h.
 EXPORTED_SYMBOLS = [
-    "pf_create_toy", "pf_create", "pf_destroy", "pf_last_error",
+    "pf_create_toy", "pf_create", "pf_create_pixart", "pf_set_text", "pf_block_kind",
+    "pf_layer_forward_t", "pf_destroy", "pf_last_error",
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
@@ -41,7 +42,7 @@ EXPORTED_SYMBOLS = [
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
-                "sampler"]
+                "sampler", "gemm_cross_q", "cross_attention", "gemm_cross_out", "conditioning"]
 
 PF_OK, PF_NUMERIC, PF_VALIDATION, PF_CUDA = 0, 1, 2, 3
 PF_ROW_MAJOR, PF_COL_MAJOR = 0, 1
@@ -91,6 +92,11 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
                                   ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
     lib.pf_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(dptr), dptr, i32,
                               ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_create_pixart.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32,
+                                     ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_set_text.argtypes = [vp, dptr, i64, i32]
+    lib.pf_block_kind.argtypes = [vp]
+    lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
     lib.pf_destroy.argtypes = [vp]
     lib.pf_destroy.restype = None
     lib.pf_last_error.argtypes = [vp]
@@ -179,7 +185,7 @@ class ToyDiTCuda:
 
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, workers: int = 1,
-                 devices: Optional[Sequence[int]] = None, _weights=None):
+                 devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         self.layers, self.hidden_size, self.heads = layers, hidden_size, heads
@@ -190,7 +196,11 @@ class ToyDiTCuda:
         if len(devs) != workers:
             raise ValidationError("devices must list one CUDA device per worker")
         dev_arr = (ctypes.c_int * max(1, workers))(*devs)
-        if _weights is None:
+        if _text_tokens:
+            st = self._lib.pf_create_pixart(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                            _text_tokens, dev_arr, workers,
+                                            ctypes.byref(self._ctx))
+        elif _weights is None:
             st = self._lib.pf_create_toy(ctypes.c_uint64(seed), ctypes.byref(desc),
                                          dev_arr, workers, ctypes.byref(self._ctx))
         else:
@@ -318,3 +328,35 @@ class ToyDiTCuda:
 
     def synchronize(self, stream_ptr: int = 0) -> None:
         _raise(self._lib.pf_synchronize(self._ctx, ctypes.c_void_p(stream_ptr)), self._err())
+
+
+class PixArtCuda(ToyDiTCuda):
+    """The PixArt-alpha block variant under the same
+    PipeFusion executor: adaLN-single modulation, LayerNorm folded through the
+    GEMMs, self-attention over the stale/fresh K/V buffer, cross-attention over
+    `text_tokens` text tokens, GELU(tanh) MLP. Parameters and text come from
+    `seed` as oracle/px_oracle.c (pxo_build) specifies."""
+
+    def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
+                 mlp_ratio: float, seq_len: int, text_tokens: int, workers: int = 1,
+                 devices: Optional[Sequence[int]] = None):
+        if text_tokens < 1:
+            raise ValidationError("PixArt block needs at least one text token")
+        self.text_tokens = text_tokens
+        super().__init__(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers,
+                         devices, _text_tokens=text_tokens)
+
+    def set_text(self, y) -> None:
+        y = _f64c(y)
+        _raise(self._lib.pf_set_text(self._ctx, _dptr(y), y.shape[0], PF_ROW_MAJOR),
+               self._err())
+
+    def layer_forward_t(self, layer: int, t: int, steps: int, h, k_buf, v_buf, row0: int):
+        """One PixArt block at timestep index t of a `steps`-step run; (h, k, v)."""
+        h = _f64c(h).copy()
+        k = _f64c(k_buf).copy()
+        v = _f64c(v_buf).copy()
+        status = self._lib.pf_layer_forward_t(self._ctx, layer, t, steps, _dptr(h), h.shape[0],
+                                              row0, _dptr(k), _dptr(v), PF_ROW_MAJOR)
+        _raise(status, self._err())
+        return h, k, v

@@ -65,7 +65,8 @@ struct AttnSmem {
 __host__ __device__ constexpr int attn_tiles_per_cta(int /*dhp*/) { return 2; }
 
 struct AttnParams {
-  int P;            // kv rows in the buffer (= sequence length)
+  int P;            // kv rows per head in the K/V buffers (= sequence length)
+  int q_stride;     // rows per head of the Q buffer (= P for self-attention)
   int rows;         // query rows this launch
   int row0;         // first query row
   int heads, dh, hs;
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     if constexpr (NT == 2) ptx::setmaxnreg_dec<56>();
     if (warp == 0 && lane == 0) {
       // ------------------------------------------------------------ TMA
-      const int qrow = head * prm.P + prm.row0 + qt * (NT * kAttnBM);
+      const int qrow = head * prm.q_stride + prm.row0 + qt * (NT * kAttnBM);
       ptx::mbar_arrive_expect_tx(q_full, NT * L::kTileBytes);
 #pragma unroll
       for (int t = 0; t < NT; ++t)

@@ -167,6 +167,76 @@ pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
   });
 }
 
+pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                           const int* devices, int n_stages, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.block = pf::kBlockPixArt;
+    s.T = text_tokens;
+    ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    // Parameter stream of the PixArt block variant (oracle/px_oracle.c,
+    // pxo_build): one mt19937_64 seeded with seed ^ "PIXART-A", per layer the
+    // 17 parameters in PXO_* order, then the timestep-embedder weights and
+    // the condition bias; text tokens from seed ^ "TXT-TOKS".
+    std::mt19937_64 rng(seed ^ 0x5049584152542d41ULL);
+    const int hs = s.hs, mlp = s.mlp;
+    const double sh = 1.0 / std::sqrt(double(hs)), sm = 1.0 / std::sqrt(double(mlp));
+    struct P { int rows, cols; double scale; };
+    const P spec[17] = {{hs, 3 * hs, sh}, {1, 3 * hs, 0.1}, {hs, hs, sh}, {1, hs, 0.1},
+                        {hs, hs, sh},     {1, hs, 0.1},     {hs, hs, sh}, {1, hs, 0.1},
+                        {hs, hs, sh},     {1, hs, 0.1},     {hs, hs, sh}, {1, hs, 0.1},
+                        {hs, mlp, sh},    {1, mlp, 0.1},    {mlp, hs, sm}, {1, hs, 0.1},
+                        {6, hs, sh}};
+    std::vector<double> w[17];
+    for (int l = 0; l < s.layers; ++l) {
+      const double* ptrs[17];
+      for (int i = 0; i < 17; ++i) {
+        fill(rng, w[i], spec[i].rows, spec[i].cols, spec[i].scale);
+        ptrs[i] = w[i].data();
+      }
+      ctx->engine->load_layer_px(l, ptrs);
+    }
+    std::vector<double> g[6], cb;
+    fill(rng, g[0], 256, hs, 1.0 / 16.0);
+    fill(rng, g[1], 1, hs, 0.1);
+    fill(rng, g[2], hs, hs, sh);
+    fill(rng, g[3], 1, hs, 0.1);
+    fill(rng, g[4], hs, 6 * hs, sh);
+    fill(rng, g[5], 1, 6 * hs, 0.1);
+    fill(rng, cb, 1, hs, 1.0);
+    const double* gp[6] = {g[0].data(), g[1].data(), g[2].data(),
+                           g[3].data(), g[4].data(), g[5].data()};
+    ctx->engine->load_px_globals(gp);
+    ctx->engine->load_condition_bias(cb.data());
+    std::mt19937_64 trng(seed ^ 0x5458542d544f4b53ULL);
+    std::vector<double> y;
+    fill(trng, y, text_tokens, hs, 1.0);
+    ctx->engine->set_text(y.data());
+    *out = ctx.release();
+  });
+}
+
+pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout layout) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    const pf::ModelShape& m = ctx->engine->shape();
+    if (m.block != pf::kBlockPixArt) throw pf::ValidationError("model has no text conditioning");
+    if (!y) throw pf::ValidationError("NULL text pointer");
+    if (tokens != m.T) throw pf::ValidationError("text token count does not match the model");
+    std::vector<double> rm(size_t(tokens) * m.hs);
+    for (int64_t r = 0; r < tokens; ++r)
+      for (int c = 0; c < m.hs; ++c)
+        rm[size_t(r) * m.hs + c] =
+            layout == PF_COL_MAJOR ? y[size_t(c) * tokens + r] : y[size_t(r) * m.hs + c];
+    ctx->engine->set_text(rm.data());
+  });
+}
+
+int pf_block_kind(const pf_ctx* ctx) { return ctx ? ctx->engine->shape().block : -1; }
+
 pf_status pf_create(const pf_model_desc* desc, const double* const* weights,
                     const double* condition_bias, pf_layout layout,
                     const int* devices, int n_stages, pf_ctx** out) {
@@ -267,6 +337,17 @@ pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,
     if (!h || !k_buf || !v_buf) throw pf::ValidationError("NULL buffer pointer");
     ctx->engine->layer_forward_host(layer, h, rows, row0, k_buf, v_buf,
                                     layout == PF_COL_MAJOR);
+  });
+}
+
+pf_status pf_layer_forward_t(pf_ctx* ctx, int layer, int timestep, int steps, double* h,
+                             int64_t rows, int64_t row0, double* k_buf, double* v_buf,
+                             pf_layout layout) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!h || !k_buf || !v_buf) throw pf::ValidationError("NULL buffer pointer");
+    ctx->engine->layer_forward_host(layer, h, rows, row0, k_buf, v_buf,
+                                    layout == PF_COL_MAJOR, timestep, steps);
   });
 }
 

@@ -17,12 +17,30 @@
 // tile's main loop.
 #pragma once
 
+#include <type_traits>
+
 #include "sm100_ptx.cuh"
 
 namespace pf {
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;  // 64 bf16 = 128 B = one SW128 atom row
+
+// Epilogue functors may carry per-row state computed once per tile before
+// the accumulator is ready (e.g. LayerNorm statistics of the A rows):
+// `typename E::RowState E::row_state(int row) const` and
+// `E::operator()(row, col0, v, nvalid, const RowState&)`.
+struct NoRowState {};
+template <class E, class = void>
+struct epi_row_state {
+  static constexpr bool value = false;
+  using type = NoRowState;
+};
+template <class E>
+struct epi_row_state<E, std::void_t<typename E::RowState>> {
+  static constexpr bool value = true;
+  using type = typename E::RowState;
+};
 
 template <int BN, int STAGES>
 struct GemmSmem {
@@ -155,6 +173,10 @@ __global__ void __launch_bounds__(256, 1)
             epi.preload(row0 + local_row, col0, pre[c], (N - col0) < 32 ? (N - col0) : 32);
         }
       }
+      typename epi_row_state<Epi>::type rs{};
+      if constexpr (epi_row_state<Epi>::value) {
+        if (row_ok) rs = epi.row_state(row0 + local_row);
+      }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
 #pragma unroll
@@ -171,6 +193,8 @@ __global__ void __launch_bounds__(256, 1)
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
           if constexpr (Epi::kPreload) {
             epi.apply(row0 + local_row, col0, v, pre[c], nvalid);
+          } else if constexpr (epi_row_state<Epi>::value) {
+            epi(row0 + local_row, col0, v, nvalid, rs);
           } else {
             epi(row0 + local_row, col0, v, nvalid);
           }
@@ -329,6 +353,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
             epi.preload(row0 + local_row, col0, pre[c], (N - col0) < 32 ? (N - col0) : 32);
         }
       }
+      typename epi_row_state<Epi>::type rs{};
+      if constexpr (epi_row_state<Epi>::value) {
+        if (row_ok) rs = epi.row_state(row0 + local_row);
+      }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
 #pragma unroll
@@ -345,6 +373,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
           if constexpr (Epi::kPreload) {
             epi.apply(row0 + local_row, col0, v, pre[c], nvalid);
+          } else if constexpr (epi_row_state<Epi>::value) {
+            epi(row0 + local_row, col0, v, nvalid, rs);
           } else {
             epi(row0 + local_row, col0, v, nvalid);
           }
@@ -383,7 +413,75 @@ struct ResidTmaArgs {
   float* h;        // for the finite check only
   int* flag;
   int code;
+  // PixArt block (kMod kernels only):
+  //   h += gate[n] * (acc + bias[n])            (null gate -> 1, null bias -> 0)
+  //   hb = bf16(h * (1 + colscale[n]))          (null colscale -> bf16(h)): the
+  //        next LayerNorm consumer's adaLN scale, folded into its A operand
+  //   stats[(n / 32) * stats_ld + row] = (sum h, sum h^2) over the 32 columns
+  const float* bias = nullptr;
+  const float* gate = nullptr;
+  const float* colscale = nullptr;
+  float2* stats = nullptr;
+  int stats_ld = 0;
 };
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// One thread's 32-column chunk of the TMA residual epilogue: fp32 residual
+// tile (SW128, 4 x [128 rows x 32 fp32]) updated in place, bf16 copy written
+// into the SW128 bf16 tile (2 x [128 rows x 64 bf16]). Returns "non-finite".
+template <bool kMod>
+__device__ __forceinline__ bool resid_chunk(uint8_t* sC, uint8_t* sD, int r, int c,
+                                            const uint32_t (&v)[32], int col0, int grow,
+                                            const ResidTmaArgs& args) {
+  const uint32_t sw = uint32_t(r & 7);
+  uint8_t* crow = sC + c * 16384 + r * 128;
+  uint8_t* drow = sD + (c >> 1) * 16384 + r * 128;
+  bool bad = false;
+  float s = 0.f, ss = 0.f;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {  // 16-byte piece g of the 32 fp32 columns
+    float4* pc = reinterpret_cast<float4*>(crow + ((uint32_t(g) ^ sw) << 4));
+    float4 x = *pc;
+    float4 a = make_float4(__uint_as_float(v[4 * g + 0]), __uint_as_float(v[4 * g + 1]),
+                           __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3]));
+    float4 y;
+    if constexpr (kMod) {
+      const int n = col0 + 4 * g;
+      if (args.bias) {
+        const float4 b = ldg4(args.bias + n);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      if (args.gate) {
+        const float4 gt = ldg4(args.gate + n);
+        a.x *= gt.x; a.y *= gt.y; a.z *= gt.z; a.w *= gt.w;
+      }
+      x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
+      s += (x.x + x.y) + (x.z + x.w);
+      ss += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
+      y = x;
+      if (args.colscale) {
+        const float4 cs = ldg4(args.colscale + n);
+        y.x *= 1.f + cs.x; y.y *= 1.f + cs.y; y.z *= 1.f + cs.z; y.w *= 1.f + cs.w;
+      }
+    } else {
+      x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
+      y = x;
+    }
+    *pc = x;
+    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+    // bf16 copy: columns 32c + 4g .. +3 -> byte 64 (c&1) + 8 g of the row
+    const uint32_t byte = uint32_t(64 * (c & 1) + 8 * g);
+    uint2* pd = reinterpret_cast<uint2*>(drow + ((((byte >> 4) ^ sw) << 4) | (byte & 15)));
+    *pd = make_uint2(ptx::pack_bf16x2(y.x, y.y), ptx::pack_bf16x2(y.z, y.w));
+  }
+  if constexpr (kMod) {
+    if (args.stats) args.stats[size_t(col0 >> 5) * args.stats_ld + grow] = make_float2(s, ss);
+  }
+  return bad;
+}
 
 template <int STAGES>
 struct GemmResSmem {
@@ -398,7 +496,7 @@ struct GemmResSmem {
   static_assert(kTotal <= 232448, "residual GEMM smem budget");
 };
 
-template <int STAGES>
+template <int STAGES, bool kMod>
 __global__ void __launch_bounds__(256, 1)
     gemm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b,
@@ -514,7 +612,6 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int r = 32 * q + int(lane);  // row within the tile == TMEM lane
-    const uint32_t sw = uint32_t(r & 7);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t c_phase = 0;
@@ -530,23 +627,8 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t v[32];
         ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, v);
         ptx::tmem_wait_ld();
-        uint8_t* crow = sC + c * 16384 + r * 128;
-        uint8_t* drow = sD + (c >> 1) * 16384 + r * 128;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {  // 16-byte piece g of the 32 fp32 columns
-          float4* pc = reinterpret_cast<float4*>(crow + ((uint32_t(g) ^ sw) << 4));
-          float4 x = *pc;
-          x.x += __uint_as_float(v[4 * g + 0]);
-          x.y += __uint_as_float(v[4 * g + 1]);
-          x.z += __uint_as_float(v[4 * g + 2]);
-          x.w += __uint_as_float(v[4 * g + 3]);
-          *pc = x;
-          bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-          // bf16 copy: columns 32c + 4g .. +3 -> byte 64 (c&1) + 8 g of the row
-          const uint32_t byte = uint32_t(64 * (c & 1) + 8 * g);
-          uint2* pd = reinterpret_cast<uint2*>(drow + ((((byte >> 4) ^ sw) << 4) | (byte & 15)));
-          *pd = make_uint2(ptx::pack_bf16x2(x.x, x.y), ptx::pack_bf16x2(x.z, x.w));
-        }
+        bad |= resid_chunk<kMod>(sC, sD, r, c, v, nt * BN + 32 * c,
+                                 row0 + mt * kGemmBM + r, args);
       }
       if (bad && args.flag) atomicMin(args.flag, args.code);
       ptx::tc_fence_before();
@@ -597,7 +679,7 @@ struct Gemm2SmResSmem {
   static_assert(kTotal <= 232448, "2-SM residual GEMM smem budget");
 };
 
-template <int STAGES>
+template <int STAGES, bool kMod>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm2sm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                              const __grid_constant__ CUtensorMap tma_b,
@@ -717,7 +799,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int r = 32 * q + int(lane);
-    const uint32_t sw = uint32_t(r & 7);
     const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -734,22 +815,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         uint32_t v[32];
         ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, v);
         ptx::tmem_wait_ld();
-        uint8_t* crow = sC + c * 16384 + r * 128;
-        uint8_t* drow = sD + (c >> 1) * 16384 + r * 128;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float4* pc = reinterpret_cast<float4*>(crow + ((uint32_t(g) ^ sw) << 4));
-          float4 x = *pc;
-          x.x += __uint_as_float(v[4 * g + 0]);
-          x.y += __uint_as_float(v[4 * g + 1]);
-          x.z += __uint_as_float(v[4 * g + 2]);
-          x.w += __uint_as_float(v[4 * g + 3]);
-          *pc = x;
-          bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-          const uint32_t byte = uint32_t(64 * (c & 1) + 8 * g);
-          uint2* pd = reinterpret_cast<uint2*>(drow + ((((byte >> 4) ^ sw) << 4) | (byte & 15)));
-          *pd = make_uint2(ptx::pack_bf16x2(x.x, x.y), ptx::pack_bf16x2(x.z, x.w));
-        }
+        bad |= resid_chunk<kMod>(sC, sD, r, c, v, nt * BN + 32 * c,
+                                 row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM + r, args);
       }
       if (bad && args.flag) atomicMin(args.flag, args.code);
       ptx::tc_fence_before();

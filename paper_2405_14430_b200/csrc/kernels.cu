@@ -250,6 +250,194 @@ struct EpiQKV {
   }
 };
 
+// ---- PixArt block epilogues -------------------------------------------
+
+// LayerNorm fold vectors: rows 2s = (1 + scale_s) . W (c1), rows 2s+1 =
+// shift_s . W + b (c2), stored fp32.
+struct EpiFold {
+  static constexpr bool kPreload = false;
+  float* out;
+  int ld;
+  const float* bias;
+  __device__ void operator()(int row, int col0, const float (&v)[32], int nvalid) const {
+    float* o = out + size_t(row) * ld + col0;
+    const bool odd = (row & 1) && bias;
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (e < nvalid) o[e] = v[e] + (odd ? __ldg(bias + col0 + e) : 0.f);
+  }
+};
+
+// LayerNorm of the A row from the per-32-column (sum, sum^2) statistics the
+// producing residual epilogue wrote: (rstd, -rstd * mean); (1, 0) without.
+struct AffineRow {
+  float a, b;
+};
+__device__ __forceinline__ AffineRow ln_row_state(const float2* stats, int ld, int cols,
+                                                  float eps, int row) {
+  if (!stats) return {1.f, 0.f};
+  float s = 0.f, ss = 0.f;
+  const int chunks = cols >> 5;
+  // 12 independent loads in flight per round trip (hs 1152: 3 round trips)
+  for (int c0 = 0; c0 < chunks; c0 += 12) {
+    float2 v[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      v[j] = c0 + j < chunks ? __ldg(stats + size_t(c0 + j) * ld + row) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      s += v[j].x;
+      ss += v[j].y;
+    }
+  }
+  const float inv = 1.f / float(cols);
+  const float mean = s * inv;
+  const float var = fmaxf(ss * inv - mean * mean, 0.f);
+  const float rstd = rsqrtf(var + eps);
+  return {rstd, -rstd * mean};
+}
+
+__device__ __forceinline__ void affine32(float (&y)[32], const float (&acc)[32], int col0,
+                                         int nvalid, const AffineRow& rs, const float* c1,
+                                         const float* c2) {
+#pragma unroll
+  for (int e = 0; e < 32; ++e) y[e] = rs.a * acc[e];
+  if (nvalid == 32) {
+    if (c1) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        const float4 c = __ldg(reinterpret_cast<const float4*>(c1 + col0 + e));
+        y[e] += rs.b * c.x; y[e + 1] += rs.b * c.y; y[e + 2] += rs.b * c.z; y[e + 3] += rs.b * c.w;
+      }
+    }
+    if (c2) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        const float4 c = __ldg(reinterpret_cast<const float4*>(c2 + col0 + e));
+        y[e] += c.x; y[e + 1] += c.y; y[e + 2] += c.z; y[e + 3] += c.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      if (e < nvalid) {
+        if (c1) y[e] += rs.b * __ldg(c1 + col0 + e);
+        if (c2) y[e] += __ldg(c2 + col0 + e);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k = 0.7978845608028654f;  // sqrt(2/pi)
+  return 0.5f * x * (1.f + ptx::tanh_approx(k * fmaf(0.044715f * x, x * x, x)));
+}
+
+// QKV projection with the LayerNorm/adaLN fold (or a plain bias) before the
+// head-major scatter of EpiQKV.
+struct EpiQKVAffine {
+  static constexpr bool kPreload = false;
+  using RowState = AffineRow;
+  EpiQKV scatter;
+  const float2* stats;
+  int stats_ld, ln_cols;
+  float eps;
+  const float* c1;
+  const float* c2;
+  __device__ AffineRow row_state(int row) const {
+    return ln_row_state(stats, stats_ld, ln_cols, eps, row);
+  }
+  __device__ void operator()(int row, int col0, const float (&acc)[32], int nvalid,
+                             const AffineRow& rs) const {
+    float y[32];
+    affine32(y, acc, col0, nvalid, rs, c1, c2);
+    scatter(row, col0, y, nvalid);
+  }
+};
+
+// MLP-in projection with the LayerNorm/adaLN fold and GELU(tanh).
+struct EpiGeluAffine {
+  static constexpr bool kPreload = false;
+  using RowState = AffineRow;
+  bf16* z;
+  int ld;
+  const float2* stats;
+  int stats_ld, ln_cols;
+  float eps;
+  const float* c1;
+  const float* c2;
+  __device__ AffineRow row_state(int row) const {
+    return ln_row_state(stats, stats_ld, ln_cols, eps, row);
+  }
+  __device__ void operator()(int row, int col0, const float (&acc)[32], int nvalid,
+                             const AffineRow& rs) const {
+    float y[32];
+    affine32(y, acc, col0, nvalid, rs, c1, c2);
+    bf16* o = z + size_t(row) * ld + col0;
+    if (nvalid == 32) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        uint4 pk;
+        pk.x = ptx::pack_bf16x2(gelu_tanh(y[e + 0]), gelu_tanh(y[e + 1]));
+        pk.y = ptx::pack_bf16x2(gelu_tanh(y[e + 2]), gelu_tanh(y[e + 3]));
+        pk.z = ptx::pack_bf16x2(gelu_tanh(y[e + 4]), gelu_tanh(y[e + 5]));
+        pk.w = ptx::pack_bf16x2(gelu_tanh(y[e + 6]), gelu_tanh(y[e + 7]));
+        *reinterpret_cast<uint4*>(o + e) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < nvalid) o[e] = __float2bfloat16_rn(gelu_tanh(y[e]));
+    }
+  }
+};
+
+// Residual epilogue of the PixArt block for the non-TMA kernels (row blocks
+// that are not whole 128-row tiles): gate, bias, adaLN-scaled bf16 copy and
+// LayerNorm statistics, as resid_chunk<true> does for the TMA kernels.
+struct EpiResidualMod {
+  static constexpr bool kPreload = true;
+  float* h;
+  bf16* hb;
+  int ld;
+  int* flag;
+  int code;
+  const float* bias;
+  const float* gate;
+  const float* colscale;
+  float2* stats;
+  int stats_ld;
+  __device__ void preload(int row, int col0, float (&pre)[32], int nvalid) const {
+    const float* hr = h + size_t(row) * ld + col0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) pre[e] = e < nvalid ? hr[e] : 0.f;
+  }
+  __device__ void apply(int row, int col0, const float (&v)[32], const float (&pre)[32],
+                        int nvalid) const {
+    float* hr = h + size_t(row) * ld + col0;
+    bf16* br = hb + size_t(row) * ld + col0;
+    bool bad = false;
+    float s = 0.f, ss = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+      if (e < nvalid) {
+        const int n = col0 + e;
+        float a = v[e];
+        if (bias) a += __ldg(bias + n);
+        if (gate) a *= __ldg(gate + n);
+        const float x = pre[e] + a;
+        hr[e] = x;
+        s += x;
+        ss += x * x;
+        br[e] = __float2bfloat16_rn(colscale ? x * (1.f + __ldg(colscale + n)) : x);
+        bad |= !isfinite(x);
+      }
+    }
+    if (stats) stats[size_t(col0 >> 5) * stats_ld + row] = make_float2(s, ss);
+    if (bad && flag) atomicMin(flag, code);
+  }
+};
+
 template <int BN, int STAGES, class E>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int rows,
                         int row0, int N, int K, const E& epi, int sm_count,
@@ -293,13 +481,34 @@ cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
     case Epi::StoreF32:
       return go(EpiStoreF32{ep.out_f32, ep.ld});
     case Epi::Residual:
+      if (ep.mod())
+        return go(EpiResidualMod{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code, ep.bias,
+                                 ep.gate, ep.colscale, ep.stats_out, ep.stats_ld});
       return go(EpiResidual{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code});
     case Epi::Tanh:
       return go(EpiTanh{ep.out_bf16, ep.ld});
     case Epi::QKV:
+      if (ep.stats_in || ep.c1 || ep.c2)
+        return go(EpiQKVAffine{EpiQKV{ep.q, ep.k, ep.v, ep.hs, ep.dh, ep.dhp, ep.P},
+                               ep.stats_in, ep.stats_ld, ep.ln_cols, ep.ln_eps, ep.c1, ep.c2});
       return go(EpiQKV{ep.q, ep.k, ep.v, ep.hs, ep.dh, ep.dhp, ep.P});
+    case Epi::Fold:
+      return go(EpiFold{ep.out_f32, ep.ld, ep.bias});
+    case Epi::Gelu:
+      return go(EpiGeluAffine{ep.out_bf16, ep.ld, ep.stats_in, ep.stats_ld, ep.ln_cols,
+                              ep.ln_eps, ep.c1, ep.c2});
   }
   return cudaErrorInvalidValue;
+}
+
+template <auto kern>
+cudaError_t launch_resid2(int grid, uint32_t smem, cudaStream_t stream, const CUtensorMap& a,
+                          const CUtensorMap& b, const EpiParams& ep, int rows, int row0, int N,
+                          int K, const ResidTmaArgs& args) {
+  cudaError_t e = ensure_smem_attr<kern>(smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, 256, smem, stream>>>(a, b, *ep.tm_h32, *ep.tm_hb, rows, row0, N, K, args);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -331,28 +540,28 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
     // operand traffic of the main loop
     constexpr int kStages = 5;
     using L = Gemm2SmResSmem<kStages>;
-    constexpr auto kern = gemm2sm_resid_tma_kernel<kStages>;
-    cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
-    if (e != cudaSuccess) return e;
     const int tiles = (rows / (2 * kGemmBM)) * ((N + L::BN - 1) / L::BN);
     const int pairs = sm_count / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    kern<<<grid, 256, L::kTotal, stream>>>(a, b.two_sm_128, *ep.tm_h32, *ep.tm_hb, rows, row0, N, K,
-                                           ResidTmaArgs{ep.out_f32, ep.flag, ep.code});
-    return cudaGetLastError();
+    const ResidTmaArgs args{ep.out_f32, ep.flag, ep.code, ep.bias, ep.gate, ep.colscale,
+                            ep.stats_out, ep.stats_ld};
+    return ep.mod() ? launch_resid2<gemm2sm_resid_tma_kernel<kStages, true>>(
+                          grid, L::kTotal, stream, a, b.two_sm_128, ep, rows, row0, N, K, args)
+                    : launch_resid2<gemm2sm_resid_tma_kernel<kStages, false>>(
+                          grid, L::kTotal, stream, a, b.two_sm_128, ep, rows, row0, N, K, args);
   }
   if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % kGemmBM == 0 && N % 32 == 0 &&
       gemm_bn_1sm(N) == 128) {
     constexpr int kStages = 4;
     using L = GemmResSmem<kStages>;
-    constexpr auto kern = gemm_resid_tma_kernel<kStages>;
-    cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
-    if (e != cudaSuccess) return e;
     const int tiles = (rows / kGemmBM) * ((N + L::BN - 1) / L::BN);
     const int grid = tiles < sm_count ? tiles : sm_count;
-    kern<<<grid, 256, L::kTotal, stream>>>(a, b.one_sm, *ep.tm_h32, *ep.tm_hb, rows, row0, N, K,
-                                           ResidTmaArgs{ep.out_f32, ep.flag, ep.code});
-    return cudaGetLastError();
+    const ResidTmaArgs args{ep.out_f32, ep.flag, ep.code, ep.bias, ep.gate, ep.colscale,
+                            ep.stats_out, ep.stats_ld};
+    return ep.mod() ? launch_resid2<gemm_resid_tma_kernel<kStages, true>>(
+                          grid, L::kTotal, stream, a, b.one_sm, ep, rows, row0, N, K, args)
+                    : launch_resid2<gemm_resid_tma_kernel<kStages, false>>(
+                          grid, L::kTotal, stream, a, b.one_sm, ep, rows, row0, N, K, args);
   }
   // The CTA-pair kernel wins where its 256 x 256 tiles apply (the MLP-in
   // projection, 78 % of peak vs 60 % for 1-SM 128 x 128 tiles); for narrower
@@ -406,6 +615,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   const int splits = attn_splits(a, sm_count);
   AttnParams prm;
   prm.P = a.P;
+  prm.q_stride = a.q_stride > 0 ? a.q_stride : a.P;
   prm.rows = a.rows;
   prm.row0 = a.row0;
   prm.heads = a.heads;

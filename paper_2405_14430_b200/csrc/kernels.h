@@ -26,13 +26,14 @@ bool encode_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t inner,
 
 int device_sm_count(int device);
 
-enum class Epi : int { StoreF32 = 0, QKV = 1, Residual = 2, Tanh = 3 };
+enum class Epi : int { StoreF32 = 0, QKV = 1, Residual = 2, Tanh = 3, Gelu = 4, Fold = 5 };
 
 struct EpiParams {
   // StoreF32: out_f32[row*ld + n] = acc
   // Residual: h = out_f32[row*ld + n] + acc; out_f32 = h; out_bf16 = bf16(h);
   //           non-finite h -> atomicMin(flag, code)
   // Tanh:     out_bf16[row*ld + n] = bf16(tanh(acc))
+  // Fold:     out_f32[row*ld + n] = acc + (row odd ? bias[n] : 0)
   // QKV:      n in [0,hs): q, [hs,2hs): k, [2hs,3hs): v, each [heads][P][dhp]
   float* out_f32 = nullptr;
   bf16* out_bf16 = nullptr;
@@ -47,6 +48,26 @@ struct EpiParams {
   // out_bf16 (bf16, box 64 x 128, SW128) enable the TMA epilogue.
   const CUtensorMap* tm_h32 = nullptr;
   const CUtensorMap* tm_hb = nullptr;
+  // ---- PixArt block extensions (all optional) ----
+  // Residual: h += gate[n] * (acc + bias[n]); out_bf16 = bf16(h * (1 + colscale[n]));
+  //           stats_out[(n/32) * stats_ld + row] = (sum, sum of squares) of h
+  //           over the chunk's 32 columns (LayerNorm statistics for the consumer).
+  // QKV/Gelu: affine epilogue  y = a_row * acc + b_row * c1[n] + c2[n]  where,
+  //           with stats_in, (a_row, b_row) = (rstd, -rstd * mean) of the A row
+  //           (LayerNorm folded through the GEMM: the A operand holds
+  //           h * (1 + scale) and c1 = (1 + scale) . W, c2 = shift . W + bias),
+  //           else (1, 0); Gelu then applies gelu_tanh and stores bf16.
+  const float* bias = nullptr;
+  const float* gate = nullptr;
+  const float* colscale = nullptr;
+  float2* stats_out = nullptr;
+  const float2* stats_in = nullptr;
+  int stats_ld = 0;    // rows of the stats buffer (= P)
+  int ln_cols = 0;     // LayerNorm width (hs): stats_in holds ln_cols / 32 chunks
+  float ln_eps = 1e-6f;
+  const float* c1 = nullptr;
+  const float* c2 = nullptr;
+  bool mod() const { return bias || gate || colscale || stats_out; }
 };
 
 // Tensor maps over a weight B [N x K] (K-major bf16) for both GEMM paths:
@@ -70,12 +91,14 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
 
 // Attention of query rows [row0, row0+rows) against all P kv rows.
 struct AttnLaunch {
+  // P: kv rows per head (buffer height); Q rows per head = q_stride (0 -> P)
   int dhp, P, rows, row0, heads, dh, hs;
   float scale;           // 1/sqrt(dh)
   bf16* out;             // [P][hs]
   float* work;           // split-KV partials (may be null if splits == 1)
   size_t work_floats;    // capacity of `work`
   unsigned long long* trace = nullptr;  // debug timeline (see AttnParams)
+  int q_stride = 0;      // cross-attention: Q buffer [heads][q_stride][dhp]
 };
 int attn_splits(const AttnLaunch& a, int sm_count);
 size_t attn_work_floats(int dhp, int heads, int rows, int splits);
@@ -94,6 +117,27 @@ cudaError_t latent_update(float* x, const float* src, float eta, size_t n,
                           cudaStream_t stream);
 // hb[i] = bf16(h32[i]), i < n
 cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream);
+// ---- PixArt block conditioning (pixart.cu) ----
+// sinusoid(1000 t / S) rows for t < S: [S x 256] (cos | sin)
+cudaError_t px_sinusoid(float* out, int S, cudaStream_t stream);
+// out[s][n] = act(sum_k act(in[s][k]) W[n][k] + b[n]); W fp32 [N x K]
+cudaError_t px_gemv(const float* in, int S, int K, const float* W, const float* b, int N,
+                    float* out, bool silu_in, bool silu_out, cudaStream_t stream);
+// mod[l][s][:] = sst[l][:] + tv[s][:]   (w6 = 6 hs)
+cudaError_t px_mod(const float* sst, int nl, const float* tv, int S, int w6, float* mod,
+                   cudaStream_t stream);
+// GEMM operands of the LayerNorm fold (see pixart.cu): per local layer a
+// [rpad x hs] bf16 block with rows 2s = 1 + scale_s, 2s+1 = shift_s, for the
+// attention (aq: mod columns [0, 2hs)) and MLP (am: [3hs, 5hs)) branches.
+// gemm(..., Epi::Fold) then gives c1 (row 2s) and c2 = shift . W + b (row 2s+1).
+cudaError_t px_fold_rows(const float* mod, int nl, int S, int hs, bf16* aq, bf16* am,
+                         int rpad, cudaStream_t stream);
+// rows [row0, row0+rows): if (update) x -= eta eps; h32 = x + cb;
+// hb = bf16(h32 (1 + scale)); stats[(c/32) stats_ld + row] = (sum, sum^2)
+cudaError_t px_patch_prepare(float* x, const float* eps, const float* cb, const float* scale,
+                             float* h32, bf16* hb, float2* stats, int stats_ld, int row0,
+                             int rows, int hs, float eta, bool update, cudaStream_t stream);
+
 // Device-side finite-check flag reset: *flag = INT_MAX
 cudaError_t reset_flag(int* flag, cudaStream_t stream);
 

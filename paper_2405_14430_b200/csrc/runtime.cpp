@@ -90,6 +90,13 @@ void validate_shape(const ModelShape& s) {
     throw ValidationError("CUDA backend needs hidden_size and mlp hidden size divisible by 8");
   if (s.P % 8 != 0) throw ValidationError("CUDA backend needs seq_len divisible by 8");
   if (s.hs / s.heads > 128) throw ValidationError("CUDA backend supports head dim <= 128");
+  if (s.block != kBlockToy && s.block != kBlockPixArt)
+    throw ValidationError("unknown block kind");
+  if (s.block == kBlockPixArt) {
+    if (s.hs % 32 != 0)
+      throw ValidationError("PixArt block needs hidden_size divisible by 32");
+    if (s.T < 1) throw ValidationError("PixArt block needs at least one text token");
+  }
 }
 
 Engine::Engine(const ModelShape& shape_in, const std::vector<int>& devices)
@@ -217,6 +224,72 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
     s.x = dalloc<float>(P * hs);
     s.cb = dalloc<float>(hs);
   }
+  if (m.block == kBlockPixArt) {
+    const size_t T = size_t(m.T), Tpad = (T + 127) / 128 * 128;
+    const size_t kvc_rows = heads * T + 128;  // + one TMA box of zero rows
+    for (StageLayer& L : s.layers) {
+      L.bqkv = dalloc<float>(3 * hs);
+      L.bo = dalloc<float>(hs);
+      L.bqc = dalloc<float>(hs);
+      L.bkvc = dalloc<float>(2 * hs);
+      L.boc = dalloc<float>(hs);
+      L.b1 = dalloc<float>(mlp);
+      L.b2 = dalloc<float>(hs);
+      L.wqc = dalloc<bf16>(hs * hs);
+      L.wkvc = dalloc<bf16>(2 * hs * hs);
+      L.woc = dalloc<bf16>(hs * hs);
+      L.kc = dalloc<bf16>(kvc_rows * dhp);
+      L.vc = dalloc<bf16>(kvc_rows * dhp);
+      if (!make_weight_maps(&L.tm_wqc, L.wqc, int(hs), int(hs)) ||
+          !make_weight_maps(&L.tm_wkvc, L.wkvc, int(2 * hs), int(hs)) ||
+          !make_weight_maps(&L.tm_woc, L.woc, int(hs), int(hs)))
+        throw CudaError("cuTensorMapEncodeTiled failed for a cross-attention weight");
+      L.tm_kc = tmap(L.kc, dhp, kvc_rows, dhp * 2, 16, 128, 32);
+      L.tm_vc = tmap(L.vc, dhp, kvc_rows, dhp * 2, 16, 128, 32);
+    }
+    PxStage& px = s.px;
+    px.wt1 = dalloc<float>(hs * kPxFreq);
+    px.bt1 = dalloc<float>(hs);
+    px.wt2 = dalloc<float>(hs * hs);
+    px.bt2 = dalloc<float>(hs);
+    px.wt0 = dalloc<float>(6 * hs * hs);
+    px.bt0 = dalloc<float>(6 * hs);
+    px.sst = dalloc<float>(size_t(count + 1) * 6 * hs);
+    px.text = dalloc<bf16>(Tpad * hs);
+    px.tm_text = tmap(px.text, hs, Tpad, hs * 2, 64, 128, 128);
+    px.stats = dalloc<float2>((hs / 32) * P);
+    px.zeros = dalloc<float>(hs);
+  }
+}
+
+// Per-run PixArt buffers, sized for `steps` timesteps (outside any capture).
+static void px_alloc_run(Stage& s, const ModelShape& m, int steps) {
+  PxStage& px = s.px;
+  if (steps <= px.steps_cap) return;
+  DeviceGuard g(s.device);
+  if (s.stream) cudaStreamSynchronize(s.stream);
+  for (float* p : {px.sinus, px.e1, px.temb, px.tv, px.mod, px.foldq, px.foldm}) dfree(p);
+  dfree(px.fold_aq);
+  dfree(px.fold_am);
+  const size_t S = size_t(steps), hs = size_t(m.hs), nl = size_t(s.layer_count);
+  px.sinus = dalloc<float>(S * kPxFreq);
+  px.e1 = dalloc<float>(S * hs);
+  px.temb = dalloc<float>(S * hs);
+  px.tv = dalloc<float>(S * 6 * hs);
+  px.mod = dalloc<float>((nl + 1) * S * 6 * hs);
+  px.fold_rpad = int((2 * S + 127) / 128 * 128);
+  const size_t rp = size_t(px.fold_rpad);
+  px.fold_aq = dalloc<bf16>(nl * rp * hs);
+  px.fold_am = dalloc<bf16>(nl * rp * hs);
+  px.tm_aq.resize(nl);
+  px.tm_am.resize(nl);
+  for (size_t l = 0; l < nl; ++l) {
+    px.tm_aq[l] = tmap(px.fold_aq + l * rp * hs, hs, rp, hs * 2, 64, 128, 128);
+    px.tm_am[l] = tmap(px.fold_am + l * rp * hs, hs, rp, hs * 2, 64, 128, 128);
+  }
+  px.foldq = dalloc<float>(nl * 2 * S * 3 * hs);
+  px.foldm = dalloc<float>(nl * 2 * S * size_t(m.mlp));
+  px.steps_cap = steps;
 }
 
 void Engine::free_stage(Stage& s) {
@@ -226,6 +299,20 @@ void Engine::free_stage(Stage& s) {
   for (StageLayer& L : s.layers) {
     dfree(L.wqkv); dfree(L.wo); dfree(L.win); dfree(L.wout);
     dfree(L.k); dfree(L.v);
+  }
+  for (StageLayer& L : s.layers) {
+    for (float* p : {L.bqkv, L.bo, L.bqc, L.bkvc, L.boc, L.b1, L.b2}) dfree(p);
+    dfree(L.wqc); dfree(L.wkvc); dfree(L.woc); dfree(L.kc); dfree(L.vc);
+  }
+  {
+    PxStage& px = s.px;
+    for (float* p : {px.wt1, px.bt1, px.wt2, px.bt2, px.wt0, px.bt0, px.sst, px.zeros, px.sinus,
+                     px.e1, px.temb, px.tv, px.mod, px.foldq, px.foldm})
+      dfree(p);
+    dfree(px.fold_aq);
+    dfree(px.fold_am);
+    dfree(px.text);
+    dfree(px.stats);
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
@@ -393,6 +480,13 @@ void Engine::send_rows(int from, int row0, int rows) {
                                   cudaMemcpyDefault, src.stream));
     PF_CUDA_CHECK(cudaMemcpyAsync(dst.hb + off, src.hb + off, cnt * 2,
                                   cudaMemcpyDefault, src.stream));
+    if (shape_.block == kBlockPixArt) {
+      // LayerNorm partial sums of the rows ([hs/32][P] float2)
+      const size_t pitch = size_t(shape_.P) * sizeof(float2);
+      PF_CUDA_CHECK(cudaMemcpy2DAsync(dst.px.stats + row0, pitch, src.px.stats + row0, pitch,
+                                      size_t(rows) * sizeof(float2), size_t(shape_.hs / 32),
+                                      cudaMemcpyDefault, src.stream));
+    }
     PF_CUDA_CHECK(cudaEventRecord(src.ev_fwd, src.stream));
     DeviceGuard g2(dst.device);
     PF_CUDA_CHECK(cudaStreamWaitEvent(dst.stream, src.ev_fwd, 0));
@@ -424,7 +518,8 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     throw ValidationError(os.str());
   }
   Stage& s0 = stages_[0];
-  prepare_run(patches);
+  prepare_run(patches, steps);
+  const bool px = m.block == kBlockPixArt;
 
   // Host bookkeeping: StageBuffers::src (execute.cpp:38-49), sentinel = steps.
   std::vector<std::vector<std::vector<int>>> src(static_cast<size_t>(n));
@@ -467,6 +562,15 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     codes_.emplace_back(t, layer);
     return int(codes_.size()) - 1;
   };
+  if (px)
+    for (Stage& s : stages_) {
+      DeviceGuard g(s.device);
+      px_conditioning(s, steps);
+    }
+  auto forward = [&](Stage& s, int lf, int rows, int row0, int t, int code) {
+    if (px) layer_forward_px(s, lf, rows, row0, t, code);
+    else layer_forward(s, lf, rows, row0, code);
+  };
 
   // ---- warmup: synchronous full-sequence steps (execute.cpp:181-190)
   for (int w = 0; w < warmup; ++w) {
@@ -474,8 +578,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     {
       DeviceGuard g(s0.device);
       prof_begin(s0, kSampler, 0, double(m.P) * m.hs * (4 + 4 + 2));
-      check(patch_prepare(x_dev, nullptr, s0.cb, s0.h32, s0.hb, 0, int(m.P), m.hs,
-                          0.f, false, s0.stream), "patch_prepare");
+      if (px)
+        px_patch_prepare(x_dev, false, 0, int(m.P), t, 0.f);
+      else
+        check(patch_prepare(x_dev, nullptr, s0.cb, s0.h32, s0.hb, 0, int(m.P), m.hs,
+                            0.f, false, s0.stream), "patch_prepare");
       prof_end(s0);
       ++launches_;
     }
@@ -486,7 +593,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         auto& sv = src[size_t(d)][size_t(lf)];
         std::fill(sv.begin(), sv.end(), t);
         st.fresh += patches;
-        layer_forward(s, lf, int(m.P), 0, next_code(t, s.first_layer + lf));
+        forward(s, lf, int(m.P), 0, t, next_code(t, s.first_layer + lf));
       }
       send_rows(d, 0, int(m.P));
     }
@@ -515,8 +622,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         if (q > 0 && n > 1)
           PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[size_t(j)], 0));
         prof_begin(s0, kSampler, 0, double(r) * m.hs * (q > 0 ? 4 + 4 + 4 + 4 + 2 : 4 + 4 + 2));
-        check(patch_prepare(x_dev, s0.eps, s0.cb, s0.h32, s0.hb, row0, r, m.hs, eta,
-                            q > 0, s0.stream), "patch_prepare");
+        if (px)
+          px_patch_prepare(x_dev, q > 0, row0, r, t, eta);
+        else
+          check(patch_prepare(x_dev, s0.eps, s0.cb, s0.h32, s0.hb, row0, r, m.hs, eta,
+                              q > 0, s0.stream), "patch_prepare");
         prof_end(s0);
         ++launches_;
       }
@@ -539,7 +649,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
               throw NumericError(os.str());
             }
           }
-          layer_forward(s, lf, r, row0, next_code(t, s.first_layer + lf));
+          forward(s, lf, r, row0, t, next_code(t, s.first_layer + lf));
         }
         // fresh_fraction(src[0], t) after the stage (execute.cpp:67-73,164)
         {
@@ -575,9 +685,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
 }
 
 // Allocations and events a run needs, created outside any stream capture.
-void Engine::prepare_run(int patches) {
+void Engine::prepare_run(int patches, int steps) {
   const int n = stage_count();
   Stage& s0 = stages_[0];
+  if (shape_.block == kBlockPixArt && steps >= 1)
+    for (Stage& s : stages_) px_alloc_run(s, shape_, steps);
   if (!ev_start_) {
     DeviceGuard g(s0.device);
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
@@ -599,7 +711,7 @@ void Engine::prepare_run(int patches) {
 
 void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
                  cudaStream_t caller, RunStats* stats) {
-  if (patches >= 1) prepare_run(patches);
+  if (patches >= 1) prepare_run(patches, steps);
   bool single_device = true;
   for (const Stage& s : stages_) single_device &= s.device == stages_[0].device;
   if (!graphs_enabled_ || profiling_ || caller == nullptr || !single_device) {
@@ -659,7 +771,8 @@ void Engine::finish(cudaStream_t caller) {
 }
 
 void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0,
-                                double* k_buf, double* v_buf, bool col_major) {
+                                double* k_buf, double* v_buf, bool col_major, int t,
+                                int steps) {
   const ModelShape& m = shape_;
   const int d = stage_of_layer(layer);
   if (d < 0) throw ValidationError("layer index out of range");
@@ -699,7 +812,21 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
   check(reset_flag(s.flag, s.stream), "reset_flag");
   codes_.assign(1, {0, layer});
   launches_ = 1;
-  layer_forward(s, layer - s.first_layer, int(rows), int(row0), 0);
+  if (m.block == kBlockPixArt) {
+    if (steps < 1 || t < 0 || t >= steps)
+      throw ValidationError("timestep index outside [0, steps)");
+    px_alloc_run(s, m, steps);
+    px_conditioning(s, steps);
+    const int lf = layer - s.first_layer;
+    const float* scale1 = s.px.mod + (size_t(lf) * steps + t) * 6 * hs + hs;
+    // LayerNorm inputs of the uploaded rows (h32 += 0 in place)
+    check(pf::px_patch_prepare(s.h32, nullptr, s.px.zeros, scale1, s.h32, s.hb, s.px.stats,
+                               int(P), int(row0), int(rows), hs, 0.f, false, s.stream),
+          "px_patch_prepare");
+    layer_forward_px(s, lf, int(rows), int(row0), t, 0);
+  } else {
+    layer_forward(s, layer - s.first_layer, int(rows), int(row0), 0);
+  }
   PF_CUDA_CHECK(cudaMemcpyAsync(h32.data(), s.h32 + row0 * hs, h32.size() * 4,
                                 cudaMemcpyDeviceToHost, s.stream));
   PF_CUDA_CHECK(cudaMemcpyAsync(kd.data(), L.k, kd.size() * 2, cudaMemcpyDeviceToHost, s.stream));
@@ -720,6 +847,284 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
     os << "non-finite activation at timestep 0, layer " << layer;
     throw NumericError(os.str());
   }
+}
+
+// ============================================================== PixArt block
+namespace {
+// Transpose an fp64 [K x N] (x.W orientation) matrix to [N x K] (K-major).
+template <class T, class Cvt>
+std::vector<T> transpose_kn(const double* w, int K, int N, Cvt cvt) {
+  std::vector<T> out(size_t(N) * K);
+  for (int k = 0; k < K; ++k)
+    for (int n = 0; n < N; ++n) out[size_t(n) * K + k] = cvt(w[size_t(k) * N + n]);
+  return out;
+}
+inline bf16 to_bf(double v) { return __float2bfloat16_rn(float(v)); }
+inline float to_f(double v) { return float(v); }
+std::vector<float> to_f32(const double* v, size_t n) {
+  std::vector<float> out(n);
+  for (size_t i = 0; i < n; ++i) out[i] = float(v[i]);
+  return out;
+}
+}  // namespace
+
+void Engine::load_layer_px(int layer, const double* const* prm) {
+  if (shape_.block != kBlockPixArt) throw ValidationError("model is not a PixArt block model");
+  const int d = stage_of_layer(layer);
+  if (d < 0) throw ValidationError("layer index out of range");
+  Stage& s = stages_[size_t(d)];
+  StageLayer& L = s.layers[size_t(layer - s.first_layer)];
+  const int hs = shape_.hs, mlp = shape_.mlp;
+  // PXO_* order: WQKV BQKV WO BO WQC BQC WKC BKC WVC BVC WOC BOC W1 B1 W2 B2 SST
+  auto up = [&](void* dst, const void* src, size_t bytes) {
+    PF_CUDA_CHECK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  };
+  DeviceGuard g(s.device);
+  auto wqkv = transpose_kn<bf16>(prm[0], hs, 3 * hs, to_bf);
+  auto wo = transpose_kn<bf16>(prm[2], hs, hs, to_bf);
+  auto wqc = transpose_kn<bf16>(prm[4], hs, hs, to_bf);
+  auto wkc = transpose_kn<bf16>(prm[6], hs, hs, to_bf);
+  auto wvc = transpose_kn<bf16>(prm[8], hs, hs, to_bf);
+  auto woc = transpose_kn<bf16>(prm[10], hs, hs, to_bf);
+  auto w1 = transpose_kn<bf16>(prm[12], hs, mlp, to_bf);
+  auto w2 = transpose_kn<bf16>(prm[14], mlp, hs, to_bf);
+  up(L.wqkv, wqkv.data(), wqkv.size() * 2);
+  up(L.wo, wo.data(), wo.size() * 2);
+  up(L.wqc, wqc.data(), wqc.size() * 2);
+  up(L.wkvc, wkc.data(), wkc.size() * 2);
+  up(L.wkvc + size_t(hs) * hs, wvc.data(), wvc.size() * 2);
+  up(L.woc, woc.data(), woc.size() * 2);
+  up(L.win, w1.data(), w1.size() * 2);
+  up(L.wout, w2.data(), w2.size() * 2);
+  auto bqkv = to_f32(prm[1], size_t(3) * hs);
+  up(L.bqkv, bqkv.data(), bqkv.size() * 4);
+  auto bo = to_f32(prm[3], hs);
+  up(L.bo, bo.data(), bo.size() * 4);
+  auto bqc = to_f32(prm[5], hs);
+  up(L.bqc, bqc.data(), bqc.size() * 4);
+  auto bkc = to_f32(prm[7], hs);
+  auto bvc = to_f32(prm[9], hs);
+  up(L.bkvc, bkc.data(), bkc.size() * 4);
+  up(L.bkvc + hs, bvc.data(), bvc.size() * 4);
+  auto boc = to_f32(prm[11], hs);
+  up(L.boc, boc.data(), boc.size() * 4);
+  auto b1 = to_f32(prm[13], size_t(mlp));
+  up(L.b1, b1.data(), b1.size() * 4);
+  auto b2 = to_f32(prm[15], hs);
+  up(L.b2, b2.data(), b2.size() * 4);
+  auto sst = to_f32(prm[16], size_t(6) * hs);
+  const size_t row = size_t(6) * hs;
+  up(s.px.sst + size_t(layer - s.first_layer) * row, sst.data(), row * 4);
+  // The previous stage's last epilogue folds this layer's adaLN scale into
+  // the bf16 operand it sends: keep a copy as that stage's "next" row.
+  if (layer == s.first_layer && d > 0) {
+    Stage& prev = stages_[size_t(d - 1)];
+    DeviceGuard gp(prev.device);
+    up(prev.px.sst + size_t(prev.layer_count) * row, sst.data(), row * 4);
+  }
+}
+
+void Engine::load_px_globals(const double* const* gw) {
+  if (shape_.block != kBlockPixArt) throw ValidationError("model is not a PixArt block model");
+  const int hs = shape_.hs;
+  auto wt1 = transpose_kn<float>(gw[0], kPxFreq, hs, to_f);
+  auto bt1 = to_f32(gw[1], hs);
+  auto wt2 = transpose_kn<float>(gw[2], hs, hs, to_f);
+  auto bt2 = to_f32(gw[3], hs);
+  auto wt0 = transpose_kn<float>(gw[4], hs, 6 * hs, to_f);
+  auto bt0 = to_f32(gw[5], size_t(6) * hs);
+  for (Stage& s : stages_) {
+    DeviceGuard g(s.device);
+    PF_CUDA_CHECK(cudaMemcpy(s.px.wt1, wt1.data(), wt1.size() * 4, cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(s.px.bt1, bt1.data(), bt1.size() * 4, cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(s.px.wt2, wt2.data(), wt2.size() * 4, cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(s.px.bt2, bt2.data(), bt2.size() * 4, cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(s.px.wt0, wt0.data(), wt0.size() * 4, cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(s.px.bt0, bt0.data(), bt0.size() * 4, cudaMemcpyHostToDevice));
+  }
+}
+
+void Engine::set_text(const double* y) {
+  if (shape_.block != kBlockPixArt) throw ValidationError("model is not a PixArt block model");
+  std::vector<bf16> t(size_t(shape_.T) * shape_.hs);
+  for (size_t i = 0; i < t.size(); ++i) t[i] = to_bf(y[i]);
+  for (Stage& s : stages_) {
+    DeviceGuard g(s.device);
+    if (s.stream) PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
+    PF_CUDA_CHECK(cudaMemcpy(s.px.text, t.data(), t.size() * 2, cudaMemcpyHostToDevice));
+  }
+}
+
+// Per-run conditioning of one stage (adaLN-single, px_oracle.c pxo_tvec):
+// timestep embeddings for every t < steps, per-layer modulation vectors,
+// LayerNorm fold vectors, and the cross-attention K/V of the text tokens.
+void Engine::px_conditioning(Stage& s, int steps) {
+  const ModelShape& m = shape_;
+  PxStage& px = s.px;
+  const int hs = m.hs, w6 = 6 * m.hs, nl = s.layer_count, S = steps;
+  prof_begin(s, kPxCond, 0, 0);
+  check(px_sinusoid(px.sinus, S, s.stream), "px_sinusoid");
+  check(px_gemv(px.sinus, S, kPxFreq, px.wt1, px.bt1, hs, px.e1, false, true, s.stream), "t_embedder.0");
+  // temb is only consumed through t_block = Linear(SiLU(temb)): store silu(temb)
+  check(px_gemv(px.e1, S, hs, px.wt2, px.bt2, hs, px.temb, false, true, s.stream), "t_embedder.2");
+  check(px_gemv(px.temb, S, hs, px.wt0, px.bt0, w6, px.tv, false, false, s.stream), "t_block");
+  check(px_mod(px.sst, nl + 1, px.tv, S, w6, px.mod, s.stream), "adaLN modulation");
+  check(px_fold_rows(px.mod, nl, S, hs, px.fold_aq, px.fold_am, px.fold_rpad, s.stream),
+        "LayerNorm fold operands");
+  launches_ += 6;
+  for (int lf = 0; lf < nl; ++lf) {
+    StageLayer& L = s.layers[size_t(lf)];
+    EpiParams fq;
+    fq.out_f32 = px.foldq + size_t(lf) * 2 * S * 3 * hs;
+    fq.ld = 3 * hs;
+    fq.bias = L.bqkv;
+    check(gemm(px.tm_aq[size_t(lf)], L.tm_wqkv, 2 * S, 0, 3 * hs, hs, Epi::Fold, fq, s.sm_count,
+               s.stream), "LayerNorm fold (attention)");
+    EpiParams fm;
+    fm.out_f32 = px.foldm + size_t(lf) * 2 * S * m.mlp;
+    fm.ld = m.mlp;
+    fm.bias = L.b1;
+    check(gemm(px.tm_am[size_t(lf)], L.tm_win, 2 * S, 0, m.mlp, hs, Epi::Fold, fm, s.sm_count,
+               s.stream), "LayerNorm fold (MLP)");
+    EpiParams kv;
+    kv.q = L.kc;
+    kv.k = L.vc;
+    kv.hs = hs;
+    kv.dh = m.dh;
+    kv.dhp = m.dhp;
+    kv.P = m.T;
+    kv.c2 = L.bkvc;
+    check(gemm(px.tm_text, L.tm_wkvc, m.T, 0, 2 * hs, hs, Epi::QKV, kv, s.sm_count, s.stream),
+          "cross K/V projection");
+    launches_ += 3;
+  }
+  prof_end(s);
+  px_steps_ = S;
+}
+
+// Stage-0 patch split for the PixArt block: sampler update, h = x + cb, the
+// first layer's adaLN-scaled bf16 operand and its LayerNorm statistics.
+void Engine::px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta) {
+  Stage& s0 = stages_[0];
+  const int hs = shape_.hs;
+  const float* scale1 = s0.px.mod + size_t(t) * 6 * hs + hs;  // layer 0 = stage 0, lf 0
+  check(pf::px_patch_prepare(x_dev, s0.eps, s0.cb, scale1, s0.h32, s0.hb, s0.px.stats,
+                             int(shape_.P), row0, rows, hs, eta, update, s0.stream),
+        "px_patch_prepare");
+}
+
+// One PixArt block over rows [row0, row0+rows) at timestep index t
+// (px_oracle.c pxo_layer_forward_mod).
+void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code) {
+  const ModelShape& m = shape_;
+  StageLayer& L = s.layers[size_t(lf)];
+  PxStage& px = s.px;
+  const int hs = m.hs, w6 = 6 * hs, S = px_steps_;
+  const double r = rows, dhs = hs, mlp = m.mlp, P = double(m.P), T = double(m.T);
+  const float* modl = px.mod + (size_t(lf) * S + t) * w6;
+  const float* gate1 = modl + 2 * hs;
+  const float* scale2 = modl + 4 * hs;
+  const float* gate2 = modl + 5 * hs;
+  const bool last_model_layer = s.first_layer + lf + 1 == m.layers;
+  const float* next_scale1 =
+      last_model_layer ? nullptr : px.mod + (size_t(lf + 1) * S + t) * w6 + hs;
+
+  // 1. q, k, v = (LN(h)(1 + scale1) + shift1) Wqkv + bqkv; k, v rows in place
+  EpiParams qkv;
+  qkv.q = s.q;
+  qkv.k = L.k;
+  qkv.v = L.v;
+  qkv.hs = hs;
+  qkv.dh = m.dh;
+  qkv.dhp = m.dhp;
+  qkv.P = int(m.P);
+  qkv.stats_in = px.stats;
+  qkv.stats_ld = int(m.P);
+  qkv.ln_cols = hs;
+  qkv.c1 = px.foldq + (size_t(lf) * 2 * S + 2 * t) * 3 * hs;
+  qkv.c2 = qkv.c1 + 3 * hs;
+  prof_begin(s, kGemmQKV, 2 * r * dhs * 3 * dhs, 0);
+  check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * hs, hs, Epi::QKV, qkv, s.sm_count, s.stream),
+        "gemm qkv");
+  prof_end(s);
+  // 2. self-attention over the full (fresh + stale) K/V buffer
+  AttnLaunch a{m.dhp, int(m.P), rows, row0, m.heads, m.dh, hs,
+               float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
+               s.attn_work_floats};
+  prof_begin(s, kAttention, 4 * r * P * dhs, 0);
+  check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
+  prof_end(s);
+  // 3. h += gate1 (attn Wo + bo); raw bf16 copy for the cross-attention query
+  EpiParams res;
+  res.out_f32 = s.h32;
+  res.out_bf16 = s.hb;
+  res.ld = hs;
+  res.flag = s.flag;
+  res.code = code;
+  res.tm_h32 = &s.tm_h32;
+  res.tm_hb = &s.tm_hb;
+  res.stats_ld = int(m.P);
+  EpiParams r1 = res;
+  r1.bias = L.bo;
+  r1.gate = gate1;
+  prof_begin(s, kGemmOut, 2 * r * dhs * dhs, 0);
+  check(gemm(s.tm_attn, L.tm_wo, rows, row0, hs, hs, Epi::Residual, r1, s.sm_count, s.stream),
+        "gemm out-proj");
+  prof_end(s);
+  // 4. cross-attention query h Wqc + bqc
+  EpiParams cq;
+  cq.q = s.q;
+  cq.hs = hs;
+  cq.dh = m.dh;
+  cq.dhp = m.dhp;
+  cq.P = int(m.P);
+  cq.c2 = L.bqc;
+  prof_begin(s, kGemmCrossQ, 2 * r * dhs * dhs, 0);
+  check(gemm(s.tm_hb, L.tm_wqc, rows, row0, hs, hs, Epi::QKV, cq, s.sm_count, s.stream),
+        "gemm cross q");
+  prof_end(s);
+  // 5. cross-attention over the T text tokens
+  AttnLaunch ca{m.dhp, m.T, rows, row0, m.heads, m.dh, hs,
+                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
+                s.attn_work_floats};
+  ca.q_stride = int(m.P);
+  prof_begin(s, kCrossAttention, 4 * r * T * dhs, 0);
+  check(attention(s.tm_q, L.tm_kc, L.tm_vc, ca, s.sm_count, s.stream), "cross attention");
+  prof_end(s);
+  // 6. h += cross Woc + boc; operand bf16(h (1 + scale2)) + LayerNorm stats
+  EpiParams r2 = res;
+  r2.bias = L.boc;
+  r2.colscale = scale2;
+  r2.stats_out = px.stats;
+  prof_begin(s, kGemmCrossOut, 2 * r * dhs * dhs, 0);
+  check(gemm(s.tm_attn, L.tm_woc, rows, row0, hs, hs, Epi::Residual, r2, s.sm_count, s.stream),
+        "gemm cross out-proj");
+  prof_end(s);
+  // 7. z = gelu_tanh((LN(h)(1 + scale2) + shift2) W1 + b1)
+  EpiParams ge;
+  ge.out_bf16 = s.z;
+  ge.ld = m.mlp;
+  ge.stats_in = px.stats;
+  ge.stats_ld = int(m.P);
+  ge.ln_cols = hs;
+  ge.c1 = px.foldm + (size_t(lf) * 2 * S + 2 * t) * m.mlp;
+  ge.c2 = ge.c1 + m.mlp;
+  prof_begin(s, kGemmMlpIn, 2 * r * dhs * mlp, 0);
+  check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, hs, Epi::Gelu, ge, s.sm_count, s.stream),
+        "gemm mlp-in");
+  prof_end(s);
+  // 8. h += gate2 (z W2 + b2); operand for the next layer's LayerNorm
+  EpiParams r3 = res;
+  r3.bias = L.b2;
+  r3.gate = gate2;
+  r3.colscale = next_scale1;
+  r3.stats_out = px.stats;
+  prof_begin(s, kGemmMlpOut, 2 * r * dhs * mlp, 0);
+  check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, r3, s.sm_count, s.stream),
+        "gemm mlp-out");
+  prof_end(s);
+  launches_ += 8 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0) +
+               (attn_splits(ca, s.sm_count) > 1 ? 1 : 0);
 }
 
 }  // namespace pf

@@ -50,7 +50,13 @@ struct ModelShape {
   int64_t P = 0;  // sequence length = K/V buffer rows
   int dh = 0;
   int dhp = 0;    // dh rounded up to a multiple of 16
+  int block = 0;  // kBlockToy (toy_model.cpp:145-177) or kBlockPixArt
+  int T = 0;      // PixArt: text tokens in the cross-attention K/V
 };
+
+constexpr int kBlockToy = 0;
+constexpr int kBlockPixArt = 1;
+constexpr int kPxFreq = 256;  // sinusoidal timestep features
 
 // Host fp64 source of one layer's weights, in the reference's orientation
 // (x . W). `at(r, c)` reads element (r, c).
@@ -72,6 +78,33 @@ struct StageLayer {
   bf16* v = nullptr;     // [heads][P][dhp]
   WeightMaps tm_wqkv, tm_wo, tm_win, tm_wout;
   CUtensorMap tm_k, tm_v;
+  // PixArt block (oracle/px_oracle.c): biases fp32, cross-attention weights,
+  // per-image cross K/V of the text tokens [heads][T][dhp]
+  float *bqkv = nullptr, *bo = nullptr, *bqc = nullptr, *bkvc = nullptr, *boc = nullptr,
+        *b1 = nullptr, *b2 = nullptr;
+  bf16 *wqc = nullptr, *wkvc = nullptr, *woc = nullptr;  // [hs x hs], [2hs x hs], [hs x hs]
+  WeightMaps tm_wqc, tm_wkvc, tm_woc;
+  bf16 *kc = nullptr, *vc = nullptr;
+  CUtensorMap tm_kc, tm_vc;
+};
+
+// PixArt per-stage conditioning state (adaLN-single and the LayerNorm fold).
+struct PxStage {
+  float *wt1 = nullptr, *bt1 = nullptr;  // [hs x 256], [hs]   (N x K fp32)
+  float *wt2 = nullptr, *bt2 = nullptr;  // [hs x hs], [hs]
+  float *wt0 = nullptr, *bt0 = nullptr;  // [6hs x hs], [6hs]
+  float* sst = nullptr;    // [(layer_count + 1) x 6hs]; last row = next stage's first layer
+  bf16* text = nullptr;    // [Tpad x hs] text tokens (rows >= T zero)
+  CUtensorMap tm_text;
+  float2* stats = nullptr; // [hs/32][P] LayerNorm partial sums of the residual stream
+  float* zeros = nullptr;  // [hs]
+  // per run, sized for steps_cap timesteps
+  int steps_cap = 0;
+  float *sinus = nullptr, *e1 = nullptr, *temb = nullptr, *tv = nullptr, *mod = nullptr;
+  int fold_rpad = 0;                      // rows of one fold operand block (>= 2S)
+  bf16 *fold_aq = nullptr, *fold_am = nullptr;  // [nl][fold_rpad x hs]
+  std::vector<CUtensorMap> tm_aq, tm_am;   // per local layer
+  float *foldq = nullptr, *foldm = nullptr;  // [nl][2S x 3hs], [nl][2S x mlp]
 };
 
 struct Stage {
@@ -97,12 +130,14 @@ struct Stage {
   float* eps = nullptr;  // [P x hs] noise landing buffer (== last stage h32 when N == 1)
   float* cb = nullptr;   // [hs] condition bias
   std::vector<cudaEvent_t> ev_eps;  // per patch, recorded by the last stage
+  PxStage px;
 };
 
 // Kernel kinds for the optional per-launch CUDA-event profile.
 enum KernelKind : int {
   kGemmQKV = 0, kAttention = 1, kGemmOut = 2, kGemmMlpIn = 3, kGemmMlpOut = 4,
-  kSampler = 5, kKindCount = 6
+  kSampler = 5, kGemmCrossQ = 6, kCrossAttention = 7, kGemmCrossOut = 8, kPxCond = 9,
+  kKindCount = 10
 };
 
 struct KernelProfile {
@@ -128,6 +163,14 @@ class Engine {
   // Upload one layer (fp64 host matrices in the reference orientation).
   void load_layer(int layer, const HostMatrix (&w)[6]);
   void load_condition_bias(const double* cb);
+  // PixArt block: one layer's 17 parameters in oracle/px_oracle.c order
+  // (PXO_WQKV .. PXO_SST, x.W orientation [in x out], fp64 row-major).
+  void load_layer_px(int layer, const double* const* params);
+  // t_embedder / t_block weights (x.W orientation): wt1 [256 x hs], bt1,
+  // wt2 [hs x hs], bt2, wt0 [hs x 6hs], bt0.
+  void load_px_globals(const double* const* g);
+  // Text tokens y [T x hs] (row-major fp64) used by every stage's cross-attention.
+  void set_text(const double* y);
 
   const ModelShape& shape() const { return shape_; }
   int stage_count() const { return int(stages_.size()); }
@@ -148,8 +191,11 @@ class Engine {
   void finish(cudaStream_t caller);
 
   // Single layer (unit parity), on stage owning `layer`.
+  // PixArt: the block's conditioning is that of timestep index t of a
+  // `steps`-step run (ignored for the toy block).
   void layer_forward_host(int layer, double* h, int64_t rows, int64_t row0,
-                          double* k_buf, double* v_buf, bool col_major);
+                          double* k_buf, double* v_buf, bool col_major, int t = 0,
+                          int steps = 1);
 
   float* stage0_x() { return stages_[0].x; }
 
@@ -162,8 +208,12 @@ class Engine {
   void alloc_stage(Stage& s, int first, int count, bool is_first);
   void free_stage(Stage& s);
   void layer_forward(Stage& s, int lf, int rows, int row0, int code);
+  void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
+  void px_conditioning(Stage& s, int steps);
+  void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
   void send_rows(int from, int row0, int rows);
-  void prepare_run(int patches);
+  void prepare_run(int patches, int steps);
+  int px_steps_ = 0;  // S of the enqueued run (layout of the per-run PixArt buffers)
   cudaEvent_t ev_start_ = nullptr;
   int stage_of_layer(int layer) const;
 

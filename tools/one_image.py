@@ -24,7 +24,11 @@ ap.add_argument("--stages", type=int, default=1)
 ap.add_argument("--repeat", type=int, default=1)
 a = ap.parse_args()
 c = bench.CONFIGS[a.config]
-m = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], a.stages, [0] * a.stages)
+if c.get("block") == "pixart":
+    m = pf.PixArtCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], a.stages,
+                      [0] * a.stages)
+else:
+    m = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], a.stages, [0] * a.stages)
 x0 = torch.from_numpy(pf.make_initial_latent(0, c["p"], c["hs"]).astype(np.float32)).cuda()
 s = torch.cuda.Stream()
 for _ in range(a.repeat):
