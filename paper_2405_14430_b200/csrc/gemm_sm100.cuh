@@ -42,13 +42,93 @@ struct epi_row_state<E, std::void_t<typename E::RowState>> {
   using type = typename E::RowState;
 };
 
+// Epilogues may also declare `static constexpr int kColVecs` per-column fp32
+// vectors (`const float* colvec(int v) const`, null = zeros). The epilogue
+// warps stage the tile's BN columns of each vector in shared memory before
+// waiting for the accumulator (double-buffered by tile parity) and pass a
+// ColView to `operator()(row, col0, v, nvalid, rs, cv)`: cv.p[k * cv.stride + e]
+// is vector k at column col0 + e.
+struct ColView {
+  const float* p;
+  int stride;
+};
+template <class E, class = void>
+struct epi_colvecs {
+  static constexpr int value = 0;
+};
+template <class E>
+struct epi_colvecs<E, std::void_t<decltype(E::kColVecs)>> {
+  static constexpr int value = E::kColVecs;
+};
+constexpr int kMaxColVecs = 2;
+
+// Stage the tile's columns [n0, n0 + BN) of the epilogue's column vectors
+// into `dst` ([NV][BN] fp32); the 128 epilogue threads (tid 0..127) then
+// synchronise on named barrier 2.
+template <int BN, class Epi>
+__device__ __forceinline__ void stage_colvecs(const Epi& epi, float* dst, int n0, int N,
+                                              int tid) {
+  constexpr int NV = epi_colvecs<Epi>::value;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const float* src = epi.colvec(v);
+    for (int c = tid; c < BN; c += 128)
+      dst[v * BN + c] = (src && n0 + c < N) ? __ldg(src + n0 + c) : 0.f;
+  }
+  ptx::named_bar_sync(2, 128);
+}
+
+// One 32-column chunk of a non-preloading epilogue.
+template <int BN, class Epi, class RS>
+__device__ __forceinline__ void epilogue_chunk(const Epi& epi, const uint32_t (&r)[32], int c,
+                                               int grow, bool row_ok, int n0, int N,
+                                               const RS& rs, const float* colbuf) {
+  const int col0 = n0 + 32 * c;
+  if (!row_ok || col0 >= N) return;
+  const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
+  float v[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+  if constexpr (epi_colvecs<Epi>::value > 0) {
+    epi(grow, col0, v, nvalid, rs, ColView{colbuf + 32 * c, BN});
+  } else if constexpr (epi_row_state<Epi>::value) {
+    epi(grow, col0, v, nvalid, rs);
+  } else {
+    epi(grow, col0, v, nvalid);
+  }
+}
+
+// The tile's BN / 32 chunks, not unrolled (the functor bodies are large and
+// a fully unrolled tile overflows the instruction cache), with the TMEM load
+// of chunk c + 1 in flight while chunk c is processed.
+template <int BN, class Epi, class RS>
+__device__ __forceinline__ void epilogue_chunks(const Epi& epi, uint32_t taddr, int grow,
+                                                bool row_ok, int n0, int N, const RS& rs,
+                                                const float* colbuf) {
+  constexpr int NC = BN / 32;
+  static_assert(NC % 2 == 0, "chunk pairs");
+  uint32_t ra[32], rb[32];
+  ptx::tmem_ld32(taddr, ra);
+  ptx::tmem_wait_ld();
+#pragma unroll 1
+  for (int c = 0; c < NC; c += 2) {
+    ptx::tmem_ld32(taddr + 32 * (c + 1), rb);
+    epilogue_chunk<BN>(epi, ra, c, grow, row_ok, n0, N, rs, colbuf);
+    ptx::tmem_wait_ld();
+    if (c + 2 < NC) ptx::tmem_ld32(taddr + 32 * (c + 2), ra);
+    epilogue_chunk<BN>(epi, rb, c + 1, grow, row_ok, n0, N, rs, colbuf);
+    ptx::tmem_wait_ld();
+  }
+}
+
 template <int BN, int STAGES>
 struct GemmSmem {
   static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;
   static constexpr uint32_t kBBytes = BN * kGemmBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
-  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;  // + align slack
+  static constexpr uint32_t kColOffset = kBarOffset + 256;  // [2][kMaxColVecs][BN] fp32
+  static constexpr uint32_t kTotal = kColOffset + 2 * kMaxColVecs * BN * 4 + 1024;
   static constexpr uint32_t kTmemCols = (2 * BN <= 32)    ? 32
                                         : (2 * BN <= 64)  ? 64
                                         : (2 * BN <= 128) ? 128
@@ -156,6 +236,7 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int tile_count = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int mt = tile % m_tiles;
       const int nt = tile / m_tiles;
@@ -177,28 +258,32 @@ __global__ void __launch_bounds__(256, 1)
       if constexpr (epi_row_state<Epi>::value) {
         if (row_ok) rs = epi.row_state(row0 + local_row);
       }
+      constexpr int kNV = epi_colvecs<Epi>::value;
+      float* colbuf = reinterpret_cast<float*>(smem + L::kColOffset) +
+                      (tile_count & 1) * kMaxColVecs * BN;
+      if constexpr (kNV > 0) stage_colvecs<BN>(epi, colbuf, nt * BN, N, int(threadIdx.x) - 128);
+      ++tile_count;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + acc * BN;
+      if constexpr (Epi::kPreload) {
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        const int col0 = nt * BN + 32 * c;
-        if (col0 >= N) break;
-        uint32_t r[32];
-        ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, r);
-        ptx::tmem_wait_ld();
-        if (row_ok) {
-          const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
-          float v[32];
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + 32 * c;
+          if (col0 >= N) break;
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + 32 * c, r);
+          ptx::tmem_wait_ld();
+          if (row_ok) {
+            const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
+            float v[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-          if constexpr (Epi::kPreload) {
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
             epi.apply(row0 + local_row, col0, v, pre[c], nvalid);
-          } else if constexpr (epi_row_state<Epi>::value) {
-            epi(row0 + local_row, col0, v, nvalid, rs);
-          } else {
-            epi(row0 + local_row, col0, v, nvalid);
           }
         }
+      } else {
+        epilogue_chunks<BN>(epi, taddr, row0 + local_row, row_ok, nt * BN, N, rs, colbuf);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
@@ -229,7 +314,8 @@ struct Gemm2SmSmem {
   static constexpr uint32_t kBBytes = (BN / 2) * kGemmBK * 2;       // half of B
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kBarOffset = STAGES * kStageBytes;
-  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;
+  static constexpr uint32_t kColOffset = kBarOffset + 256;  // [2][kMaxColVecs][BN] fp32
+  static constexpr uint32_t kTotal = kColOffset + 2 * kMaxColVecs * BN * 4 + 1024;
   static constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static_assert(BN % 32 == 0 && BN <= 256, "2-SM tile N");
   static_assert(((BN / 2) * 128) % 1024 == 0, "B half must keep 1024-B aligned stages");
@@ -339,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int tile_count = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
       const int mt = tile % m_tiles;
       const int nt = tile / m_tiles;
@@ -357,28 +444,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       if constexpr (epi_row_state<Epi>::value) {
         if (row_ok) rs = epi.row_state(row0 + local_row);
       }
+      constexpr int kNV = epi_colvecs<Epi>::value;
+      float* colbuf = reinterpret_cast<float*>(smem + L::kColOffset) +
+                      (tile_count & 1) * kMaxColVecs * BN;
+      if constexpr (kNV > 0) stage_colvecs<BN>(epi, colbuf, nt * BN, N, int(threadIdx.x) - 128);
+      ++tile_count;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + acc * BN;
+      if constexpr (Epi::kPreload) {
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        const int col0 = nt * BN + 32 * c;
-        if (col0 >= N) break;
-        uint32_t r[32];
-        ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, r);
-        ptx::tmem_wait_ld();
-        if (row_ok) {
-          const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
-          float v[32];
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + 32 * c;
+          if (col0 >= N) break;
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + 32 * c, r);
+          ptx::tmem_wait_ld();
+          if (row_ok) {
+            const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
+            float v[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-          if constexpr (Epi::kPreload) {
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
             epi.apply(row0 + local_row, col0, v, pre[c], nvalid);
-          } else if constexpr (epi_row_state<Epi>::value) {
-            epi(row0 + local_row, col0, v, nvalid, rs);
-          } else {
-            epi(row0 + local_row, col0, v, nvalid);
           }
         }
+      } else {
+        epilogue_chunks<BN>(epi, taddr, row0 + local_row, row_ok, nt * BN, N, rs, colbuf);
       }
       // All four epilogue warps of this CTA have drained accumulator `acc`:
       // one elected thread tells the pair's MMA issuer (in the even CTA).

@@ -297,34 +297,17 @@ __device__ __forceinline__ AffineRow ln_row_state(const float2* stats, int ld, i
   return {rstd, -rstd * mean};
 }
 
-__device__ __forceinline__ void affine32(float (&y)[32], const float (&acc)[32], int col0,
-                                         int nvalid, const AffineRow& rs, const float* c1,
-                                         const float* c2) {
+// y = a_row * acc + b_row * c1 + c2 with c1, c2 staged in shared memory.
+__device__ __forceinline__ void affine32(float (&y)[32], const float (&acc)[32],
+                                         const AffineRow& rs, const ColView& cv) {
 #pragma unroll
-  for (int e = 0; e < 32; ++e) y[e] = rs.a * acc[e];
-  if (nvalid == 32) {
-    if (c1) {
-#pragma unroll
-      for (int e = 0; e < 32; e += 4) {
-        const float4 c = __ldg(reinterpret_cast<const float4*>(c1 + col0 + e));
-        y[e] += rs.b * c.x; y[e + 1] += rs.b * c.y; y[e + 2] += rs.b * c.z; y[e + 3] += rs.b * c.w;
-      }
-    }
-    if (c2) {
-#pragma unroll
-      for (int e = 0; e < 32; e += 4) {
-        const float4 c = __ldg(reinterpret_cast<const float4*>(c2 + col0 + e));
-        y[e] += c.x; y[e + 1] += c.y; y[e + 2] += c.z; y[e + 3] += c.w;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      if (e < nvalid) {
-        if (c1) y[e] += rs.b * __ldg(c1 + col0 + e);
-        if (c2) y[e] += __ldg(c2 + col0 + e);
-      }
-    }
+  for (int e = 0; e < 32; e += 4) {
+    const float4 c1 = *reinterpret_cast<const float4*>(cv.p + e);
+    const float4 c2 = *reinterpret_cast<const float4*>(cv.p + cv.stride + e);
+    y[e + 0] = fmaf(rs.a, acc[e + 0], fmaf(rs.b, c1.x, c2.x));
+    y[e + 1] = fmaf(rs.a, acc[e + 1], fmaf(rs.b, c1.y, c2.y));
+    y[e + 2] = fmaf(rs.a, acc[e + 2], fmaf(rs.b, c1.z, c2.z));
+    y[e + 3] = fmaf(rs.a, acc[e + 3], fmaf(rs.b, c1.w, c2.w));
   }
 }
 
@@ -337,6 +320,7 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 // head-major scatter of EpiQKV.
 struct EpiQKVAffine {
   static constexpr bool kPreload = false;
+  static constexpr int kColVecs = 2;
   using RowState = AffineRow;
   EpiQKV scatter;
   const float2* stats;
@@ -347,10 +331,11 @@ struct EpiQKVAffine {
   __device__ AffineRow row_state(int row) const {
     return ln_row_state(stats, stats_ld, ln_cols, eps, row);
   }
+  __device__ const float* colvec(int v) const { return v == 0 ? c1 : c2; }
   __device__ void operator()(int row, int col0, const float (&acc)[32], int nvalid,
-                             const AffineRow& rs) const {
+                             const AffineRow& rs, const ColView& cv) const {
     float y[32];
-    affine32(y, acc, col0, nvalid, rs, c1, c2);
+    affine32(y, acc, rs, cv);
     scatter(row, col0, y, nvalid);
   }
 };
@@ -358,6 +343,7 @@ struct EpiQKVAffine {
 // MLP-in projection with the LayerNorm/adaLN fold and GELU(tanh).
 struct EpiGeluAffine {
   static constexpr bool kPreload = false;
+  static constexpr int kColVecs = 2;
   using RowState = AffineRow;
   bf16* z;
   int ld;
@@ -369,10 +355,11 @@ struct EpiGeluAffine {
   __device__ AffineRow row_state(int row) const {
     return ln_row_state(stats, stats_ld, ln_cols, eps, row);
   }
+  __device__ const float* colvec(int v) const { return v == 0 ? c1 : c2; }
   __device__ void operator()(int row, int col0, const float (&acc)[32], int nvalid,
-                             const AffineRow& rs) const {
+                             const AffineRow& rs, const ColView& cv) const {
     float y[32];
-    affine32(y, acc, col0, nvalid, rs, c1, c2);
+    affine32(y, acc, rs, cv);
     bf16* o = z + size_t(row) * ld + col0;
     if (nvalid == 32) {
 #pragma unroll
