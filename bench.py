@@ -25,9 +25,13 @@ tokens = 1024 px), random-init weights from the reference's own RNG stream
            sampled toy_layer_forward units at the true shape, extrapolated to
            a full image (a full C2 image is ~1e14 FLOP on an fp64 scalar loop).
 
-Under torchrun with N > 1 ranks, rank 0 drives all N GPUs of the node (one
-stage per GPU, one CUDA stream per stage); the other ranks join the barriers
-and the max-over-ranks timing reduction.
+Under torchrun with N > 1 ranks there is one process per GPU: rank d owns
+pipeline stage d (its L/N layers) on GPU LOCAL_RANK, and stage-boundary
+activations / the returned eps go straight into the neighbour's landing
+buffers over peer memory (NVLink, CUDA IPC; rank_plan.h). Each rank times
+its own stream with CUDA events; the reported time is the max over ranks.
+Without torchrun, --gpus N drives N devices from one process (one stream
+per stage).
 """
 from __future__ import annotations
 
@@ -238,73 +242,96 @@ def run_ours(args, c, world, rank):
     n = args.gpus
     M = args.patches or n
     peaks, peak_kind = load_peaks()
-    result = None
-    if rank == 0:
+    px = c.get("block") == "pixart"
+    t_build = time.perf_counter()
+    if world > 1:
+        # one process per GPU: this rank owns stage `rank` (rank mode); stage
+        # boundaries go over peer memory (NVLink / CUDA IPC), see rank_plan.h
+        if world != n:
+            raise SystemExit(f"--gpus {n} must equal the torchrun world size {world}")
+        # (on a box with fewer GPUs than ranks, ranks share devices round-robin:
+        # correctness runs of the multi-process path on one GPU)
+        local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        if px:
+            model = pf.PixArtCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"],
+                                             c["T"], rank, world, local)
+        else:
+            model = pf.ToyDiTCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], rank,
+                                             world, local)
+        pf.connect_distributed(model)
+        devices = [local]
+    else:
         torch.cuda.set_device(0)
         devices = list(range(n))
-        t_build = time.perf_counter()
-        if c.get("block") == "pixart":
-            model = pf.PixArtCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n, devices)
+        if px:
+            model = pf.PixArtCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n,
+                                  devices)
         else:
             model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
-        t_build = time.perf_counter() - t_build
-        mlp = model.mlp_hidden
-        x0 = pf.make_initial_latent(0, c["p"], c["hs"])
-        x0_dev = torch.from_numpy(x0.astype(np.float32)).cuda()
-        x_dev = torch.empty_like(x0_dev)
-        stream = torch.cuda.Stream()
-        sp = stream.cuda_stream
+    t_build = time.perf_counter() - t_build
+    mlp = model.mlp_hidden
+    x0 = pf.make_initial_latent(0, c["p"], c["hs"])
+    holds_x = rank == 0
+    x0_dev = torch.from_numpy(x0.astype(np.float32)).cuda() if holds_x else None
+    x_dev = torch.empty_like(x0_dev) if holds_x else None
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
 
-        def one_image():
+    def one_image():
+        if holds_x:
             x_dev.copy_(x0_dev)
-            model.run_pipefusion_device(x_dev.data_ptr(), c["S"], M, c["W"], 0.1, sp)
+        model.run_pipefusion_device(x_dev.data_ptr() if holds_x else 0, c["S"], M, c["W"], 0.1,
+                                    sp)
 
-        with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                one_image()
-            model.synchronize(sp)
-            launches = model.last_launch_count()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            one_image()
+        model.synchronize(sp)
+        launches = model.last_launch_count()
     barrier(world)
-    if rank == 0:
+    torch.cuda.synchronize()
+    with ClockSampler(devices if world == 1 else [devices[0]]) as clocks:
+        with torch.cuda.stream(stream):
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            for _ in range(args.steps):
+                one_image()
+            ev1.record(stream)
+            model.synchronize(sp)
         torch.cuda.synchronize()
-        with ClockSampler(list(range(n))) as clocks:
-            with torch.cuda.stream(stream):
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev0.record(stream)
-                for _ in range(args.steps):
-                    one_image()
-                ev1.record(stream)
-                model.synchronize(sp)
-            torch.cuda.synchronize()
-            ms = ev0.elapsed_time(ev1)
-        clock_info = clocks.summary()
-    else:
-        ms = 0.0
+        ms = ev0.elapsed_time(ev1)
+    clock_info = clocks.summary()
     ms = max_over_ranks(ms, world)
     barrier(world)
-    if rank != 0:
-        return None
 
     sec_per_image = ms / 1e3 / args.steps
-    # ---- e2e through the C ABI with host buffers
+    # ---- e2e through the C ABI with host buffers (all ranks call it together)
     e2e_times = []
     out = None
     for i in range(max(2, args.steps) + 1):
+        barrier(world)
         t0 = time.perf_counter()
-        out = model.run_pipefusion(x0, c["S"], M, c["W"], 0.1)
-        dt = time.perf_counter() - t0
+        out = model.run_pipefusion(x0 if holds_x else None, c["S"], M, c["W"], 0.1)
+        dt = max_over_ranks(time.perf_counter() - t0, world)
         if i > 0:
             e2e_times.append(dt)
     e2e = statistics.mean(e2e_times)
-    finite = bool(np.isfinite(out.final_x).all())
-    # ---- per-kernel CUDA-event profile of one extra image
+    # ---- per-kernel CUDA-event profile of one extra image (every rank profiles
+    # its own stage; rank 0's is reported)
     model.set_profiling(True)
+    barrier(world)
     with torch.cuda.stream(stream):
         one_image()
         model.synchronize(sp)
     prof = model.kernel_profile()
     model.set_profiling(False)
+    barrier(world)
+    if rank != 0:
+        return None
+    finite = bool(np.isfinite(out.final_x).all())
+    # ---- per-kernel CUDA-event profile of one extra image
     gemm_kinds = ["gemm_qkv", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out", "gemm_cross_q",
                   "gemm_cross_out"]
     dom = max((k for k in prof if k not in ("sampler", "conditioning")),
@@ -339,6 +366,8 @@ def run_ours(args, c, world, rank):
         "metric": METRIC, "value": sec_per_image, "unit": UNIT, "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "processes": ("one per GPU (rank mode, peer-memory stage boundaries)" if world > 1
+                      else "one"),
         "dtype": "bf16", "data": "synthetic (reference RNG: build_toy_model seed 0, "
                                   "make_initial_latent seed 0)",
         "config": {"workload": c["name"], "layers": c["L"], "hidden_size": c["hs"],
@@ -358,6 +387,7 @@ def run_ours(args, c, world, rank):
                      "gemm_all_frac": (gemm_fl / (gemm_ms * 1e-3) / 1e12) / peak_tf},
         "kernels": kernels,
         "gpu_launches": launches * args.steps,
+        "gpu_launches_note": ("rank 0's kernels" if world > 1 else "all stages"),
         "clocks": clock_info,
         "finite": finite,
         "model_build_s": t_build,

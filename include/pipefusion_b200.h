@@ -100,6 +100,39 @@ pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout la
 /* 0 = toy block, 1 = PixArt block, -1 = NULL context. */
 int pf_block_kind(const pf_ctx* ctx);
 
+/* ---- One process per GPU ("rank mode") ----
+ * The reference runs one worker thread per stage exchanging PatchMsg values
+ * over bounded channels (run_pipefusion_threads, execute.cpp:231-385). In rank
+ * mode each process (or each context of one process) owns stage `rank` of
+ * `world` on CUDA device `device` (layers [rank*L/world, (rank+1)*L/world)),
+ * and the stage-boundary messages -- activations to rank+1, the last stage's
+ * eps back to rank 0 -- are written straight into the receiver's landing
+ * buffers over peer memory (NVLink / CUDA IPC), with stream-ordered
+ * signal/acknowledge counters instead of channels. Setup:
+ *   1. pf_create_*_rank on every rank (same seed and shape everywhere);
+ *   2. pf_export_peer -> a pf_peer_blob_size() byte blob per rank, exchanged
+ *      through any host channel (the Python layer uses torch.distributed);
+ *   3. pf_connect_peers(ctx, blob of rank-1, blob of rank+1) (mod world).
+ * Then every rank calls pf_run_pipefusion[_device] with the same arguments;
+ * only rank 0 reads x_init and writes x_out (NULL is fine elsewhere), and
+ * the stats are this rank's stage's share (sum fresh/stale over ranks). */
+pf_status pf_create_toy_rank(uint64_t seed, const pf_model_desc* desc, int rank, int world,
+                             int device, pf_ctx** out);
+pf_status pf_create_pixart_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                                int rank, int world, int device, pf_ctx** out);
+size_t pf_peer_blob_size(void);
+pf_status pf_export_peer(pf_ctx* ctx, void* blob, size_t capacity);
+pf_status pf_connect_peers(pf_ctx* ctx, const void* pred_blob, const void* succ_blob);
+/* rank / world of a context (0 / 1 for a single-process context) */
+int pf_rank(const pf_ctx* ctx);
+int pf_world(const pf_ctx* ctx);
+/* The op list rank `rank` executes (rank_plan.h; host only, no GPU):
+ * 8 int32 per op {kind, t, patch, row0, rows, msg, overlap, flag}; kinds
+ * 0 prepare, 1 compute, 2 send, 3 recv, 4 ack, 5 latent update. Returns the
+ * op count (ops may be NULL to query it), or -1 on invalid arguments. */
+int64_t pf_rank_plan(int rank, int world, int steps, int patches, int warmup, int64_t seq_len,
+                     int32_t* ops, int64_t capacity);
+
 void pf_destroy(pf_ctx* ctx);
 
 /* Message of the last failure on this context (or of the last failed

@@ -25,7 +25,8 @@ import numpy as np
 __all__ = [
     "LIB_PATH", "load_library", "ValidationError", "NumericError", "CudaError",
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
-    "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda",
+    "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda", "rank_plan",
+    "PLAN_KINDS", "connect_ranks", "connect_distributed",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
@@ -33,7 +34,9 @@ LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
 # Every symbol declared in include/pipefusion_b200.h and pipefusion_b200_debug.h.
 EXPORTED_SYMBOLS = [
     "pf_create_toy", "pf_create", "pf_create_pixart", "pf_set_text", "pf_block_kind",
-    "pf_layer_forward_t", "pf_destroy", "pf_last_error",
+    "pf_layer_forward_t", "pf_destroy", "pf_last_error", "pf_create_toy_rank",
+    "pf_create_pixart_rank", "pf_peer_blob_size", "pf_export_peer", "pf_connect_peers",
+    "pf_rank", "pf_world", "pf_rank_plan",
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
@@ -97,6 +100,18 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_set_text.argtypes = [vp, dptr, i64, i32]
     lib.pf_block_kind.argtypes = [vp]
     lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
+    lib.pf_create_toy_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
+                                       ctypes.POINTER(vp)]
+    lib.pf_create_pixart_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32,
+                                          i32, i32, ctypes.POINTER(vp)]
+    lib.pf_peer_blob_size.restype = ctypes.c_size_t
+    lib.pf_export_peer.argtypes = [vp, vp, ctypes.c_size_t]
+    lib.pf_connect_peers.argtypes = [vp, vp, vp]
+    lib.pf_rank.argtypes = [vp]
+    lib.pf_world.argtypes = [vp]
+    lib.pf_rank_plan.argtypes = [i32, i32, i32, i32, i32, i64, ctypes.POINTER(ctypes.c_int32),
+                                 i64]
+    lib.pf_rank_plan.restype = i64
     lib.pf_destroy.argtypes = [vp]
     lib.pf_destroy.restype = None
     lib.pf_last_error.argtypes = [vp]
@@ -185,13 +200,29 @@ class ToyDiTCuda:
 
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, workers: int = 1,
-                 devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0):
+                 devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0,
+                 _rank=None):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         self.layers, self.hidden_size, self.heads = layers, hidden_size, heads
         self.mlp_hidden = mlp_hidden_of(hidden_size, mlp_ratio)
         self.seq_len, self.workers = seq_len, workers
         desc = _Desc(layers, hidden_size, heads, self.mlp_hidden, seq_len)
+        self.rank, self.world = 0, 1
+        if _rank is not None:
+            # rank mode: this context holds stage `rank` of `workers` on `device`
+            rank, device = _rank
+            self.rank, self.world = rank, workers
+            if _text_tokens:
+                st = self._lib.pf_create_pixart_rank(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                                     _text_tokens, rank, workers, device,
+                                                     ctypes.byref(self._ctx))
+            else:
+                st = self._lib.pf_create_toy_rank(ctypes.c_uint64(seed), ctypes.byref(desc), rank,
+                                                  workers, device, ctypes.byref(self._ctx))
+            if st != PF_OK:
+                _raise(st, self._lib.pf_last_error(None).decode())
+            return
         devs = list(devices) if devices is not None else [0] * workers
         if len(devs) != workers:
             raise ValidationError("devices must list one CUDA device per worker")
@@ -212,6 +243,25 @@ class ToyDiTCuda:
                                      dev_arr, workers, ctypes.byref(self._ctx))
         if st != PF_OK:
             _raise(st, self._lib.pf_last_error(None).decode())
+
+    @classmethod
+    def rank_stage(cls, seed: int, layers: int, hidden_size: int, heads: int, mlp_ratio: float,
+                   seq_len: int, rank: int, world: int, device: int = 0) -> "ToyDiTCuda":
+        """One process (or context) per stage: stage `rank` of `world` on
+        `device` (the reference's worker thread d of run_pipefusion_threads).
+        Connect the ranks with connect_ranks / connect_distributed."""
+        obj = cls.__new__(cls)
+        ToyDiTCuda.__init__(obj, seed, layers, hidden_size, heads, mlp_ratio, seq_len, world,
+                            None, _rank=(rank, device))
+        return obj
+
+    def export_peer(self) -> bytes:
+        buf = ctypes.create_string_buffer(int(self._lib.pf_peer_blob_size()))
+        _raise(self._lib.pf_export_peer(self._ctx, buf, len(buf)), self._err())
+        return buf.raw
+
+    def connect_peers(self, pred: bytes, succ: bytes) -> None:
+        _raise(self._lib.pf_connect_peers(self._ctx, pred, succ), self._err())
 
     @classmethod
     def from_weights(cls, layer_mats, condition_bias, heads: int, seq_len: int,
@@ -263,19 +313,29 @@ class ToyDiTCuda:
     def run_pipefusion(self, x_init, steps: int, patches: int, warmup: int,
                        eta: float) -> ParallelRunResult:
         """ditsim::run_pipefusion (execute.hpp:124-127) on the GPU stages."""
+        per = max(0, patches * (steps - warmup))
+        stages = 1 if self.world > 1 else self.workers
+        cap = stages * per
+        ff = (ctypes.c_double * max(1, cap))()
+        st = _Stats(0, 0, ff, cap)
+        if self.rank > 0:
+            # rank mode, not rank 0: the latent lives on rank 0
+            status = self._lib.pf_run_pipefusion(self._ctx, None, PF_ROW_MAJOR, steps, patches,
+                                                 warmup, ctypes.c_double(eta), None,
+                                                 ctypes.byref(st))
+            _raise(status, self._err())
+            return ParallelRunResult(None, StalenessStats(st.fresh_patch_reads,
+                                                          st.stale_patch_reads,
+                                                          [list(ff[:per])]))
         x = _f64c(x_init)
         if x.shape != (self.seq_len, self.hidden_size):
             raise ValidationError("latent width does not match the model hidden size")
         out = np.empty_like(x)
-        per = max(0, patches * (steps - warmup))
-        cap = self.workers * per
-        ff = (ctypes.c_double * max(1, cap))()
-        st = _Stats(0, 0, ff, cap)
         status = self._lib.pf_run_pipefusion(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
                                              patches, warmup, ctypes.c_double(eta),
                                              _dptr(out), ctypes.byref(st))
         _raise(status, self._err())
-        fr = [list(ff[d * per:(d + 1) * per]) for d in range(self.workers)]
+        fr = [list(ff[d * per:(d + 1) * per]) for d in range(stages)]
         return ParallelRunResult(out, StalenessStats(st.fresh_patch_reads,
                                                      st.stale_patch_reads, fr))
 
@@ -346,6 +406,16 @@ class PixArtCuda(ToyDiTCuda):
         super().__init__(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers,
                          devices, _text_tokens=text_tokens)
 
+    @classmethod
+    def rank_stage(cls, seed: int, layers: int, hidden_size: int, heads: int, mlp_ratio: float,
+                   seq_len: int, text_tokens: int, rank: int, world: int,
+                   device: int = 0) -> "PixArtCuda":
+        obj = cls.__new__(cls)
+        obj.text_tokens = text_tokens
+        ToyDiTCuda.__init__(obj, seed, layers, hidden_size, heads, mlp_ratio, seq_len, world,
+                            None, _text_tokens=text_tokens, _rank=(rank, device))
+        return obj
+
     def set_text(self, y) -> None:
         y = _f64c(y)
         _raise(self._lib.pf_set_text(self._ctx, _dptr(y), y.shape[0], PF_ROW_MAJOR),
@@ -360,3 +430,38 @@ class PixArtCuda(ToyDiTCuda):
                                               row0, _dptr(k), _dptr(v), PF_ROW_MAJOR)
         _raise(status, self._err())
         return h, k, v
+
+
+PLAN_KINDS = ["prepare", "compute", "send", "recv", "ack", "latent_update"]
+
+
+def rank_plan(rank: int, world: int, steps: int, patches: int, warmup: int,
+              seq_len: int) -> np.ndarray:
+    """Op list of `rank` (include/pipefusion_b200.h pf_rank_plan): int32
+    [n_ops x 8] = kind, t, patch, row0, rows, msg, overlap, flag. Host only."""
+    lib = load_library()
+    n = lib.pf_rank_plan(rank, world, steps, patches, warmup, seq_len, None, 0)
+    if n < 0:
+        raise ValidationError("invalid rank plan arguments")
+    out = np.zeros((max(n, 1), 8), dtype=np.int32)
+    lib.pf_rank_plan(rank, world, steps, patches, warmup, seq_len,
+                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n)
+    return out[:n]
+
+
+def connect_ranks(stages: Sequence[ToyDiTCuda]) -> None:
+    """Connect the rank-mode contexts of one process (stages[d] = rank d)."""
+    blobs = [s.export_peer() for s in stages]
+    n = len(stages)
+    for d, s in enumerate(stages):
+        s.connect_peers(blobs[(d - 1) % n], blobs[(d + 1) % n])
+
+
+def connect_distributed(stage: ToyDiTCuda, group=None) -> None:
+    """Connect this process's rank-mode context to its neighbours, exchanging
+    peer blobs over torch.distributed (any backend; gloo is enough)."""
+    import torch.distributed as dist
+    blobs = [None] * stage.world
+    dist.all_gather_object(blobs, stage.export_peer(), group=group)
+    d, n = stage.rank, stage.world
+    stage.connect_peers(blobs[(d - 1) % n], blobs[(d + 1) % n])

@@ -131,6 +131,12 @@ void export_stats(const pf::RunStats& rs, pf_stats* out) {
   }
 }
 
+// build_toy_model (toy_model.cpp:44-82) streamed layer by layer into the
+// engine (rank-mode engines keep only their own layers).
+void load_toy(pf::Engine& eng, uint64_t seed);
+// pxo_build (oracle/px_oracle.c) streamed likewise.
+void load_pixart(pf::Engine& eng, uint64_t seed, int text_tokens);
+
 }  // namespace
 
 extern "C" {
@@ -143,7 +149,86 @@ pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
     auto ctx = std::make_unique<pf_ctx>();
     pf::ModelShape s = shape_of(desc);
     ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
-    // build_toy_model (toy_model.cpp:44-82), streamed layer by layer.
+    load_toy(*ctx->engine, seed);
+    *out = ctx.release();
+  });
+}
+
+pf_status pf_create_toy_rank(uint64_t seed, const pf_model_desc* desc, int rank, int world,
+                             int device, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    ctx->engine = std::make_unique<pf::Engine>(shape_of(desc), device, rank, world);
+    load_toy(*ctx->engine, seed);
+    *out = ctx.release();
+  });
+}
+
+pf_status pf_create_pixart_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                                int rank, int world, int device, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.block = pf::kBlockPixArt;
+    s.T = text_tokens;
+    ctx->engine = std::make_unique<pf::Engine>(s, device, rank, world);
+    load_pixart(*ctx->engine, seed, text_tokens);
+    *out = ctx.release();
+  });
+}
+
+size_t pf_peer_blob_size(void) { return sizeof(pf::PeerBlob); }
+
+pf_status pf_export_peer(pf_ctx* ctx, void* blob, size_t capacity) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!blob || capacity < sizeof(pf::PeerBlob))
+      throw pf::ValidationError("peer blob buffer too small");
+    const pf::PeerBlob b = ctx->engine->export_peer();
+    std::memcpy(blob, &b, sizeof(b));
+  });
+}
+
+pf_status pf_connect_peers(pf_ctx* ctx, const void* pred_blob, const void* succ_blob) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!pred_blob || !succ_blob) throw pf::ValidationError("NULL peer blob");
+    pf::PeerBlob pred, succ;
+    std::memcpy(&pred, pred_blob, sizeof(pred));
+    std::memcpy(&succ, succ_blob, sizeof(succ));
+    ctx->engine->connect_peers(pred, succ);
+  });
+}
+
+int pf_rank(const pf_ctx* ctx) { return ctx ? ctx->engine->rank() : -1; }
+int pf_world(const pf_ctx* ctx) { return ctx ? ctx->engine->world() : 0; }
+
+int64_t pf_rank_plan(int rank, int world, int steps, int patches, int warmup, int64_t seq_len,
+                     int32_t* ops, int64_t capacity) {
+  if (world < 2 || rank < 0 || rank >= world || steps < 1 || patches < 1 || warmup < 0 ||
+      warmup > steps || seq_len < 1 || seq_len % patches != 0)
+    return -1;
+  const auto plan = pf::build_rank_plan(rank, world, steps, patches, warmup, seq_len);
+  if (ops) {
+    for (size_t i = 0; i < plan.size() && int64_t(i) < capacity; ++i) {
+      const pf::PlanOp& o = plan[i];
+      const int32_t v[8] = {o.kind, o.t, o.patch, o.row0, o.rows, o.msg, o.overlap, o.flag};
+      std::memcpy(ops + 8 * i, v, sizeof(v));
+    }
+  }
+  return int64_t(plan.size());
+}
+
+}  // extern "C"
+
+namespace {
+
+void load_toy(pf::Engine& eng, uint64_t seed) {
+    const pf::ModelShape& s = eng.shape();
     std::mt19937_64 rng(seed);
     const double scale = 1.0 / std::sqrt(double(s.hs));
     std::vector<double> w[6];
@@ -158,14 +243,16 @@ pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
           {w[0].data(), s.hs, s.hs, false},  {w[1].data(), s.hs, s.hs, false},
           {w[2].data(), s.hs, s.hs, false},  {w[3].data(), s.hs, s.hs, false},
           {w[4].data(), s.hs, s.mlp, false}, {w[5].data(), s.mlp, s.hs, false}};
-      ctx->engine->load_layer(l, hm);
+      eng.load_layer(l, hm);
     }
     std::vector<double> cb;
     fill(rng, cb, 1, s.hs, 1.0);
-    ctx->engine->load_condition_bias(cb.data());
-    *out = ctx.release();
-  });
+    eng.load_condition_bias(cb.data());
 }
+
+}  // namespace
+
+extern "C" {
 
 pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_tokens,
                            const int* devices, int n_stages, pf_ctx** out) {
@@ -177,6 +264,17 @@ pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_to
     s.block = pf::kBlockPixArt;
     s.T = text_tokens;
     ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    load_pixart(*ctx->engine, seed, text_tokens);
+    *out = ctx.release();
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void load_pixart(pf::Engine& eng, uint64_t seed, int text_tokens) {
+    const pf::ModelShape& s = eng.shape();
     // Parameter stream of the PixArt block variant (oracle/px_oracle.c,
     // pxo_build): one mt19937_64 seeded with seed ^ "PIXART-A", per layer the
     // 17 parameters in PXO_* order, then the timestep-embedder weights and
@@ -197,7 +295,7 @@ pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_to
         fill(rng, w[i], spec[i].rows, spec[i].cols, spec[i].scale);
         ptrs[i] = w[i].data();
       }
-      ctx->engine->load_layer_px(l, ptrs);
+      eng.load_layer_px(l, ptrs);
     }
     std::vector<double> g[6], cb;
     fill(rng, g[0], 256, hs, 1.0 / 16.0);
@@ -209,15 +307,17 @@ pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_to
     fill(rng, cb, 1, hs, 1.0);
     const double* gp[6] = {g[0].data(), g[1].data(), g[2].data(),
                            g[3].data(), g[4].data(), g[5].data()};
-    ctx->engine->load_px_globals(gp);
-    ctx->engine->load_condition_bias(cb.data());
+    eng.load_px_globals(gp);
+    eng.load_condition_bias(cb.data());
     std::mt19937_64 trng(seed ^ 0x5458542d544f4b53ULL);
     std::vector<double> y;
     fill(trng, y, text_tokens, hs, 1.0);
-    ctx->engine->set_text(y.data());
-    *out = ctx.release();
-  });
+    eng.set_text(y.data());
 }
+
+}  // namespace
+
+extern "C" {
 
 pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout layout) {
   if (!ctx) return PF_VALIDATION;
@@ -283,6 +383,19 @@ pf_status pf_run_pipefusion(pf_ctx* ctx, const double* x_init, pf_layout layout,
                             double* x_out, pf_stats* stats) {
   if (!ctx) return PF_VALIDATION;
   return guarded(&ctx->last_error, [&] {
+    const bool holds_latent = ctx->engine->rank() == 0;  // rank mode: only rank 0 samples
+    if (!holds_latent) {
+      pf::RunStats rs;
+      const pf::Stage& s0 = ctx->engine->stage(0);
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(s0.device);
+      struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
+      ctx->engine->run(nullptr, steps, patches, warmup, float(eta), s0.stream, &rs);
+      ctx->engine->finish(s0.stream);
+      export_stats(rs, stats);
+      return;
+    }
     if (!x_init || !x_out) throw pf::ValidationError("NULL latent pointer");
     upload_x(ctx, x_init, layout);
     pf::RunStats rs;
@@ -303,7 +416,7 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
                                    void* stream, pf_stats* stats) {
   if (!ctx) return PF_VALIDATION;
   return guarded(&ctx->last_error, [&] {
-    if (!x_dev) throw pf::ValidationError("NULL latent pointer");
+    if (!x_dev && ctx->engine->rank() == 0) throw pf::ValidationError("NULL latent pointer");
     pf::RunStats rs;
     ctx->engine->run(x_dev, steps, patches, warmup, float(eta),
                      static_cast<cudaStream_t>(stream), &rs);

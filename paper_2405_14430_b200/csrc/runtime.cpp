@@ -5,7 +5,10 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <sstream>
+
+#include <unistd.h>
 
 namespace pf {
 
@@ -156,6 +159,15 @@ Engine::~Engine() {
   if (ev_start_) {
     DeviceGuard g(stages_[0].device);
     cudaEventDestroy(ev_start_);
+  }
+  if (!stages_.empty()) {
+    DeviceGuard g(stages_[0].device);
+    if (send_stream_) cudaStreamSynchronize(send_stream_);
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (cudaEvent_t e : ev_sent_) cudaEventDestroy(e);
+    if (ev_compute_) cudaEventDestroy(ev_compute_);
+    if (send_stream_) cudaStreamDestroy(send_stream_);
+    dfree(sig_);
   }
   for (auto& kv : graphs_)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -335,6 +347,7 @@ int Engine::stage_of_layer(int layer) const {
 
 void Engine::load_layer(int layer, const HostMatrix (&w)[6]) {
   const int d = stage_of_layer(layer);
+  if (d < 0 && rank_mode() && layer >= 0 && layer < shape_.layers) return;  // another rank's
   if (d < 0) throw ValidationError("layer index out of range");
   Stage& s = stages_[size_t(d)];
   StageLayer& L = s.layers[size_t(layer - s.first_layer)];
@@ -364,6 +377,7 @@ void Engine::load_condition_bias(const double* cb) {
   std::vector<float> v(size_t(shape_.hs));
   for (int i = 0; i < shape_.hs; ++i) v[size_t(i)] = float(cb[i]);
   Stage& s = stages_[0];
+  if (!s.cb) return;  // rank mode, rank > 0: the sampler lives on rank 0
   DeviceGuard g(s.device);
   PF_CUDA_CHECK(cudaMemcpy(s.cb, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
 }
@@ -497,12 +511,10 @@ void Engine::send_rows(int from, int row0, int rows) {
   }
 }
 
-void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
-                         float eta, cudaStream_t caller, RunStats* stats) {
+// check_pipefusion_args (execute.cpp:97-131), with the layer divisibility
+// relaxed (stages may hold L/N rounded up or down).
+void Engine::validate_run(int steps, int patches, int warmup) const {
   const ModelShape& m = shape_;
-  const int n = stage_count();
-  // check_pipefusion_args (execute.cpp:97-131), with the layer divisibility
-  // relaxed (stages may hold L/N rounded up or down).
   if (steps < 1) throw ValidationError("steps must be >= 1");
   if (patches < 1) throw ValidationError("workers and patches must be >= 1");
   if (warmup < 0 || warmup > steps) throw ValidationError("warmup must lie in [0, steps]");
@@ -517,10 +529,17 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     os << "CUDA backend needs seq_len / patches divisible by 8 (got " << r << ")";
     throw ValidationError(os.str());
   }
+}
+
+void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
+                         float eta, cudaStream_t caller, RunStats* stats) {
+  const ModelShape& m = shape_;
+  const int n = stage_count();
+  validate_run(steps, patches, warmup);
+  const int r = int(m.P / patches);
   Stage& s0 = stages_[0];
   prepare_run(patches, steps);
   const bool px = m.block == kBlockPixArt;
-
   // Host bookkeeping: StageBuffers::src (execute.cpp:38-49), sentinel = steps.
   std::vector<std::vector<std::vector<int>>> src(static_cast<size_t>(n));
   RunStats local;
@@ -711,6 +730,10 @@ void Engine::prepare_run(int patches, int steps) {
 
 void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
                  cudaStream_t caller, RunStats* stats) {
+  if (rank_mode()) {
+    enqueue_rank_run(x_dev, steps, patches, warmup, eta, caller, stats);
+    return;
+  }
   if (patches >= 1) prepare_run(patches, steps);
   bool single_device = true;
   for (const Stage& s : stages_) single_device &= s.device == stages_[0].device;
@@ -753,6 +776,7 @@ void Engine::finish(cudaStream_t caller) {
   {
     DeviceGuard g(stages_[0].device);
     PF_CUDA_CHECK(cudaStreamSynchronize(caller));
+    if (send_stream_) PF_CUDA_CHECK(cudaStreamSynchronize(send_stream_));
   }
   int first = INT_MAX;
   for (Stage& s : stages_) {
@@ -849,6 +873,323 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
   }
 }
 
+// ============================================================== rank mode
+namespace {
+
+using MemOpFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct MemOps {
+  MemOpFn wait = nullptr, write = nullptr;
+  bool flush = false;
+};
+
+const MemOps& memops(int device) {
+  static MemOps ops;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      ops.wait = reinterpret_cast<MemOpFn>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      ops.write = reinterpret_cast<MemOpFn>(p);
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, device);
+    ops.flush = v != 0;
+  });
+  if (!ops.wait || !ops.write) throw CudaError("stream memory operations are unavailable");
+  return ops;
+}
+
+// Stream-ordered "wait until *addr >= value" / "*addr = value" (the
+// latter after all prior work of the stream, with a memory barrier).
+void stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t value, int device) {
+  const MemOps& m = memops(device);
+  const unsigned flags = 0x0 /*CU_STREAM_WAIT_VALUE_GEQ*/ | (m.flush ? 0x40000000u : 0u);
+  if (m.wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), value, flags) !=
+      CUDA_SUCCESS)
+    throw CudaError("cuStreamWaitValue32 failed");
+}
+
+void stream_write(cudaStream_t st, uint32_t* addr, uint32_t value, int device) {
+  const MemOps& m = memops(device);
+  if (m.write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), value, 0) !=
+      CUDA_SUCCESS)
+    throw CudaError("cuStreamWriteValue32 failed");
+}
+
+}  // namespace
+
+Engine::Engine(const ModelShape& shape_in, int device, int rank, int world)
+    : shape_(shape_in), rank_(rank), world_(world) {
+  shape_.dh = shape_.hs / std::max(shape_.heads, 1);
+  shape_.dhp = (shape_.dh + 15) / 16 * 16;
+  validate_shape(shape_);
+  if (world < 1 || rank < 0 || rank >= world)
+    throw ValidationError("rank must lie in [0, world)");
+  if (world > shape_.layers) {
+    std::ostringstream os;
+    os << "layer count " << shape_.layers << " is not divisible by workers " << world
+       << " (fewer layers than stages)";
+    throw ValidationError(os.str());
+  }
+  int dev_count = 0;
+  PF_CUDA_CHECK(cudaGetDeviceCount(&dev_count));
+  if (device < 0 || device >= dev_count) {
+    std::ostringstream os;
+    os << "CUDA device " << device << " not present (" << dev_count << " visible)";
+    throw ValidationError(os.str());
+  }
+  stages_.resize(1);
+  Stage& s = stages_[0];
+  s.device = device;
+  try {
+    const int first = int(int64_t(rank) * shape_.layers / world);
+    const int last = int(int64_t(rank + 1) * shape_.layers / world);
+    alloc_stage(s, first, last - first, rank == 0);
+    DeviceGuard g(device);
+    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&send_stream_, cudaStreamNonBlocking));
+    PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming));
+    sig_ = dalloc<uint32_t>(64);
+    if (rank == 0 && world > 1) s.eps = dalloc<float>(size_t(shape_.P) * shape_.hs);
+  } catch (...) {
+    free_stage(s);
+    throw;
+  }
+}
+
+PeerBlob Engine::export_peer() {
+  if (!rank_mode()) throw ValidationError("export_peer needs a rank-mode engine");
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  PeerBlob b;
+  b.rank = rank_;
+  b.world = world_;
+  b.device = s.device;
+  b.block = shape_.block;
+  b.pid = int64_t(getpid());
+  std::memset(&b.h_h32, 0, sizeof(b.h_h32));
+  std::memset(&b.h_hb, 0, sizeof(b.h_hb));
+  std::memset(&b.h_stats, 0, sizeof(b.h_stats));
+  std::memset(&b.h_eps, 0, sizeof(b.h_eps));
+  std::memset(&b.h_sig, 0, sizeof(b.h_sig));
+  PF_CUDA_CHECK(cudaIpcGetMemHandle(&b.h_h32, s.h32));
+  PF_CUDA_CHECK(cudaIpcGetMemHandle(&b.h_hb, s.hb));
+  PF_CUDA_CHECK(cudaIpcGetMemHandle(&b.h_sig, sig_));
+  if (s.px.stats) PF_CUDA_CHECK(cudaIpcGetMemHandle(&b.h_stats, s.px.stats));
+  if (s.eps) PF_CUDA_CHECK(cudaIpcGetMemHandle(&b.h_eps, s.eps));
+  b.p_h32 = reinterpret_cast<uint64_t>(s.h32);
+  b.p_hb = reinterpret_cast<uint64_t>(s.hb);
+  b.p_stats = reinterpret_cast<uint64_t>(s.px.stats);
+  b.p_eps = reinterpret_cast<uint64_t>(s.eps);
+  b.p_sig = reinterpret_cast<uint64_t>(sig_);
+  return b;
+}
+
+void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
+  if (!rank_mode()) throw ValidationError("connect_peers needs a rank-mode engine");
+  for (const PeerBlob* b : {&pred, &succ}) {
+    if (b->magic != 0x50465042) throw ValidationError("peer blob is not a pipefusion endpoint");
+    if (b->world != world_ || b->block != shape_.block)
+      throw ValidationError("peer was created for a different world or block");
+  }
+  if (succ.rank != (rank_ + 1) % world_ || pred.rank != (rank_ - 1 + world_) % world_)
+    throw ValidationError("peer blobs do not belong to this rank's neighbours");
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  const int64_t me = int64_t(getpid());
+  auto open = [&](const PeerBlob& b, const cudaIpcMemHandle_t& h, uint64_t raw) -> void* {
+    if (b.pid == me) {
+      // same process: UVA pointer; enable peer access when on another device
+      if (b.device != s.device) {
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, s.device, b.device);
+        if (ok) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
+      }
+      return reinterpret_cast<void*>(raw);
+    }
+    void* p = nullptr;
+    PF_CUDA_CHECK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ipc_opened_.push_back(p);
+    return p;
+  };
+  succ_sig_ = static_cast<uint32_t*>(open(succ, succ.h_sig, succ.p_sig));
+  pred_sig_ = static_cast<uint32_t*>(open(pred, pred.h_sig, pred.p_sig));
+  if (succ.rank == 0) {
+    succ_eps_ = static_cast<float*>(open(succ, succ.h_eps, succ.p_eps));
+  } else {
+    succ_h32_ = static_cast<float*>(open(succ, succ.h_h32, succ.p_h32));
+    succ_hb_ = static_cast<bf16*>(open(succ, succ.h_hb, succ.p_hb));
+    if (shape_.block == kBlockPixArt)
+      succ_stats_ = static_cast<float2*>(open(succ, succ.h_stats, succ.p_stats));
+  }
+  connected_ = true;
+}
+
+// One rank's share of run_pipefusion (rank_plan.h): its stage's layers on the
+// compute stream, boundary transfers on the send stream, and the message
+// protocol as stream-ordered waits/writes on the peers' signal pages.
+void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, float eta,
+                              cudaStream_t caller, RunStats* stats) {
+  const ModelShape& m = shape_;
+  if (!connected_) throw ValidationError("rank-mode engine is not connected to its peers");
+  validate_run(steps, patches, warmup);
+  if (rank_ == 0 && !x_dev) throw ValidationError("NULL latent pointer");
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  const int dev = s.device;
+  const bool px = m.block == kBlockPixArt;
+  const int r = int(m.P / patches);
+  const size_t hs = size_t(m.hs);
+  if (px) px_alloc_run(s, m, steps);
+  if (int(ev_sent_.size()) < patches) {
+    while (int(ev_sent_.size()) < patches) {
+      cudaEvent_t e;
+      PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev_sent_.push_back(e);
+    }
+  }
+  if (!ev_start_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+  std::vector<bool> sent_before(size_t(patches), false);
+
+  RunStats local;
+  RunStats& st = stats ? *stats : local;
+  st.fresh = 0;
+  st.stale = 0;
+  st.fresh_fraction.assign(1, {});
+  std::vector<std::vector<int>> src(size_t(s.layer_count), std::vector<int>(size_t(patches), steps));
+  codes_.clear();
+  launches_ = 0;
+  prof_.clear();
+  prof_used_.assign(stages_.size(), 0);
+
+  PF_CUDA_CHECK(cudaEventRecord(ev_start_, caller));
+  PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start_, 0));
+  PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_start_, 0));
+  check(reset_flag(s.flag, s.stream), "reset_flag");
+  ++launches_;
+  if (warmup == 0) {
+    const size_t kv = size_t(m.heads) * size_t(m.P) * size_t(m.dhp) * sizeof(bf16);
+    for (StageLayer& L : s.layers) {
+      PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
+      PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kv, s.stream));
+    }
+  }
+  if (px) px_conditioning(s, steps);
+
+  const uint32_t base_in = msgs_in_base_, base_out = msgs_out_base_;
+  const auto plan = build_rank_plan(rank_, world_, steps, patches, warmup, m.P);
+  for (const PlanOp& op : plan) {
+    const int row0 = op.row0, rows = op.rows;
+    switch (op.kind) {
+      case PlanOp::kRecv:
+        stream_wait_geq(s.stream, sig_, base_in + uint32_t(op.msg), dev);
+        break;
+      case PlanOp::kAck:
+        stream_write(op.flag ? send_stream_ : s.stream, pred_sig_ + 1, base_in + uint32_t(op.msg),
+                     dev);
+        break;
+      case PlanOp::kPrepare: {
+        // this rank's previous send of the same rows must have finished reading h32
+        for (int j = 0; j < patches; ++j)
+          if ((op.patch < 0 || op.patch == j) && sent_before[size_t(j)])
+            PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_sent_[size_t(j)], 0));
+        prof_begin(s, kSampler, 0, double(rows) * hs * (op.flag ? 18 : 10));
+        if (px)
+          px_patch_prepare(x_dev, op.flag != 0, row0, rows, op.t, eta);
+        else
+          check(patch_prepare(x_dev, s.eps, s.cb, s.h32, s.hb, row0, rows, m.hs, eta,
+                              op.flag != 0, s.stream), "patch_prepare");
+        prof_end(s);
+        ++launches_;
+        break;
+      }
+      case PlanOp::kLatentUpdate:
+        prof_begin(s, kSampler, 0, double(m.P) * hs * 12);
+        check(latent_update(x_dev, s.eps, eta, size_t(m.P) * hs, s.stream), "latent_update");
+        prof_end(s);
+        ++launches_;
+        break;
+      case PlanOp::kCompute: {
+        const int t = op.t;
+        for (int lf = 0; lf < s.layer_count; ++lf) {
+          auto& sv = src[size_t(lf)];
+          if (op.patch < 0) {
+            std::fill(sv.begin(), sv.end(), t);
+            st.fresh += patches;
+          } else {
+            sv[size_t(op.patch)] = t;
+            for (size_t pi = 0; pi < sv.size(); ++pi) {
+              if (sv[pi] == t) {
+                ++st.fresh;
+              } else if (sv[pi] == t + 1) {
+                ++st.stale;
+              } else {
+                std::ostringstream os;
+                os << "staleness bound violated: patch " << pi << " carries timestep " << sv[pi]
+                   << " while computing timestep " << t;
+                throw NumericError(os.str());
+              }
+            }
+          }
+          codes_.emplace_back(t, s.first_layer + lf);
+          const int code = int(codes_.size()) - 1;
+          if (px) layer_forward_px(s, lf, rows, row0, t, code);
+          else layer_forward(s, lf, rows, row0, code);
+        }
+        if (op.patch >= 0) {
+          int fresh = 0;
+          for (int v : src[0]) fresh += (v == t);
+          st.fresh_fraction[0].push_back(double(fresh) / double(patches));
+        }
+        break;
+      }
+      case PlanOp::kSend: {
+        PF_CUDA_CHECK(cudaEventRecord(ev_compute_, s.stream));
+        PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_compute_, 0));
+        if (op.overlap > 0)
+          stream_wait_geq(send_stream_, sig_ + 1, base_out + uint32_t(op.overlap), dev);
+        const size_t off = size_t(row0) * hs, cnt = size_t(rows) * hs;
+        if (succ_eps_) {
+          PF_CUDA_CHECK(cudaMemcpyAsync(succ_eps_ + off, s.h32 + off, cnt * 4,
+                                        cudaMemcpyDefault, send_stream_));
+        } else {
+          PF_CUDA_CHECK(cudaMemcpyAsync(succ_h32_ + off, s.h32 + off, cnt * 4,
+                                        cudaMemcpyDefault, send_stream_));
+          PF_CUDA_CHECK(cudaMemcpyAsync(succ_hb_ + off, s.hb + off, cnt * 2, cudaMemcpyDefault,
+                                        send_stream_));
+          if (px) {
+            const size_t pitch = size_t(m.P) * sizeof(float2);
+            PF_CUDA_CHECK(cudaMemcpy2DAsync(succ_stats_ + row0, pitch, s.px.stats + row0, pitch,
+                                            size_t(rows) * sizeof(float2), size_t(m.hs / 32),
+                                            cudaMemcpyDefault, send_stream_));
+          }
+        }
+        stream_write(send_stream_, succ_sig_, base_out + uint32_t(op.msg), dev);
+        for (int j = 0; j < patches; ++j)
+          if (op.patch < 0 || op.patch == j) {
+            PF_CUDA_CHECK(cudaEventRecord(ev_sent_[size_t(j)], send_stream_));
+            sent_before[size_t(j)] = true;
+          }
+        break;
+      }
+    }
+  }
+  const uint32_t per_run = uint32_t(plan_messages_per_run(steps, patches, warmup));
+  msgs_in_base_ += per_run;
+  msgs_out_base_ += per_run;
+  // join: the caller waits for both streams
+  PF_CUDA_CHECK(cudaEventRecord(s.ev_fwd, s.stream));
+  PF_CUDA_CHECK(cudaStreamWaitEvent(caller, s.ev_fwd, 0));
+  PF_CUDA_CHECK(cudaEventRecord(ev_compute_, send_stream_));
+  PF_CUDA_CHECK(cudaStreamWaitEvent(caller, ev_compute_, 0));
+}
+
 // ============================================================== PixArt block
 namespace {
 // Transpose an fp64 [K x N] (x.W orientation) matrix to [N x K] (K-major).
@@ -871,6 +1212,18 @@ std::vector<float> to_f32(const double* v, size_t n) {
 void Engine::load_layer_px(int layer, const double* const* prm) {
   if (shape_.block != kBlockPixArt) throw ValidationError("model is not a PixArt block model");
   const int d = stage_of_layer(layer);
+  if (d < 0 && rank_mode() && layer >= 0 && layer < shape_.layers) {
+    // another rank's layer; keep its adaLN row if it is the one after ours
+    Stage& s = stages_[0];
+    if (layer == s.first_layer + s.layer_count) {
+      std::vector<float> sst(size_t(6) * shape_.hs);
+      for (size_t i = 0; i < sst.size(); ++i) sst[i] = float(prm[16][i]);
+      DeviceGuard g(s.device);
+      PF_CUDA_CHECK(cudaMemcpy(s.px.sst + size_t(s.layer_count) * sst.size(), sst.data(),
+                               sst.size() * 4, cudaMemcpyHostToDevice));
+    }
+    return;
+  }
   if (d < 0) throw ValidationError("layer index out of range");
   Stage& s = stages_[size_t(d)];
   StageLayer& L = s.layers[size_t(layer - s.first_layer)];

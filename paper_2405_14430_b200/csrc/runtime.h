@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "rank_plan.h"
 
 namespace pf {
 
@@ -153,9 +154,26 @@ struct RunStats {
   std::vector<std::vector<double>> fresh_fraction;  // per stage
 };
 
+// Peer-memory endpoint of one rank (one process per GPU): IPC handles and,
+// for ranks living in the same process, raw pointers of the buffers its
+// predecessor writes into (landing rows, rank 0's eps) and of its signal
+// page (sig[0]: messages delivered to it, sig[1]: acknowledgements from its
+// successor). Exchanged as an opaque blob through the caller's host channel.
+struct PeerBlob {
+  uint32_t magic = 0x50465042;  // "PFPB"
+  int32_t rank = 0, world = 1, device = 0, block = 0;
+  int64_t pid = 0;
+  cudaIpcMemHandle_t h_h32, h_hb, h_stats, h_eps, h_sig;
+  uint64_t p_h32 = 0, p_hb = 0, p_stats = 0, p_eps = 0, p_sig = 0;
+};
+
 class Engine {
  public:
   Engine(const ModelShape& shape, const std::vector<int>& devices);
+  // Rank mode: one process (or context) per stage. This engine holds stage
+  // `rank` of `world` on `device`; stage boundaries are crossed over peer
+  // memory once connect_peers() has been called on every rank.
+  Engine(const ModelShape& shape, int device, int rank, int world);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -171,6 +189,16 @@ class Engine {
   void load_px_globals(const double* const* g);
   // Text tokens y [T x hs] (row-major fp64) used by every stage's cross-attention.
   void set_text(const double* y);
+
+  // Rank mode.
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  bool rank_mode() const { return world_ > 1; }
+  bool owns_layer(int layer) const { return stage_of_layer(layer) >= 0; }
+  PeerBlob export_peer();
+  void connect_peers(const PeerBlob& pred, const PeerBlob& succ);
+  void enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, float eta,
+                        cudaStream_t caller, RunStats* stats);
 
   const ModelShape& shape() const { return shape_; }
   int stage_count() const { return int(stages_.size()); }
@@ -213,6 +241,22 @@ class Engine {
   void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
   void send_rows(int from, int row0, int rows);
   void prepare_run(int patches, int steps);
+  void validate_run(int steps, int patches, int warmup) const;
+  // rank mode
+  int rank_ = 0, world_ = 1;
+  cudaStream_t send_stream_ = nullptr;
+  uint32_t* sig_ = nullptr;        // local signal page (device): [0] delivered, [1] acked
+  float* succ_h32_ = nullptr;      // successor's landing buffers (peer memory)
+  bf16* succ_hb_ = nullptr;
+  float2* succ_stats_ = nullptr;
+  float* succ_eps_ = nullptr;      // last rank: rank 0's eps buffer
+  uint32_t* succ_sig_ = nullptr;   // successor's signal page
+  uint32_t* pred_sig_ = nullptr;   // predecessor's signal page
+  std::vector<void*> ipc_opened_;
+  bool connected_ = false;
+  uint32_t msgs_in_base_ = 0, msgs_out_base_ = 0;
+  cudaEvent_t ev_compute_ = nullptr;
+  std::vector<cudaEvent_t> ev_sent_;  // per patch: last send of its rows finished
   int px_steps_ = 0;  // S of the enqueued run (layout of the per-run PixArt buffers)
   cudaEvent_t ev_start_ = nullptr;
   int stage_of_layer(int layer) const;
