@@ -206,6 +206,17 @@ pf_status pf_set_profiling(pf_ctx* ctx, int enabled);
 pf_status pf_kernel_profile(pf_ctx* ctx, int kind, double* total_ms,
                             int64_t* launches, double* flops, double* bytes);
 
+/* Measured timeline (the reference's simulate() Timeline, simulate.hpp:32-48,
+ * for comparison with its cost model): when enabled, the next runs record
+ * one span per (stage, patch, step) compute -- stage 0's includes the
+ * sampler / patch split -- and per boundary transfer, with CUDA events (no
+ * graph replay while enabled). pf_timeline() resolves the last run into
+ * `spans`: 6 doubles per span {stage, stream (0 compute, 1 comm), patch
+ * (-1 full), timestep, start_us, dur_us} relative to the run's start on the
+ * caller stream; returns the span count (spans may be NULL) or -1. */
+pf_status pf_set_timeline(pf_ctx* ctx, int enabled);
+int64_t pf_timeline(pf_ctx* ctx, double* spans, int64_t capacity);
+
 /* Introspection for tests and benchmarks. */
 int pf_stage_count(const pf_ctx* ctx);
 int pf_stage_first_layer(const pf_ctx* ctx, int stage);

@@ -250,6 +250,31 @@ class Restatement(_Impl):
         super().__init__(path or RESTATEMENT_LIB)
 
 
+def simulate_pipefusion(layers, hs, heads, seq_len, steps, warmup, devices, patches,
+                        device_flops, link_bandwidth, link_latency=0.0, mlp_ratio=4.0,
+                        bytes_per_element=2, per_message_overhead_s=50e-6):
+    """The reference's own PipeFusion cost model (simulate.cpp:263-342) and
+    trace JSON (timeline_to_trace_json): (makespan_s, trace dict)."""
+    import json
+    lib = ctypes.CDLL(str(REFERENCE_LIB))
+    fn = lib.ref_simulate_pipefusion
+    fn.restype = ctypes.c_longlong
+    fn.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                   ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                   ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _d,
+                   ctypes.c_char_p, ctypes.c_longlong, ctypes.c_char_p, ctypes.c_int]
+    mk = ctypes.c_double()
+    err = ctypes.create_string_buffer(256)
+    args = (layers, hs, heads, mlp_ratio, bytes_per_element, seq_len, steps, warmup, devices,
+            patches, device_flops, link_bandwidth, link_latency, per_message_overhead_s)
+    n = fn(*args, ctypes.byref(mk), None, 0, err, 256)
+    if n < 0:
+        raise OracleError(int(-n), err.value.decode())
+    buf = ctypes.create_string_buffer(int(n) + 1)
+    fn(*args, ctypes.byref(mk), buf, n + 1, err, 256)
+    return mk.value, json.loads(buf.value.decode())
+
+
 class Reference(_Impl):
     prefix = "ref_"
 

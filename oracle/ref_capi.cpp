@@ -1,6 +1,7 @@
 // extern "C" bridge over the UNMODIFIED reference sources (TEST
 // INFRASTRUCTURE ONLY). Built by oracle/Makefile into oracle/_ref/ from
-// /root/reference/proj/src/{toy_model,execute,model,schedule,freshness}.cpp
+// /root/reference/proj/src/{toy_model,execute,model,schedule,freshness,
+// simulate,costmodel}.cpp
 // against oracle/shim/Eigen/Core; it is the reference itself run here, used
 // to pin oracle/pf_oracle.c and as the CPU baseline of bench.py.
 //
@@ -14,6 +15,7 @@
 #include "ditsim/execute.hpp"
 #include "ditsim/freshness.hpp"
 #include "ditsim/schedule.hpp"
+#include "ditsim/simulate.hpp"
 
 using namespace ditsim;
 
@@ -182,3 +184,46 @@ int ref_fresh_series(int n, int m, int steps, int warmup, double* out, int cap) 
 }
 
 }  // extern "C"
+
+
+// simulate() of a PipeFusion plan (simulate.cpp:263-342, 398-415) and its
+// trace JSON (timeline_to_trace_json, simulate.cpp:607-645). Returns the
+// JSON length (copied into out when it fits), or -1/-2 on error.
+extern "C" long long ref_simulate_pipefusion(int layers, int hs, int heads, double mlp_ratio,
+                                             int bytes_per_element, long long seq_len,
+                                             int steps, int warmup, int devices, int patches,
+                                             double device_flops, double link_bandwidth,
+                                             double link_latency, double per_message_overhead_s,
+                                             double* makespan_s, char* out, long long cap,
+                                             char* err, int errcap) {
+  try {
+    ModelSpec model;
+    model.layers = layers;
+    model.hidden_size = hs;
+    model.heads = heads;
+    model.mlp_ratio = mlp_ratio;
+    model.bytes_per_element = bytes_per_element;
+    WorkloadSpec wl;
+    wl.seq_len = seq_len;
+    wl.diffusion_steps = steps;
+    wl.warmup_steps = warmup;
+    ClusterSpec cl;
+    cl.device_count = devices;
+    cl.device_flops = device_flops;
+    cl.link_bandwidth = link_bandwidth;
+    cl.link_latency = link_latency;
+    ComputeModel cm;
+    cm.per_message_overhead_s = per_message_overhead_s;
+    ParallelPlan plan;
+    plan.strategy = Strategy::PipeFusion;
+    plan.degree = devices;
+    plan.patches = patches;
+    const Timeline tl = simulate(plan, model, wl, cl, cm);
+    if (makespan_s) *makespan_s = tl.makespan_s;
+    const std::string js = timeline_to_trace_json(tl);
+    if (out && cap > (long long)js.size()) std::memcpy(out, js.c_str(), js.size() + 1);
+    return (long long)js.size();
+  } catch (const std::exception& e) {
+    return -report(e, err, errcap);
+  }
+}

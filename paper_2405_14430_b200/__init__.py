@@ -26,7 +26,7 @@ __all__ = [
     "LIB_PATH", "load_library", "ValidationError", "NumericError", "CudaError",
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
     "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda", "rank_plan",
-    "PLAN_KINDS", "connect_ranks", "connect_distributed",
+    "PLAN_KINDS", "connect_ranks", "connect_distributed", "trace_json",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "pf_create_toy", "pf_create", "pf_create_pixart", "pf_set_text", "pf_block_kind",
     "pf_layer_forward_t", "pf_destroy", "pf_last_error", "pf_create_toy_rank",
     "pf_create_pixart_rank", "pf_peer_blob_size", "pf_export_peer", "pf_connect_peers",
-    "pf_rank", "pf_world", "pf_rank_plan",
+    "pf_rank", "pf_world", "pf_rank_plan", "pf_set_timeline", "pf_timeline",
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
@@ -112,6 +112,9 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_rank_plan.argtypes = [i32, i32, i32, i32, i32, i64, ctypes.POINTER(ctypes.c_int32),
                                  i64]
     lib.pf_rank_plan.restype = i64
+    lib.pf_set_timeline.argtypes = [vp, i32]
+    lib.pf_timeline.argtypes = [vp, dptr, i64]
+    lib.pf_timeline.restype = i64
     lib.pf_destroy.argtypes = [vp]
     lib.pf_destroy.restype = None
     lib.pf_last_error.argtypes = [vp]
@@ -386,6 +389,21 @@ class ToyDiTCuda:
             out[name] = dict(ms=ms.value, launches=n.value, flops=fl.value, bytes=by.value)
         return out
 
+    def set_timeline(self, enabled: bool) -> None:
+        self._lib.pf_set_timeline(self._ctx, 1 if enabled else 0)
+
+    def timeline(self) -> List[dict]:
+        """Spans of the last run with the timeline enabled (pf_timeline)."""
+        n = self._lib.pf_timeline(self._ctx, None, 0)
+        if n < 0:
+            raise CudaError(self._err())
+        buf = np.zeros((max(n, 1), 6))
+        self._lib.pf_timeline(self._ctx, _dptr(buf), n)
+        return [dict(device=int(r[0]), stream="compute" if r[1] == 0 else "comm",
+                     patch=None if r[2] < 0 else int(r[2]),
+                     timestep=None if r[3] < 0 else int(r[3]), start_us=float(r[4]),
+                     dur_us=float(r[5])) for r in buf[:n]]
+
     def synchronize(self, stream_ptr: int = 0) -> None:
         _raise(self._lib.pf_synchronize(self._ctx, ctypes.c_void_p(stream_ptr)), self._err())
 
@@ -465,3 +483,24 @@ def connect_distributed(stage: ToyDiTCuda, group=None) -> None:
     dist.all_gather_object(blobs, stage.export_peer(), group=group)
     d, n = stage.rank, stage.world
     stage.connect_peers(blobs[(d - 1) % n], blobs[(d + 1) % n])
+
+
+def trace_json(spans: Sequence[dict]) -> dict:
+    """A measured timeline in the reference's trace format
+    (timeline_to_trace_json, simulate.cpp:607-645): events sorted by start,
+    device, stream, label; labels as simulate_pipefusion names them
+    ("warmup t<t>", "stage t<t> p<j>", "send t<t>[ p<j>]")."""
+    events = []
+    for e in spans:
+        t, j = e["timestep"], e["patch"]
+        if e["stream"] == "compute":
+            name = f"warmup t{t}" if j is None else f"stage t{t} p{j}"
+        else:
+            name = f"send t{t}" if j is None else f"send t{t} p{j}"
+        events.append({"name": name, "device": e["device"], "stream": e["stream"],
+                       "start_us": e["start_us"], "dur_us": e["dur_us"], "patch": j,
+                       "timestep": t})
+    events.sort(key=lambda ev: (ev["start_us"], ev["device"], ev["stream"] != "compute",
+                                ev["name"]))
+    makespan = max((ev["start_us"] + ev["dur_us"] for ev in events), default=0.0)
+    return {"makespan_us": makespan, "events": events}

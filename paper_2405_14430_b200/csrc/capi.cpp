@@ -500,6 +500,27 @@ pf_status pf_kernel_profile(pf_ctx* ctx, int kind, double* total_ms, int64_t* la
   });
 }
 
+pf_status pf_set_timeline(pf_ctx* ctx, int enabled) {
+  if (!ctx) return PF_VALIDATION;
+  ctx->engine->set_timeline(enabled != 0);
+  return PF_OK;
+}
+
+int64_t pf_timeline(pf_ctx* ctx, double* spans, int64_t capacity) {
+  if (!ctx) return -1;
+  std::vector<pf::TimelineSpan> tl;
+  pf_status st = guarded(&ctx->last_error, [&] { tl = ctx->engine->collect_timeline(); });
+  if (st != PF_OK) return -1;
+  if (spans)
+    for (size_t i = 0; i < tl.size() && int64_t(i) < capacity; ++i) {
+      const pf::TimelineSpan& e = tl[i];
+      const double v[6] = {double(e.stage), double(e.stream), double(e.patch),
+                           double(e.timestep), e.start_us, e.dur_us};
+      std::memcpy(spans + 6 * i, v, sizeof(v));
+    }
+  return int64_t(tl.size());
+}
+
 int pf_stage_count(const pf_ctx* ctx) { return ctx ? ctx->engine->stage_count() : 0; }
 int pf_stage_first_layer(const pf_ctx* ctx, int stage) {
   if (!ctx || stage < 0 || stage >= ctx->engine->stage_count()) return -1;

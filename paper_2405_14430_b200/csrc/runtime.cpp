@@ -175,6 +175,10 @@ Engine::~Engine() {
     DeviceGuard g(stages_[d].device);
     for (cudaEvent_t e : prof_pool_[d]) cudaEventDestroy(e);
   }
+  if (tl_origin_) {
+    DeviceGuard g(stages_[0].device);
+    cudaEventDestroy(tl_origin_);
+  }
   for (Stage& s : stages_) free_stage(s);
 }
 
@@ -557,8 +561,13 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
 
   // Fork: every stage stream waits for the caller's prior work.
   cudaEvent_t ev_start = ev_start_;
+  tl_.clear();
   {
     DeviceGuard g(s0.device);
+    if (timeline_on_) {
+      if (!tl_origin_) PF_CUDA_CHECK(cudaEventCreate(&tl_origin_));
+      PF_CUDA_CHECK(cudaEventRecord(tl_origin_, caller));
+    }
     PF_CUDA_CHECK(cudaEventRecord(ev_start, caller));
   }
   for (Stage& s : stages_) {
@@ -596,6 +605,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     const int t = steps - 1 - w;
     {
       DeviceGuard g(s0.device);
+      tl_begin(0, 0, -1, t, s0.stream);
       prof_begin(s0, kSampler, 0, double(m.P) * m.hs * (4 + 4 + 2));
       if (px)
         px_patch_prepare(x_dev, false, 0, int(m.P), t, 0.f);
@@ -608,13 +618,17 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     for (int d = 0; d < n; ++d) {
       Stage& s = stages_[size_t(d)];
       DeviceGuard g(s.device);
+      if (d > 0) tl_begin(d, 0, -1, t, s.stream);
       for (int lf = 0; lf < s.layer_count; ++lf) {
         auto& sv = src[size_t(d)][size_t(lf)];
         std::fill(sv.begin(), sv.end(), t);
         st.fresh += patches;
         forward(s, lf, int(m.P), 0, t, next_code(t, s.first_layer + lf));
       }
+      tl_end(s.stream);
+      if (n > 1) tl_begin(d, 1, -1, t, s.stream);
       send_rows(d, 0, int(m.P));
+      if (n > 1) tl_end(s.stream);
     }
     if (n > 1) {
       Stage& last = stages_[size_t(n - 1)];
@@ -640,6 +654,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         DeviceGuard g(s0.device);
         if (q > 0 && n > 1)
           PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[size_t(j)], 0));
+        tl_begin(0, 0, j, t, s0.stream);
         prof_begin(s0, kSampler, 0, double(r) * m.hs * (q > 0 ? 4 + 4 + 4 + 4 + 2 : 4 + 4 + 2));
         if (px)
           px_patch_prepare(x_dev, q > 0, row0, r, t, eta);
@@ -652,6 +667,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       for (int d = 0; d < n; ++d) {
         Stage& s = stages_[size_t(d)];
         DeviceGuard g(s.device);
+        if (d > 0) tl_begin(d, 0, j, t, s.stream);
         for (int lf = 0; lf < s.layer_count; ++lf) {
           auto& sv = src[size_t(d)][size_t(lf)];
           sv[size_t(j)] = t;
@@ -677,7 +693,10 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
           for (int v : s0v) fresh += (v == t);
           st.fresh_fraction[size_t(d)].push_back(double(fresh) / double(s0v.size()));
         }
+        tl_end(s.stream);
+        if (n > 1) tl_begin(d, 1, j, t, s.stream);
         send_rows(d, row0, r);
+        if (n > 1) tl_end(s.stream);
         if (d == n - 1 && n > 1)
           PF_CUDA_CHECK(cudaEventRecord(s0.ev_eps[size_t(j)], s.stream));
       }
@@ -737,7 +756,7 @@ void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
   if (patches >= 1) prepare_run(patches, steps);
   bool single_device = true;
   for (const Stage& s : stages_) single_device &= s.device == stages_[0].device;
-  if (!graphs_enabled_ || profiling_ || caller == nullptr || !single_device) {
+  if (!graphs_enabled_ || profiling_ || timeline_on_ || caller == nullptr || !single_device) {
     enqueue_run(x_dev, steps, patches, warmup, eta, caller, stats);
     return;
   }
@@ -871,6 +890,35 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
     os << "non-finite activation at timestep 0, layer " << layer;
     throw NumericError(os.str());
   }
+}
+
+// ============================================================== timeline
+void Engine::tl_begin(int stage, int stream, int patch, int t, cudaStream_t st) {
+  if (!timeline_on_) return;
+  const int d = stage < int(stages_.size()) ? stage : 0;
+  TlRec r{stage, stream, patch, t, prof_event(d), prof_event(d)};
+  PF_CUDA_CHECK(cudaEventRecord(r.a, st));
+  tl_.push_back(r);
+}
+
+void Engine::tl_end(cudaStream_t st) {
+  if (!timeline_on_) return;
+  PF_CUDA_CHECK(cudaEventRecord(tl_.back().b, st));
+}
+
+std::vector<TimelineSpan> Engine::collect_timeline() {
+  std::vector<TimelineSpan> out;
+  if (!tl_origin_) return out;
+  DeviceGuard g(stages_[0].device);
+  PF_CUDA_CHECK(cudaEventSynchronize(tl_origin_));
+  for (const TlRec& r : tl_) {
+    PF_CUDA_CHECK(cudaEventSynchronize(r.b));
+    float a = 0.f, b = 0.f;
+    PF_CUDA_CHECK(cudaEventElapsedTime(&a, tl_origin_, r.a));
+    PF_CUDA_CHECK(cudaEventElapsedTime(&b, tl_origin_, r.b));
+    out.push_back({r.stage, r.stream, r.patch, r.t, 1e3 * double(a), 1e3 * double(b - a)});
+  }
+  return out;
 }
 
 // ============================================================== rank mode
@@ -1068,6 +1116,11 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   prof_.clear();
   prof_used_.assign(stages_.size(), 0);
 
+  tl_.clear();
+  if (timeline_on_) {
+    if (!tl_origin_) PF_CUDA_CHECK(cudaEventCreate(&tl_origin_));
+    PF_CUDA_CHECK(cudaEventRecord(tl_origin_, caller));
+  }
   PF_CUDA_CHECK(cudaEventRecord(ev_start_, caller));
   PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start_, 0));
   PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_start_, 0));
@@ -1099,6 +1152,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         for (int j = 0; j < patches; ++j)
           if ((op.patch < 0 || op.patch == j) && sent_before[size_t(j)])
             PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_sent_[size_t(j)], 0));
+        tl_begin(rank_, 0, op.patch, op.t, s.stream);
         prof_begin(s, kSampler, 0, double(rows) * hs * (op.flag ? 18 : 10));
         if (px)
           px_patch_prepare(x_dev, op.flag != 0, row0, rows, op.t, eta);
@@ -1117,6 +1171,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         break;
       case PlanOp::kCompute: {
         const int t = op.t;
+        if (rank_ != 0) tl_begin(rank_, 0, op.patch, t, s.stream);
         for (int lf = 0; lf < s.layer_count; ++lf) {
           auto& sv = src[size_t(lf)];
           if (op.patch < 0) {
@@ -1142,6 +1197,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           if (px) layer_forward_px(s, lf, rows, row0, t, code);
           else layer_forward(s, lf, rows, row0, code);
         }
+        tl_end(s.stream);
         if (op.patch >= 0) {
           int fresh = 0;
           for (int v : src[0]) fresh += (v == t);
@@ -1154,6 +1210,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_compute_, 0));
         if (op.overlap > 0)
           stream_wait_geq(send_stream_, sig_ + 1, base_out + uint32_t(op.overlap), dev);
+        tl_begin(rank_, 1, op.patch, op.t, send_stream_);
         const size_t off = size_t(row0) * hs, cnt = size_t(rows) * hs;
         if (succ_eps_) {
           PF_CUDA_CHECK(cudaMemcpyAsync(succ_eps_ + off, s.h32 + off, cnt * 4,
@@ -1170,6 +1227,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
                                             cudaMemcpyDefault, send_stream_));
           }
         }
+        tl_end(send_stream_);
         stream_write(send_stream_, succ_sig_, base_out + uint32_t(op.msg), dev);
         for (int j = 0; j < patches; ++j)
           if (op.patch < 0 || op.patch == j) {

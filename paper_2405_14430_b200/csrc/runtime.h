@@ -148,6 +148,17 @@ struct KernelProfile {
   double bytes[kKindCount] = {0};     // algorithmic HBM bytes (sampler)
 };
 
+// One measured span of a run (the reference's TimelineEvent,
+// simulate.hpp:32-42): a stage's compute for one (patch, step) -- stage 0's
+// span includes the sampler / patch split -- or a boundary transfer.
+struct TimelineSpan {
+  int stage = 0;
+  int stream = 0;  // 0 compute, 1 comm
+  int patch = -1;  // -1: full sequence (warmup)
+  int timestep = -1;
+  double start_us = 0.0, dur_us = 0.0;
+};
+
 struct RunStats {
   int64_t fresh = 0;
   int64_t stale = 0;
@@ -229,6 +240,10 @@ class Engine {
 
   // Bracket every kernel of the next runs with CUDA events (stage streams).
   void set_profiling(bool on) { profiling_ = on; }
+  // Record per-(stage, patch, step) compute and transfer spans of the next
+  // runs (single-device engines and rank mode; disables graph replay).
+  void set_timeline(bool on) { timeline_on_ = on; }
+  std::vector<TimelineSpan> collect_timeline();
   // Resolve the events of the last profiled run (after finish()).
   KernelProfile collect_profile();
 
@@ -282,6 +297,15 @@ class Engine {
   bool graphs_enabled_ = true;
 
   bool profiling_ = false;
+  bool timeline_on_ = false;
+  struct TlRec {
+    int stage, stream, patch, t;
+    cudaEvent_t a, b;
+  };
+  std::vector<TlRec> tl_;
+  cudaEvent_t tl_origin_ = nullptr;
+  void tl_begin(int stage, int stream, int patch, int t, cudaStream_t st);
+  void tl_end(cudaStream_t st);
   std::vector<ProfRec> prof_;
   std::vector<std::vector<cudaEvent_t>> prof_pool_;  // per stage
   std::vector<size_t> prof_used_;
