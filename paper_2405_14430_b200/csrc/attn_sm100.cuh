@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
+  ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
 
   // With NT = 2 (384 threads) registers move from the producer warpgroup
   // (TMA, MMA, allocator) to the two softmax warpgroups.

@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
+  ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
 
   if (warp == 0) {
     if (lane == 0) {
@@ -365,6 +367,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
+  ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
 
   if (warp == 0) {
     if (lane == 0) {
@@ -638,6 +642,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
+  ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
 
   if (warp == 0) {
     if (lane == 0) {
@@ -825,6 +831,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
+  ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
 
   if (warp == 0) {
     if (lane == 0) {

@@ -1,6 +1,7 @@
 // Kernel instantiations and host launchers: tcgen05 GEMM with the toy-DiT
 // epilogues, tcgen05 attention, and the bandwidth-bound sampler kernels.
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -74,6 +75,14 @@ static bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void*
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 int device_sm_count(int device) {
@@ -435,8 +444,7 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int rows,
   if (e != cudaSuccess) return e;
   const int tiles = ((rows + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
   const int grid = tiles < sm_count ? tiles : sm_count;
-  kern<<<grid, 256, L::kTotal, stream>>>(a, b, rows, row0, N, K, epi);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N, K, epi);
 }
 
 template <int BN, int STAGES, class E>
@@ -450,8 +458,7 @@ cudaError_t launch_gemm2sm(const CUtensorMap& a, const CUtensorMap& b, int rows,
   const int tiles = ((rows + 2 * kGemmBM - 1) / (2 * kGemmBM)) * ((N + BN - 1) / BN);
   const int pairs = sm_count / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, 256, L::kTotal, stream>>>(a, b, rows, row0, N, K, epi);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N, K, epi);
 }
 
 template <bool kTwoSm, int BN, int STAGES>
@@ -494,8 +501,8 @@ cudaError_t launch_resid2(int grid, uint32_t smem, cudaStream_t stream, const CU
                           int K, const ResidTmaArgs& args) {
   cudaError_t e = ensure_smem_attr<kern>(smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, 256, smem, stream>>>(a, b, *ep.tm_h32, *ep.tm_hb, rows, row0, N, K, args);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(256), smem, stream, a, b, *ep.tm_h32, *ep.tm_hb, rows,
+                    row0, N, K, args);
 }
 
 }  // namespace
@@ -623,8 +630,8 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.part_ml = a.work + size_t(splits) * a.heads * prm.rows_pad * DHP;
   }
   dim3 grid(q_ctas, a.heads, splits);
-  attn_fwd_kernel<DHP, NT><<<grid, L::kThreads, L::kTotal, stream>>>(q, k, v, prm);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(attn_fwd_kernel<DHP, NT>, grid, dim3(L::kThreads), L::kTotal,
+                             stream, q, k, v, prm);
   if (e != cudaSuccess || splits == 1) return e;
   const int total = a.rows * a.heads * (DHP / 16);
   attn_combine_kernel<DHP><<<(total + 255) / 256, 256, 0, stream>>>(prm);
@@ -661,6 +668,8 @@ __global__ void patch_prepare_kernel(float* __restrict__ x,
                                      float* __restrict__ h32, bf16* __restrict__ hb,
                                      size_t base, size_t n4, int hs4, float eta,
                                      int update) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
        i += size_t(gridDim.x) * blockDim.x) {
     const size_t off = base + 4 * i;
@@ -687,6 +696,8 @@ __global__ void patch_prepare_kernel(float* __restrict__ x,
 __global__ void latent_update_kernel(float* __restrict__ x,
                                      const float* __restrict__ src, float eta,
                                      size_t n4) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
        i += size_t(gridDim.x) * blockDim.x) {
     float4 xv = reinterpret_cast<float4*>(x)[i];
@@ -726,15 +737,14 @@ cudaError_t patch_prepare(float* x, const float* eps, const float* cb, float* h3
                           bool update, cudaStream_t stream) {
   const size_t base = size_t(row0) * hs;
   const size_t n4 = size_t(rows) * hs / 4;
-  patch_prepare_kernel<<<ew_grid(n4), 256, 0, stream>>>(
-      x, eps, cb, h32, hb, base, n4, hs / 4, eta, update ? 1 : 0);
-  return cudaGetLastError();
+  return launch_pdl(patch_prepare_kernel, dim3(ew_grid(n4)), dim3(256), 0, stream, x, eps, cb,
+                    h32, hb, base, n4, hs / 4, eta, update ? 1 : 0);
 }
 
 cudaError_t latent_update(float* x, const float* src, float eta, size_t n,
                           cudaStream_t stream) {
-  latent_update_kernel<<<ew_grid(n / 4), 256, 0, stream>>>(x, src, eta, n / 4);
-  return cudaGetLastError();
+  return launch_pdl(latent_update_kernel, dim3(ew_grid(n / 4)), dim3(256), 0, stream, x, src, eta,
+                    n / 4);
 }
 
 cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream) {

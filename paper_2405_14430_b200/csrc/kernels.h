@@ -8,6 +8,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <utility>
 
 namespace pf {
 
@@ -25,6 +26,26 @@ bool encode_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t inner,
                         uint32_t box_outer, int swizzle_bytes);
 
 int device_sm_count(int device);
+
+// Launch with programmatic dependent launch enabled (the kernel calls
+// ptx::pdl_wait() before its first dependent memory access). PF_NO_PDL=1 in
+// the environment turns the attribute off (plain stream serialisation).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 enum class Epi : int { StoreF32 = 0, QKV = 1, Residual = 2, Tanh = 3, Gelu = 4, Fold = 5 };
 

@@ -132,6 +132,8 @@ __global__ void px_patch_prepare_kernel(float* __restrict__ x, const float* __re
                                         float* __restrict__ h32, bf16* __restrict__ hb,
                                         float2* __restrict__ stats, int stats_ld, int row0,
                                         size_t n4, int hs4, float eta, int update) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
   const size_t stride = size_t(gridDim.x) * blockDim.x;
   for (size_t i0 = size_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < n4; i0 += stride) {
     const size_t i = i0 + (threadIdx.x & 31);
@@ -212,9 +214,9 @@ cudaError_t px_patch_prepare(float* x, const float* eps, const float* cb, const 
                              int rows, int hs, float eta, bool update, cudaStream_t stream) {
   if (hs % 32 != 0) return cudaErrorInvalidValue;
   const size_t n4 = size_t(rows) * hs / 4;
-  px_patch_prepare_kernel<<<grid_for(n4, 256), 256, 0, stream>>>(
-      x, eps, cb, scale, h32, hb, stats, stats_ld, row0, n4, hs / 4, eta, update ? 1 : 0);
-  return cudaGetLastError();
+  return launch_pdl(px_patch_prepare_kernel, dim3(grid_for(n4, 256)), dim3(256), 0, stream, x,
+                    eps, cb, scale, h32, hb, stats, stats_ld, row0, n4, hs / 4, eta,
+                    update ? 1 : 0);
 }
 
 }  // namespace pf

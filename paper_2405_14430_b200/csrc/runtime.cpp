@@ -486,12 +486,13 @@ KernelProfile Engine::collect_profile() {
 // stage -> stage 0 (noise estimate eps, fp32). Stream-ordered on the sender;
 // the receiver's stream waits on an event (the reference's Channel::push/pop,
 // channel.hpp:33-57).
-void Engine::send_rows(int from, int row0, int rows) {
+void Engine::send_rows(int from, int row0, int rows, int patch, int t) {
   const int n = stage_count();
   Stage& src = stages_[size_t(from)];
   const size_t off = size_t(row0) * shape_.hs;
   const size_t cnt = size_t(rows) * shape_.hs;
   DeviceGuard g(src.device);
+  if (n > 1) tl_begin(from, 1, patch, t, src.stream);
   if (from + 1 < n) {
     Stage& dst = stages_[size_t(from + 1)];
     PF_CUDA_CHECK(cudaMemcpyAsync(dst.h32 + off, src.h32 + off, cnt * 4,
@@ -505,6 +506,7 @@ void Engine::send_rows(int from, int row0, int rows) {
                                       size_t(rows) * sizeof(float2), size_t(shape_.hs / 32),
                                       cudaMemcpyDefault, src.stream));
     }
+    tl_end(src.stream);  // before the handoff event: its stamp bounds the receiver's start
     PF_CUDA_CHECK(cudaEventRecord(src.ev_fwd, src.stream));
     DeviceGuard g2(dst.device);
     PF_CUDA_CHECK(cudaStreamWaitEvent(dst.stream, src.ev_fwd, 0));
@@ -512,6 +514,7 @@ void Engine::send_rows(int from, int row0, int rows) {
     Stage& s0 = stages_[0];
     PF_CUDA_CHECK(cudaMemcpyAsync(s0.eps + off, src.h32 + off, cnt * 4,
                                   cudaMemcpyDefault, src.stream));
+    tl_end(src.stream);
   }
 }
 
@@ -626,9 +629,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         forward(s, lf, int(m.P), 0, t, next_code(t, s.first_layer + lf));
       }
       tl_end(s.stream);
-      if (n > 1) tl_begin(d, 1, -1, t, s.stream);
-      send_rows(d, 0, int(m.P));
-      if (n > 1) tl_end(s.stream);
+      send_rows(d, 0, int(m.P), -1, t);
     }
     if (n > 1) {
       Stage& last = stages_[size_t(n - 1)];
@@ -694,9 +695,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
           st.fresh_fraction[size_t(d)].push_back(double(fresh) / double(s0v.size()));
         }
         tl_end(s.stream);
-        if (n > 1) tl_begin(d, 1, j, t, s.stream);
-        send_rows(d, row0, r);
-        if (n > 1) tl_end(s.stream);
+        send_rows(d, row0, r, j, t);
         if (d == n - 1 && n > 1)
           PF_CUDA_CHECK(cudaEventRecord(s0.ev_eps[size_t(j)], s.stream));
       }

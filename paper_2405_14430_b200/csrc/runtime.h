@@ -254,7 +254,7 @@ class Engine {
   void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
   void px_conditioning(Stage& s, int steps);
   void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
-  void send_rows(int from, int row0, int rows);
+  void send_rows(int from, int row0, int rows, int patch, int t);
   void prepare_run(int patches, int steps);
   void validate_run(int steps, int patches, int warmup) const;
   // rank mode

@@ -31,6 +31,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
                "r"(count));
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its
+// predecessor is still running; it must call pdl_wait() before touching any
+// global memory the predecessor produces or consumes. pdl_launch() lets the
+// successor start its own prologue once every CTA of this grid has issued it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
