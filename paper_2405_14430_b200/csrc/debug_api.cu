@@ -36,6 +36,20 @@ extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
   pf::EpiParams ep;
   ep.out_f32 = C - size_t(row0) * N;  // epilogue indexes by global row
   ep.ld = N;
+  // split-K workspace as the runtime attaches it (skinny problems split K)
+  static float* ws = nullptr;
+  static int* counters = nullptr;
+  constexpr size_t kWsFloats = size_t(4) << 20;
+  constexpr int kCounters = 4096;
+  if (!ws) {
+    cudaMalloc(reinterpret_cast<void**>(&ws), kWsFloats * 4);
+    cudaMalloc(reinterpret_cast<void**>(&counters), kCounters * sizeof(int));
+    cudaMemset(counters, 0, kCounters * sizeof(int));
+  }
+  ep.splitk_ws = ws;
+  ep.splitk_ws_floats = kWsFloats;
+  ep.splitk_counters = counters;
+  ep.splitk_counter_cap = kCounters;
   return int(pf::gemm(ta, tb, rows, row0, N, K, pf::Epi::StoreF32, ep,
                       pf::device_sm_count(dev), static_cast<cudaStream_t>(stream)));
 }

@@ -136,11 +136,22 @@ struct GemmSmem {
                                                           : 512;
 };
 
+// Deterministic split-K for skinny problems (few output tiles, long K): the
+// K loop of every tile is cut into `splits` ranges processed by different
+// CTAs; each stores its fp32 partial tile to `ws`, and the CTA that finishes
+// a tile last (per-tile counter) sums the partials in split order and runs
+// the epilogue. splits == 1 is the ordinary persistent kernel.
+struct SplitK {
+  int splits = 1;
+  float* ws = nullptr;     // [tiles][splits][128][BN] fp32
+  int* counters = nullptr; // [tiles], zero between launches
+};
+
 template <int BN, int STAGES, class Epi>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, int rows,
-                        int row0, int N, int K, Epi epi) {
+                        int row0, int N, int K, Epi epi, SplitK sk) {
   using L = GemmSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -150,6 +161,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(smem + L::kBarOffset + 248);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = ptx::lane_id();
@@ -157,6 +169,9 @@ __global__ void __launch_bounds__(256, 1)
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+  const int splits = sk.splits;
+  const int num_units = num_tiles * splits;
+  const int kb_per = (kblocks + splits - 1) / splits;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tma_a);
@@ -183,10 +198,14 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int tile = unit / splits;
+        const int split = unit - tile * splits;
         const int mt = tile % m_tiles;
         const int nt = tile / m_tiles;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        const int kb0 = split * kb_per;
+        const int kb1 = min(kblocks, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
@@ -208,11 +227,14 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int split = unit % splits;
+        const int kb0 = split * kb_per;
+        const int kb1 = min(kblocks, kb0 + kb_per);
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
@@ -221,7 +243,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int k = 0; k < kGemmBK / 16; ++k) {
             ptx::umma_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
                               ptx::desc_kmajor_sw128(b_base + k * 32), idesc,
-                              (kb | k) != 0);
+                              (kb != kb0 || k != 0));
           }
           ptx::umma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -236,14 +258,89 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
+    const int tid = int(threadIdx.x) - 128;  // 0..127 = accumulator row within the tile
     int acc = 0;
     uint32_t acc_phase = 0;
     int tile_count = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+      const int tile = unit / splits;
+      const int split = unit - tile * splits;
       const int mt = tile % m_tiles;
       const int nt = tile / m_tiles;
       const int local_row = mt * kGemmBM + 32 * q + int(lane);
       const bool row_ok = local_row < rows;
+      const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + acc * BN;
+      constexpr int kNV = epi_colvecs<Epi>::value;
+      float* colbuf = reinterpret_cast<float*>(smem + L::kColOffset) +
+                      (tile_count & 1) * kMaxColVecs * BN;
+      if (splits > 1) {
+        // ---- partial tile -> workspace; the last CTA of the tile reduces
+        float* wsp = sk.ws + ((size_t(tile) * splits + split) * kGemmBM + tid) * BN;
+        ptx::mbar_wait(&tfull[acc], acc_phase);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + 32 * c, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(wsp + 32 * c + e) =
+                make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
+                            __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (tid == 0) *s_last = atomicAdd(sk.counters + tile, 1) == splits - 1;
+        ptx::named_bar_sync(1, 128);
+        if (!*s_last) continue;
+        __threadfence();
+        typename epi_row_state<Epi>::type rs{};
+        if constexpr (epi_row_state<Epi>::value) {
+          if (row_ok) rs = epi.row_state(row0 + local_row);
+        }
+        if constexpr (kNV > 0) stage_colvecs<BN>(epi, colbuf, nt * BN, N, tid);
+        ++tile_count;
+        const float* wst = sk.ws + (size_t(tile) * splits * kGemmBM + tid) * BN;
+        const size_t sstride = size_t(kGemmBM) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int col0 = nt * BN + 32 * c;
+          if (!row_ok || col0 >= N) continue;
+          const int nvalid = (N - col0) < 32 ? (N - col0) : 32;
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 a = __ldcg(reinterpret_cast<const float4*>(wst + 32 * c + e));
+            v[e] = a.x; v[e + 1] = a.y; v[e + 2] = a.z; v[e + 3] = a.w;
+          }
+          for (int sp = 1; sp < splits; ++sp) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              const float4 a =
+                  __ldcg(reinterpret_cast<const float4*>(wst + sp * sstride + 32 * c + e));
+              v[e] += a.x; v[e + 1] += a.y; v[e + 2] += a.z; v[e + 3] += a.w;
+            }
+          }
+          if constexpr (Epi::kPreload) {
+            float pre[32];
+            epi.preload(row0 + local_row, col0, pre, nvalid);
+            epi.apply(row0 + local_row, col0, v, pre, nvalid);
+          } else if constexpr (kNV > 0) {
+            epi(row0 + local_row, col0, v, nvalid, rs, ColView{colbuf + 32 * c, BN});
+          } else if constexpr (epi_row_state<Epi>::value) {
+            epi(row0 + local_row, col0, v, nvalid, rs);
+          } else {
+            epi(row0 + local_row, col0, v, nvalid);
+          }
+        }
+        if (tid == 0) sk.counters[tile] = 0;  // ready for the next launch / graph replay
+        continue;
+      }
       // Epilogues that read an existing output (the residual stream) issue
       // those loads before waiting for the accumulator, so they overlap the
       // tile's main loop instead of sitting on the critical path.
@@ -260,14 +357,10 @@ __global__ void __launch_bounds__(256, 1)
       if constexpr (epi_row_state<Epi>::value) {
         if (row_ok) rs = epi.row_state(row0 + local_row);
       }
-      constexpr int kNV = epi_colvecs<Epi>::value;
-      float* colbuf = reinterpret_cast<float*>(smem + L::kColOffset) +
-                      (tile_count & 1) * kMaxColVecs * BN;
-      if constexpr (kNV > 0) stage_colvecs<BN>(epi, colbuf, nt * BN, N, int(threadIdx.x) - 128);
+      if constexpr (kNV > 0) stage_colvecs<BN>(epi, colbuf, nt * BN, N, tid);
       ++tile_count;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + acc * BN;
       if constexpr (Epi::kPreload) {
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {

@@ -1,6 +1,7 @@
 // Kernel instantiations and host launchers: tcgen05 GEMM with the toy-DiT
 // epilogues, tcgen05 attention, and the bandwidth-bound sampler kernels.
 #include <climits>
+#include <algorithm>
 #include <cstdlib>
 #include <cstdio>
 #include <mutex>
@@ -75,6 +76,12 @@ static bool encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void*
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// Experiment switches (read once): "1" enables.
+bool tune_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '1';
 }
 
 bool pdl_enabled() {
@@ -437,14 +444,15 @@ struct EpiResidualMod {
 template <int BN, int STAGES, class E>
 cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int rows,
                         int row0, int N, int K, const E& epi, int sm_count,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const SplitK& sk) {
   using L = GemmSmem<BN, STAGES>;
   constexpr auto kern = gemm_bf16_tn_kernel<BN, STAGES, E>;
   cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
   if (e != cudaSuccess) return e;
-  const int tiles = ((rows + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
-  const int grid = tiles < sm_count ? tiles : sm_count;
-  return launch_pdl(kern, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N, K, epi);
+  const int units = ((rows + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN) * sk.splits;
+  const int grid = units < sm_count ? units : sm_count;
+  return launch_pdl(kern, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N, K, epi,
+                    sk);
 }
 
 template <int BN, int STAGES, class E>
@@ -464,12 +472,12 @@ cudaError_t launch_gemm2sm(const CUtensorMap& a, const CUtensorMap& b, int rows,
 template <bool kTwoSm, int BN, int STAGES>
 cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
                           int row0, int N, int K, Epi kind, const EpiParams& ep,
-                          int sm_count, cudaStream_t stream) {
+                          int sm_count, cudaStream_t stream, SplitK sk = SplitK{}) {
   auto go = [&](const auto& epi) {
     if constexpr (kTwoSm)
       return launch_gemm2sm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream);
     else
-      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream);
+      return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream, sk);
   };
   switch (kind) {
     case Epi::StoreF32:
@@ -524,12 +532,40 @@ bool make_weight_maps(WeightMaps* maps, const bf16* w, int N, int K) {
                              64, 128);
 }
 
+int gemm_splits(int rows, int N, int K, const EpiParams& ep, int sm_count) {
+  // Opt-in (PF_SPLITK=1): measured slower than plain tiles for the 512-row
+  // patch GEMMs of C2 (the last-arriving CTA's serial reduction dominates;
+  // profiles/r1_splitk_m8.txt). Kept for narrower-K experiments.
+  static const bool on = tune_flag("PF_SPLITK");
+  if (!on || !ep.splitk_ws || !ep.splitk_counters) return 1;
+  const int bn = gemm_bn_1sm(N);
+  const int tiles = ((rows + kGemmBM - 1) / kGemmBM) * ((N + bn - 1) / bn);
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+  if (2 * tiles > sm_count || kblocks < 8 || tiles > ep.splitk_counter_cap) return 1;
+  int s = sm_count / tiles;
+  s = std::min(s, kblocks / 4);
+  s = std::min(s, 8);
+  const size_t per_split = size_t(tiles) * kGemmBM * bn;
+  while (s > 1 && per_split * s > ep.splitk_ws_floats) --s;
+  return s < 1 ? 1 : s;
+}
+
 cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  int N, int K, Epi kind, const EpiParams& ep, int sm_count,
                  cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
+  // Skinny problems (a small patch: fewer output tiles than half the SMs)
+  // split K across CTAs (deterministic in-kernel reduction), 1-SM tiles.
+  if (const int splits = gemm_splits(rows, N, K, ep, sm_count); splits > 1) {
+    const SplitK sk{splits, ep.splitk_ws, ep.splitk_counters};
+    if (gemm_bn_1sm(N) == 64)
+      return gemm_dispatch<false, 64, 8>(a, b.one_sm, rows, row0, N, K, kind, ep, sm_count,
+                                         stream, sk);
+    return gemm_dispatch<false, 128, 6>(a, b.one_sm, rows, row0, N, K, kind, ep, sm_count,
+                                        stream, sk);
+  }
   if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % (2 * kGemmBM) == 0 &&
-      N % 32 == 0 && sm_count >= 2 && K >= 2048) {
+      N % 32 == 0 && sm_count >= 2 && (K >= 2048 || tune_flag("PF_RESID_2SM"))) {
     // long-K residual GEMM (MLP-out): CTA pairs halve the per-SM smem
     // operand traffic of the main loop
     constexpr int kStages = 5;
@@ -561,7 +597,12 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
   // projection, 78 % of peak vs 60 % for 1-SM 128 x 128 tiles); for narrower
   // N the row-per-thread epilogue, not the MMA, bounds the kernel and the
   // 1-SM tiling keeps more CTAs in flight (measured: profiles/).
-  if (rows >= 2 * kGemmBM && sm_count >= 2 && gemm_bn_2sm(N) == 256) {
+  // CTA pairs need enough pair tiles to fill the SMs at least twice over;
+  // otherwise the 1-SM tiling keeps more SMs busy (small patches).
+  const int pair_tiles = ((rows + 2 * kGemmBM - 1) / (2 * kGemmBM)) *
+                         ((N + gemm_bn_2sm(N) - 1) / gemm_bn_2sm(N));
+  if (rows >= 2 * kGemmBM && sm_count >= 2 && pair_tiles >= sm_count &&
+      (gemm_bn_2sm(N) == 256 || gemm_bn_2sm(N) == 192)) {
     switch (gemm_bn_2sm(N)) {
       case 256: return gemm_dispatch<true, 256, 6>(a, b.two_sm, rows, row0, N, K, kind, ep, sm_count, stream);
       case 192: return gemm_dispatch<true, 192, 7>(a, b.two_sm, rows, row0, N, K, kind, ep, sm_count, stream);

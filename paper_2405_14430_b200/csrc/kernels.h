@@ -88,6 +88,12 @@ struct EpiParams {
   float ln_eps = 1e-6f;
   const float* c1 = nullptr;
   const float* c2 = nullptr;
+  // Split-K workspace (fp32) and per-tile counters (zeroed, left zeroed by
+  // the kernel) for skinny GEMMs; null disables split-K.
+  float* splitk_ws = nullptr;
+  size_t splitk_ws_floats = 0;
+  int* splitk_counters = nullptr;
+  int splitk_counter_cap = 0;
   bool mod() const { return bias || gate || colscale || stats_out; }
 };
 

@@ -66,6 +66,15 @@ CUtensorMap tmap(const void* base, uint64_t inner, uint64_t outer,
   return m;
 }
 
+// The stage's split-K workspace attached to a GEMM's epilogue parameters.
+EpiParams sk(const Stage& s, EpiParams ep) {
+  ep.splitk_ws = s.splitk_ws;
+  ep.splitk_ws_floats = s.splitk_ws_floats;
+  ep.splitk_counters = s.splitk_counters;
+  ep.splitk_counter_cap = s.splitk_counter_cap;
+  return ep;
+}
+
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     std::ostringstream os;
@@ -198,6 +207,11 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
   s.attn = dalloc<bf16>(P * hs);
   s.z = dalloc<bf16>(P * mlp);
   s.flag = dalloc<int>(1);
+  // split-K workspace: enough for ~2 waves of 128 x 128 partial tiles
+  s.splitk_ws_floats = size_t(4) << 20;
+  s.splitk_ws = dalloc<float>(s.splitk_ws_floats);
+  s.splitk_counter_cap = 4096;
+  s.splitk_counters = dalloc<int>(size_t(s.splitk_counter_cap));
   // Split-KV workspace sized for the worst case (a single 128-row q tile).
   {
     AttnLaunch probe{int(dhp), int(P), 128, 0, int(heads), m.dh, int(hs), 1.f,
@@ -332,7 +346,7 @@ void Engine::free_stage(Stage& s) {
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
-  dfree(s.attn_work); dfree(s.flag); dfree(s.x); dfree(s.cb);
+  dfree(s.attn_work); dfree(s.flag); dfree(s.splitk_ws); dfree(s.splitk_counters); dfree(s.x); dfree(s.cb);
   if (s.eps && s.eps != s.h32) dfree(s.eps);
   for (cudaEvent_t e : s.ev_eps) cudaEventDestroy(e);
   s.ev_eps.clear();
@@ -402,7 +416,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
   qkv.dhp = m.dhp;
   qkv.P = int(m.P);
   prof_begin(s, kGemmQKV, 2 * r * hs * 3 * hs, 0);
-  check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * m.hs, m.hs, Epi::QKV, qkv,
+  check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * m.hs, m.hs, Epi::QKV, sk(s, qkv),
              s.sm_count, s.stream), "gemm qkv");
   prof_end(s);
   AttnLaunch a{m.dhp, int(m.P), rows, row0, m.heads, m.dh, m.hs,
@@ -422,18 +436,18 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
     res.tm_hb = &s.tm_hb;
   }
   prof_begin(s, kGemmOut, 2 * r * hs * hs, 0);
-  check(gemm(s.tm_attn, L.tm_wo, rows, row0, m.hs, m.hs, Epi::Residual, res,
+  check(gemm(s.tm_attn, L.tm_wo, rows, row0, m.hs, m.hs, Epi::Residual, sk(s, res),
              s.sm_count, s.stream), "gemm out-proj");
   prof_end(s);
   EpiParams th;
   th.out_bf16 = s.z;
   th.ld = m.mlp;
   prof_begin(s, kGemmMlpIn, 2 * r * hs * mlp, 0);
-  check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, m.hs, Epi::Tanh, th,
+  check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, m.hs, Epi::Tanh, sk(s, th),
              s.sm_count, s.stream), "gemm mlp-in");
   prof_end(s);
   prof_begin(s, kGemmMlpOut, 2 * r * hs * mlp, 0);
-  check(gemm(s.tm_z, L.tm_wout, rows, row0, m.hs, m.mlp, Epi::Residual, res,
+  check(gemm(s.tm_z, L.tm_wout, rows, row0, m.hs, m.mlp, Epi::Residual, sk(s, res),
              s.sm_count, s.stream), "gemm mlp-out");
   prof_end(s);
   const int splits = attn_splits(a, s.sm_count);
@@ -1454,7 +1468,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   qkv.c1 = px.foldq + (size_t(lf) * 2 * S + 2 * t) * 3 * hs;
   qkv.c2 = qkv.c1 + 3 * hs;
   prof_begin(s, kGemmQKV, 2 * r * dhs * 3 * dhs, 0);
-  check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * hs, hs, Epi::QKV, qkv, s.sm_count, s.stream),
+  check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * hs, hs, Epi::QKV, sk(s, qkv), s.sm_count, s.stream),
         "gemm qkv");
   prof_end(s);
   // 2. self-attention over the full (fresh + stale) K/V buffer
@@ -1478,7 +1492,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   r1.bias = L.bo;
   r1.gate = gate1;
   prof_begin(s, kGemmOut, 2 * r * dhs * dhs, 0);
-  check(gemm(s.tm_attn, L.tm_wo, rows, row0, hs, hs, Epi::Residual, r1, s.sm_count, s.stream),
+  check(gemm(s.tm_attn, L.tm_wo, rows, row0, hs, hs, Epi::Residual, sk(s, r1), s.sm_count, s.stream),
         "gemm out-proj");
   prof_end(s);
   // 4. cross-attention query h Wqc + bqc
@@ -1490,7 +1504,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   cq.P = int(m.P);
   cq.c2 = L.bqc;
   prof_begin(s, kGemmCrossQ, 2 * r * dhs * dhs, 0);
-  check(gemm(s.tm_hb, L.tm_wqc, rows, row0, hs, hs, Epi::QKV, cq, s.sm_count, s.stream),
+  check(gemm(s.tm_hb, L.tm_wqc, rows, row0, hs, hs, Epi::QKV, sk(s, cq), s.sm_count, s.stream),
         "gemm cross q");
   prof_end(s);
   // 5. cross-attention over the T text tokens
@@ -1507,7 +1521,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   r2.colscale = scale2;
   r2.stats_out = px.stats;
   prof_begin(s, kGemmCrossOut, 2 * r * dhs * dhs, 0);
-  check(gemm(s.tm_attn, L.tm_woc, rows, row0, hs, hs, Epi::Residual, r2, s.sm_count, s.stream),
+  check(gemm(s.tm_attn, L.tm_woc, rows, row0, hs, hs, Epi::Residual, sk(s, r2), s.sm_count, s.stream),
         "gemm cross out-proj");
   prof_end(s);
   // 7. z = gelu_tanh((LN(h)(1 + scale2) + shift2) W1 + b1)
@@ -1520,7 +1534,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   ge.c1 = px.foldm + (size_t(lf) * 2 * S + 2 * t) * m.mlp;
   ge.c2 = ge.c1 + m.mlp;
   prof_begin(s, kGemmMlpIn, 2 * r * dhs * mlp, 0);
-  check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, hs, Epi::Gelu, ge, s.sm_count, s.stream),
+  check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, hs, Epi::Gelu, sk(s, ge), s.sm_count, s.stream),
         "gemm mlp-in");
   prof_end(s);
   // 8. h += gate2 (z W2 + b2); operand for the next layer's LayerNorm
@@ -1530,7 +1544,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   r3.colscale = next_scale1;
   r3.stats_out = px.stats;
   prof_begin(s, kGemmMlpOut, 2 * r * dhs * mlp, 0);
-  check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, r3, s.sm_count, s.stream),
+  check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, r3), s.sm_count, s.stream),
         "gemm mlp-out");
   prof_end(s);
   launches_ += 8 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0) +

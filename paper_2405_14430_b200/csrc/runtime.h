@@ -123,6 +123,10 @@ struct Stage {
   float* attn_work = nullptr;
   size_t attn_work_floats = 0;
   int* flag = nullptr;    // first non-finite (ordinal), INT_MAX if none
+  float* splitk_ws = nullptr;    // split-K partial tiles (skinny GEMMs)
+  size_t splitk_ws_floats = 0;
+  int* splitk_counters = nullptr;
+  int splitk_counter_cap = 0;
   CUtensorMap tm_hb, tm_attn, tm_z, tm_q;
   CUtensorMap tm_h32;  // fp32 residual stream, box 32 x 128 (TMA epilogue)
   cudaEvent_t ev_fwd = nullptr;  // "rows sent to stage d+1"

@@ -39,13 +39,17 @@ def _gemm(A, B, rows, row0):
     (4096, 4096, 0, 4608, 1152),    # PixArt MLP-in (2-SM, BN 256)
     (1024, 1000, 24, 4608, 1152),   # 2-SM with a ragged last row tile
     (512, 300, 100, 96, 64),        # 2-SM with N < BN (B half partly out of range)
-    (2048, 256, 1792, 3456, 1152),  # one 2-SM row tile, BN 192
+    (2048, 256, 1792, 3456, 1152),  # one 2-SM row tile, BN 192 (split-K 2 on 1-SM tiles)
+    (4096, 512, 512, 1152, 1152),   # out-proj of a 512-row patch: split-K
+    (4096, 512, 3584, 1152, 4608),  # MLP-out of a 512-row patch: split-K 4
+    (1024, 100, 7, 1152, 1152),     # ragged rows, split-K
 ])
 def test_gemm_matches_fp32(total, rows, row0, N, K):
     g = torch.Generator(device="cuda").manual_seed(total + N + K)
     A = (torch.rand(total, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
     B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
     C = _gemm(A, B, rows, row0)
+    assert torch.equal(C, _gemm(A, B, rows, row0))  # deterministic (split-K order fixed)
     ref = A[row0:row0 + rows].float() @ B.float().T
     err = (C - ref).abs().max().item()
     scale = ref.abs().max().item()
