@@ -29,7 +29,9 @@
 //                 P is packed to bf16 and stored into TMEM over the consumed
 //                 scores, so P never touches shared memory (the SS-mode MMAs
 //                 and TMA already use most of the smem bandwidth). exp2 is
-//                 split 3:1 between MUFU.EX2 and an FMA-pipe polynomial.
+//                 split 3:1 between MUFU.EX2 and an FMA-pipe polynomial
+//                 (measured alternatives: 1:1, 1:0, packed f16x2 MUFU exp --
+//                 all slower on B200, whose f16x2 ex2 issues two MUFU ops).
 // With kv_splits > 1 each split writes an unnormalised partial (O, m, l) in
 // fp32 and `attn_combine_kernel` merges the splits in a fixed order.
 #pragma once
@@ -89,7 +91,10 @@ __device__ __forceinline__ void attn_trace(const AttnParams& prm, int slot) {
     prm.trace[slot] = clock64();
 }
 
-template <int DHP, int NT>
+// kPoly: bit (g & 7) set -> 4-element group g of a score row takes the
+// FMA-pipe exp2 polynomial instead of MUFU.EX2. kPingPong: serialise the two
+// softmax warpgroups' exp sections (named barriers 1/2).
+template <int DHP, int NT, int kPoly = 0x88, bool kPingPong = false>
 __global__ void __launch_bounds__(128 + 128 * NT, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
@@ -266,9 +271,8 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     float m_ref = -INFINITY;  // running (lazy) max, scaled log2 domain
     float l_sum = 0.f;
     // Warpgroup 0 takes the first exp turn.
-    if constexpr (NT == 2) {
-      if (t == 1) ptx::named_bar_arrive(1, 256);
-    }
+    constexpr bool pp = NT == 2 && kPingPong;
+    if (pp && t == 1) ptx::named_bar_arrive(1, 256);
     for (int i = 0; i < nblk; ++i) {
       const int kv0 = (blk_begin + i) * kAttnBN;
       // S_{t,i} complete; so is PV_{t,i-1} (issued before it), hence O_t is
@@ -303,11 +307,11 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       const bool need = bmax > m_ref + 8.0f;
       const float m_new = need ? bmax : m_ref;
       const float alpha = need ? ptx::ex2_approx(m_ref - m_new) : 1.0f;  // 0 on first block
-      // Ping-pong the exp-heavy section between the two softmax warpgroups
-      // (named barriers 1/2): while one warpgroup exponentiates, the tensor
-      // pipe runs the other tile's PV and next S, and the MUFU is not shared.
+      // Optional ping-pong of the exp-heavy section between the two softmax
+      // warpgroups (named barriers 1/2). Off by default: letting both
+      // warpgroups exponentiate concurrently measured 4 % faster at dh 72.
       attn_trace(prm, 2048 * t + 8 * i + 2);
-      if constexpr (NT == 2) ptx::named_bar_sync(1 + t, 256);
+      if (pp) ptx::named_bar_sync(1 + t, 256);
       attn_trace(prm, 2048 * t + 8 * i + 3);
       if (i > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
           const float2 x0 = ptx::ffma2(make_float2(s[e], s[e + 1]), sc2, nm2);
           const float2 x1 = ptx::ffma2(make_float2(s[e + 2], s[e + 3]), sc2, nm2);
           float2 p0, p1;
-          if ((g & 3) == 3) {
+          if ((kPoly >> (g & 7)) & 1) {
             p0 = ptx::ex2_poly2(x0);
             p1 = ptx::ex2_poly2(x1);
           } else {
@@ -345,9 +349,7 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
           pk[2 * g] = ptx::pack_bf16x2(p0.x, p0.y);
           pk[2 * g + 1] = ptx::pack_bf16x2(p1.x, p1.y);
         }
-        if (h == 1) {
-          if constexpr (NT == 2) ptx::named_bar_arrive(2 - t, 256);  // hand the turn over
-        }
+        if (h == 1 && pp) ptx::named_bar_arrive(2 - t, 256);  // hand the turn over
         ptx::tmem_st32(tmem_p + 32 * h, pk);
       }
       ptx::tmem_wait_st();
@@ -369,9 +371,7 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       attn_trace(prm, 2048 * t + 8 * i + 5);
     }
     // Balance the ping-pong: warpgroup 0 consumes warpgroup 1's last hand-off.
-    if constexpr (NT == 2) {
-      if (t == 0) ptx::named_bar_sync(1, 256);
-    }
+    if (pp && t == 0) ptx::named_bar_sync(1, 256);
 
     // Epilogue: wait for the last PV, read O, normalise, store.
     ptx::mbar_wait(&o_done[t], 0);

@@ -641,10 +641,6 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
                         cudaStream_t stream) {
   constexpr int NT = attn_tiles_per_cta(DHP);
   using L = AttnSmem<DHP, NT>;
-  {
-    cudaError_t e = ensure_smem_attr<attn_fwd_kernel<DHP, NT>>(L::kTotal);
-    if (e != cudaSuccess) return e;
-  }
   const int q_ctas = (a.rows + NT * kAttnBM - 1) / (NT * kAttnBM);
   const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
   const int splits = attn_splits(a, sm_count);
@@ -664,6 +660,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   prm.part_o = nullptr;
   prm.part_ml = nullptr;
   prm.trace = a.trace;
+
   if (splits > 1) {
     const size_t need = attn_work_floats(DHP, a.heads, a.rows, splits);
     if (!a.work || a.work_floats < need) return cudaErrorInvalidValue;
@@ -671,8 +668,17 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.part_ml = a.work + size_t(splits) * a.heads * prm.rows_pad * DHP;
   }
   dim3 grid(q_ctas, a.heads, splits);
-  cudaError_t e = launch_pdl(attn_fwd_kernel<DHP, NT>, grid, dim3(L::kThreads), L::kTotal,
-                             stream, q, k, v, prm);
+  auto go = [&](auto kern) {
+    cudaError_t e2 = ensure_smem_attr<decltype(kern)::value>(L::kTotal);
+    if (e2 != cudaSuccess) return e2;
+    return launch_pdl(decltype(kern)::value, grid, dim3(L::kThreads), L::kTotal, stream, q, k,
+                      v, prm);
+  };
+  // Two softmax warpgroups exponentiate concurrently (no ping-pong) with 2 of
+  // every 8 four-column groups on the FMA-pipe exp2: measured best of the
+  // ping-pong / poly-ratio / f16x2-exp variants at C2 (119 vs 123.5 us).
+  cudaError_t e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT>),
+                                            &attn_fwd_kernel<DHP, NT>>{});
   if (e != cudaSuccess || splits == 1) return e;
   const int total = a.rows * a.heads * (DHP / 16);
   attn_combine_kernel<DHP><<<(total + 255) / 256, 256, 0, stream>>>(prm);
