@@ -156,6 +156,20 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
                                    int patches, int warmup, double eta,
                                    void* stream, pf_stats* stats);
 
+/* ditsim::run_distrifusion(toy, x_init, steps, workers, warmup, eta) --
+ * execute.hpp:131-133, execute.cpp:431-531 (displaced patch parallelism):
+ * `workers` row shards; warmup steps are full-sequence and synchronous,
+ * steady steps attend over the worker's own fresh K/V rows and every other
+ * shard's rows from the previous step. Needs a single-stage context; the
+ * workers share its GPU. CUDA constraint: seq_len / workers divisible by
+ * 128 (workers > 1). stats->fresh_fraction receives workers x (steps-warmup)
+ * values, worker-major. */
+pf_status pf_run_distrifusion(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps,
+                              int workers, int warmup, double eta, double* x_out,
+                              pf_stats* stats);
+pf_status pf_run_distrifusion_device(pf_ctx* ctx, float* x_dev, int steps, int workers,
+                                     int warmup, double eta, void* stream, pf_stats* stats);
+
 /* Wait for work enqueued by pf_run_pipefusion_device and report deferred
  * numeric errors (non-finite activations). */
 pf_status pf_synchronize(pf_ctx* ctx, void* stream);

@@ -281,10 +281,26 @@ class Reference(_Impl):
     def __init__(self, path: Optional[Path] = None):
         super().__init__(path or REFERENCE_LIB)
 
-    def run_distrifusion(self, m, x, steps, workers, warmup, eta, backend="threads"):
+    def run_distrifusion(self, m, x, steps, workers, warmup, eta, backend="threads",
+                         with_stats=False):
         x = _c(x)
         out = np.empty_like(x)
         err = ctypes.create_string_buffer(256)
+        if with_stats:
+            per = max(0, steps - warmup)
+            ff = np.zeros(max(1, workers * per))
+            fresh, stale = ctypes.c_int64(), ctypes.c_int64()
+            fn = self.lib.ref_distrifusion_stats
+            fn.argtypes = [ctypes.c_void_p, _d, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_double, ctypes.c_int, _d, _i64p, _i64p, _d,
+                           ctypes.c_int64, ctypes.c_char_p, ctypes.c_int]
+            rc = fn(m.h, _p(x), x.shape[0], steps, workers, warmup, eta,
+                    1 if backend == "inline" else 0, _p(out), ctypes.byref(fresh),
+                    ctypes.byref(stale), _p(ff), workers * per, err, 256)
+            if rc:
+                raise OracleError(rc, err.value.decode())
+            return out, (fresh.value, stale.value,
+                         [list(ff[w * per:(w + 1) * per]) for w in range(workers)])
         fn = self.lib.ref_distrifusion
         fn.argtypes = [ctypes.c_void_p, _d, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                        ctypes.c_int, ctypes.c_double, ctypes.c_int, _d, ctypes.c_char_p,

@@ -133,6 +133,30 @@ int ref_distrifusion(void* h, const double* x, std::int64_t p, int steps, int wo
   }
 }
 
+// run_distrifusion with its StalenessStats (fresh, stale, per-worker series
+// of `per` values each, worker-major into ff).
+int ref_distrifusion_stats(void* h, const double* x, std::int64_t p, int steps, int workers,
+                           int warmup, double eta, int backend, double* out,
+                           std::int64_t* fresh, std::int64_t* stale, double* ff,
+                           std::int64_t ff_cap, char* err, int cap) {
+  try {
+    const ToyDiT& t = *static_cast<ToyDiT*>(h);
+    ParallelRunResult r =
+        run_distrifusion(t, from_rm(x, p, t.hidden_size), steps, workers, warmup, eta,
+                         backend == 1 ? Backend::Inline : Backend::Threads);
+    to_rm(r.final.x, out);
+    *fresh = r.stats.fresh_patch_reads;
+    *stale = r.stats.stale_patch_reads;
+    std::int64_t k = 0;
+    for (const auto& w : r.stats.per_worker_fresh_fraction)
+      for (double f : w)
+        if (k < ff_cap) ff[k++] = f;
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, cap);
+  }
+}
+
 double ref_divergence(const double* a, const double* b, std::int64_t rows, std::int64_t cols) {
   LatentState sa{from_rm(a, rows, cols), -1};
   LatentState sb{from_rm(b, rows, cols), -1};

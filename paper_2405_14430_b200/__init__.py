@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = [
     "pf_layer_forward_t", "pf_destroy", "pf_last_error", "pf_create_toy_rank",
     "pf_create_pixart_rank", "pf_peer_blob_size", "pf_export_peer", "pf_connect_peers",
     "pf_rank", "pf_world", "pf_rank_plan", "pf_set_timeline", "pf_timeline",
+    "pf_run_distrifusion", "pf_run_distrifusion_device",
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
@@ -112,6 +113,10 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_rank_plan.argtypes = [i32, i32, i32, i32, i32, i64, ctypes.POINTER(ctypes.c_int32),
                                  i64]
     lib.pf_rank_plan.restype = i64
+    lib.pf_run_distrifusion.argtypes = [vp, dptr, i32, i32, i32, i32, dbl, dptr,
+                                        ctypes.POINTER(_Stats)]
+    lib.pf_run_distrifusion_device.argtypes = [vp, vp, i32, i32, i32, dbl, vp,
+                                               ctypes.POINTER(_Stats)]
     lib.pf_set_timeline.argtypes = [vp, i32]
     lib.pf_timeline.argtypes = [vp, dptr, i64]
     lib.pf_timeline.restype = i64
@@ -339,6 +344,23 @@ class ToyDiTCuda:
                                              _dptr(out), ctypes.byref(st))
         _raise(status, self._err())
         fr = [list(ff[d * per:(d + 1) * per]) for d in range(stages)]
+        return ParallelRunResult(out, StalenessStats(st.fresh_patch_reads,
+                                                     st.stale_patch_reads, fr))
+
+    def run_distrifusion(self, x_init, steps: int, workers: int, warmup: int,
+                         eta: float) -> ParallelRunResult:
+        """ditsim::run_distrifusion (execute.hpp:131-133) on this context's GPU."""
+        x = _f64c(x_init)
+        out = np.empty_like(x)
+        per = max(0, steps - warmup)
+        cap = workers * per
+        ff = (ctypes.c_double * max(1, cap))()
+        st = _Stats(0, 0, ff, cap)
+        status = self._lib.pf_run_distrifusion(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
+                                               workers, warmup, ctypes.c_double(eta),
+                                               _dptr(out), ctypes.byref(st))
+        _raise(status, self._err())
+        fr = [list(ff[w * per:(w + 1) * per]) for w in range(workers)]
         return ParallelRunResult(out, StalenessStats(st.fresh_patch_reads,
                                                      st.stale_patch_reads, fr))
 

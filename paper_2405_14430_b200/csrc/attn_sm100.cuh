@@ -75,6 +75,7 @@ __host__ __device__ constexpr int attn_tiles_per_cta(int /*dhp*/) { return 2; }
 struct AttnParams {
   int P;            // kv rows per head in the K/V buffers (= sequence length)
   int q_stride;     // rows per head of the Q buffer (= P for self-attention)
+  int fresh_lo, fresh_hi;  // kv rows [lo, hi) (128-aligned) read from tm_k2/tm_v2
   int rows;         // query rows this launch
   int row0;         // first query row
   int heads, dh, hs;
@@ -104,7 +105,9 @@ template <int DHP, int NT, int kPoly = 0x88, bool kPingPong = false>
 __global__ void __launch_bounds__(128 + 128 * NT, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, AttnParams prm) {
+                    const __grid_constant__ CUtensorMap tm_v,
+                    const __grid_constant__ CUtensorMap tm_k2,
+                    const __grid_constant__ CUtensorMap tm_v2, AttnParams prm) {
   using L = AttnSmem<DHP, NT>;
   constexpr int S = L::kStages;
   constexpr int kChunks = DHP / 16;
@@ -140,6 +143,10 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     ptx::prefetch_tmap(&tm_q);
     ptx::prefetch_tmap(&tm_k);
     ptx::prefetch_tmap(&tm_v);
+    if (prm.fresh_lo < prm.fresh_hi) {
+      ptx::prefetch_tmap(&tm_k2);
+      ptx::prefetch_tmap(&tm_v2);
+    }
     ptx::mbar_init(q_full, 1);
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&k_full[s], 1);
@@ -182,20 +189,25 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
         const int s = i % S;
         const uint32_t ph = ((i / S) & 1) ^ 1;
         const int kvrow = head * prm.P + (blk_begin + i) * kAttnBN;
+        // DistriFusion: the worker's own (fresh) rows come from a second buffer
+        const int kvr = (blk_begin + i) * kAttnBN;
+        const bool fresh = kvr >= prm.fresh_lo && kvr < prm.fresh_hi;
+        const CUtensorMap* km = fresh ? &tm_k2 : &tm_k;
+        const CUtensorMap* vm = fresh ? &tm_v2 : &tm_v;
         attn_trace(prm, 6144 + 8 * i + 0);
         ptx::mbar_wait(&k_empty[s], ph);
         attn_trace(prm, 6144 + 8 * i + 1);
         ptx::mbar_arrive_expect_tx(&k_full[s], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sK + s * L::kTileAlloc + c * (kAttnBN * 32), &tm_k, &k_full[s],
+          ptx::tma_load_2d(sK + s * L::kTileAlloc + c * (kAttnBN * 32), km, &k_full[s],
                            c * 16, kvrow);
         ptx::mbar_wait(&v_empty[s], ph);
         attn_trace(prm, 6144 + 8 * i + 2);
         ptx::mbar_arrive_expect_tx(&v_full[s], L::kTileBytes);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sV + s * L::kTileAlloc + c * (kAttnBN * 32), &tm_v, &v_full[s],
+          ptx::tma_load_2d(sV + s * L::kTileAlloc + c * (kAttnBN * 32), vm, &v_full[s],
                            c * 16, kvrow);
       }
     } else if (warp == 1 && lane == 0) {

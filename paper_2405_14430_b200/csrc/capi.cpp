@@ -424,6 +424,39 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
   });
 }
 
+pf_status pf_run_distrifusion(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps,
+                              int workers, int warmup, double eta, double* x_out,
+                              pf_stats* stats) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!x_init || !x_out) throw pf::ValidationError("NULL latent pointer");
+    upload_x(ctx, x_init, layout);
+    pf::RunStats rs;
+    const pf::Stage& s0 = ctx->engine->stage(0);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s0.device);
+    struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
+    ctx->engine->enqueue_distrifusion(ctx->x_scratch, steps, workers, warmup, float(eta),
+                                      s0.stream, &rs);
+    ctx->engine->finish(s0.stream);
+    download_x(ctx, x_out, layout);
+    export_stats(rs, stats);
+  });
+}
+
+pf_status pf_run_distrifusion_device(pf_ctx* ctx, float* x_dev, int steps, int workers,
+                                     int warmup, double eta, void* stream, pf_stats* stats) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!x_dev) throw pf::ValidationError("NULL latent pointer");
+    pf::RunStats rs;
+    ctx->engine->enqueue_distrifusion(x_dev, steps, workers, warmup, float(eta),
+                                      static_cast<cudaStream_t>(stream), &rs);
+    export_stats(rs, stats);
+  });
+}
+
 pf_status pf_synchronize(pf_ctx* ctx, void* stream) {
   if (!ctx) return PF_VALIDATION;
   return guarded(&ctx->last_error,

@@ -647,6 +647,8 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   AttnParams prm;
   prm.P = a.P;
   prm.q_stride = a.q_stride > 0 ? a.q_stride : a.P;
+  prm.fresh_lo = (a.k2 && a.v2) ? a.fresh_lo : 0;
+  prm.fresh_hi = (a.k2 && a.v2) ? a.fresh_hi : 0;
   prm.rows = a.rows;
   prm.row0 = a.row0;
   prm.heads = a.heads;
@@ -672,7 +674,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     cudaError_t e2 = ensure_smem_attr<decltype(kern)::value>(L::kTotal);
     if (e2 != cudaSuccess) return e2;
     return launch_pdl(decltype(kern)::value, grid, dim3(L::kThreads), L::kTotal, stream, q, k,
-                      v, prm);
+                      v, a.k2 ? *a.k2 : k, a.v2 ? *a.v2 : v, prm);
   };
   // Two softmax warpgroups exponentiate concurrently (no ping-pong) with 2 of
   // every 8 four-column groups on the FMA-pipe exp2: measured best of the

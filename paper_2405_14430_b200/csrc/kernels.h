@@ -126,6 +126,11 @@ struct AttnLaunch {
   size_t work_floats;    // capacity of `work`
   unsigned long long* trace = nullptr;  // debug timeline (see AttnParams)
   int q_stride = 0;      // cross-attention: Q buffer [heads][q_stride][dhp]
+  // DistriFusion: kv rows [fresh_lo, fresh_hi) (multiples of 128) come from
+  // k2/v2 (this worker's fresh K/V), the rest from k/v (previous step)
+  int fresh_lo = 0, fresh_hi = 0;
+  const CUtensorMap* k2 = nullptr;
+  const CUtensorMap* v2 = nullptr;
 };
 int attn_splits(const AttnLaunch& a, int sm_count);
 size_t attn_work_floats(int dhp, int heads, int rows, int splits);

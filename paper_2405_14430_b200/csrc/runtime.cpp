@@ -332,6 +332,7 @@ void Engine::free_stage(Stage& s) {
   }
   for (StageLayer& L : s.layers) {
     for (float* p : {L.bqkv, L.bo, L.bqc, L.bkvc, L.boc, L.b1, L.b2}) dfree(p);
+    dfree(L.k2); dfree(L.v2);
     dfree(L.wqc); dfree(L.wkvc); dfree(L.woc); dfree(L.kc); dfree(L.vc);
   }
   {
@@ -403,14 +404,14 @@ void Engine::load_condition_bias(const double* cb) {
 // One toy DiT layer over rows [row0, row0+rows) (toy_model.cpp:169-177):
 // fused QKV projection writing this block's K/V rows into the full buffers,
 // attention over all P rows, out-proj residual, tanh MLP, MLP residual.
-void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
+void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const KvView* kv) {
   const ModelShape& m = shape_;
   StageLayer& L = s.layers[size_t(lf)];
   const double r = rows, hs = m.hs, mlp = m.mlp, P = double(m.P);
   EpiParams qkv;
   qkv.q = s.q;
-  qkv.k = L.k;
-  qkv.v = L.v;
+  qkv.k = kv ? kv->k : L.k;
+  qkv.v = kv ? kv->v : L.v;
   qkv.hs = m.hs;
   qkv.dh = m.dh;
   qkv.dhp = m.dhp;
@@ -422,8 +423,15 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code) {
   AttnLaunch a{m.dhp, int(m.P), rows, row0, m.heads, m.dh, m.hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
+  if (kv) {
+    a.k2 = kv->tm_k2;
+    a.v2 = kv->tm_v2;
+    a.fresh_lo = kv->fresh_lo;
+    a.fresh_hi = kv->fresh_hi;
+  }
   prof_begin(s, kAttention, 4 * r * P * hs, 0);
-  check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
+  check(attention(s.tm_q, kv ? *kv->tm_k : L.tm_k, kv ? *kv->tm_v : L.tm_v, a, s.sm_count,
+                  s.stream), "attention");
   prof_end(s);
   EpiParams res;
   res.out_f32 = s.h32;
@@ -903,6 +911,126 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
     os << "non-finite activation at timestep 0, layer " << layer;
     throw NumericError(os.str());
   }
+}
+
+// ============================================================== DistriFusion
+// run_distrifusion_inline (execute.cpp:431-531): per step, warmup steps run
+// layer-lockstep over the full sequence (all shards fresh); steady steps run
+// each worker's shard through all layers attending over [its fresh rows |
+// every other shard's rows of the previous step], then install all shards.
+// Two K/V buffers per layer alternate as "previous step" and "this step":
+// every shard's rows of "this step" are rewritten by its worker during the
+// step, so swapping the roles afterwards is the reference's install().
+void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warmup, float eta,
+                                  cudaStream_t caller, RunStats* stats) {
+  const ModelShape& m = shape_;
+  if (stage_count() != 1 || rank_mode())
+    throw ValidationError("DistriFusion runs on a single-stage engine (one device per worker "
+                          "in the reference; here the workers share the stage's GPU)");
+  if (m.block != kBlockToy) throw ValidationError("DistriFusion is defined for the toy block");
+  if (steps < 1) throw ValidationError("steps must be >= 1");
+  if (workers < 1) throw ValidationError("workers must be >= 1");
+  if (warmup < 0 || warmup > steps) throw ValidationError("warmup must lie in [0, steps]");
+  if (m.P % workers != 0) {
+    std::ostringstream os;
+    os << "seq_len " << m.P << " is not divisible by workers " << workers;
+    throw ValidationError(os.str());
+  }
+  const int r = int(m.P / workers);
+  if (workers > 1 && r % 128 != 0) {
+    std::ostringstream os;
+    os << "CUDA DistriFusion needs seq_len / workers divisible by 128 (got " << r << ")";
+    throw ValidationError(os.str());
+  }
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  const size_t kvn = size_t(m.heads) * size_t(m.P) * size_t(m.dhp);
+  for (StageLayer& L : s.layers)
+    if (!L.k2) {
+      PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
+      L.k2 = dalloc<bf16>(kvn);
+      L.v2 = dalloc<bf16>(kvn);
+      L.tm_k2 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
+      L.tm_v2 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
+    }
+  if (!ev_start_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+  RunStats local;
+  RunStats& st = stats ? *stats : local;
+  st.fresh = 0;
+  st.stale = 0;
+  st.fresh_fraction.assign(size_t(workers), {});
+  codes_.clear();
+  launches_ = 0;
+  prof_.clear();
+  prof_used_.assign(stages_.size(), 0);
+  tl_.clear();
+
+  PF_CUDA_CHECK(cudaEventRecord(ev_start_, caller));
+  PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start_, 0));
+  check(reset_flag(s.flag, s.stream), "reset_flag");
+  ++launches_;
+  // slot 0 = (k, v), slot 1 = (k2, v2); `prev` holds the previous step
+  int prev = 0;
+  if (warmup == 0)  // StageBuffers are zero-initialised (execute.cpp:42-48)
+    for (StageLayer& L : s.layers) {
+      PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kvn * sizeof(bf16), s.stream));
+      PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kvn * sizeof(bf16), s.stream));
+    }
+  auto view = [&](StageLayer& L, int fresh_lo, int fresh_hi) {
+    const int nxt = 1 - prev;
+    KvView kv;
+    kv.k = nxt ? L.k2 : L.k;
+    kv.v = nxt ? L.v2 : L.v;
+    kv.tm_k = prev ? &L.tm_k2 : &L.tm_k;
+    kv.tm_v = prev ? &L.tm_v2 : &L.tm_v;
+    kv.tm_k2 = nxt ? &L.tm_k2 : &L.tm_k;
+    kv.tm_v2 = nxt ? &L.tm_v2 : &L.tm_v;
+    kv.fresh_lo = fresh_lo;
+    kv.fresh_hi = fresh_hi;
+    return kv;
+  };
+  const size_t hs = size_t(m.hs);
+  for (int step = 0; step < steps; ++step) {
+    const int t = steps - 1 - step;
+    if (step < warmup) {
+      // every worker sees every shard fresh: one full-sequence pass
+      check(patch_prepare(x_dev, nullptr, s.cb, s.h32, s.hb, 0, int(m.P), m.hs, 0.f, false,
+                          s.stream), "patch_prepare");
+      ++launches_;
+      for (int l = 0; l < s.layer_count; ++l) {
+        st.fresh += int64_t(workers) * workers;
+        codes_.emplace_back(t, l);
+        KvView kv = view(s.layers[size_t(l)], 0, int(m.P));
+        kv.tm_k = kv.tm_k2;  // attend over this step's buffer only
+        kv.tm_v = kv.tm_v2;
+        layer_forward(s, l, int(m.P), 0, int(codes_.size()) - 1, &kv);
+      }
+      check(latent_update(x_dev, s.h32, eta, size_t(m.P) * hs, s.stream), "latent_update");
+      ++launches_;
+    } else {
+      for (int i = 0; i < workers; ++i) {
+        const int row0 = i * r;
+        check(patch_prepare(x_dev, nullptr, s.cb, s.h32, s.hb, row0, r, m.hs, 0.f, false,
+                            s.stream), "patch_prepare");
+        ++launches_;
+        for (int l = 0; l < s.layer_count; ++l) {
+          // own shard fresh (t), the others installed last step (t + 1)
+          st.fresh += 1;
+          st.stale += workers - 1;
+          codes_.emplace_back(t, l);
+          KvView kv = view(s.layers[size_t(l)], row0, row0 + r);
+          layer_forward(s, l, r, row0, int(codes_.size()) - 1, &kv);
+        }
+        st.fresh_fraction[size_t(i)].push_back(1.0 / double(workers));
+        check(latent_update(x_dev + size_t(row0) * hs, s.h32 + size_t(row0) * hs, eta,
+                            size_t(r) * hs, s.stream), "latent_update");
+        ++launches_;
+      }
+    }
+    prev = 1 - prev;  // install: this step's buffer becomes the previous step's
+  }
+  PF_CUDA_CHECK(cudaEventRecord(s.ev_fwd, s.stream));
+  PF_CUDA_CHECK(cudaStreamWaitEvent(caller, s.ev_fwd, 0));
 }
 
 // ============================================================== timeline

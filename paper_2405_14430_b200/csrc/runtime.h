@@ -79,6 +79,10 @@ struct StageLayer {
   bf16* v = nullptr;     // [heads][P][dhp]
   WeightMaps tm_wqkv, tm_wo, tm_win, tm_wout;
   CUtensorMap tm_k, tm_v;
+  // DistriFusion: second K/V buffer (the two alternate as previous-step /
+  // this-step per denoising step), allocated on first use
+  bf16 *k2 = nullptr, *v2 = nullptr;
+  CUtensorMap tm_k2, tm_v2;
   // PixArt block (oracle/px_oracle.c): biases fp32, cross-attention weights,
   // per-image cross K/V of the text tokens [heads][T][dhp]
   float *bqkv = nullptr, *bo = nullptr, *bqc = nullptr, *bkvc = nullptr, *boc = nullptr,
@@ -205,6 +209,14 @@ class Engine {
   // Text tokens y [T x hs] (row-major fp64) used by every stage's cross-attention.
   void set_text(const double* y);
 
+  // ditsim::run_distrifusion (execute.hpp:131-133, execute.cpp:431-531) on
+  // a single-stage engine: `workers` row shards, each attending over its own
+  // fresh K/V rows and every other shard's rows from the previous step
+  // (warmup steps: all fresh, layer-lockstep). The workers of a step are
+  // independent; here they run back to back on the stage's GPU.
+  void enqueue_distrifusion(float* x_dev, int steps, int workers, int warmup, float eta,
+                            cudaStream_t caller, RunStats* stats);
+
   // Rank mode.
   int rank() const { return rank_; }
   int world() const { return world_; }
@@ -254,7 +266,15 @@ class Engine {
  private:
   void alloc_stage(Stage& s, int first, int count, bool is_first);
   void free_stage(Stage& s);
-  void layer_forward(Stage& s, int lf, int rows, int row0, int code);
+  // K/V source of a layer forward: where the QKV epilogue writes this
+  // block's K/V rows, and which buffers the attention reads (DistriFusion).
+  struct KvView {
+    bf16 *k = nullptr, *v = nullptr;
+    const CUtensorMap *tm_k = nullptr, *tm_v = nullptr, *tm_k2 = nullptr, *tm_v2 = nullptr;
+    int fresh_lo = 0, fresh_hi = 0;
+  };
+  void layer_forward(Stage& s, int lf, int rows, int row0, int code,
+                     const KvView* kv = nullptr);
   void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
   void px_conditioning(Stage& s, int steps);
   void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
