@@ -68,6 +68,10 @@ CONFIGS = {
     "c3px": dict(name="PixArt-alpha DiT block variant 2048px (28 layers, hidden 1152, 16 heads, "
                       "16384 tokens, 120 text tokens), 20 steps, 1 warmup",
                  L=28, hs=1152, heads=16, p=16384, S=20, W=1, block="pixart", T=120),
+    "c4": dict(name="SD3-medium-shaped joint-attention DiT 1024px (24 blocks, hidden 1536, "
+                    "24 heads, 4096 image + 333 text tokens in one K/V buffer; toy arithmetic "
+                    "per stream), 20 steps, 1 warmup",
+               L=24, hs=1536, heads=24, p=4096, S=20, W=1, block="joint", T=333),
     "c1": dict(name="tiny DiT (4 layers, hidden 128, 4 heads, 256 tokens), 5 steps, 1 warmup",
                L=4, hs=128, heads=4, p=256, S=5, W=1),
     "cref": dict(name="reference_execute.cfg (4 layers, hidden 32, 4 heads, 64 tokens), 20 "
@@ -79,6 +83,11 @@ def flops_per_image(c, mlp):
     """The reference's ComputeModel (simulate.cpp:30-44) for mlp_ratio 4:
     S * L * (24 p hs^2 + 4 p^2 hs); generalised to mlp = 4 hs."""
     p, hs = c["p"], c["hs"]
+    if c.get("block") == "joint":
+        # both streams' GEMMs over their rows and joint attention over p + T
+        # rows, per step and layer; the text rows run once per step
+        pt = p + c["T"]
+        return c["S"] * c["L"] * (8 * pt * hs * hs + 4 * pt * hs * mlp + 4 * pt * pt * hs)
     if c.get("block") == "pixart":
         # QKV 6, out 2, cross-q 2, cross-out 2 (x p hs^2), MLP 4 p hs mlp, self- and
         # cross-attention 4 p (p + T) hs per step and layer; text K/V once per image
@@ -206,12 +215,14 @@ def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
     model = ref.build_toy_model(0, 1, c["hs"], c["heads"], 4.0)
     cores = min(os.cpu_count() or 1, 64)
     rng = np.random.default_rng(0)
-    k = rng.uniform(-1, 1, (c["p"], c["hs"]))
-    v = rng.uniform(-1, 1, (c["p"], c["hs"]))
+    # joint block: each stream's rows run the toy block against all p + T rows
+    kvp = c["p"] + (c["T"] if c.get("block") == "joint" else 0)
+    k = rng.uniform(-1, 1, (kvp, c["hs"]))
+    v = rng.uniform(-1, 1, (kvp, c["hs"]))
 
     def one(i):
         h = np.random.default_rng(i).uniform(-1, 1, (sample_rows, c["hs"]))
-        row0 = (i * sample_rows) % c["p"]
+        row0 = (i * sample_rows) % kvp
         model.layer_forward(0, h, k, v, row0)
         return 1
 
@@ -223,12 +234,12 @@ def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
                 break
     wall = time.perf_counter() - t0
     per_sample = wall / done  # throughput-equivalent seconds per sample
-    samples_per_image = c["S"] * c["L"] * (c["p"] / sample_rows)
+    samples_per_image = c["S"] * c["L"] * (kvp / sample_rows)
     return {
         "value": per_sample * samples_per_image, "unit": UNIT, "cores": cores,
         "kind": "reference",
         "sample": (f"{done} toy_layer_forward units of {sample_rows} query rows x "
-                   f"{c['p']}-row K/V at hs={c['hs']} heads={c['heads']} (reference "
+                   f"{kvp}-row K/V at hs={c['hs']} heads={c['heads']} (reference "
                    f"toy_model.cpp, fp64, {cores} threads in {wall:.1f}s); extrapolated "
                    f"x{samples_per_image:.0f} units/image (linear in rows)"),
     }
@@ -267,6 +278,9 @@ def run_ours(args, c, world, rank):
         if px:
             model = pf.PixArtCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n,
                                   devices)
+        elif c.get("block") == "joint":
+            model = pf.JointDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n,
+                                    devices)
         else:
             model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
     t_build = time.perf_counter() - t_build

@@ -94,10 +94,22 @@ pf_status pf_create(const pf_model_desc* desc, const double* const* weights,
 pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_tokens,
                            const int* devices, int n_stages, pf_ctx** out);
 
-/* Replace the text tokens y [tokens x hidden_size] of a PixArt model. */
+/* SD3-style joint-attention (MMDiT double-stream) block, toy arithmetic per
+ * stream (no reference analogue): `text_tokens` text
+ * rows with their own weights precede the image rows in every activation and
+ * K/V buffer; both streams attend over all joint rows. In PipeFusion the text
+ * rows re-enter from the text tokens every step and travel with patch 0, so
+ * their K/V rows are always fresh; the image rows follow the reference's
+ * patch schedule. Parameters from `seed` (one mt19937_64 stream seeded with
+ * seed ^ "JOINT-DI": per layer the image then the text stream's toy matrices,
+ * then the condition bias); text tokens from seed ^ "TXT-TOKS". */
+pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                          const int* devices, int n_stages, pf_ctx** out);
+
+/* Replace the text tokens y [tokens x hidden_size] of a PixArt / joint model. */
 pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout layout);
 
-/* 0 = toy block, 1 = PixArt block, -1 = NULL context. */
+/* 0 = toy block, 1 = PixArt block, 2 = joint block, -1 = NULL context. */
 int pf_block_kind(const pf_ctx* ctx);
 
 /* ---- One process per GPU ("rank mode") ----

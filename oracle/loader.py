@@ -410,3 +410,34 @@ class PixArtOracle:
         if rc:
             raise OracleError(rc, err.value.decode())
         return out, (fresh.value, stale.value)
+
+
+def uniform_stream(seed: int, n: int) -> np.ndarray:
+    """n next_uniform values of mt19937_64(seed) (pf_oracle.c pfo_uniform_stream)."""
+    lib = ctypes.CDLL(str(RESTATEMENT_LIB))
+    lib.pfo_uniform_stream.argtypes = [ctypes.c_uint64, ctypes.c_int64, _d]
+    out = np.empty(n)
+    lib.pfo_uniform_stream(ctypes.c_uint64(seed), n, _p(out))
+    return out
+
+
+def joint_model(seed, layers, hs, mlp, text_tokens):
+    """Parameters of pf_create_joint(seed, ...) (include/pipefusion_b200.h):
+    per layer (image six, text six) toy matrices, condition bias, text y."""
+    sizes = [(hs, hs)] * 4 + [(hs, mlp), (mlp, hs)]
+    per_layer = 2 * sum(a * b for a, b in sizes)
+    u = uniform_stream(seed ^ 0x4a4f494e542d4449, layers * per_layer + hs)
+    scale = 1.0 / np.sqrt(hs)
+    out, k = [], 0
+    for _ in range(layers):
+        streams = []
+        for _st in range(2):
+            mats = []
+            for a, b in sizes:
+                mats.append(u[k:k + a * b].reshape(a, b) * scale)
+                k += a * b
+            streams.append(tuple(mats))
+        out.append((streams[0], streams[1]))
+    cb = u[k:k + hs] * 1.0
+    y = uniform_stream(seed ^ 0x5458542d544f4b53, text_tokens * hs).reshape(text_tokens, hs)
+    return out, cb, y

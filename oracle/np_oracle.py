@@ -172,3 +172,59 @@ def px_pipefusion(o, x, steps, patches, warmup, eta):
     if steady > 0:
         x = x - eta * pending
     return x
+
+
+# ---------------------------------------------------------------- joint block
+# SD3-style joint-attention (MMDiT double-stream) block with the toy block's
+# arithmetic per stream (csrc/runtime.cpp layer_forward_joint): text rows
+# [0, J) use the text weights, image rows the image weights, every query row
+# attends over all joint K/V rows.
+def joint_layer_forward(w_img, w_txt, heads, h, k_buf, v_buf, row0, J):
+    rows = h.shape[0]
+    t_rows = max(0, min(row0 + rows, J) - row0)
+    parts = [(w_txt, 0, t_rows)] if t_rows else []
+    if rows > t_rows:
+        parts.append((w_img, t_rows, rows))
+    q = np.empty_like(h)
+    for w, a, b in parts:
+        q[a:b] = h[a:b] @ w[0]
+        k_buf[row0 + a:row0 + b] = h[a:b] @ w[1]
+        v_buf[row0 + a:row0 + b] = h[a:b] @ w[2]
+    att = attention_rows(q, k_buf, v_buf, heads)
+    out = h.copy()
+    for w, a, b in parts:
+        out[a:b] = out[a:b] + att[a:b] @ w[3]
+        out[a:b] = out[a:b] + np.tanh(out[a:b] @ w[4]) @ w[5]
+    return out
+
+
+def joint_pipefusion(layers, cb, y, heads, x_init, steps, patches, warmup, eta):
+    """The reference's inline PipeFusion loop (execute.cpp:167-223) with the
+    joint block; the text rows re-enter from y with patch 0 of every step."""
+    p, hs = x_init.shape
+    J = y.shape[0]
+    r = p // patches
+    kv = [[np.zeros((J + p, hs)), np.zeros((J + p, hs))] for _ in layers]
+    x = np.array(x_init, dtype=np.float64)
+    for _ in range(warmup):
+        h = np.concatenate([y, x + cb])
+        for (wi, wt), (kb, vb) in zip(layers, kv):
+            h = joint_layer_forward(wi, wt, heads, h, kb, vb, 0, J)
+        x = x - eta * h[J:]
+    steady = steps - warmup
+    eps = np.zeros_like(x)
+    pending = np.zeros_like(x)
+    for q in range(steady):
+        for j in range(patches):
+            rows = slice(j * r, (j + 1) * r)
+            if q > 0:
+                x[rows] -= eta * pending[rows]
+            hi = x[rows] + cb
+            h, row0 = (np.concatenate([y, hi]), 0) if j == 0 else (hi, J + j * r)
+            for (wi, wt), (kb, vb) in zip(layers, kv):
+                h = joint_layer_forward(wi, wt, heads, h, kb, vb, row0, J)
+            eps[rows] = h[-r:]
+        pending = eps.copy()
+    if steady > 0:
+        x = x - eta * pending
+    return x

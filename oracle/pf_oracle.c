@@ -137,6 +137,14 @@ const double* pfo_weight(const pfo_model* m, int layer, int idx) {
 
 const double* pfo_condition_bias(const pfo_model* m) { return m->cb; }
 
+/* n values of next_uniform (toy_model.cpp:28-30) from mt19937_64(seed): the
+ * raw stream test specs build their parameters from. */
+void pfo_uniform_stream(uint64_t seed, int64_t n, double* out) {
+  mt64 r;
+  mt64_seed(&r, seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = next_uniform(&r);
+}
+
 /* make_initial_latent, toy_model.cpp:84-91 */
 void pfo_latent(uint64_t seed, int64_t p, int hs, double* out) {
   mt64 r;

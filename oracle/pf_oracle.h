@@ -31,6 +31,9 @@ int pfo_mlp_hidden(const pfo_model* m);
 const double* pfo_weight(const pfo_model* m, int layer, int idx);
 const double* pfo_condition_bias(const pfo_model* m);
 
+/* n next_uniform values of mt19937_64(seed) */
+void pfo_uniform_stream(uint64_t seed, int64_t n, double* out);
+
 /* make_initial_latent, toy_model.cpp:84-91 */
 void pfo_latent(uint64_t seed, int64_t p, int hs, double* out);
 

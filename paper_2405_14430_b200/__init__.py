@@ -26,7 +26,7 @@ __all__ = [
     "LIB_PATH", "load_library", "ValidationError", "NumericError", "CudaError",
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
     "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda", "rank_plan",
-    "PLAN_KINDS", "connect_ranks", "connect_distributed", "trace_json",
+    "PLAN_KINDS", "connect_ranks", "connect_distributed", "trace_json", "JointDiTCuda",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = [
     "pf_layer_forward_t", "pf_destroy", "pf_last_error", "pf_create_toy_rank",
     "pf_create_pixart_rank", "pf_peer_blob_size", "pf_export_peer", "pf_connect_peers",
     "pf_rank", "pf_world", "pf_rank_plan", "pf_set_timeline", "pf_timeline",
-    "pf_run_distrifusion", "pf_run_distrifusion_device",
+    "pf_run_distrifusion", "pf_run_distrifusion_device", "pf_create_joint",
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
@@ -99,6 +99,8 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_create_pixart.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32,
                                      ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
     lib.pf_set_text.argtypes = [vp, dptr, i64, i32]
+    lib.pf_create_joint.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32,
+                                    ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
     lib.pf_block_kind.argtypes = [vp]
     lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
     lib.pf_create_toy_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
@@ -209,7 +211,7 @@ class ToyDiTCuda:
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, workers: int = 1,
                  devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0,
-                 _rank=None):
+                 _rank=None, _joint=False):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         self.layers, self.hidden_size, self.heads = layers, hidden_size, heads
@@ -235,7 +237,11 @@ class ToyDiTCuda:
         if len(devs) != workers:
             raise ValidationError("devices must list one CUDA device per worker")
         dev_arr = (ctypes.c_int * max(1, workers))(*devs)
-        if _text_tokens:
+        if _joint:
+            st = self._lib.pf_create_joint(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                           _text_tokens, dev_arr, workers,
+                                           ctypes.byref(self._ctx))
+        elif _text_tokens:
             st = self._lib.pf_create_pixart(ctypes.c_uint64(seed), ctypes.byref(desc),
                                             _text_tokens, dev_arr, workers,
                                             ctypes.byref(self._ctx))
@@ -526,3 +532,24 @@ def trace_json(spans: Sequence[dict]) -> dict:
                                 ev["name"]))
     makespan = max((ev["start_us"] + ev["dur_us"] for ev in events), default=0.0)
     return {"makespan_us": makespan, "events": events}
+
+
+class JointDiTCuda(ToyDiTCuda):
+    """SD3-style joint-attention (MMDiT double-stream) block with the toy
+    block's arithmetic per stream: `text_tokens` text
+    rows with their own weights share the K/V buffer with the image rows;
+    under PipeFusion they re-enter every step with patch 0 (always fresh)."""
+
+    def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
+                 mlp_ratio: float, seq_len: int, text_tokens: int, workers: int = 1,
+                 devices: Optional[Sequence[int]] = None):
+        if text_tokens < 1:
+            raise ValidationError("joint block needs at least one text token")
+        self.text_tokens = text_tokens
+        super().__init__(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers,
+                         devices, _text_tokens=text_tokens, _joint=True)
+
+    def set_text(self, y) -> None:
+        y = _f64c(y)
+        _raise(self._lib.pf_set_text(self._ctx, _dptr(y), y.shape[0], PF_ROW_MAJOR),
+               self._err())

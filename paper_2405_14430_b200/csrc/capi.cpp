@@ -323,7 +323,8 @@ pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout la
   if (!ctx) return PF_VALIDATION;
   return guarded(&ctx->last_error, [&] {
     const pf::ModelShape& m = ctx->engine->shape();
-    if (m.block != pf::kBlockPixArt) throw pf::ValidationError("model has no text conditioning");
+    if (m.block != pf::kBlockPixArt && m.block != pf::kBlockJoint)
+      throw pf::ValidationError("model has no text conditioning");
     if (!y) throw pf::ValidationError("NULL text pointer");
     if (tokens != m.T) throw pf::ValidationError("text token count does not match the model");
     std::vector<double> rm(size_t(tokens) * m.hs);
@@ -332,6 +333,50 @@ pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout la
         rm[size_t(r) * m.hs + c] =
             layout == PF_COL_MAJOR ? y[size_t(c) * tokens + r] : y[size_t(r) * m.hs + c];
     ctx->engine->set_text(rm.data());
+  });
+}
+
+pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                          const int* devices, int n_stages, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.block = pf::kBlockJoint;
+    s.T = text_tokens;
+    ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    // One mt19937_64 stream seeded with seed ^ "JOINT-DI": per layer the
+    // image stream's six toy matrices then the text stream's, in
+    // build_toy_model's order and scale (toy_model.cpp:44-82); then the
+    // condition bias. Text tokens from seed ^ "TXT-TOKS".
+    std::mt19937_64 rng(seed ^ 0x4a4f494e542d4449ULL);
+    const double scale = 1.0 / std::sqrt(double(s.hs));
+    std::vector<double> w[12];
+    for (int l = 0; l < s.layers; ++l) {
+      for (int st = 0; st < 2; ++st) {
+        fill(rng, w[6 * st + 0], s.hs, s.hs, scale);
+        fill(rng, w[6 * st + 1], s.hs, s.hs, scale);
+        fill(rng, w[6 * st + 2], s.hs, s.hs, scale);
+        fill(rng, w[6 * st + 3], s.hs, s.hs, scale);
+        fill(rng, w[6 * st + 4], s.hs, s.mlp, scale);
+        fill(rng, w[6 * st + 5], s.mlp, s.hs, scale);
+      }
+      pf::HostMatrix hm[12];
+      for (int i = 0; i < 12; ++i) {
+        const int k = i % 6;
+        hm[i] = {w[i].data(), k == 5 ? s.mlp : s.hs, k == 4 ? s.mlp : s.hs, false};
+      }
+      ctx->engine->load_layer_joint(l, hm);
+    }
+    std::vector<double> cb;
+    fill(rng, cb, 1, s.hs, 1.0);
+    ctx->engine->load_condition_bias(cb.data());
+    std::mt19937_64 trng(seed ^ 0x5458542d544f4b53ULL);
+    std::vector<double> y;
+    fill(trng, y, text_tokens, s.hs, 1.0);
+    ctx->engine->set_text(y.data());
+    *out = ctx.release();
   });
 }
 

@@ -102,8 +102,10 @@ void validate_shape(const ModelShape& s) {
     throw ValidationError("CUDA backend needs hidden_size and mlp hidden size divisible by 8");
   if (s.P % 8 != 0) throw ValidationError("CUDA backend needs seq_len divisible by 8");
   if (s.hs / s.heads > 128) throw ValidationError("CUDA backend supports head dim <= 128");
-  if (s.block != kBlockToy && s.block != kBlockPixArt)
+  if (s.block != kBlockToy && s.block != kBlockPixArt && s.block != kBlockJoint)
     throw ValidationError("unknown block kind");
+  if (s.block == kBlockJoint && s.T < 1)
+    throw ValidationError("joint block needs at least one text token");
   if (s.block == kBlockPixArt) {
     if (s.hs % 32 != 0)
       throw ValidationError("PixArt block needs hidden_size divisible by 32");
@@ -194,7 +196,8 @@ Engine::~Engine() {
 void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
   DeviceGuard g(s.device);
   const ModelShape& m = shape_;
-  const size_t P = size_t(m.P), hs = size_t(m.hs), mlp = size_t(m.mlp);
+  // activation / K/V buffers hold the joint rows (text rows first, joint block)
+  const size_t P = size_t(m.rows_total()), hs = size_t(m.hs), mlp = size_t(m.mlp);
   const size_t heads = size_t(m.heads), dhp = size_t(m.dhp);
   s.first_layer = first;
   s.layer_count = count;
@@ -250,9 +253,24 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
     L.tm_k = tmap(L.k, dhp, heads * P, dhp * 2, 16, 128, 32);
     L.tm_v = tmap(L.v, dhp, heads * P, dhp * 2, 16, 128, 32);
   }
+  s.zeros = dalloc<float>(hs);
   if (is_first) {
-    s.x = dalloc<float>(P * hs);
+    s.x = dalloc<float>(size_t(m.P) * hs);
     s.cb = dalloc<float>(hs);
+    if (m.block == kBlockJoint) s.text = dalloc<float>(size_t(m.T) * hs);
+  }
+  if (m.block == kBlockJoint) {
+    for (StageLayer& L : s.layers) {
+      L.t_wqkv = dalloc<bf16>(3 * hs * hs);
+      L.t_wo = dalloc<bf16>(hs * hs);
+      L.t_win = dalloc<bf16>(mlp * hs);
+      L.t_wout = dalloc<bf16>(hs * mlp);
+      if (!make_weight_maps(&L.tm_t_wqkv, L.t_wqkv, int(3 * hs), int(hs)) ||
+          !make_weight_maps(&L.tm_t_wo, L.t_wo, int(hs), int(hs)) ||
+          !make_weight_maps(&L.tm_t_win, L.t_win, int(mlp), int(hs)) ||
+          !make_weight_maps(&L.tm_t_wout, L.t_wout, int(hs), int(mlp)))
+        throw CudaError("cuTensorMapEncodeTiled failed for a text-stream weight");
+    }
   }
   if (m.block == kBlockPixArt) {
     const size_t T = size_t(m.T), Tpad = (T + 127) / 128 * 128;
@@ -333,6 +351,7 @@ void Engine::free_stage(Stage& s) {
   for (StageLayer& L : s.layers) {
     for (float* p : {L.bqkv, L.bo, L.bqc, L.bkvc, L.boc, L.b1, L.b2}) dfree(p);
     dfree(L.k2); dfree(L.v2);
+    dfree(L.t_wqkv); dfree(L.t_wo); dfree(L.t_win); dfree(L.t_wout);
     dfree(L.wqc); dfree(L.wkvc); dfree(L.woc); dfree(L.kc); dfree(L.vc);
   }
   {
@@ -347,8 +366,9 @@ void Engine::free_stage(Stage& s) {
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
-  dfree(s.attn_work); dfree(s.flag); dfree(s.splitk_ws); dfree(s.splitk_counters); dfree(s.x); dfree(s.cb);
-  if (s.eps && s.eps != s.h32) dfree(s.eps);
+  dfree(s.attn_work); dfree(s.flag); dfree(s.splitk_ws); dfree(s.splitk_counters);
+  dfree(s.zeros); dfree(s.text); dfree(s.x); dfree(s.cb);
+  if (s.eps_owned) dfree(s.eps);
   for (cudaEvent_t e : s.ev_eps) cudaEventDestroy(e);
   s.ev_eps.clear();
   if (s.ev_fwd) cudaEventDestroy(s.ev_fwd);
@@ -364,32 +384,50 @@ int Engine::stage_of_layer(int layer) const {
   return -1;
 }
 
+namespace {
+// One stream's six toy matrices (x.W orientation) -> bf16 N x K (K-major).
+void upload_toy_weights(int device, int hs, int mlp, const HostMatrix* w, bf16* wqkv, bf16* wo,
+                        bf16* win, bf16* wout) {
+  auto pack = [](const HostMatrix& W, std::vector<bf16>& dst, size_t n_off, int K) {
+    for (int n = 0; n < W.cols; ++n)
+      for (int k = 0; k < K; ++k)
+        dst[(n_off + size_t(n)) * size_t(K) + size_t(k)] = __float2bfloat16_rn(float(W.at(k, n)));
+  };
+  std::vector<bf16> qkv(size_t(3) * hs * hs), o(size_t(hs) * hs), in(size_t(mlp) * hs),
+      out(size_t(hs) * mlp);
+  pack(w[0], qkv, 0, hs);
+  pack(w[1], qkv, size_t(hs), hs);
+  pack(w[2], qkv, size_t(2) * hs, hs);
+  pack(w[3], o, 0, hs);
+  pack(w[4], in, 0, hs);
+  pack(w[5], out, 0, mlp);
+  DeviceGuard g(device);
+  PF_CUDA_CHECK(cudaMemcpy(wqkv, qkv.data(), qkv.size() * 2, cudaMemcpyHostToDevice));
+  PF_CUDA_CHECK(cudaMemcpy(wo, o.data(), o.size() * 2, cudaMemcpyHostToDevice));
+  PF_CUDA_CHECK(cudaMemcpy(win, in.data(), in.size() * 2, cudaMemcpyHostToDevice));
+  PF_CUDA_CHECK(cudaMemcpy(wout, out.data(), out.size() * 2, cudaMemcpyHostToDevice));
+}
+}  // namespace
+
 void Engine::load_layer(int layer, const HostMatrix (&w)[6]) {
   const int d = stage_of_layer(layer);
   if (d < 0 && rank_mode() && layer >= 0 && layer < shape_.layers) return;  // another rank's
   if (d < 0) throw ValidationError("layer index out of range");
   Stage& s = stages_[size_t(d)];
   StageLayer& L = s.layers[size_t(layer - s.first_layer)];
-  const int hs = shape_.hs, mlp = shape_.mlp;
-  // Transpose to N x K (K-major) bf16: dst[n*K + k] = W[k][n].
-  auto pack = [](const HostMatrix& W, std::vector<bf16>& dst, size_t n_off, int K) {
-    for (int n = 0; n < W.cols; ++n)
-      for (int k = 0; k < K; ++k)
-        dst[(n_off + size_t(n)) * size_t(K) + size_t(k)] = __float2bfloat16_rn(float(W.at(k, n)));
-  };
-  std::vector<bf16> qkv(size_t(3) * hs * hs), wo(size_t(hs) * hs),
-      win(size_t(mlp) * hs), wout(size_t(hs) * mlp);
-  pack(w[0], qkv, 0, hs);
-  pack(w[1], qkv, size_t(hs), hs);
-  pack(w[2], qkv, size_t(2) * hs, hs);
-  pack(w[3], wo, 0, hs);
-  pack(w[4], win, 0, hs);
-  pack(w[5], wout, 0, mlp);
-  DeviceGuard g(s.device);
-  PF_CUDA_CHECK(cudaMemcpy(L.wqkv, qkv.data(), qkv.size() * 2, cudaMemcpyHostToDevice));
-  PF_CUDA_CHECK(cudaMemcpy(L.wo, wo.data(), wo.size() * 2, cudaMemcpyHostToDevice));
-  PF_CUDA_CHECK(cudaMemcpy(L.win, win.data(), win.size() * 2, cudaMemcpyHostToDevice));
-  PF_CUDA_CHECK(cudaMemcpy(L.wout, wout.data(), wout.size() * 2, cudaMemcpyHostToDevice));
+  upload_toy_weights(s.device, shape_.hs, shape_.mlp, w, L.wqkv, L.wo, L.win, L.wout);
+}
+
+void Engine::load_layer_joint(int layer, const HostMatrix (&w)[12]) {
+  if (shape_.block != kBlockJoint) throw ValidationError("model is not a joint-block model");
+  const int d = stage_of_layer(layer);
+  if (d < 0 && rank_mode() && layer >= 0 && layer < shape_.layers) return;
+  if (d < 0) throw ValidationError("layer index out of range");
+  Stage& s = stages_[size_t(d)];
+  StageLayer& L = s.layers[size_t(layer - s.first_layer)];
+  upload_toy_weights(s.device, shape_.hs, shape_.mlp, w, L.wqkv, L.wo, L.win, L.wout);
+  upload_toy_weights(s.device, shape_.hs, shape_.mlp, w + 6, L.t_wqkv, L.t_wo, L.t_win,
+                     L.t_wout);
 }
 
 void Engine::load_condition_bias(const double* cb) {
@@ -533,9 +571,15 @@ void Engine::send_rows(int from, int row0, int rows, int patch, int t) {
     DeviceGuard g2(dst.device);
     PF_CUDA_CHECK(cudaStreamWaitEvent(dst.stream, src.ev_fwd, 0));
   } else if (n > 1) {
+    // eps: image rows only, image-indexed on stage 0 (joint rows start at J)
     Stage& s0 = stages_[0];
-    PF_CUDA_CHECK(cudaMemcpyAsync(s0.eps + off, src.h32 + off, cnt * 4,
-                                  cudaMemcpyDefault, src.stream));
+    const int64_t J = shape_.J();
+    const int64_t i0 = std::max<int64_t>(row0, J), i1 = int64_t(row0) + rows;
+    if (i1 > i0)
+      PF_CUDA_CHECK(cudaMemcpyAsync(s0.eps + size_t(i0 - J) * shape_.hs,
+                                    src.h32 + size_t(i0) * shape_.hs,
+                                    size_t(i1 - i0) * shape_.hs * 4, cudaMemcpyDefault,
+                                    src.stream));
     tl_end(src.stream);
   }
 }
@@ -604,7 +648,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     // warmup the zero rows are read as stale context, so clear them; with
     // warmup every row is rewritten before it is read.
     if (warmup == 0) {
-      const size_t kv = size_t(m.heads) * size_t(m.P) * size_t(m.dhp) * sizeof(bf16);
+      const size_t kv = size_t(m.heads) * size_t(m.rows_total()) * size_t(m.dhp) * sizeof(bf16);
       for (StageLayer& L : s.layers) {
         PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
         PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kv, s.stream));
@@ -620,10 +664,21 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       DeviceGuard g(s.device);
       px_conditioning(s, steps);
     }
+  const bool joint = m.block == kBlockJoint;
+  const int J = int(m.J());  // joint block: text rows [0, J) precede the image rows
   auto forward = [&](Stage& s, int lf, int rows, int row0, int t, int code) {
     if (px) layer_forward_px(s, lf, rows, row0, t, code);
+    else if (joint) layer_forward_joint(s, lf, rows, row0, code);
     else layer_forward(s, lf, rows, row0, code);
   };
+  // joint block: the text stream re-enters from the text tokens every step
+  auto text_prepare = [&]() {
+    check(patch_prepare(s0.text, nullptr, s0.zeros, s0.h32, s0.hb, 0, J, m.hs, 0.f, false,
+                        s0.stream), "text rows");
+    ++launches_;
+  };
+  float* h32_img = s0.h32 + size_t(J) * m.hs;  // image row 0 of the activations
+  bf16* hb_img = s0.hb + size_t(J) * m.hs;
 
   // ---- warmup: synchronous full-sequence steps (execute.cpp:181-190)
   for (int w = 0; w < warmup; ++w) {
@@ -632,10 +687,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       DeviceGuard g(s0.device);
       tl_begin(0, 0, -1, t, s0.stream);
       prof_begin(s0, kSampler, 0, double(m.P) * m.hs * (4 + 4 + 2));
+      if (joint) text_prepare();
       if (px)
         px_patch_prepare(x_dev, false, 0, int(m.P), t, 0.f);
       else
-        check(patch_prepare(x_dev, nullptr, s0.cb, s0.h32, s0.hb, 0, int(m.P), m.hs,
+        check(patch_prepare(x_dev, nullptr, s0.cb, h32_img, hb_img, 0, int(m.P), m.hs,
                             0.f, false, s0.stream), "patch_prepare");
       prof_end(s0);
       ++launches_;
@@ -648,10 +704,10 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         auto& sv = src[size_t(d)][size_t(lf)];
         std::fill(sv.begin(), sv.end(), t);
         st.fresh += patches;
-        forward(s, lf, int(m.P), 0, t, next_code(t, s.first_layer + lf));
+        forward(s, lf, int(m.rows_total()), 0, t, next_code(t, s.first_layer + lf));
       }
       tl_end(s.stream);
-      send_rows(d, 0, int(m.P), -1, t);
+      send_rows(d, 0, int(m.rows_total()), -1, t);
     }
     if (n > 1) {
       Stage& last = stages_[size_t(n - 1)];
@@ -672,17 +728,21 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
   for (int q = 0; q < steady; ++q) {
     const int t = steady - 1 - q;
     for (int j = 0; j < patches; ++j) {
-      const int row0 = j * r;
+      const int row0 = j * r;  // image rows of patch j
+      // the block's joint rows: the text rows travel with patch 0
+      const int brow0 = joint && j > 0 ? J + row0 : 0;
+      const int brows = joint && j == 0 ? J + r : r;
       {
         DeviceGuard g(s0.device);
         if (q > 0 && n > 1)
           PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[size_t(j)], 0));
         tl_begin(0, 0, j, t, s0.stream);
         prof_begin(s0, kSampler, 0, double(r) * m.hs * (q > 0 ? 4 + 4 + 4 + 4 + 2 : 4 + 4 + 2));
+        if (joint && j == 0) text_prepare();
         if (px)
           px_patch_prepare(x_dev, q > 0, row0, r, t, eta);
         else
-          check(patch_prepare(x_dev, s0.eps, s0.cb, s0.h32, s0.hb, row0, r, m.hs, eta,
+          check(patch_prepare(x_dev, s0.eps, s0.cb, h32_img, hb_img, row0, r, m.hs, eta,
                               q > 0, s0.stream), "patch_prepare");
         prof_end(s0);
         ++launches_;
@@ -707,7 +767,8 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
               throw NumericError(os.str());
             }
           }
-          forward(s, lf, r, row0, t, next_code(t, s.first_layer + lf));
+          forward(s, lf, joint ? brows : r, joint ? brow0 : row0, t,
+                  next_code(t, s.first_layer + lf));
         }
         // fresh_fraction(src[0], t) after the stage (execute.cpp:67-73,164)
         {
@@ -717,7 +778,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
           st.fresh_fraction[size_t(d)].push_back(double(fresh) / double(s0v.size()));
         }
         tl_end(s.stream);
-        send_rows(d, row0, r, j, t);
+        send_rows(d, joint ? brow0 : row0, joint ? brows : r, j, t);
         if (d == n - 1 && n > 1)
           PF_CUDA_CHECK(cudaEventRecord(s0.ev_eps[size_t(j)], s.stream));
       }
@@ -753,11 +814,12 @@ void Engine::prepare_run(int patches, int steps) {
     DeviceGuard g(s0.device);
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
   }
-  if (n > 1 && !s0.eps) {
+  if (n > 1 && !s0.eps_owned) {
     DeviceGuard g(s0.device);
     s0.eps = dalloc<float>(size_t(shape_.P) * shape_.hs);
+    s0.eps_owned = true;
   }
-  if (n == 1) s0.eps = s0.h32;
+  if (n == 1) s0.eps = s0.h32 + size_t(shape_.J()) * shape_.hs;  // image rows of h
   if (int(s0.ev_eps.size()) < patches) {
     DeviceGuard g(stages_[size_t(n - 1)].device);
     while (int(s0.ev_eps.size()) < patches) {
@@ -838,6 +900,8 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
                                 double* k_buf, double* v_buf, bool col_major, int t,
                                 int steps) {
   const ModelShape& m = shape_;
+  if (m.block == kBlockJoint)
+    throw ValidationError("single-layer entry point not available for the joint block");
   const int d = stage_of_layer(layer);
   if (d < 0) throw ValidationError("layer index out of range");
   if (rows < 1 || row0 < 0 || row0 + rows > m.P)
@@ -911,6 +975,81 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
     os << "non-finite activation at timestep 0, layer " << layer;
     throw NumericError(os.str());
   }
+}
+
+// ============================================================== joint block
+// SD3-style MMDiT double-stream block with the toy block's arithmetic per
+// stream: rows [0, T) are the text stream (own weights), rows [T, T + P)
+// the image stream; both streams' queries attend over all joint K/V rows.
+// A row block [row0, row0 + rows) is the text rows plus image patch 0, or an
+// image patch alone.
+void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code) {
+  const ModelShape& m = shape_;
+  StageLayer& L = s.layers[size_t(lf)];
+  const int J = int(m.J()), Pt = int(m.rows_total()), hs = m.hs;
+  const int t_rows = row0 < J ? std::min(row0 + rows, J) - row0 : 0;
+  const int i_row0 = std::max(row0, J), i_rows = row0 + rows - i_row0;
+  auto both = [&](auto&& fn) {
+    if (t_rows > 0) fn(true, row0, t_rows);
+    if (i_rows > 0) fn(false, i_row0, i_rows);
+  };
+  const double dhs = hs, mlp = m.mlp;
+  EpiParams qkv;
+  qkv.q = s.q;
+  qkv.k = L.k;
+  qkv.v = L.v;
+  qkv.hs = hs;
+  qkv.dh = m.dh;
+  qkv.dhp = m.dhp;
+  qkv.P = Pt;
+  both([&](bool txt, int r0, int n) {
+    prof_begin(s, kGemmQKV, 2.0 * n * dhs * 3 * dhs, 0);
+    check(gemm(s.tm_hb, txt ? L.tm_t_wqkv : L.tm_wqkv, n, r0, 3 * hs, hs, Epi::QKV,
+               sk(s, qkv), s.sm_count, s.stream), "gemm qkv (joint)");
+    prof_end(s);
+    ++launches_;
+  });
+  AttnLaunch a{m.dhp, Pt, rows, row0, m.heads, m.dh, hs,
+               float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
+               s.attn_work_floats};
+  prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
+  check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (joint)");
+  prof_end(s);
+  launches_ += 1 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0);
+  EpiParams res;
+  res.out_f32 = s.h32;
+  res.out_bf16 = s.hb;
+  res.ld = hs;
+  res.flag = s.flag;
+  res.code = code;
+  if (hs % 32 == 0) {
+    res.tm_h32 = &s.tm_h32;
+    res.tm_hb = &s.tm_hb;
+  }
+  both([&](bool txt, int r0, int n) {
+    prof_begin(s, kGemmOut, 2.0 * n * dhs * dhs, 0);
+    check(gemm(s.tm_attn, txt ? L.tm_t_wo : L.tm_wo, n, r0, hs, hs, Epi::Residual, sk(s, res),
+               s.sm_count, s.stream), "gemm out-proj (joint)");
+    prof_end(s);
+    ++launches_;
+  });
+  EpiParams th;
+  th.out_bf16 = s.z;
+  th.ld = m.mlp;
+  both([&](bool txt, int r0, int n) {
+    prof_begin(s, kGemmMlpIn, 2.0 * n * dhs * mlp, 0);
+    check(gemm(s.tm_hb, txt ? L.tm_t_win : L.tm_win, n, r0, m.mlp, hs, Epi::Tanh, sk(s, th),
+               s.sm_count, s.stream), "gemm mlp-in (joint)");
+    prof_end(s);
+    ++launches_;
+  });
+  both([&](bool txt, int r0, int n) {
+    prof_begin(s, kGemmMlpOut, 2.0 * n * dhs * mlp, 0);
+    check(gemm(s.tm_z, txt ? L.tm_t_wout : L.tm_wout, n, r0, hs, m.mlp, Epi::Residual,
+               sk(s, res), s.sm_count, s.stream), "gemm mlp-out (joint)");
+    prof_end(s);
+    ++launches_;
+  });
 }
 
 // ============================================================== DistriFusion
@@ -1124,6 +1263,8 @@ Engine::Engine(const ModelShape& shape_in, int device, int rank, int world)
        << " (fewer layers than stages)";
     throw ValidationError(os.str());
   }
+  if (shape_.block == kBlockJoint)
+    throw ValidationError("rank mode supports the toy and PixArt blocks");
   int dev_count = 0;
   PF_CUDA_CHECK(cudaGetDeviceCount(&dev_count));
   if (device < 0 || device >= dev_count) {
@@ -1142,7 +1283,10 @@ Engine::Engine(const ModelShape& shape_in, int device, int rank, int world)
     PF_CUDA_CHECK(cudaStreamCreateWithFlags(&send_stream_, cudaStreamNonBlocking));
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming));
     sig_ = dalloc<uint32_t>(64);
-    if (rank == 0 && world > 1) s.eps = dalloc<float>(size_t(shape_.P) * shape_.hs);
+    if (rank == 0 && world > 1) {
+      s.eps = dalloc<float>(size_t(shape_.P) * shape_.hs);
+      s.eps_owned = true;
+    }
   } catch (...) {
     free_stage(s);
     throw;
@@ -1497,6 +1641,16 @@ void Engine::load_px_globals(const double* const* gw) {
 }
 
 void Engine::set_text(const double* y) {
+  if (shape_.block == kBlockJoint) {
+    Stage& s0 = stages_[0];
+    if (!s0.text) return;  // rank mode, rank > 0: text enters the pipeline on rank 0
+    std::vector<float> t(size_t(shape_.T) * shape_.hs);
+    for (size_t i = 0; i < t.size(); ++i) t[i] = float(y[i]);
+    DeviceGuard g(s0.device);
+    PF_CUDA_CHECK(cudaStreamSynchronize(s0.stream));
+    PF_CUDA_CHECK(cudaMemcpy(s0.text, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    return;
+  }
   if (shape_.block != kBlockPixArt) throw ValidationError("model is not a PixArt block model");
   std::vector<bf16> t(size_t(shape_.T) * shape_.hs);
   for (size_t i = 0; i < t.size(); ++i) t[i] = to_bf(y[i]);

@@ -51,12 +51,19 @@ struct ModelShape {
   int64_t P = 0;  // sequence length = K/V buffer rows
   int dh = 0;
   int dhp = 0;    // dh rounded up to a multiple of 16
-  int block = 0;  // kBlockToy (toy_model.cpp:145-177) or kBlockPixArt
-  int T = 0;      // PixArt: text tokens in the cross-attention K/V
+  int block = 0;  // kBlockToy (toy_model.cpp:145-177), kBlockPixArt or kBlockJoint
+  int T = 0;      // text tokens (PixArt: cross-attention K/V; joint: rows 0..T-1)
+  // joint-row offset of image row 0 and rows of the activation / K/V buffers
+  int64_t J() const { return block == 2 ? T : 0; }
+  int64_t rows_total() const { return P + J(); }
 };
 
 constexpr int kBlockToy = 0;
 constexpr int kBlockPixArt = 1;
+// SD3-style joint-attention block (MMDiT double stream, toy arithmetic per
+// stream): T text rows precede the P image rows in every activation and K/V
+// buffer ("joint rows"); text rows are recomputed with patch 0 of every step.
+constexpr int kBlockJoint = 2;
 constexpr int kPxFreq = 256;  // sinusoidal timestep features
 
 // Host fp64 source of one layer's weights, in the reference's orientation
@@ -85,6 +92,9 @@ struct StageLayer {
   CUtensorMap tm_k2, tm_v2;
   // PixArt block (oracle/px_oracle.c): biases fp32, cross-attention weights,
   // per-image cross K/V of the text tokens [heads][T][dhp]
+  // joint block: the text stream's weights (same roles as wqkv .. wout)
+  bf16 *t_wqkv = nullptr, *t_wo = nullptr, *t_win = nullptr, *t_wout = nullptr;
+  WeightMaps tm_t_wqkv, tm_t_wo, tm_t_win, tm_t_wout;
   float *bqkv = nullptr, *bo = nullptr, *bqc = nullptr, *bkvc = nullptr, *boc = nullptr,
         *b1 = nullptr, *b2 = nullptr;
   bf16 *wqc = nullptr, *wkvc = nullptr, *woc = nullptr;  // [hs x hs], [2hs x hs], [hs x hs]
@@ -137,7 +147,10 @@ struct Stage {
   // stage 0 only
   float* x = nullptr;    // [P x hs] latent
   float* eps = nullptr;  // [P x hs] noise landing buffer (== last stage h32 when N == 1)
+  bool eps_owned = false;
   float* cb = nullptr;   // [hs] condition bias
+  float* zeros = nullptr;  // [hs]
+  float* text = nullptr;   // joint block: [T x hs] text tokens (fp32), stage 0
   std::vector<cudaEvent_t> ev_eps;  // per patch, recorded by the last stage
   PxStage px;
 };
@@ -208,6 +221,9 @@ class Engine {
   void load_px_globals(const double* const* g);
   // Text tokens y [T x hs] (row-major fp64) used by every stage's cross-attention.
   void set_text(const double* y);
+  // Joint block: one layer's 12 matrices, image stream (w_q, w_k, w_v, w_o,
+  // w_mlp_in, w_mlp_out) then text stream, x.W orientation as load_layer.
+  void load_layer_joint(int layer, const HostMatrix (&w)[12]);
 
   // ditsim::run_distrifusion (execute.hpp:131-133, execute.cpp:431-531) on
   // a single-stage engine: `workers` row shards, each attending over its own
@@ -276,6 +292,7 @@ class Engine {
   void layer_forward(Stage& s, int lf, int rows, int row0, int code,
                      const KvView* kv = nullptr);
   void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
+  void layer_forward_joint(Stage& s, int lf, int rows, int row0, int code);
   void px_conditioning(Stage& s, int steps);
   void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
   void send_rows(int from, int row0, int rows, int patch, int t);
