@@ -72,6 +72,10 @@ CONFIGS = {
                     "24 heads, 4096 image + 333 text tokens in one K/V buffer; toy arithmetic "
                     "per stream), 20 steps, 1 warmup",
                L=24, hs=1536, heads=24, p=4096, S=20, W=1, block="joint", T=333),
+    "c5": dict(name="Flux.1-shaped DiT 2048px (19 double-stream + 38 single-stream blocks, "
+                    "hidden 3072, 24 heads, 16384 image + 512 text tokens, ~8.6B toy-block "
+                    "parameters), 28 steps, 1 warmup",
+               L=57, hs=3072, heads=24, p=16384, S=28, W=1, block="joint", T=512, D=19),
     "c1": dict(name="tiny DiT (4 layers, hidden 128, 4 heads, 256 tokens), 5 steps, 1 warmup",
                L=4, hs=128, heads=4, p=256, S=5, W=1),
     "cref": dict(name="reference_execute.cfg (4 layers, hidden 32, 4 heads, 64 tokens), 20 "
@@ -280,7 +284,7 @@ def run_ours(args, c, world, rank):
                                   devices)
         elif c.get("block") == "joint":
             model = pf.JointDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n,
-                                    devices)
+                                    devices, double_layers=c.get("D"))
         else:
             model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
     t_build = time.perf_counter() - t_build

@@ -100,11 +100,15 @@ pf_status pf_create_pixart(uint64_t seed, const pf_model_desc* desc, int text_to
  * K/V buffer; both streams attend over all joint rows. In PipeFusion the text
  * rows re-enter from the text tokens every step and travel with patch 0, so
  * their K/V rows are always fresh; the image rows follow the reference's
- * patch schedule. Parameters from `seed` (one mt19937_64 stream seeded with
- * seed ^ "JOINT-DI": per layer the image then the text stream's toy matrices,
- * then the condition bias); text tokens from seed ^ "TXT-TOKS". */
+ * patch schedule. Layers [double_layers, layers) are Flux-style single-stream
+ * blocks instead (one weight set for all joint rows, attention and MLP in
+ * parallel: h += attn(h) Wo + tanh(h Win) Wout). Parameters from `seed` (one
+ * mt19937_64 stream seeded with seed ^ "JOINT-DI": per layer the image
+ * stream's toy matrices, then for double-stream layers the text stream's,
+ * then the condition bias; w_o and w_mlp_out carry an extra 1/sqrt(2 layers)
+ * so deep unnormalised stacks stay finite); text tokens from seed ^ "TXT-TOKS". */
 pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tokens,
-                          const int* devices, int n_stages, pf_ctx** out);
+                          int double_layers, const int* devices, int n_stages, pf_ctx** out);
 
 /* Replace the text tokens y [tokens x hidden_size] of a PixArt / joint model. */
 pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout layout);

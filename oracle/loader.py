@@ -421,23 +421,27 @@ def uniform_stream(seed: int, n: int) -> np.ndarray:
     return out
 
 
-def joint_model(seed, layers, hs, mlp, text_tokens):
+def joint_model(seed, layers, hs, mlp, text_tokens, double_layers=None):
     """Parameters of pf_create_joint(seed, ...) (include/pipefusion_b200.h):
-    per layer (image six, text six) toy matrices, condition bias, text y."""
+    per layer (image six, text six | None for single-stream layers) toy
+    matrices, condition bias, text y."""
+    D = layers if double_layers is None else double_layers
     sizes = [(hs, hs)] * 4 + [(hs, mlp), (mlp, hs)]
-    per_layer = 2 * sum(a * b for a, b in sizes)
-    u = uniform_stream(seed ^ 0x4a4f494e542d4449, layers * per_layer + hs)
+    per_stream = sum(a * b for a, b in sizes)
+    total = (D * 2 + (layers - D)) * per_stream + hs
+    u = uniform_stream(seed ^ 0x4a4f494e542d4449, total)
     scale = 1.0 / np.sqrt(hs)
+    rscale = scale / np.sqrt(2.0 * layers)  # w_o, w_mlp_out: depth-scaled
     out, k = [], 0
-    for _ in range(layers):
+    for l in range(layers):
         streams = []
-        for _st in range(2):
+        for _st in range(2 if l < D else 1):
             mats = []
-            for a, b in sizes:
-                mats.append(u[k:k + a * b].reshape(a, b) * scale)
+            for i, (a, b) in enumerate(sizes):
+                mats.append(u[k:k + a * b].reshape(a, b) * (rscale if i in (3, 5) else scale))
                 k += a * b
             streams.append(tuple(mats))
-        out.append((streams[0], streams[1]))
+        out.append((streams[0], streams[1] if l < D else None))
     cb = u[k:k + hs] * 1.0
     y = uniform_stream(seed ^ 0x5458542d544f4b53, text_tokens * hs).reshape(text_tokens, hs)
     return out, cb, y

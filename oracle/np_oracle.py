@@ -198,6 +198,24 @@ def joint_layer_forward(w_img, w_txt, heads, h, k_buf, v_buf, row0, J):
     return out
 
 
+def single_layer_forward(w, heads, h, k_buf, v_buf, row0):
+    """Flux-style single-stream block, toy arithmetic: attention and MLP both
+    read the block input; one weight set for every joint row."""
+    r = h.shape[0]
+    q = h @ w[0]
+    k_buf[row0:row0 + r] = h @ w[1]
+    v_buf[row0:row0 + r] = h @ w[2]
+    z = np.tanh(h @ w[4])
+    return h + attention_rows(q, k_buf, v_buf, heads) @ w[3] + z @ w[5]
+
+
+def _joint_or_single(layer, heads, h, kb, vb, row0, J):
+    wi, wt = layer
+    if wt is None:
+        return single_layer_forward(wi, heads, h, kb, vb, row0)
+    return joint_layer_forward(wi, wt, heads, h, kb, vb, row0, J)
+
+
 def joint_pipefusion(layers, cb, y, heads, x_init, steps, patches, warmup, eta):
     """The reference's inline PipeFusion loop (execute.cpp:167-223) with the
     joint block; the text rows re-enter from y with patch 0 of every step."""
@@ -208,8 +226,8 @@ def joint_pipefusion(layers, cb, y, heads, x_init, steps, patches, warmup, eta):
     x = np.array(x_init, dtype=np.float64)
     for _ in range(warmup):
         h = np.concatenate([y, x + cb])
-        for (wi, wt), (kb, vb) in zip(layers, kv):
-            h = joint_layer_forward(wi, wt, heads, h, kb, vb, 0, J)
+        for lw, (kb, vb) in zip(layers, kv):
+            h = _joint_or_single(lw, heads, h, kb, vb, 0, J)
         x = x - eta * h[J:]
     steady = steps - warmup
     eps = np.zeros_like(x)
@@ -221,8 +239,8 @@ def joint_pipefusion(layers, cb, y, heads, x_init, steps, patches, warmup, eta):
                 x[rows] -= eta * pending[rows]
             hi = x[rows] + cb
             h, row0 = (np.concatenate([y, hi]), 0) if j == 0 else (hi, J + j * r)
-            for (wi, wt), (kb, vb) in zip(layers, kv):
-                h = joint_layer_forward(wi, wt, heads, h, kb, vb, row0, J)
+            for lw, (kb, vb) in zip(layers, kv):
+                h = _joint_or_single(lw, heads, h, kb, vb, row0, J)
             eps[rows] = h[-r:]
         pending = eps.copy()
     if steady > 0:

@@ -99,7 +99,7 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_create_pixart.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32,
                                      ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
     lib.pf_set_text.argtypes = [vp, dptr, i64, i32]
-    lib.pf_create_joint.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32,
+    lib.pf_create_joint.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32,
                                     ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
     lib.pf_block_kind.argtypes = [vp]
     lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
@@ -211,7 +211,7 @@ class ToyDiTCuda:
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, workers: int = 1,
                  devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0,
-                 _rank=None, _joint=False):
+                 _rank=None, _joint=None):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         self.layers, self.hidden_size, self.heads = layers, hidden_size, heads
@@ -237,9 +237,9 @@ class ToyDiTCuda:
         if len(devs) != workers:
             raise ValidationError("devices must list one CUDA device per worker")
         dev_arr = (ctypes.c_int * max(1, workers))(*devs)
-        if _joint:
+        if _joint is not None:
             st = self._lib.pf_create_joint(ctypes.c_uint64(seed), ctypes.byref(desc),
-                                           _text_tokens, dev_arr, workers,
+                                           _text_tokens, _joint, dev_arr, workers,
                                            ctypes.byref(self._ctx))
         elif _text_tokens:
             st = self._lib.pf_create_pixart(ctypes.c_uint64(seed), ctypes.byref(desc),
@@ -542,12 +542,15 @@ class JointDiTCuda(ToyDiTCuda):
 
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, text_tokens: int, workers: int = 1,
-                 devices: Optional[Sequence[int]] = None):
+                 devices: Optional[Sequence[int]] = None, double_layers: Optional[int] = None):
+        """double_layers: leading double-stream layers (default: all); the rest
+        are Flux-style single-stream blocks."""
         if text_tokens < 1:
             raise ValidationError("joint block needs at least one text token")
         self.text_tokens = text_tokens
+        self.double_layers = layers if double_layers is None else double_layers
         super().__init__(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers,
-                         devices, _text_tokens=text_tokens, _joint=True)
+                         devices, _text_tokens=text_tokens, _joint=self.double_layers)
 
     def set_text(self, y) -> None:
         y = _f64c(y)

@@ -337,7 +337,7 @@ pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout la
 }
 
 pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tokens,
-                          const int* devices, int n_stages, pf_ctx** out) {
+                          int double_layers, const int* devices, int n_stages, pf_ctx** out) {
   if (out) *out = nullptr;
   return guarded(&g_create_error, [&] {
     if (!out) throw pf::ValidationError("output pointer is NULL");
@@ -345,22 +345,28 @@ pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tok
     pf::ModelShape s = shape_of(desc);
     s.block = pf::kBlockJoint;
     s.T = text_tokens;
+    s.double_layers = double_layers;
     ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
     // One mt19937_64 stream seeded with seed ^ "JOINT-DI": per layer the
-    // image stream's six toy matrices then the text stream's, in
-    // build_toy_model's order and scale (toy_model.cpp:44-82); then the
-    // condition bias. Text tokens from seed ^ "TXT-TOKS".
+    // image stream's six toy matrices then (double-stream layers only) the
+    // text stream's, in build_toy_model's order and scale
+    // (toy_model.cpp:44-82); then the condition bias. Text tokens from
+    // seed ^ "TXT-TOKS".
     std::mt19937_64 rng(seed ^ 0x4a4f494e542d4449ULL);
     const double scale = 1.0 / std::sqrt(double(s.hs));
+    // residual projections (w_o, w_mlp_out) additionally scaled by
+    // 1/sqrt(2 layers) (depth-scaled init) so deep stacks without
+    // normalisation (57 Flux-shaped layers) stay finite
+    const double rscale = scale / std::sqrt(2.0 * s.layers);
     std::vector<double> w[12];
     for (int l = 0; l < s.layers; ++l) {
-      for (int st = 0; st < 2; ++st) {
+      for (int st = 0; st < (l < double_layers ? 2 : 1); ++st) {
         fill(rng, w[6 * st + 0], s.hs, s.hs, scale);
         fill(rng, w[6 * st + 1], s.hs, s.hs, scale);
         fill(rng, w[6 * st + 2], s.hs, s.hs, scale);
-        fill(rng, w[6 * st + 3], s.hs, s.hs, scale);
+        fill(rng, w[6 * st + 3], s.hs, s.hs, rscale);
         fill(rng, w[6 * st + 4], s.hs, s.mlp, scale);
-        fill(rng, w[6 * st + 5], s.mlp, s.hs, scale);
+        fill(rng, w[6 * st + 5], s.mlp, s.hs, rscale);
       }
       pf::HostMatrix hm[12];
       for (int i = 0; i < 12; ++i) {

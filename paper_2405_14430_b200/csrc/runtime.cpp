@@ -106,6 +106,8 @@ void validate_shape(const ModelShape& s) {
     throw ValidationError("unknown block kind");
   if (s.block == kBlockJoint && s.T < 1)
     throw ValidationError("joint block needs at least one text token");
+  if (s.block == kBlockJoint && (s.double_layers < 0 || s.double_layers > s.layers))
+    throw ValidationError("double-stream layer count must lie in [0, layers]");
   if (s.block == kBlockPixArt) {
     if (s.hs % 32 != 0)
       throw ValidationError("PixArt block needs hidden_size divisible by 32");
@@ -260,7 +262,9 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
     if (m.block == kBlockJoint) s.text = dalloc<float>(size_t(m.T) * hs);
   }
   if (m.block == kBlockJoint) {
-    for (StageLayer& L : s.layers) {
+    for (int lf = 0; lf < count; ++lf) {
+      if (first + lf >= m.double_layers) continue;  // single-stream: shared weights
+      StageLayer& L = s.layers[size_t(lf)];
       L.t_wqkv = dalloc<bf16>(3 * hs * hs);
       L.t_wo = dalloc<bf16>(hs * hs);
       L.t_win = dalloc<bf16>(mlp * hs);
@@ -426,8 +430,9 @@ void Engine::load_layer_joint(int layer, const HostMatrix (&w)[12]) {
   Stage& s = stages_[size_t(d)];
   StageLayer& L = s.layers[size_t(layer - s.first_layer)];
   upload_toy_weights(s.device, shape_.hs, shape_.mlp, w, L.wqkv, L.wo, L.win, L.wout);
-  upload_toy_weights(s.device, shape_.hs, shape_.mlp, w + 6, L.t_wqkv, L.t_wo, L.t_win,
-                     L.t_wout);
+  if (layer < shape_.double_layers)
+    upload_toy_weights(s.device, shape_.hs, shape_.mlp, w + 6, L.t_wqkv, L.t_wo, L.t_win,
+                       L.t_wout);
 }
 
 void Engine::load_condition_bias(const double* cb) {
@@ -668,7 +673,10 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
   const int J = int(m.J());  // joint block: text rows [0, J) precede the image rows
   auto forward = [&](Stage& s, int lf, int rows, int row0, int t, int code) {
     if (px) layer_forward_px(s, lf, rows, row0, t, code);
-    else if (joint) layer_forward_joint(s, lf, rows, row0, code);
+    else if (joint && s.first_layer + lf < m.double_layers)
+      layer_forward_joint(s, lf, rows, row0, code);
+    else if (joint)
+      layer_forward_single(s, lf, rows, row0, code);
     else layer_forward(s, lf, rows, row0, code);
   };
   // joint block: the text stream re-enters from the text tokens every step
@@ -1050,6 +1058,60 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     prof_end(s);
     ++launches_;
   });
+}
+
+// Flux-style single-stream block with the toy arithmetic: one weight set
+// for all joint rows; attention and MLP both read the block input h:
+//   h += attention(h Wq, K, V) Wo + tanh(h Win) Wout
+void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code) {
+  const ModelShape& m = shape_;
+  StageLayer& L = s.layers[size_t(lf)];
+  const int Pt = int(m.rows_total()), hs = m.hs;
+  const double r = rows, dhs = hs, mlp = m.mlp;
+  EpiParams qkv;
+  qkv.q = s.q;
+  qkv.k = L.k;
+  qkv.v = L.v;
+  qkv.hs = hs;
+  qkv.dh = m.dh;
+  qkv.dhp = m.dhp;
+  qkv.P = Pt;
+  prof_begin(s, kGemmQKV, 2 * r * dhs * 3 * dhs, 0);
+  check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * hs, hs, Epi::QKV, sk(s, qkv), s.sm_count,
+             s.stream), "gemm qkv (single)");
+  prof_end(s);
+  EpiParams th;
+  th.out_bf16 = s.z;
+  th.ld = m.mlp;
+  prof_begin(s, kGemmMlpIn, 2 * r * dhs * mlp, 0);
+  check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, hs, Epi::Tanh, sk(s, th), s.sm_count,
+             s.stream), "gemm mlp-in (single)");
+  prof_end(s);
+  AttnLaunch a{m.dhp, Pt, rows, row0, m.heads, m.dh, hs,
+               float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
+               s.attn_work_floats};
+  prof_begin(s, kAttention, 4 * r * double(Pt) * dhs, 0);
+  check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (single)");
+  prof_end(s);
+  EpiParams res;
+  res.out_f32 = s.h32;
+  res.out_bf16 = s.hb;
+  res.ld = hs;
+  res.flag = s.flag;
+  res.code = code;
+  if (hs % 32 == 0) {
+    res.tm_h32 = &s.tm_h32;
+    res.tm_hb = &s.tm_hb;
+  }
+  prof_begin(s, kGemmOut, 2 * r * dhs * dhs, 0);
+  check(gemm(s.tm_attn, L.tm_wo, rows, row0, hs, hs, Epi::Residual, sk(s, res), s.sm_count,
+             s.stream), "gemm out-proj (single)");
+  prof_end(s);
+  prof_begin(s, kGemmMlpOut, 2 * r * dhs * mlp, 0);
+  check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, res), s.sm_count,
+             s.stream), "gemm mlp-out (single)");
+  prof_end(s);
+  launches_ += 5 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0);
 }
 
 // ============================================================== DistriFusion

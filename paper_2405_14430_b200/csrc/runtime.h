@@ -53,6 +53,10 @@ struct ModelShape {
   int dhp = 0;    // dh rounded up to a multiple of 16
   int block = 0;  // kBlockToy (toy_model.cpp:145-177), kBlockPixArt or kBlockJoint
   int T = 0;      // text tokens (PixArt: cross-attention K/V; joint: rows 0..T-1)
+  // joint block: layers [0, double_layers) are double-stream (text weights of
+  // their own), the rest single-stream parallel blocks (Flux-style: shared
+  // weights over all joint rows, attention and MLP both read the block input)
+  int double_layers = 0;
   // joint-row offset of image row 0 and rows of the activation / K/V buffers
   int64_t J() const { return block == 2 ? T : 0; }
   int64_t rows_total() const { return P + J(); }
@@ -293,6 +297,7 @@ class Engine {
                      const KvView* kv = nullptr);
   void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
   void layer_forward_joint(Stage& s, int lf, int rows, int row0, int code);
+  void layer_forward_single(Stage& s, int lf, int rows, int row0, int code);
   void px_conditioning(Stage& s, int steps);
   void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
   void send_rows(int from, int row0, int rows, int patch, int t);

@@ -54,3 +54,15 @@ def test_joint_stage_invariance_rerun_and_text():
         got = m.run_pipefusion(x0, 3, 2, 1, 0.1).final_x
     assert rel(got, ref) <= TOL
     assert rel(outs[0], ref) > 3 * rel(got, ref)  # the text reaches the image rows
+
+
+@pytest.mark.parametrize("D,N,M,W", [(2, 1, 2, 1), (1, 2, 2, 1), (0, 2, 4, 0)])
+def test_flux_style_single_stream_layers(D, N, M, W):
+    # Flux.1 layout: D double-stream layers, then single-stream parallel blocks
+    seed, L, hs, heads, p, T, S = 5, 4, 64, 4, 256, 16, 3
+    layers, cb, y = loader.joint_model(seed, L, hs, 4 * hs, T, double_layers=D)
+    x0 = make_initial_latent(6, p, hs)
+    ref = npo.joint_pipefusion(layers, cb, y, heads, x0, S, M, W, 0.1)
+    with JointDiTCuda(seed, L, hs, heads, 4.0, p, T, N, double_layers=D) as m:
+        res = m.run_pipefusion(x0, S, M, W, 0.1)
+    assert rel(res.final_x, ref) <= TOL, rel(res.final_x, ref)
