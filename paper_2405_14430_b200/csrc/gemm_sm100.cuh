@@ -742,7 +742,6 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t c_phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int mt = tile % m_tiles;
         const int nt = tile / m_tiles;
@@ -758,8 +757,17 @@ __global__ void __launch_bounds__(256, 1)
             phase ^= 1;
           }
         }
-        // residual tile (previous tile's stores must have drained the buffer)
-        ptx::mbar_wait(c_empty, c_phase ^ 1);
+      }
+    }
+  } else if (warp == 3) {
+    // residual tiles on their own warp: the operand producer never waits for
+    // the previous tile's epilogue stores
+    if (lane == 0) {
+      uint32_t c_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        ptx::mbar_wait(c_empty, c_phase ^ 1);  // previous tile's stores drained sC
         ptx::mbar_arrive_expect_tx(c_full, 4 * 16384);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -853,11 +861,13 @@ __global__ void __launch_bounds__(256, 1)
 
 
 // ---------------------------------------------------------------------------
-// CTA-pair residual GEMM with the TMA epilogue (256 x 128 pair tiles): the
-// 2-SM main loop of gemm2sm_bf16_tn_kernel and the smem residual epilogue of
-// gemm_resid_tma_kernel, each CTA handling its own 128 rows.
+// CTA-pair residual GEMM with the TMA epilogue, 256 x 128 pair tiles, whole-
+// tile epilogue buffer (measured faster than the part-streamed kernel below
+// at this width): the 2-SM main loop of gemm2sm_bf16_tn_kernel and the smem
+// residual epilogue of gemm_resid_tma_kernel, each CTA handling its own 128
+// rows.
 template <int STAGES>
-struct Gemm2SmResSmem {
+struct Gemm2SmRes128Smem {
   static constexpr int BN = 128;
   static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;
   static constexpr uint32_t kBBytes = (BN / 2) * kGemmBK * 2;
@@ -871,12 +881,12 @@ struct Gemm2SmResSmem {
 
 template <int STAGES, bool kMod>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    gemm2sm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
+    gemm2sm_resid128_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                              const __grid_constant__ CUtensorMap tma_b,
                              const __grid_constant__ CUtensorMap tma_h32,
                              const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
                              int N, int K, ResidTmaArgs args) {
-  using L = Gemm2SmResSmem<STAGES>;
+  using L = Gemm2SmRes128Smem<STAGES>;
   constexpr int BN = L::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -1037,6 +1047,225 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm<256>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair residual GEMM with the TMA epilogue (256 x BN pair tiles, BN 128 or
+// 192): the 2-SM main loop of gemm2sm_bf16_tn_kernel and the smem residual
+// epilogue of gemm_resid_tma_kernel, each CTA handling its own 128 rows.
+// Wider pair tiles cut the L2 -> SM traffic of the A operand (each A row tile
+// is re-read N / BN times). The epilogue streams the tile in 64-column parts
+// through two smem buffers (fp32 residual 2 x [128 x 32], bf16 copy
+// [128 x 64]): warp 3 TMA-loads part g + 1's residual while part g is added
+// and TMA-stored.
+template <int BN_, int STAGES>
+struct Gemm2SmResSmem {
+  static constexpr int BN = BN_;
+  static constexpr int kParts = BN / 64;
+  static constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr uint32_t kBBytes = (BN / 2) * kGemmBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kPartBytes = 2 * 16384 + 16384;  // fp32 2 x 16 KB + bf16 16 KB
+  static constexpr uint32_t kCOff = STAGES * kStageBytes;
+  static constexpr uint32_t kBarOffset = kCOff + 2 * kPartBytes;
+  static constexpr uint32_t kTotal = kBarOffset + 256 + 1024;
+  static constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static_assert(BN % 64 == 0 && BN <= 256, "residual pair tile");
+  static_assert(((BN / 2) * 128) % 1024 == 0 || BN == 192, "B half alignment");
+  static_assert(kTotal <= 232448, "2-SM residual GEMM smem budget");
+};
+
+template <int BN, int STAGES, bool kMod>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm2sm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
+                             const __grid_constant__ CUtensorMap tma_b,
+                             const __grid_constant__ CUtensorMap tma_h32,
+                             const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
+                             int N, int K, ResidTmaArgs args) {
+  using L = Gemm2SmResSmem<BN, STAGES>;
+  constexpr int kParts = L::kParts;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sE = smem + L::kCOff;  // 2 x part buffers: [fp32 32 KB | bf16 16 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* c_full = tempty + 2;   // [2]
+  uint64_t* c_empty = c_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int m_tiles = rows / (2 * kGemmBM);
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tma_a);
+    ptx::prefetch_tmap(&tma_b);
+    ptx::prefetch_tmap(&tma_h32);
+    ptx::prefetch_tmap(&tma_hb);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 2);
+      ptx::mbar_init(&c_full[a], 1);
+      ptx::mbar_init(&c_empty[a], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm<L::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
+  ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        const int my_row = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
+          ptx::tma_load_2d_2sm(sa, &tma_a, &full[stage], kb * kGemmBK, my_row);
+          ptx::tma_load_2d_2sm(sb, &tma_b, &full[stage], kb * kGemmBK,
+                               nt * BN + int(rank) * (BN / 2));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // residual parts, one ahead of the epilogue (double-buffered)
+    if (lane == 0) {
+      int g = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int mt = tile % m_tiles;
+        const int nt = tile / m_tiles;
+        const int my_row = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
+        for (int part = 0; part < kParts; ++part, ++g) {
+          const int b = g & 1;
+          uint8_t* sc = sE + b * L::kPartBytes;
+          ptx::mbar_wait(&c_empty[b], ((g >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&c_full[b], 2 * 16384);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            ptx::tma_load_2d(sc + c * 16384, &tma_h32, &c_full[b], nt * BN + 64 * part + 32 * c,
+                             my_row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t b_base = a_base + L::kABytes;
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k)
+            ptx::umma2_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
+                               ptx::desc_kmajor_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+          ptx::umma2_commit_mc(&empty[stage], 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma2_commit_mc(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = 32 * q + int(lane);
+    const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
+    const bool elect = warp == 4 && lane == 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int g = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      const int mt = tile % m_tiles;
+      const int nt = tile / m_tiles;
+      const int gr = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      bool bad = false;
+      for (int part = 0; part < kParts; ++part, ++g) {
+        const int b = g & 1;
+        uint8_t* sc = sE + b * L::kPartBytes;
+        uint8_t* sd = sc + 2 * 16384;
+        uint32_t v0[32], v1[32];
+        const uint32_t tcol = tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 64 * part;
+        ptx::tmem_ld32(tcol, v0);
+        ptx::tmem_ld32(tcol + 32, v1);
+        ptx::mbar_wait(&c_full[b], (g >> 1) & 1);
+        ptx::tmem_wait_ld();
+        if (part == kParts - 1) {
+          // every TMEM column of this accumulator is in registers
+          ptx::tc_fence_before();
+          ptx::named_bar_sync(1, 128);
+          if (elect) ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        }
+        bad |= resid_chunk<kMod>(sc, sd, r, 0, v0, nt * BN + 64 * part, gr + r, args);
+        bad |= resid_chunk<kMod>(sc, sd, r, 1, v1, nt * BN + 64 * part + 32, gr + r, args);
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, 128);
+        if (elect) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            ptx::tma_store_2d(&tma_h32, sc + c * 16384, nt * BN + 64 * part + 32 * c, gr);
+          ptx::tma_store_2d(&tma_hb, sd, nt * BN + 64 * part, gr);
+          ptx::tma_store_commit();
+          // release the buffer to the loader as soon as the stores have read
+          // it (the other epilogue threads meanwhile load the next part)
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          ptx::mbar_arrive(&c_empty[b]);
+        }
+      }
+      if (bad && args.flag) atomicMin(args.flag, args.code);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (elect) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm<L::kTmemCols>(tmem_base);
   }
 }
 

@@ -528,8 +528,12 @@ bool make_weight_maps(WeightMaps* maps, const bf16* w, int N, int K) {
                              uint32_t(gemm_bn_1sm(N)), 128) &&
          encode_tmap_bf16_2d(&maps->two_sm, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
                              uint32_t(gemm_bn_2sm(N) / 2), 128) &&
-         encode_tmap_bf16_2d(&maps->two_sm_128, w, uint64_t(K), uint64_t(N), uint64_t(K) * 2, 64,
-                             64, 128);
+         encode_tmap_bf16_2d(&maps->two_sm_res[0], w, uint64_t(K), uint64_t(N), uint64_t(K) * 2,
+                             64, 64, 128) &&
+         encode_tmap_bf16_2d(&maps->two_sm_res[1], w, uint64_t(K), uint64_t(N), uint64_t(K) * 2,
+                             64, 96, 128) &&
+         encode_tmap_bf16_2d(&maps->two_sm_res[2], w, uint64_t(K), uint64_t(N), uint64_t(K) * 2,
+                             64, 128, 128);
 }
 
 int gemm_splits(int rows, int N, int K, const EpiParams& ep, int sm_count) {
@@ -568,17 +572,51 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
       N % 32 == 0 && sm_count >= 2 && (K >= 2048 || tune_flag("PF_RESID_2SM"))) {
     // long-K residual GEMM (MLP-out): CTA pairs halve the per-SM smem
     // operand traffic of the main loop
-    constexpr int kStages = 5;
-    using L = Gemm2SmResSmem<kStages>;
-    const int tiles = (rows / (2 * kGemmBM)) * ((N + L::BN - 1) / L::BN);
-    const int pairs = sm_count / 2;
-    const int grid = 2 * (tiles < pairs ? tiles : pairs);
     const ResidTmaArgs args{ep.out_f32, ep.flag, ep.code, ep.bias, ep.gate, ep.colscale,
                             ep.stats_out, ep.stats_ld};
-    return ep.mod() ? launch_resid2<gemm2sm_resid_tma_kernel<kStages, true>>(
-                          grid, L::kTotal, stream, a, b.two_sm_128, ep, rows, row0, N, K, args)
-                    : launch_resid2<gemm2sm_resid_tma_kernel<kStages, false>>(
-                          grid, L::kTotal, stream, a, b.two_sm_128, ep, rows, row0, N, K, args);
+    const int pairs = sm_count / 2;
+    auto run = [&](auto bn, auto stages, const CUtensorMap& bmap) {
+      constexpr int BN = decltype(bn)::value, ST = decltype(stages)::value;
+      using L = Gemm2SmResSmem<BN, ST>;
+      const int tiles = (rows / (2 * kGemmBM)) * ((N + BN - 1) / BN);
+      const int grid = 2 * (tiles < pairs ? tiles : pairs);
+      return ep.mod() ? launch_resid2<gemm2sm_resid_tma_kernel<BN, ST, true>>(
+                            grid, L::kTotal, stream, a, bmap, ep, rows, row0, N, K, args)
+                      : launch_resid2<gemm2sm_resid_tma_kernel<BN, ST, false>>(
+                            grid, L::kTotal, stream, a, bmap, ep, rows, row0, N, K, args);
+    };
+    // The main loop is bound by L2 -> SM operand traffic (16 KB of A + BN/16 KB
+    // of B per SM and 64-deep K block), so a tile costs ~(16 + BN/16); pick
+    // the BN with the fewest (whole waves of pair tiles) x (tile cost).
+    int best = 0;
+    double best_cost = 1e30;
+    const int bns[3] = {128, 192, 256};
+    for (int i = 0; i < 3; ++i) {
+      const int tiles = (rows / (2 * kGemmBM)) * ((N + bns[i] - 1) / bns[i]);
+      const double cost = double((tiles + pairs - 1) / pairs) * (16.0 + bns[i] / 16.0);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best = i;
+      }
+    }
+    if (best == 2)
+      return run(std::integral_constant<int, 256>{}, std::integral_constant<int, 4>{},
+                 b.two_sm_res[2]);
+    if (best == 1)
+      return run(std::integral_constant<int, 192>{}, std::integral_constant<int, 4>{},
+                 b.two_sm_res[1]);
+    {
+      constexpr int kStages = 5;
+      using L = Gemm2SmRes128Smem<kStages>;
+      const int tiles = (rows / (2 * kGemmBM)) * ((N + L::BN - 1) / L::BN);
+      const int grid = 2 * (tiles < pairs ? tiles : pairs);
+      return ep.mod() ? launch_resid2<gemm2sm_resid128_tma_kernel<kStages, true>>(
+                            grid, L::kTotal, stream, a, b.two_sm_res[0], ep, rows, row0, N, K,
+                            args)
+                      : launch_resid2<gemm2sm_resid128_tma_kernel<kStages, false>>(
+                            grid, L::kTotal, stream, a, b.two_sm_res[0], ep, rows, row0, N, K,
+                            args);
+    }
   }
   if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % kGemmBM == 0 && N % 32 == 0 &&
       gemm_bn_1sm(N) == 128) {

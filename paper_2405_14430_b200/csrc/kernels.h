@@ -102,7 +102,7 @@ struct EpiParams {
 struct WeightMaps {
   CUtensorMap one_sm;
   CUtensorMap two_sm;
-  CUtensorMap two_sm_128;  // box 64 x 64: CTA-pair tiles of N = 128 (residual GEMMs)
+  CUtensorMap two_sm_res[3];  // box 64 x {64, 96, 128}: CTA-pair residual tiles BN 128/192/256
 };
 int gemm_bn_1sm(int N);
 int gemm_bn_2sm(int N);
