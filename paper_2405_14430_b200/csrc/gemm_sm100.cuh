@@ -597,6 +597,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 // TMA-stores both tiles. Global traffic is bulk and coalesced instead of
 // one row per thread. Requires rows % 128 == 0 (whole row tiles: stores must
 // not touch rows of other patches) and N % 32 == 0.
+// The residual tile is loaded through tma_h32 and stored through
+// tma_h32_out / tma_hb_out: the same buffers normally, another GPU's landing
+// buffers when the last layer of a pipeline stage writes its output straight
+// to the next stage (rank mode).
 struct ResidTmaArgs {
   float* h;        // for the finite check only
   int* flag;
@@ -689,7 +693,9 @@ __global__ void __launch_bounds__(256, 1)
     gemm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b,
                           const __grid_constant__ CUtensorMap tma_h32,
-                          const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
+                          const __grid_constant__ CUtensorMap tma_hb,
+                          const __grid_constant__ CUtensorMap tma_h32_out,
+                          const __grid_constant__ CUtensorMap tma_hb_out, int rows, int row0,
                           int N, int K, ResidTmaArgs args) {
   using L = GemmResSmem<STAGES>;
   constexpr int BN = L::BN;
@@ -718,6 +724,8 @@ __global__ void __launch_bounds__(256, 1)
     ptx::prefetch_tmap(&tma_b);
     ptx::prefetch_tmap(&tma_h32);
     ptx::prefetch_tmap(&tma_hb);
+    ptx::prefetch_tmap(&tma_h32_out);
+    ptx::prefetch_tmap(&tma_hb_out);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -836,9 +844,9 @@ __global__ void __launch_bounds__(256, 1)
       if (warp == 4 && lane == 0) {
         const int gr = row0 + mt * kGemmBM;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tma_store_2d(&tma_h32, sC + c * 16384, nt * BN + 32 * c, gr);
+        for (int c = 0; c < 4; ++c) ptx::tma_store_2d(&tma_h32_out, sC + c * 16384, nt * BN + 32 * c, gr);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) ptx::tma_store_2d(&tma_hb, sD + c * 16384, nt * BN + 64 * c, gr);
+        for (int c = 0; c < 2; ++c) ptx::tma_store_2d(&tma_hb_out, sD + c * 16384, nt * BN + 64 * c, gr);
         ptx::tma_store_commit();
         ptx::tma_store_wait_read();
         ptx::mbar_arrive(c_empty);
@@ -884,7 +892,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm2sm_resid128_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                              const __grid_constant__ CUtensorMap tma_b,
                              const __grid_constant__ CUtensorMap tma_h32,
-                             const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
+                             const __grid_constant__ CUtensorMap tma_hb,
+                             const __grid_constant__ CUtensorMap tma_h32_out,
+                             const __grid_constant__ CUtensorMap tma_hb_out, int rows, int row0,
                              int N, int K, ResidTmaArgs args) {
   using L = Gemm2SmRes128Smem<STAGES>;
   constexpr int BN = L::BN;
@@ -917,6 +927,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ptx::prefetch_tmap(&tma_b);
     ptx::prefetch_tmap(&tma_h32);
     ptx::prefetch_tmap(&tma_hb);
+    ptx::prefetch_tmap(&tma_h32_out);
+    ptx::prefetch_tmap(&tma_hb_out);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -1028,9 +1040,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
         const int gr = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tma_store_2d(&tma_h32, sC + c * 16384, nt * BN + 32 * c, gr);
+        for (int c = 0; c < 4; ++c) ptx::tma_store_2d(&tma_h32_out, sC + c * 16384, nt * BN + 32 * c, gr);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) ptx::tma_store_2d(&tma_hb, sD + c * 16384, nt * BN + 64 * c, gr);
+        for (int c = 0; c < 2; ++c) ptx::tma_store_2d(&tma_hb_out, sD + c * 16384, nt * BN + 64 * c, gr);
         ptx::tma_store_commit();
         ptx::tma_store_wait_read();
         ptx::mbar_arrive(c_empty);
@@ -1081,7 +1093,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm2sm_resid_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                              const __grid_constant__ CUtensorMap tma_b,
                              const __grid_constant__ CUtensorMap tma_h32,
-                             const __grid_constant__ CUtensorMap tma_hb, int rows, int row0,
+                             const __grid_constant__ CUtensorMap tma_hb,
+                             const __grid_constant__ CUtensorMap tma_h32_out,
+                             const __grid_constant__ CUtensorMap tma_hb_out, int rows, int row0,
                              int N, int K, ResidTmaArgs args) {
   using L = Gemm2SmResSmem<BN, STAGES>;
   constexpr int kParts = L::kParts;
@@ -1113,6 +1127,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ptx::prefetch_tmap(&tma_b);
     ptx::prefetch_tmap(&tma_h32);
     ptx::prefetch_tmap(&tma_hb);
+    ptx::prefetch_tmap(&tma_h32_out);
+    ptx::prefetch_tmap(&tma_hb_out);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -1245,8 +1261,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         if (elect) {
 #pragma unroll
           for (int c = 0; c < 2; ++c)
-            ptx::tma_store_2d(&tma_h32, sc + c * 16384, nt * BN + 64 * part + 32 * c, gr);
-          ptx::tma_store_2d(&tma_hb, sd, nt * BN + 64 * part, gr);
+            ptx::tma_store_2d(&tma_h32_out, sc + c * 16384, nt * BN + 64 * part + 32 * c, gr);
+          ptx::tma_store_2d(&tma_hb_out, sd, nt * BN + 64 * part, gr);
           ptx::tma_store_commit();
           // release the buffer to the loader as soon as the stores have read
           // it (the other epilogue threads meanwhile load the next part)

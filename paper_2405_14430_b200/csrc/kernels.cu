@@ -145,6 +145,8 @@ struct EpiResidual {
   int ld;
   int* flag;
   int code;
+  float* h_out;  // where the updated rows go (normally h / hb)
+  bf16* hb_out;
   __device__ void preload(int row, int col0, float (&pre)[32], int nvalid) const {
     const float* hr = h + size_t(row) * ld + col0;
     if (nvalid == 32) {
@@ -160,8 +162,8 @@ struct EpiResidual {
   }
   __device__ void apply(int row, int col0, const float (&v)[32], const float (&pre)[32],
                         int nvalid) const {
-    float* hr = h + size_t(row) * ld + col0;
-    bf16* br = hb + size_t(row) * ld + col0;
+    float* hr = h_out + size_t(row) * ld + col0;
+    bf16* br = hb_out + size_t(row) * ld + col0;
     bool bad = false;
     if (nvalid == 32) {
 #pragma unroll
@@ -410,6 +412,8 @@ struct EpiResidualMod {
   const float* colscale;
   float2* stats;
   int stats_ld;
+  float* h_out;
+  bf16* hb_out;
   __device__ void preload(int row, int col0, float (&pre)[32], int nvalid) const {
     const float* hr = h + size_t(row) * ld + col0;
 #pragma unroll
@@ -417,8 +421,8 @@ struct EpiResidualMod {
   }
   __device__ void apply(int row, int col0, const float (&v)[32], const float (&pre)[32],
                         int nvalid) const {
-    float* hr = h + size_t(row) * ld + col0;
-    bf16* br = hb + size_t(row) * ld + col0;
+    float* hr = h_out + size_t(row) * ld + col0;
+    bf16* br = hb_out + size_t(row) * ld + col0;
     bool bad = false;
     float s = 0.f, ss = 0.f;
 #pragma unroll
@@ -485,8 +489,12 @@ cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
     case Epi::Residual:
       if (ep.mod())
         return go(EpiResidualMod{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code, ep.bias,
-                                 ep.gate, ep.colscale, ep.stats_out, ep.stats_ld});
-      return go(EpiResidual{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code});
+                                 ep.gate, ep.colscale, ep.stats_out, ep.stats_ld,
+                                 ep.out_f32_dst ? ep.out_f32_dst : ep.out_f32,
+                                 ep.out_bf16_dst ? ep.out_bf16_dst : ep.out_bf16});
+      return go(EpiResidual{ep.out_f32, ep.out_bf16, ep.ld, ep.flag, ep.code,
+                            ep.out_f32_dst ? ep.out_f32_dst : ep.out_f32,
+                            ep.out_bf16_dst ? ep.out_bf16_dst : ep.out_bf16});
     case Epi::Tanh:
       return go(EpiTanh{ep.out_bf16, ep.ld});
     case Epi::QKV:
@@ -509,8 +517,9 @@ cudaError_t launch_resid2(int grid, uint32_t smem, cudaStream_t stream, const CU
                           int K, const ResidTmaArgs& args) {
   cudaError_t e = ensure_smem_attr<kern>(smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3(grid), dim3(256), smem, stream, a, b, *ep.tm_h32, *ep.tm_hb, rows,
-                    row0, N, K, args);
+  return launch_pdl(kern, dim3(grid), dim3(256), smem, stream, a, b, *ep.tm_h32, *ep.tm_hb,
+                    ep.tm_h32_dst ? *ep.tm_h32_dst : *ep.tm_h32,
+                    ep.tm_hb_dst ? *ep.tm_hb_dst : *ep.tm_hb, rows, row0, N, K, args);
 }
 
 }  // namespace

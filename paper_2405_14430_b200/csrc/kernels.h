@@ -69,6 +69,13 @@ struct EpiParams {
   // out_bf16 (bf16, box 64 x 128, SW128) enable the TMA epilogue.
   const CUtensorMap* tm_h32 = nullptr;
   const CUtensorMap* tm_hb = nullptr;
+  // Residual: write the updated rows (fp32 and bf16 copy) to these buffers /
+  // maps instead of out_f32 / out_bf16 (which are still read): a stage's last
+  // layer storing its output directly into the next stage's landing buffers.
+  float* out_f32_dst = nullptr;
+  bf16* out_bf16_dst = nullptr;
+  const CUtensorMap* tm_h32_dst = nullptr;
+  const CUtensorMap* tm_hb_dst = nullptr;
   // ---- PixArt block extensions (all optional) ----
   // Residual: h += gate[n] * (acc + bias[n]); out_bf16 = bf16(h * (1 + colscale[n]));
   //           stats_out[(n/32) * stats_ld + row] = (sum, sum of squares) of h

@@ -497,8 +497,15 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, m.hs, Epi::Tanh, sk(s, th),
              s.sm_count, s.stream), "gemm mlp-in");
   prof_end(s);
+  EpiParams res_out = res;
+  if (redirect_) {  // last layer of a rank: store straight into the next stage
+    res_out.out_f32_dst = redirect_->h32;
+    res_out.out_bf16_dst = redirect_->hb;
+    res_out.tm_h32_dst = redirect_->tm_h32;
+    res_out.tm_hb_dst = redirect_->tm_hb;
+  }
   prof_begin(s, kGemmMlpOut, 2 * r * hs * mlp, 0);
-  check(gemm(s.tm_z, L.tm_wout, rows, row0, m.hs, m.mlp, Epi::Residual, sk(s, res),
+  check(gemm(s.tm_z, L.tm_wout, rows, row0, m.hs, m.mlp, Epi::Residual, sk(s, res_out),
              s.sm_count, s.stream), "gemm mlp-out");
   prof_end(s);
   const int splits = attn_splits(a, s.sm_count);
@@ -1423,6 +1430,25 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
     if (shape_.block == kBlockPixArt)
       succ_stats_ = static_cast<float2*>(open(succ, succ.h_stats, succ.p_stats));
   }
+  // tensor maps over the successor's buffers for the fused send (the last
+  // MLP-out GEMM's TMA stores): rank 0's eps (fp32) from the last rank, the
+  // next stage's residual stream and bf16 operand otherwise
+  const size_t P = size_t(shape_.P), hs = size_t(shape_.hs);
+  float* dst32 = succ_eps_ ? succ_eps_ : succ_h32_;
+  if (!encode_tmap_f32_2d(&tm_peer_h32_, dst32, hs, P, hs * 4, 32, 128, 128))
+    throw CudaError("cuTensorMapEncodeTiled failed for a peer buffer");
+  peer_out_ = OutRedirect{};
+  peer_out_.h32 = dst32;
+  peer_out_.tm_h32 = &tm_peer_h32_;
+  if (succ_hb_) {
+    tm_peer_hb_ = tmap(succ_hb_, hs, P, hs * 2, 64, 128, 128);
+    peer_out_.hb = succ_hb_;
+    peer_out_.tm_hb = &tm_peer_hb_;
+  } else {  // eps only: the bf16 copy stays local (unused)
+    peer_out_.hb = s.hb;
+    peer_out_.tm_hb = &s.tm_hb;
+  }
+  peer_out_.stats = succ_stats_;
   connected_ = true;
 }
 
@@ -1484,15 +1510,25 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
 
   const uint32_t base_in = msgs_in_base_, base_out = msgs_out_base_;
   const auto plan = build_rank_plan(rank_, world_, steps, patches, warmup, m.P);
-  for (const PlanOp& op : plan) {
+  // Fused send (default): the stage's last MLP-out GEMM stores the message
+  // rows straight into the successor's buffers; the flow-control wait and the
+  // signal are stream-ordered around it on the compute stream. PF_RANK_COPY=1
+  // keeps the separate copy on the send stream.
+  static const bool copy_send = [] {
+    const char* e = std::getenv("PF_RANK_COPY");
+    return e && e[0] == '1';
+  }();
+  const bool fused = !copy_send;
+  for (size_t oi = 0; oi < plan.size(); ++oi) {
+    const PlanOp& op = plan[oi];
     const int row0 = op.row0, rows = op.rows;
     switch (op.kind) {
       case PlanOp::kRecv:
         stream_wait_geq(s.stream, sig_, base_in + uint32_t(op.msg), dev);
         break;
       case PlanOp::kAck:
-        stream_write(op.flag ? send_stream_ : s.stream, pred_sig_ + 1, base_in + uint32_t(op.msg),
-                     dev);
+        stream_write(op.flag && !fused ? send_stream_ : s.stream, pred_sig_ + 1,
+                     base_in + uint32_t(op.msg), dev);
         break;
       case PlanOp::kPrepare: {
         // this rank's previous send of the same rows must have finished reading h32
@@ -1541,8 +1577,25 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           }
           codes_.emplace_back(t, s.first_layer + lf);
           const int code = int(codes_.size()) - 1;
+          const bool last = lf == s.layer_count - 1;
+          const PlanOp* send = fused && last && oi + 1 < plan.size() &&
+                                       plan[oi + 1].kind == PlanOp::kSend
+                                   ? &plan[oi + 1]
+                                   : nullptr;
+          if (send && send->overlap > 0)  // landing rows free at the successor
+            stream_wait_geq(s.stream, sig_ + 1, base_out + uint32_t(send->overlap), dev);
+          redirect_ = send ? &peer_out_ : nullptr;
           if (px) layer_forward_px(s, lf, rows, row0, t, code);
           else layer_forward(s, lf, rows, row0, code);
+          redirect_ = nullptr;
+          if (send) {
+            stream_write(s.stream, succ_sig_, base_out + uint32_t(send->msg), dev);
+            for (int j = 0; j < patches; ++j)
+              if (send->patch < 0 || send->patch == j) {
+                PF_CUDA_CHECK(cudaEventRecord(ev_sent_[size_t(j)], s.stream));
+                sent_before[size_t(j)] = true;
+              }
+          }
         }
         tl_end(s.stream);
         if (op.patch >= 0) {
@@ -1553,6 +1606,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         break;
       }
       case PlanOp::kSend: {
+        if (fused) break;  // stored by the last MLP-out GEMM, signalled after it
         PF_CUDA_CHECK(cudaEventRecord(ev_compute_, s.stream));
         PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_compute_, 0));
         if (op.overlap > 0)
@@ -1887,6 +1941,13 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   r3.gate = gate2;
   r3.colscale = next_scale1;
   r3.stats_out = px.stats;
+  if (redirect_) {  // last layer of a rank: store straight into the next stage
+    r3.out_f32_dst = redirect_->h32;
+    r3.out_bf16_dst = redirect_->hb;
+    r3.tm_h32_dst = redirect_->tm_h32;
+    r3.tm_hb_dst = redirect_->tm_hb;
+    if (redirect_->stats) r3.stats_out = redirect_->stats;
+  }
   prof_begin(s, kGemmMlpOut, 2 * r * dhs * mlp, 0);
   check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, r3), s.sm_count, s.stream),
         "gemm mlp-out");

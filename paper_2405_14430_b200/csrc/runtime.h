@@ -315,6 +315,19 @@ class Engine {
   uint32_t* pred_sig_ = nullptr;   // predecessor's signal page
   std::vector<void*> ipc_opened_;
   bool connected_ = false;
+  // Fused stage-boundary send: the stage's last MLP-out GEMM stores its rows
+  // straight into the successor's landing buffers (peer memory) instead of a
+  // copy after it. Set around that one layer_forward* call.
+  struct OutRedirect {
+    float* h32 = nullptr;
+    bf16* hb = nullptr;
+    float2* stats = nullptr;
+    const CUtensorMap* tm_h32 = nullptr;
+    const CUtensorMap* tm_hb = nullptr;
+  };
+  const OutRedirect* redirect_ = nullptr;
+  OutRedirect peer_out_;
+  CUtensorMap tm_peer_h32_, tm_peer_hb_;
   uint32_t msgs_in_base_ = 0, msgs_out_base_ = 0;
   cudaEvent_t ev_compute_ = nullptr;
   std::vector<cudaEvent_t> ev_sent_;  // per patch: last send of its rows finished
