@@ -136,6 +136,9 @@ pf_status pf_create_toy_rank(uint64_t seed, const pf_model_desc* desc, int rank,
                              int device, pf_ctx** out);
 pf_status pf_create_pixart_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
                                 int rank, int world, int device, pf_ctx** out);
+pf_status pf_create_joint_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                               int double_layers, int rank, int world, int device,
+                               pf_ctx** out);
 size_t pf_peer_blob_size(void);
 pf_status pf_export_peer(pf_ctx* ctx, void* blob, size_t capacity);
 pf_status pf_connect_peers(pf_ctx* ctx, const void* pred_blob, const void* succ_blob);

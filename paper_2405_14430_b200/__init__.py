@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = [
     "pf_create_pixart_rank", "pf_peer_blob_size", "pf_export_peer", "pf_connect_peers",
     "pf_rank", "pf_world", "pf_rank_plan", "pf_set_timeline", "pf_timeline",
     "pf_run_distrifusion", "pf_run_distrifusion_device", "pf_create_joint",
+    "pf_create_joint_rank",
     "pf_run_pipefusion", "pf_run_pipefusion_device", "pf_synchronize",
     "pf_serial_reference", "pf_layer_forward", "pf_stage_count",
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
@@ -101,6 +102,8 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_set_text.argtypes = [vp, dptr, i64, i32]
     lib.pf_create_joint.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32,
                                     ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_create_joint_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
+                                         i32, i32, ctypes.POINTER(vp)]
     lib.pf_block_kind.argtypes = [vp]
     lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
     lib.pf_create_toy_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
@@ -223,7 +226,11 @@ class ToyDiTCuda:
             # rank mode: this context holds stage `rank` of `workers` on `device`
             rank, device = _rank
             self.rank, self.world = rank, workers
-            if _text_tokens:
+            if _joint is not None:
+                st = self._lib.pf_create_joint_rank(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                                    _text_tokens, _joint, rank, workers, device,
+                                                    ctypes.byref(self._ctx))
+            elif _text_tokens:
                 st = self._lib.pf_create_pixart_rank(ctypes.c_uint64(seed), ctypes.byref(desc),
                                                      _text_tokens, rank, workers, device,
                                                      ctypes.byref(self._ctx))
@@ -551,6 +558,18 @@ class JointDiTCuda(ToyDiTCuda):
         self.double_layers = layers if double_layers is None else double_layers
         super().__init__(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers,
                          devices, _text_tokens=text_tokens, _joint=self.double_layers)
+
+    @classmethod
+    def rank_stage(cls, seed: int, layers: int, hidden_size: int, heads: int, mlp_ratio: float,
+                   seq_len: int, text_tokens: int, rank: int, world: int, device: int = 0,
+                   double_layers: Optional[int] = None) -> "JointDiTCuda":
+        obj = cls.__new__(cls)
+        obj.text_tokens = text_tokens
+        obj.double_layers = layers if double_layers is None else double_layers
+        ToyDiTCuda.__init__(obj, seed, layers, hidden_size, heads, mlp_ratio, seq_len, world,
+                            None, _text_tokens=text_tokens, _rank=(rank, device),
+                            _joint=obj.double_layers)
+        return obj
 
     def set_text(self, y) -> None:
         y = _f64c(y)

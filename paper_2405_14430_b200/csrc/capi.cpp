@@ -136,6 +136,8 @@ void export_stats(const pf::RunStats& rs, pf_stats* out) {
 void load_toy(pf::Engine& eng, uint64_t seed);
 // pxo_build (oracle/px_oracle.c) streamed likewise.
 void load_pixart(pf::Engine& eng, uint64_t seed, int text_tokens);
+// pf_create_joint's parameter stream (include/pipefusion_b200.h).
+void load_joint(pf::Engine& eng, uint64_t seed, int text_tokens, int double_layers);
 
 }  // namespace
 
@@ -347,6 +349,34 @@ pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tok
     s.T = text_tokens;
     s.double_layers = double_layers;
     ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    load_joint(*ctx->engine, seed, text_tokens, double_layers);
+    *out = ctx.release();
+  });
+}
+
+pf_status pf_create_joint_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                               int double_layers, int rank, int world, int device,
+                               pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.block = pf::kBlockJoint;
+    s.T = text_tokens;
+    s.double_layers = double_layers;
+    ctx->engine = std::make_unique<pf::Engine>(s, device, rank, world);
+    load_joint(*ctx->engine, seed, text_tokens, double_layers);
+    *out = ctx.release();
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void load_joint(pf::Engine& eng, uint64_t seed, int text_tokens, int double_layers) {
+    const pf::ModelShape& s = eng.shape();
     // One mt19937_64 stream seeded with seed ^ "JOINT-DI": per layer the
     // image stream's six toy matrices then (double-stream layers only) the
     // text stream's, in build_toy_model's order and scale
@@ -373,18 +403,20 @@ pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tok
         const int k = i % 6;
         hm[i] = {w[i].data(), k == 5 ? s.mlp : s.hs, k == 4 ? s.mlp : s.hs, false};
       }
-      ctx->engine->load_layer_joint(l, hm);
+      eng.load_layer_joint(l, hm);
     }
     std::vector<double> cb;
     fill(rng, cb, 1, s.hs, 1.0);
-    ctx->engine->load_condition_bias(cb.data());
+    eng.load_condition_bias(cb.data());
     std::mt19937_64 trng(seed ^ 0x5458542d544f4b53ULL);
     std::vector<double> y;
     fill(trng, y, text_tokens, s.hs, 1.0);
-    ctx->engine->set_text(y.data());
-    *out = ctx.release();
-  });
+    eng.set_text(y.data());
 }
+
+}  // namespace
+
+extern "C" {
 
 int pf_block_kind(const pf_ctx* ctx) { return ctx ? ctx->engine->shape().block : -1; }
 

@@ -1058,10 +1058,17 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     prof_end(s);
     ++launches_;
   });
+  EpiParams res_out = res;
+  if (redirect_) {  // last layer of a rank: store straight into the next stage
+    res_out.out_f32_dst = redirect_->h32;
+    res_out.out_bf16_dst = redirect_->hb;
+    res_out.tm_h32_dst = redirect_->tm_h32;
+    res_out.tm_hb_dst = redirect_->tm_hb;
+  }
   both([&](bool txt, int r0, int n) {
     prof_begin(s, kGemmMlpOut, 2.0 * n * dhs * mlp, 0);
     check(gemm(s.tm_z, txt ? L.tm_t_wout : L.tm_wout, n, r0, hs, m.mlp, Epi::Residual,
-               sk(s, res), s.sm_count, s.stream), "gemm mlp-out (joint)");
+               sk(s, res_out), s.sm_count, s.stream), "gemm mlp-out (joint)");
     prof_end(s);
     ++launches_;
   });
@@ -1114,9 +1121,16 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
   check(gemm(s.tm_attn, L.tm_wo, rows, row0, hs, hs, Epi::Residual, sk(s, res), s.sm_count,
              s.stream), "gemm out-proj (single)");
   prof_end(s);
+  EpiParams res_out = res;
+  if (redirect_) {
+    res_out.out_f32_dst = redirect_->h32;
+    res_out.out_bf16_dst = redirect_->hb;
+    res_out.tm_h32_dst = redirect_->tm_h32;
+    res_out.tm_hb_dst = redirect_->tm_hb;
+  }
   prof_begin(s, kGemmMlpOut, 2 * r * dhs * mlp, 0);
-  check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, res), s.sm_count,
-             s.stream), "gemm mlp-out (single)");
+  check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, res_out),
+             s.sm_count, s.stream), "gemm mlp-out (single)");
   prof_end(s);
   launches_ += 5 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0);
 }
@@ -1332,8 +1346,6 @@ Engine::Engine(const ModelShape& shape_in, int device, int rank, int world)
        << " (fewer layers than stages)";
     throw ValidationError(os.str());
   }
-  if (shape_.block == kBlockJoint)
-    throw ValidationError("rank mode supports the toy and PixArt blocks");
   int dev_count = 0;
   PF_CUDA_CHECK(cudaGetDeviceCount(&dev_count));
   if (device < 0 || device >= dev_count) {
@@ -1433,7 +1445,9 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
   // tensor maps over the successor's buffers for the fused send (the last
   // MLP-out GEMM's TMA stores): rank 0's eps (fp32) from the last rank, the
   // next stage's residual stream and bf16 operand otherwise
-  const size_t P = size_t(shape_.P), hs = size_t(shape_.hs);
+  const size_t hs = size_t(shape_.hs);
+  // the eps buffer holds image rows; activations hold joint rows (text first)
+  const size_t P = succ_eps_ ? size_t(shape_.P) : size_t(shape_.rows_total());
   float* dst32 = succ_eps_ ? succ_eps_ : succ_h32_;
   if (!encode_tmap_f32_2d(&tm_peer_h32_, dst32, hs, P, hs * 4, 32, 128, 128))
     throw CudaError("cuTensorMapEncodeTiled failed for a peer buffer");
@@ -1500,7 +1514,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   check(reset_flag(s.flag, s.stream), "reset_flag");
   ++launches_;
   if (warmup == 0) {
-    const size_t kv = size_t(m.heads) * size_t(m.P) * size_t(m.dhp) * sizeof(bf16);
+    const size_t kv = size_t(m.heads) * size_t(m.rows_total()) * size_t(m.dhp) * sizeof(bf16);
     for (StageLayer& L : s.layers) {
       PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
       PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kv, s.stream));
@@ -1518,10 +1532,18 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
     const char* e = std::getenv("PF_RANK_COPY");
     return e && e[0] == '1';
   }();
-  const bool fused = !copy_send;
+  const bool joint = m.block == kBlockJoint;
+  const int J = int(m.J());
+  // joint block: the eps rows of the last rank are image rows (offset by the
+  // text rows), which the GEMM's joint-row stores cannot address: copy them
+  const bool fused = !copy_send && !(joint && succ_eps_);
   for (size_t oi = 0; oi < plan.size(); ++oi) {
     const PlanOp& op = plan[oi];
+    // plan rows are image rows; joint blocks carry the text rows with the
+    // full sequence and with patch 0
     const int row0 = op.row0, rows = op.rows;
+    const int brow0 = joint && op.patch > 0 ? J + row0 : row0;
+    const int brows = joint && op.patch <= 0 ? J + rows : rows;
     switch (op.kind) {
       case PlanOp::kRecv:
         stream_wait_geq(s.stream, sig_, base_in + uint32_t(op.msg), dev);
@@ -1537,11 +1559,16 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
             PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_sent_[size_t(j)], 0));
         tl_begin(rank_, 0, op.patch, op.t, s.stream);
         prof_begin(s, kSampler, 0, double(rows) * hs * (op.flag ? 18 : 10));
+        if (joint && op.patch <= 0) {  // the text stream re-enters each step
+          check(patch_prepare(s.text, nullptr, s.zeros, s.h32, s.hb, 0, J, m.hs, 0.f, false,
+                              s.stream), "text rows");
+          ++launches_;
+        }
         if (px)
           px_patch_prepare(x_dev, op.flag != 0, row0, rows, op.t, eta);
         else
-          check(patch_prepare(x_dev, s.eps, s.cb, s.h32, s.hb, row0, rows, m.hs, eta,
-                              op.flag != 0, s.stream), "patch_prepare");
+          check(patch_prepare(x_dev, s.eps, s.cb, s.h32 + size_t(J) * hs, s.hb + size_t(J) * hs,
+                              row0, rows, m.hs, eta, op.flag != 0, s.stream), "patch_prepare");
         prof_end(s);
         ++launches_;
         break;
@@ -1586,6 +1613,10 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
             stream_wait_geq(s.stream, sig_ + 1, base_out + uint32_t(send->overlap), dev);
           redirect_ = send ? &peer_out_ : nullptr;
           if (px) layer_forward_px(s, lf, rows, row0, t, code);
+          else if (joint && s.first_layer + lf < m.double_layers)
+            layer_forward_joint(s, lf, brows, brow0, code);
+          else if (joint)
+            layer_forward_single(s, lf, brows, brow0, code);
           else layer_forward(s, lf, rows, row0, code);
           redirect_ = nullptr;
           if (send) {
@@ -1612,9 +1643,10 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         if (op.overlap > 0)
           stream_wait_geq(send_stream_, sig_ + 1, base_out + uint32_t(op.overlap), dev);
         tl_begin(rank_, 1, op.patch, op.t, send_stream_);
-        const size_t off = size_t(row0) * hs, cnt = size_t(rows) * hs;
-        if (succ_eps_) {
-          PF_CUDA_CHECK(cudaMemcpyAsync(succ_eps_ + off, s.h32 + off, cnt * 4,
+        const size_t off = size_t(brow0) * hs, cnt = size_t(brows) * hs;
+        if (succ_eps_) {  // image rows only, image-indexed at rank 0
+          PF_CUDA_CHECK(cudaMemcpyAsync(succ_eps_ + size_t(row0) * hs,
+                                        s.h32 + size_t(J + row0) * hs, size_t(rows) * hs * 4,
                                         cudaMemcpyDefault, send_stream_));
         } else {
           PF_CUDA_CHECK(cudaMemcpyAsync(succ_h32_ + off, s.h32 + off, cnt * 4,

@@ -30,9 +30,12 @@ def _single(seed, L, hs, heads, p, N, S, M, W, x0, text=0):
     return res
 
 
-def _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0, text=0, runs=1):
+def _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0, text=0, runs=1, joint=None):
     import torch
-    if text:
+    if joint is not None:
+        ranks = [pf.JointDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, text, r, N, 0,
+                                            double_layers=joint) for r in range(N)]
+    elif text:
         ranks = [pf.PixArtCuda.rank_stage(seed, L, hs, heads, 4.0, p, text, r, N, 0)
                  for r in range(N)]
     else:
@@ -129,3 +132,15 @@ def test_process_per_rank_over_cuda_ipc():
     assert np.array_equal(got[0][0], ref.final_x)
     assert (sum(v[1] for v in got.values()), sum(v[2] for v in got.values())) == \
         (ref.stats.fresh_patch_reads, ref.stats.stale_patch_reads)
+
+
+@pytest.mark.parametrize("D,N", [(4, 2), (2, 3)])
+def test_same_process_ranks_joint(D, N):
+    # SD3 / Flux-style joint rows: text rows travel with patch 0 between ranks
+    seed, L, hs, heads, p, T = 2, 4, 64, 4, 256, 24
+    x0 = pf.make_initial_latent(3, p, hs)
+    with pf.JointDiTCuda(seed, L, hs, heads, 4.0, p, T, N, double_layers=D) as m:
+        ref = m.run_pipefusion(x0, 4, 2, 1, 0.1)
+    outs, stats = _same_process_ranks(seed, L, hs, heads, p, N, 4, 2, 1, x0, text=T, joint=D)
+    assert np.array_equal(outs[0], ref.final_x)
+    assert stats[0] == (ref.stats.fresh_patch_reads, ref.stats.stale_patch_reads)
