@@ -13,7 +13,8 @@
 struct pf_ctx {
   std::unique_ptr<pf::Engine> engine;
   std::string last_error;
-  float* x_scratch = nullptr;  // device latent for the host-buffer entry points
+  float* x_scratch = nullptr;   // device latent for the host-buffer entry points
+  double* x64_scratch = nullptr;  // the caller's fp64 latent, converted on the GPU
 };
 
 namespace {
@@ -77,46 +78,48 @@ void fill(std::mt19937_64& rng, std::vector<double>& m, int rows, int cols,
     for (int c = 0; c < cols; ++c) m[size_t(r) * cols + c] = next_uniform(rng) * scale;
 }
 
+// The host-buffer entry points move the caller's fp64 latent as is (one
+// copy each way) and convert layout and precision on the GPU.
+void ensure_latent_scratch(pf_ctx* ctx) {
+  const pf::ModelShape& m = ctx->engine->shape();
+  const size_t n = size_t(m.P) * m.hs;
+  if (!ctx->x_scratch && cudaMalloc(&ctx->x_scratch, n * 4) != cudaSuccess)
+    throw pf::CudaError("cudaMalloc latent failed");
+  if (!ctx->x64_scratch && cudaMalloc(&ctx->x64_scratch, n * 8) != cudaSuccess)
+    throw pf::CudaError("cudaMalloc latent failed");
+}
+
 void upload_x(pf_ctx* ctx, const double* x, pf_layout layout) {
   const pf::ModelShape& m = ctx->engine->shape();
-  const int64_t P = m.P;
-  const int hs = m.hs;
-  std::vector<float> xf(size_t(P) * hs);
-  for (int64_t r = 0; r < P; ++r)
-    for (int c = 0; c < hs; ++c)
-      xf[size_t(r) * hs + c] = float(layout == PF_COL_MAJOR ? x[size_t(c) * P + r]
-                                                            : x[size_t(r) * hs + c]);
   const pf::Stage& s0 = ctx->engine->stage(0);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(s0.device);
-  if (!ctx->x_scratch) {
-    if (cudaMalloc(&ctx->x_scratch, xf.size() * 4) != cudaSuccess)
-      throw pf::CudaError("cudaMalloc latent failed");
-  }
-  cudaError_t e = cudaMemcpy(ctx->x_scratch, xf.data(), xf.size() * 4, cudaMemcpyHostToDevice);
-  cudaSetDevice(prev);
+  struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
+  ensure_latent_scratch(ctx);
+  const size_t n = size_t(m.P) * m.hs;
+  cudaError_t e = cudaMemcpyAsync(ctx->x64_scratch, x, n * 8, cudaMemcpyHostToDevice, s0.stream);
+  if (e == cudaSuccess)
+    e = pf::latent_from_f64(ctx->x64_scratch, ctx->x_scratch, m.P, m.hs, layout == PF_COL_MAJOR,
+                            s0.stream);
   if (e != cudaSuccess) throw pf::CudaError(std::string("latent upload: ") + cudaGetErrorString(e));
 }
 
 void download_x(pf_ctx* ctx, double* x, pf_layout layout) {
   const pf::ModelShape& m = ctx->engine->shape();
-  const int64_t P = m.P;
-  const int hs = m.hs;
-  std::vector<float> xf(size_t(P) * hs);
   const pf::Stage& s0 = ctx->engine->stage(0);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(s0.device);
-  cudaError_t e = cudaMemcpy(xf.data(), ctx->x_scratch, xf.size() * 4, cudaMemcpyDeviceToHost);
-  cudaSetDevice(prev);
-  if (e != cudaSuccess) throw pf::CudaError(std::string("latent download: ") + cudaGetErrorString(e));
-  for (int64_t r = 0; r < P; ++r)
-    for (int c = 0; c < hs; ++c) {
-      const double v = double(xf[size_t(r) * hs + c]);
-      if (layout == PF_COL_MAJOR) x[size_t(c) * P + r] = v;
-      else x[size_t(r) * hs + c] = v;
-    }
+  struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};
+  const size_t n = size_t(m.P) * m.hs;
+  cudaError_t e = pf::latent_to_f64(ctx->x_scratch, ctx->x64_scratch, m.P, m.hs,
+                                    layout == PF_COL_MAJOR, s0.stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(x, ctx->x64_scratch, n * 8, cudaMemcpyDeviceToHost, s0.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s0.stream);
+  if (e != cudaSuccess)
+    throw pf::CudaError(std::string("latent download: ") + cudaGetErrorString(e));
 }
 
 void export_stats(const pf::RunStats& rs, pf_stats* out) {
@@ -447,11 +450,13 @@ pf_status pf_create(const pf_model_desc* desc, const double* const* weights,
 
 void pf_destroy(pf_ctx* ctx) {
   if (!ctx) return;
-  if (ctx->x_scratch) {
+  if (ctx->x_scratch || ctx->x64_scratch) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->engine->stage(0).device);
-    cudaFree(ctx->x_scratch);
+    cudaStreamSynchronize(ctx->engine->stage(0).stream);
+    if (ctx->x_scratch) cudaFree(ctx->x_scratch);
+    if (ctx->x64_scratch) cudaFree(ctx->x64_scratch);
     cudaSetDevice(prev);
   }
   delete ctx;

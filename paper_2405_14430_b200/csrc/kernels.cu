@@ -843,6 +843,47 @@ cudaError_t latent_update(float* x, const float* src, float eta, size_t n,
                     n / 4);
 }
 
+namespace {
+// Latent layout conversion for the host-buffer entry points: the reference's
+// fp64 matrices (row- or column-major) <-> the fp32 row-major device latent.
+__global__ void latent_from_f64_kernel(const double* __restrict__ src, float* __restrict__ dst,
+                                       int64_t rows, int cols, int col_major) {
+  const size_t n = size_t(rows) * cols;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    dst[i] = float(src[col_major ? c * size_t(rows) + r : i]);
+  }
+}
+__global__ void latent_to_f64_kernel(const float* __restrict__ src, double* __restrict__ dst,
+                                     int64_t rows, int cols, int col_major) {
+  const size_t n = size_t(rows) * cols;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    if (col_major) {
+      const size_t c = i / size_t(rows), r = i % size_t(rows);  // coalesced writes
+      dst[i] = double(src[r * cols + c]);
+    } else {
+      dst[i] = double(src[i]);
+    }
+  }
+}
+}  // namespace
+
+cudaError_t latent_from_f64(const double* src, float* dst, int64_t rows, int cols, bool col_major,
+                            cudaStream_t stream) {
+  latent_from_f64_kernel<<<ew_grid(size_t(rows) * cols / 4 + 1), 256, 0, stream>>>(
+      src, dst, rows, cols, col_major ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t latent_to_f64(const float* src, double* dst, int64_t rows, int cols, bool col_major,
+                          cudaStream_t stream) {
+  latent_to_f64_kernel<<<ew_grid(size_t(rows) * cols / 4 + 1), 256, 0, stream>>>(
+      src, dst, rows, cols, col_major ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream) {
   to_bf16_kernel<<<ew_grid(n / 4), 256, 0, stream>>>(h32, hb, n / 4);
   return cudaGetLastError();

@@ -154,6 +154,11 @@ cudaError_t patch_prepare(float* x, const float* eps, const float* cb,
 // x[i] -= eta * src[i], i < n
 cudaError_t latent_update(float* x, const float* src, float eta, size_t n,
                           cudaStream_t stream);
+// fp64 host-layout latent (row- or column-major) <-> fp32 row-major device latent
+cudaError_t latent_from_f64(const double* src, float* dst, int64_t rows, int cols, bool col_major,
+                            cudaStream_t stream);
+cudaError_t latent_to_f64(const float* src, double* dst, int64_t rows, int cols, bool col_major,
+                          cudaStream_t stream);
 // hb[i] = bf16(h32[i]), i < n
 cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream);
 // ---- PixArt block conditioning (pixart.cu) ----
