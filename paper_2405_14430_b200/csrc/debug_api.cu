@@ -92,10 +92,13 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
   cudaMemsetAsync(kp, 0, n * 2, s);
   cudaMemsetAsync(vp, 0, n * 2, s);
   const int total = P * hs;
+  ++pf::launch_counter();
   pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(q), qp,
                                                          nullptr, P, hs, heads, dh, dhp);
+  ++pf::launch_counter();
   pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(k), kp,
                                                          nullptr, P, hs, heads, dh, dhp);
+  ++pf::launch_counter();
   pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(v), vp,
                                                          nullptr, P, hs, heads, dh, dhp);
   CUtensorMap tq, tk, tv;

@@ -143,8 +143,11 @@ struct GemmSmem {
 // the epilogue. splits == 1 is the ordinary persistent kernel.
 struct SplitK {
   int splits = 1;
-  float* ws = nullptr;     // [tiles][splits][128][BN] fp32
+  float* ws = nullptr;     // [tiles][splits][128][BN] fp32 (in-kernel fixup)
   int* counters = nullptr; // [tiles], zero between launches
+  // partials only: split s writes rows x N fp32 at ws + s * rows * N (row-major)
+  // and no epilogue runs; a separate reduction kernel finishes the output
+  bool partials_only = false;
 };
 
 template <int BN, int STAGES, class Epi>
@@ -273,6 +276,35 @@ __global__ void __launch_bounds__(256, 1)
       constexpr int kNV = epi_colvecs<Epi>::value;
       float* colbuf = reinterpret_cast<float*>(smem + L::kColOffset) +
                       (tile_count & 1) * kMaxColVecs * BN;
+      if (splits > 1 && sk.partials_only) {
+        // ---- partial tile -> [split][rows][N] workspace, reduced elsewhere
+        ptx::mbar_wait(&tfull[acc], acc_phase);
+        ptx::tc_fence_after();
+        float* wrow = sk.ws + (size_t(split) * rows + local_row) * N;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + 32 * c, r);
+          ptx::tmem_wait_ld();
+          const int col0 = nt * BN + 32 * c;
+          if (row_ok && col0 + 32 <= N) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(wrow + col0 + e) =
+                  make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
+                              __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+          } else if (row_ok) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (col0 + e < N) wrow[col0 + e] = __uint_as_float(r[e]);
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
       if (splits > 1) {
         // ---- partial tile -> workspace; the last CTA of the tile reduces
         float* wsp = sk.ws + ((size_t(tile) * splits + split) * kGemmBM + tid) * BN;

@@ -84,6 +84,11 @@ bool tune_flag(const char* name) {
   return e && e[0] == '1';
 }
 
+int64_t& launch_counter() {
+  thread_local int64_t count = 0;
+  return count;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PF_NO_PDL");
@@ -545,6 +550,89 @@ bool make_weight_maps(WeightMaps* maps, const bf16* w, int N, int K) {
                              64, 128, 128);
 }
 
+// Split-K residual finish (the residual epilogue of a skinny GEMM run as a
+// bandwidth-bound kernel over all SMs): acc = sum of the split partials in
+// split order; h += gate (acc + bias); h_out = h; hb_out = bf16(h (1 +
+// colscale)); per-32-column (sum, sum^2) statistics; non-finite -> flag.
+// Four columns per thread; the 8 lanes of a 32-column chunk reduce by shuffle.
+__global__ void resid_reduce_kernel(const float* __restrict__ ws, int splits, int rows,
+                                    int row0, int N, const float* h_in, float* h_out,
+                                    bf16* hb_out, const float* __restrict__ bias,
+                                    const float* __restrict__ gate,
+                                    const float* __restrict__ colscale, float2* stats,
+                                    int stats_ld, int* flag, int code) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
+  const int n4 = N / 4;
+  const size_t total = size_t(rows) * n4;
+  const size_t stride = size_t(gridDim.x) * blockDim.x;
+  bool bad = false;
+  for (size_t i0 = size_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < total;
+       i0 += stride) {
+    const size_t i = i0 + (threadIdx.x & 31);
+    const bool ok = i < total;  // n4 % 8 == 0: whole 8-lane groups are in or out
+    const int r = ok ? int(i / n4) : 0;
+    const int c = ok ? 4 * int(i % n4) : 0;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) {
+      float4 a = *reinterpret_cast<const float4*>(ws + size_t(r) * N + c);
+      for (int sp = 1; sp < splits; ++sp) {
+        const float4 b = *reinterpret_cast<const float4*>(ws + (size_t(sp) * rows + r) * N + c);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      if (bias) {
+        const float4 b = *reinterpret_cast<const float4*>(bias + c);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      if (gate) {
+        const float4 g = *reinterpret_cast<const float4*>(gate + c);
+        a.x *= g.x; a.y *= g.y; a.z *= g.z; a.w *= g.w;
+      }
+      const size_t off = size_t(row0 + r) * N + c;
+      x = *reinterpret_cast<const float4*>(h_in + off);
+      x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
+      *reinterpret_cast<float4*>(h_out + off) = x;
+      float4 y = x;
+      if (colscale) {
+        const float4 cs = *reinterpret_cast<const float4*>(colscale + c);
+        y.x *= 1.f + cs.x; y.y *= 1.f + cs.y; y.z *= 1.f + cs.z; y.w *= 1.f + cs.w;
+      }
+      uint2 pk;
+      pk.x = ptx::pack_bf16x2(y.x, y.y);
+      pk.y = ptx::pack_bf16x2(y.z, y.w);
+      *reinterpret_cast<uint2*>(hb_out + off) = pk;
+      bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+    }
+    if (stats) {
+      float sm = (x.x + x.y) + (x.z + x.w);
+      float sq = (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      }
+      if (ok && ((c >> 2) & 7) == 0)
+        stats[size_t(c >> 5) * stats_ld + row0 + r] = make_float2(sm, sq);
+    }
+  }
+  if (bad && flag) atomicMin(flag, code);
+}
+
+// Split count for the workspace + reduction path of skinny residual GEMMs.
+int gemm_splits_residual(int rows, int N, int K, const EpiParams& ep, int sm_count) {
+  if (!ep.splitk_ws || tune_flag("PF_NO_RESID_SPLITK")) return 1;
+  const int bn = gemm_bn_1sm(N);
+  const int tiles = ((rows + kGemmBM - 1) / kGemmBM) * ((N + bn - 1) / bn);
+  const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+  // long K only: at K = 1152 (out-proj) the extra reduction launch costs
+  // more than the idle SMs (measured, profiles/r1_msweep_c2_splitk.txt)
+  if (2 * tiles > sm_count || kblocks < 32) return 1;
+  int s = std::min(sm_count / tiles, kblocks / 8);
+  s = std::min(s, 8);
+  while (s > 1 && size_t(s) * rows * N > ep.splitk_ws_floats) --s;
+  return s < 1 ? 1 : s;
+}
+
 int gemm_splits(int rows, int N, int K, const EpiParams& ep, int sm_count) {
   // Opt-in (PF_SPLITK=1): measured slower than plain tiles for the 512-row
   // patch GEMMs of C2 (the last-arriving CTA's serial reduction dominates;
@@ -567,6 +655,30 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  int N, int K, Epi kind, const EpiParams& ep, int sm_count,
                  cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
+  // Skinny residual GEMMs (a small patch: fewer output tiles than half the
+  // SMs): split K across CTAs into a [split][rows][N] workspace, then finish
+  // the residual epilogue with a bandwidth-bound reduction over all SMs.
+  if (kind == Epi::Residual && N % 32 == 0) {
+    const int splits = gemm_splits_residual(rows, N, K, ep, sm_count);
+    if (splits > 1) {
+      const SplitK sk{splits, ep.splitk_ws, nullptr, true};
+      cudaError_t e = gemm_bn_1sm(N) == 64
+          ? launch_gemm<64, 8>(a, b.one_sm, rows, row0, N, K, EpiStoreF32{nullptr, 0},
+                               sm_count, stream, sk)
+          : launch_gemm<128, 6>(a, b.one_sm, rows, row0, N, K, EpiStoreF32{nullptr, 0},
+                                sm_count, stream, sk);
+      if (e != cudaSuccess) return e;
+      const size_t n4 = size_t(rows) * (N / 4);
+      size_t g = (n4 + 255) / 256;
+      if (g > size_t(sm_count) * 8) g = size_t(sm_count) * 8;
+      return launch_pdl(resid_reduce_kernel, dim3(unsigned(g)), dim3(256), 0, stream,
+                        static_cast<const float*>(ep.splitk_ws), splits, rows, row0, N,
+                        static_cast<const float*>(ep.out_f32),
+                        ep.out_f32_dst ? ep.out_f32_dst : ep.out_f32,
+                        ep.out_bf16_dst ? ep.out_bf16_dst : ep.out_bf16, ep.bias, ep.gate,
+                        ep.colscale, ep.stats_out, ep.stats_ld, ep.flag, ep.code);
+    }
+  }
   // Skinny problems (a small patch: fewer output tiles than half the SMs)
   // split K across CTAs (deterministic in-kernel reduction), 1-SM tiles.
   if (const int splits = gemm_splits(rows, N, K, ep, sm_count); splits > 1) {
@@ -730,6 +842,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
                                             &attn_fwd_kernel<DHP, NT>>{});
   if (e != cudaSuccess || splits == 1) return e;
   const int total = a.rows * a.heads * (DHP / 16);
+  ++launch_counter();
   attn_combine_kernel<DHP><<<(total + 255) / 256, 256, 0, stream>>>(prm);
   return cudaGetLastError();
 }
@@ -872,6 +985,7 @@ __global__ void latent_to_f64_kernel(const float* __restrict__ src, double* __re
 
 cudaError_t latent_from_f64(const double* src, float* dst, int64_t rows, int cols, bool col_major,
                             cudaStream_t stream) {
+  ++launch_counter();
   latent_from_f64_kernel<<<ew_grid(size_t(rows) * cols / 4 + 1), 256, 0, stream>>>(
       src, dst, rows, cols, col_major ? 1 : 0);
   return cudaGetLastError();
@@ -879,17 +993,20 @@ cudaError_t latent_from_f64(const double* src, float* dst, int64_t rows, int col
 
 cudaError_t latent_to_f64(const float* src, double* dst, int64_t rows, int cols, bool col_major,
                           cudaStream_t stream) {
+  ++launch_counter();
   latent_to_f64_kernel<<<ew_grid(size_t(rows) * cols / 4 + 1), 256, 0, stream>>>(
       src, dst, rows, cols, col_major ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream) {
+  ++launch_counter();
   to_bf16_kernel<<<ew_grid(n / 4), 256, 0, stream>>>(h32, hb, n / 4);
   return cudaGetLastError();
 }
 
 cudaError_t reset_flag(int* flag, cudaStream_t stream) {
+  ++launch_counter();
   reset_flag_kernel<<<1, 1, 0, stream>>>(flag);
   return cudaGetLastError();
 }

@@ -31,6 +31,9 @@ int device_sm_count(int device);
 // ptx::pdl_wait() before its first dependent memory access). PF_NO_PDL=1 in
 // the environment turns the attribute off (plain stream serialisation).
 bool pdl_enabled();
+// Kernel launches issued by the calling thread. Every launch site in the
+// library bumps it; the runtime reports per-run deltas (pf_last_launch_count).
+int64_t& launch_counter();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t stream, Args&&... args) {
@@ -44,6 +47,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++launch_counter();
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -182,6 +182,7 @@ int grid_for(size_t n, int per_block) {
 }  // namespace
 
 cudaError_t px_sinusoid(float* out, int S, cudaStream_t stream) {
+  ++launch_counter();
   px_sinusoid_kernel<<<S, kFreq / 2, 0, stream>>>(out, S);
   return cudaGetLastError();
 }
@@ -189,6 +190,7 @@ cudaError_t px_sinusoid(float* out, int S, cudaStream_t stream) {
 cudaError_t px_gemv(const float* in, int S, int K, const float* W, const float* b, int N,
                     float* out, bool silu_in, bool silu_out, cudaStream_t stream) {
   dim3 grid((N + 7) / 8, (S + kGemvS - 1) / kGemvS);
+  ++launch_counter();
   px_gemv_kernel<<<grid, 256, 0, stream>>>(in, S, K, W, b, N, out, silu_in ? 1 : 0,
                                            silu_out ? 1 : 0);
   return cudaGetLastError();
@@ -197,6 +199,7 @@ cudaError_t px_gemv(const float* in, int S, int K, const float* W, const float* 
 cudaError_t px_mod(const float* sst, int nl, const float* tv, int S, int w6, float* mod,
                    cudaStream_t stream) {
   const size_t n = size_t(nl) * S * w6;
+  ++launch_counter();
   px_mod_kernel<<<grid_for(n, 256), 256, 0, stream>>>(sst, nl, tv, S, w6, mod);
   return cudaGetLastError();
 }
@@ -205,6 +208,7 @@ cudaError_t px_fold_rows(const float* mod, int nl, int S, int hs, bf16* aq, bf16
                          int rpad, cudaStream_t stream) {
   if (2 * S > rpad) return cudaErrorInvalidValue;
   const size_t n = size_t(nl) * S * hs;
+  ++launch_counter();
   px_fold_rows_kernel<<<grid_for(n, 256), 256, 0, stream>>>(mod, nl, S, hs, aq, am, rpad);
   return cudaGetLastError();
 }

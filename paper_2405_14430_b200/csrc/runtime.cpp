@@ -25,6 +25,14 @@ namespace pf {
 
 namespace {
 
+// Counts the kernels a run enqueues (launch_counter() delta over its scope).
+struct LaunchTally {
+  int64_t& out;
+  int64_t base;
+  explicit LaunchTally(int64_t& o) : out(o), base(launch_counter()) {}
+  ~LaunchTally() { out = launch_counter() - base; }
+};
+
 struct DeviceGuard {
   int prev = 0;
   explicit DeviceGuard(int dev) {
@@ -508,8 +516,6 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   check(gemm(s.tm_z, L.tm_wout, rows, row0, m.hs, m.mlp, Epi::Residual, sk(s, res_out),
              s.sm_count, s.stream), "gemm mlp-out");
   prof_end(s);
-  const int splits = attn_splits(a, s.sm_count);
-  launches_ += 5 + (splits > 1 ? 1 : 0);
 }
 
 cudaEvent_t Engine::prof_event(int stage) {
@@ -636,7 +642,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     src[size_t(d)].assign(size_t(stages_[size_t(d)].layer_count),
                           std::vector<int>(size_t(patches), steps));
   codes_.clear();
-  launches_ = 0;
+  LaunchTally tally(launches_);
   prof_.clear();
   prof_used_.assign(stages_.size(), 0);
 
@@ -655,7 +661,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     DeviceGuard g(s.device);
     PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start, 0));
     check(reset_flag(s.flag, s.stream), "reset_flag");
-    ++launches_;
     // StageBuffers are zero-initialised per run (execute.cpp:42-48). Without
     // warmup the zero rows are read as stale context, so clear them; with
     // warmup every row is rewritten before it is read.
@@ -690,7 +695,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
   auto text_prepare = [&]() {
     check(patch_prepare(s0.text, nullptr, s0.zeros, s0.h32, s0.hb, 0, J, m.hs, 0.f, false,
                         s0.stream), "text rows");
-    ++launches_;
   };
   float* h32_img = s0.h32 + size_t(J) * m.hs;  // image row 0 of the activations
   bf16* hb_img = s0.hb + size_t(J) * m.hs;
@@ -709,7 +713,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         check(patch_prepare(x_dev, nullptr, s0.cb, h32_img, hb_img, 0, int(m.P), m.hs,
                             0.f, false, s0.stream), "patch_prepare");
       prof_end(s0);
-      ++launches_;
     }
     for (int d = 0; d < n; ++d) {
       Stage& s = stages_[size_t(d)];
@@ -735,7 +738,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     prof_begin(s0, kSampler, 0, double(m.P) * m.hs * 12);
     check(latent_update(x_dev, s0.eps, eta, size_t(m.P) * m.hs, s0.stream), "latent_update");
     prof_end(s0);
-    ++launches_;
   }
 
   // ---- steady: patch pipeline (execute.cpp:192-212)
@@ -760,7 +762,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
           check(patch_prepare(x_dev, s0.eps, s0.cb, h32_img, hb_img, row0, r, m.hs, eta,
                               q > 0, s0.stream), "patch_prepare");
         prof_end(s0);
-        ++launches_;
       }
       for (int d = 0; d < n; ++d) {
         Stage& s = stages_[size_t(d)];
@@ -807,7 +808,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     prof_begin(s0, kSampler, 0, double(m.P) * m.hs * 12);
     check(latent_update(x_dev, s0.eps, eta, size_t(m.P) * m.hs, s0.stream), "latent_update");
     prof_end(s0);
-    ++launches_;
   }
 
   // Join: the caller's stream waits for every stage.
@@ -952,9 +952,9 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
                                 cudaMemcpyHostToDevice, s.stream));
   PF_CUDA_CHECK(cudaMemcpyAsync(L.k, kd.data(), kd.size() * 2, cudaMemcpyHostToDevice, s.stream));
   PF_CUDA_CHECK(cudaMemcpyAsync(L.v, vd.data(), vd.size() * 2, cudaMemcpyHostToDevice, s.stream));
+  LaunchTally tally(launches_);
   check(reset_flag(s.flag, s.stream), "reset_flag");
   codes_.assign(1, {0, layer});
-  launches_ = 1;
   if (m.block == kBlockPixArt) {
     if (steps < 1 || t < 0 || t >= steps)
       throw ValidationError("timestep index outside [0, steps)");
@@ -1022,7 +1022,6 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     check(gemm(s.tm_hb, txt ? L.tm_t_wqkv : L.tm_wqkv, n, r0, 3 * hs, hs, Epi::QKV,
                sk(s, qkv), s.sm_count, s.stream), "gemm qkv (joint)");
     prof_end(s);
-    ++launches_;
   });
   AttnLaunch a{m.dhp, Pt, rows, row0, m.heads, m.dh, hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
@@ -1030,7 +1029,6 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
   prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (joint)");
   prof_end(s);
-  launches_ += 1 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0);
   EpiParams res;
   res.out_f32 = s.h32;
   res.out_bf16 = s.hb;
@@ -1046,7 +1044,6 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     check(gemm(s.tm_attn, txt ? L.tm_t_wo : L.tm_wo, n, r0, hs, hs, Epi::Residual, sk(s, res),
                s.sm_count, s.stream), "gemm out-proj (joint)");
     prof_end(s);
-    ++launches_;
   });
   EpiParams th;
   th.out_bf16 = s.z;
@@ -1056,7 +1053,6 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     check(gemm(s.tm_hb, txt ? L.tm_t_win : L.tm_win, n, r0, m.mlp, hs, Epi::Tanh, sk(s, th),
                s.sm_count, s.stream), "gemm mlp-in (joint)");
     prof_end(s);
-    ++launches_;
   });
   EpiParams res_out = res;
   if (redirect_) {  // last layer of a rank: store straight into the next stage
@@ -1070,7 +1066,6 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     check(gemm(s.tm_z, txt ? L.tm_t_wout : L.tm_wout, n, r0, hs, m.mlp, Epi::Residual,
                sk(s, res_out), s.sm_count, s.stream), "gemm mlp-out (joint)");
     prof_end(s);
-    ++launches_;
   });
 }
 
@@ -1132,7 +1127,6 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
   check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, res_out),
              s.sm_count, s.stream), "gemm mlp-out (single)");
   prof_end(s);
-  launches_ += 5 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0);
 }
 
 // ============================================================== DistriFusion
@@ -1182,7 +1176,7 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
   st.stale = 0;
   st.fresh_fraction.assign(size_t(workers), {});
   codes_.clear();
-  launches_ = 0;
+  LaunchTally tally(launches_);
   prof_.clear();
   prof_used_.assign(stages_.size(), 0);
   tl_.clear();
@@ -1190,7 +1184,6 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
   PF_CUDA_CHECK(cudaEventRecord(ev_start_, caller));
   PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start_, 0));
   check(reset_flag(s.flag, s.stream), "reset_flag");
-  ++launches_;
   // slot 0 = (k, v), slot 1 = (k2, v2); `prev` holds the previous step
   int prev = 0;
   if (warmup == 0)  // StageBuffers are zero-initialised (execute.cpp:42-48)
@@ -1218,7 +1211,6 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
       // every worker sees every shard fresh: one full-sequence pass
       check(patch_prepare(x_dev, nullptr, s.cb, s.h32, s.hb, 0, int(m.P), m.hs, 0.f, false,
                           s.stream), "patch_prepare");
-      ++launches_;
       for (int l = 0; l < s.layer_count; ++l) {
         st.fresh += int64_t(workers) * workers;
         codes_.emplace_back(t, l);
@@ -1228,13 +1220,11 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
         layer_forward(s, l, int(m.P), 0, int(codes_.size()) - 1, &kv);
       }
       check(latent_update(x_dev, s.h32, eta, size_t(m.P) * hs, s.stream), "latent_update");
-      ++launches_;
     } else {
       for (int i = 0; i < workers; ++i) {
         const int row0 = i * r;
         check(patch_prepare(x_dev, nullptr, s.cb, s.h32, s.hb, row0, r, m.hs, 0.f, false,
                             s.stream), "patch_prepare");
-        ++launches_;
         for (int l = 0; l < s.layer_count; ++l) {
           // own shard fresh (t), the others installed last step (t + 1)
           st.fresh += 1;
@@ -1246,7 +1236,6 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
         st.fresh_fraction[size_t(i)].push_back(1.0 / double(workers));
         check(latent_update(x_dev + size_t(row0) * hs, s.h32 + size_t(row0) * hs, eta,
                             size_t(r) * hs, s.stream), "latent_update");
-        ++launches_;
       }
     }
     prev = 1 - prev;  // install: this step's buffer becomes the previous step's
@@ -1499,7 +1488,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   st.fresh_fraction.assign(1, {});
   std::vector<std::vector<int>> src(size_t(s.layer_count), std::vector<int>(size_t(patches), steps));
   codes_.clear();
-  launches_ = 0;
+  LaunchTally tally(launches_);
   prof_.clear();
   prof_used_.assign(stages_.size(), 0);
 
@@ -1512,7 +1501,6 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, ev_start_, 0));
   PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_start_, 0));
   check(reset_flag(s.flag, s.stream), "reset_flag");
-  ++launches_;
   if (warmup == 0) {
     const size_t kv = size_t(m.heads) * size_t(m.rows_total()) * size_t(m.dhp) * sizeof(bf16);
     for (StageLayer& L : s.layers) {
@@ -1562,7 +1550,6 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         if (joint && op.patch <= 0) {  // the text stream re-enters each step
           check(patch_prepare(s.text, nullptr, s.zeros, s.h32, s.hb, 0, J, m.hs, 0.f, false,
                               s.stream), "text rows");
-          ++launches_;
         }
         if (px)
           px_patch_prepare(x_dev, op.flag != 0, row0, rows, op.t, eta);
@@ -1570,14 +1557,12 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           check(patch_prepare(x_dev, s.eps, s.cb, s.h32 + size_t(J) * hs, s.hb + size_t(J) * hs,
                               row0, rows, m.hs, eta, op.flag != 0, s.stream), "patch_prepare");
         prof_end(s);
-        ++launches_;
         break;
       }
       case PlanOp::kLatentUpdate:
         prof_begin(s, kSampler, 0, double(m.P) * hs * 12);
         check(latent_update(x_dev, s.eps, eta, size_t(m.P) * hs, s.stream), "latent_update");
         prof_end(s);
-        ++launches_;
         break;
       case PlanOp::kCompute: {
         const int t = op.t;
@@ -1825,7 +1810,6 @@ void Engine::px_conditioning(Stage& s, int steps) {
   check(px_mod(px.sst, nl + 1, px.tv, S, w6, px.mod, s.stream), "adaLN modulation");
   check(px_fold_rows(px.mod, nl, S, hs, px.fold_aq, px.fold_am, px.fold_rpad, s.stream),
         "LayerNorm fold operands");
-  launches_ += 6;
   for (int lf = 0; lf < nl; ++lf) {
     StageLayer& L = s.layers[size_t(lf)];
     EpiParams fq;
@@ -1850,7 +1834,6 @@ void Engine::px_conditioning(Stage& s, int steps) {
     kv.c2 = L.bkvc;
     check(gemm(px.tm_text, L.tm_wkvc, m.T, 0, 2 * hs, hs, Epi::QKV, kv, s.sm_count, s.stream),
           "cross K/V projection");
-    launches_ += 3;
   }
   prof_end(s);
   px_steps_ = S;
@@ -1984,8 +1967,6 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   check(gemm(s.tm_z, L.tm_wout, rows, row0, hs, m.mlp, Epi::Residual, sk(s, r3), s.sm_count, s.stream),
         "gemm mlp-out");
   prof_end(s);
-  launches_ += 8 + (attn_splits(a, s.sm_count) > 1 ? 1 : 0) +
-               (attn_splits(ca, s.sm_count) > 1 ? 1 : 0);
 }
 
 }  // namespace pf
