@@ -15,8 +15,22 @@
 // (SWIZZLE_32B atoms), which serve both as K-major (Q, K) and MN-major (V)
 // UMMA operands.
 //
-// One CTA = NT = 2 query tiles of 128 rows (sharing every K/V tile, which
-// halves the L2->SM operand traffic per FLOP) x one head x one kv split.
+// Work item = NT = 2 query tiles of 128 rows (sharing every K/V tile, which
+// halves the L2->SM operand traffic per FLOP) x one head; its units are the
+// item's 128-row KV blocks. Stream-K schedule: the items x blocks units are
+// cut into `grid` equal contiguous ranges, one persistent CTA per range (one
+// per SM), so no SM idles in a partial last wave (C2: 256 items over 148 SMs
+// would otherwise take 2 full waves for 1.73 waves of work). A CTA walks its
+// range as segments (item, [b0, b1)): a segment covering a whole item writes
+// the normalised output; a cut segment writes an unnormalised fp32 partial
+// (O, m, l) into slot 2c (the CTA's first segment) or 2c + 1 (its last), and
+// `attn_streamk_combine_kernel` merges each cut item's partials in CTA order.
+// When every range spans at least one item (`fused`: each item meets at most
+// two CTAs) the merge happens in this kernel instead: CTAs walk their
+// segments in reverse, so the head of a cut item (CTA c-1's last segment) is
+// computed first and published (partial + release flag), and the tail
+// (CTA c's first segment) is computed last and merged with it in the
+// epilogue -- the flag is long set by then, and no CTA waits on a later one.
 // Roles (384 threads):
 //   warp 0        TMA producer: Q tiles once, then K_i and V_i in two rings
 //   warp 1        MMA issuer: S_{t,i} = Q_t K_i^T (SS: both operands in smem)
@@ -32,8 +46,6 @@
 //                 split 3:1 between MUFU.EX2 and an FMA-pipe polynomial
 //                 (measured alternatives: 1:1, 1:0, packed f16x2 MUFU exp --
 //                 all slower on B200, whose f16x2 ex2 issues two MUFU ops).
-// With kv_splits > 1 each split writes an unnormalised partial (O, m, l) in
-// fp32 and `attn_combine_kernel` merges the splits in a fixed order.
 //
 // Measured at C2 (dh 72 -> 80, 4096 x 4096 x 16 heads): ~2900 clk per
 // 128-row KV block per CTA, the softmax exp section being the largest part
@@ -45,6 +57,7 @@
 // 512-row patches: the merge then runs on one CTA per (tiles, head).
 #pragma once
 
+#include "kernels.h"  // kAttnFlagsPerCta
 #include "sm100_ptx.cuh"
 
 namespace pf {
@@ -52,19 +65,22 @@ namespace pf {
 constexpr int kAttnBM = 128;   // query rows per tile
 constexpr int kAttnBN = 128;   // kv rows per block
 
+constexpr int kAttnMaxSegs = 64;  // segments per CTA (attn_grid keeps within)
+
 // NT query tiles (of 128 rows) per CTA share every K/V tile.
 template <int DHP, int NT>
 struct AttnSmem {
   static constexpr uint32_t kTileBytes = kAttnBM * DHP * 2;  // Q, K or V tile
   static constexpr uint32_t kTileAlloc = (kTileBytes + 1023) & ~1023u;
-  static constexpr uint32_t kBudget = 232448 - 1024 - 512;
+  static constexpr uint32_t kBudget = 232448 - 1024 - 512 - 16 * kAttnMaxSegs;
   static constexpr int kStagesMax = int((kBudget - NT * kTileAlloc) / (2 * kTileAlloc));
   static constexpr int kStages = kStagesMax > 4 ? 4 : kStagesMax;
   static constexpr uint32_t kQOff = 0;
   static constexpr uint32_t kKOff = NT * kTileAlloc;
   static constexpr uint32_t kVOff = kKOff + kStages * kTileAlloc;
   static constexpr uint32_t kBarOff = kVOff + kStages * kTileAlloc;
-  static constexpr uint32_t kTotal = kBarOff + 512 + 1024;
+  static constexpr uint32_t kSegOff = kBarOff + 512;  // int4 segment table
+  static constexpr uint32_t kTotal = kSegOff + 16 * kAttnMaxSegs + 1024;
   static constexpr int kThreads = 128 + 128 * NT;
   static_assert(DHP % 16 == 0 && DHP <= 128, "head dim padding");
   static_assert(kStages >= 2, "attention smem budget");
@@ -83,12 +99,16 @@ struct AttnParams {
   int row0;         // first query row
   int heads, dh, hs;
   float scale_log2; // log2(e) / sqrt(dh)
-  int kv_splits;    // >= 1
-  int blocks_per_split;
-  __nv_bfloat16* out;  // [P][hs]   (used when kv_splits == 1)
-  float* part_o;       // [splits][heads][rows_pad][DHP] (kv_splits > 1)
-  float* part_ml;      // [splits][heads][rows_pad][2]
-  int rows_pad;        // ctas_along_q * NT * 128
+  int nq;           // query-tile groups per head (item = head * nq + group)
+  int blocks;       // kv blocks per item
+  long long units;  // items * blocks
+  int grid;         // persistent CTAs; CTA c owns units [c U / grid, (c+1) U / grid)
+  __nv_bfloat16* out;  // [P][hs]
+  float* part_o;       // [2 grid][DHP][NT * 128]  partials of cut items (column-major)
+  float* part_ml;      // [2 grid][2][NT * 128]    (m, l)
+  int* flags;          // [grid][kAttnFlagsPerCta] head partial published, per softmax
+                       // warp (fused merge; cleared by the reading warp)
+  int fused;           // merge cut items in-kernel (every range >= one item)
   // Debug timeline (clock64) of CTA (0,0,0); null in production. Slots:
   // [0, 4096) softmax t: 2048 t + 8 i + event; [4096, 6144) MMA: 8 i + event;
   // [6144, 8192) TMA: 8 i + event.
@@ -96,9 +116,11 @@ struct AttnParams {
 };
 
 __device__ __forceinline__ void attn_trace(const AttnParams& prm, int slot) {
-  if (prm.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
-      (threadIdx.x & 31) == 0)
-    prm.trace[slot] = clock64();
+  if (prm.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0) prm.trace[slot] = clock64();
+}
+
+__host__ __device__ __forceinline__ long long attn_unit_start(const AttnParams& prm, int c) {
+  return (long long)c * prm.units / prm.grid;
 }
 
 // kPoly: bit (g & 7) set -> 4-element group g of a score row takes the
@@ -128,20 +150,18 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
   uint64_t* v_empty = v_full + S;    // [S]
   uint64_t* s_full = v_empty + S;    // [NT]  S_t ready (and PV_{t,i-1} done)
   uint64_t* p_full = s_full + NT;    // [NT]  P_t written to TMEM, S_t consumed
-  uint64_t* o_done = p_full + NT;    // [NT]  last PV_t complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NT);
+  uint64_t* o_done = p_full + NT;    // [NT]  last PV_t of a segment complete
+  uint64_t* q_empty = o_done + NT;   // every S MMA of a segment complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = ptx::lane_id();
-  const int qt = blockIdx.x;  // group of NT query tiles
-  const int head = blockIdx.y;
-  const int split = blockIdx.z;
-  const int total_blocks = (prm.P + kAttnBN - 1) / kAttnBN;
-  const int blk_begin = split * prm.blocks_per_split;
-  int blk_end = blk_begin + prm.blocks_per_split;
-  if (blk_end > total_blocks) blk_end = total_blocks;
-  const int nblk = blk_end - blk_begin;  // >= 1 by construction
-
+  int4* segs = reinterpret_cast<int4*>(smem + L::kSegOff);  // {item, b0, n, -}
+  struct Seg {
+    int x, b0, n;  // item, kv blocks [b0, b0 + n)
+  };
+  int* nseg_slot = reinterpret_cast<int*>(tmem_slot + 1);
+  const int B = prm.blocks;
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tm_q);
     ptx::prefetch_tmap(&tm_k);
@@ -151,6 +171,7 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       ptx::prefetch_tmap(&tm_v2);
     }
     ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&k_full[s], 1);
       ptx::mbar_init(&k_empty[s], 1);
@@ -163,6 +184,25 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       ptx::mbar_init(&o_done[t], 1);
     }
     ptx::fence_barrier_init();
+    // Segment table of this CTA's unit range [u0, u1): natural order, or
+    // reversed when cut items are merged in-kernel (see header).
+    const long long u0 = attn_unit_start(prm, blockIdx.x);
+    const long long u1 = attn_unit_start(prm, blockIdx.x + 1);
+    int n = 0;
+    for (long long u = u0; u < u1 && n < kAttnMaxSegs; ++n) {
+      const int x = int(u / B);
+      const int b0 = int(u - (long long)x * B);
+      const int len = int(u1 - u < B - b0 ? u1 - u : B - b0);
+      segs[n] = make_int4(x, b0, len, 0);
+      u += len;
+    }
+    if (prm.fused)
+      for (int i = 0; i < n / 2; ++i) {
+        const int4 tmp = segs[i];
+        segs[i] = segs[n - 1 - i];
+        segs[n - 1 - i] = tmp;
+      }
+    *nseg_slot = n;
   }
   // TMEM columns: S_t = [128 t, 128 t + 128) fp32, P_t = S_t + 64 (64 columns
   // of packed bf16 pairs, written over consumed scores), O_t = 256 + 128 t.
@@ -171,8 +211,16 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int nseg = *nseg_slot;
+  const bool rev = prm.fused != 0;
+  const bool cta_trace = prm.trace && threadIdx.x == 0 && blockIdx.x < 1024;
+  if (cta_trace) prm.trace[8192 + 4 * blockIdx.x] = ptx::globaltimer();
   ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
   ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
+  if (cta_trace) {
+    prm.trace[8192 + 4 * blockIdx.x + 1] = ptx::globaltimer();
+    prm.trace[8192 + 4 * blockIdx.x + 3] = ptx::smid();
+  }
 
   // With NT = 2 (384 threads) registers move from the producer warpgroup
   // (TMA, MMA, allocator) to the two softmax warpgroups.
@@ -180,38 +228,49 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     if constexpr (NT == 2) ptx::setmaxnreg_dec<56>();
     if (warp == 0 && lane == 0) {
       // ------------------------------------------------------------ TMA
-      const int qrow = head * prm.q_stride + prm.row0 + qt * (NT * kAttnBM);
-      ptx::mbar_arrive_expect_tx(q_full, NT * L::kTileBytes);
+      int g = 0;  // blocks loaded so far (K/V ring position)
+      int sgi = 0;
+      for (; sgi < nseg; ++sgi) {
+        const int4 sg4 = segs[sgi];
+        const Seg sg{sg4.x, sg4.y, sg4.z};
+        const int head = sg.x / prm.nq;
+        const int qt = sg.x - head * prm.nq;
+        // Q of the previous segment is free once all its S MMAs completed
+        if (sgi > 0) ptx::mbar_wait(q_empty, (sgi - 1) & 1);
+        if (g < 256) attn_trace(prm, 6144 + 8 * g + 3);
+        const int qrow = head * prm.q_stride + prm.row0 + qt * (NT * kAttnBM);
+        ptx::mbar_arrive_expect_tx(q_full, NT * L::kTileBytes);
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
+        for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sQ + t * L::kTileAlloc + c * (kAttnBM * 32), &tm_q, q_full,
-                           c * 16, qrow + t * kAttnBM);
-      for (int i = 0; i < nblk; ++i) {
-        const int s = i % S;
-        const uint32_t ph = ((i / S) & 1) ^ 1;
-        const int kvrow = head * prm.P + (blk_begin + i) * kAttnBN;
-        // DistriFusion: the worker's own (fresh) rows come from a second buffer
-        const int kvr = (blk_begin + i) * kAttnBN;
-        const bool fresh = kvr >= prm.fresh_lo && kvr < prm.fresh_hi;
-        const CUtensorMap* km = fresh ? &tm_k2 : &tm_k;
-        const CUtensorMap* vm = fresh ? &tm_v2 : &tm_v;
-        attn_trace(prm, 6144 + 8 * i + 0);
-        ptx::mbar_wait(&k_empty[s], ph);
-        attn_trace(prm, 6144 + 8 * i + 1);
-        ptx::mbar_arrive_expect_tx(&k_full[s], L::kTileBytes);
+          for (int c = 0; c < kChunks; ++c)
+            ptx::tma_load_2d(sQ + t * L::kTileAlloc + c * (kAttnBM * 32), &tm_q, q_full,
+                             c * 16, qrow + t * kAttnBM);
+        for (int i = 0; i < sg.n; ++i, ++g) {
+          const int s = g % S;
+          const uint32_t ph = ((g / S) & 1) ^ 1;
+          const int kvr = (sg.b0 + i) * kAttnBN;
+          const int kvrow = head * prm.P + kvr;
+          // DistriFusion: the worker's own (fresh) rows come from a second buffer
+          const bool fresh = kvr >= prm.fresh_lo && kvr < prm.fresh_hi;
+          const CUtensorMap* km = fresh ? &tm_k2 : &tm_k;
+          const CUtensorMap* vm = fresh ? &tm_v2 : &tm_v;
+          if (g < 256) attn_trace(prm, 6144 + 8 * g + 0);
+          ptx::mbar_wait(&k_empty[s], ph);
+          if (g < 256) attn_trace(prm, 6144 + 8 * g + 1);
+          ptx::mbar_arrive_expect_tx(&k_full[s], L::kTileBytes);
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sK + s * L::kTileAlloc + c * (kAttnBN * 32), km, &k_full[s],
-                           c * 16, kvrow);
-        ptx::mbar_wait(&v_empty[s], ph);
-        attn_trace(prm, 6144 + 8 * i + 2);
-        ptx::mbar_arrive_expect_tx(&v_full[s], L::kTileBytes);
+          for (int c = 0; c < kChunks; ++c)
+            ptx::tma_load_2d(sK + s * L::kTileAlloc + c * (kAttnBN * 32), km, &k_full[s],
+                             c * 16, kvrow);
+          ptx::mbar_wait(&v_empty[s], ph);
+          if (g < 256) attn_trace(prm, 6144 + 8 * g + 2);
+          ptx::mbar_arrive_expect_tx(&v_full[s], L::kTileBytes);
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c)
-          ptx::tma_load_2d(sV + s * L::kTileAlloc + c * (kAttnBN * 32), vm, &v_full[s],
-                           c * 16, kvrow);
+          for (int c = 0; c < kChunks; ++c)
+            ptx::tma_load_2d(sV + s * L::kTileAlloc + c * (kAttnBN * 32), vm, &v_full[s],
+                             c * 16, kvrow);
+        }
       }
     } else if (warp == 1 && lane == 0) {
       // ------------------------------------------------------------ MMA
@@ -223,10 +282,9 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       const uint32_t q_base = ptx::smem_u32(sQ);
       const uint32_t k_base = ptx::smem_u32(sK);
       const uint32_t v_base = ptx::smem_u32(sV);
-      ptx::mbar_wait(q_full, 0);
 
-      auto issue_s = [&](int t, int i) {
-        const uint32_t kb = k_base + (i % S) * L::kTileAlloc;
+      auto issue_s = [&](int t, int g) {
+        const uint32_t kb = k_base + (g % S) * L::kTileAlloc;
         const uint32_t qb = q_base + t * L::kTileAlloc;
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
@@ -234,8 +292,8 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
                             ptx::desc_kmajor_sw32(kb + c * (kAttnBN * 32)), idesc_s, c != 0);
         ptx::umma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int i) {
-        const uint32_t vb = v_base + (i % S) * L::kTileAlloc;
+      auto issue_pv = [&](int t, int g, bool first) {
+        const uint32_t vb = v_base + (g % S) * L::kTileAlloc;
         const uint32_t pt = tmem_base + 128 * t + 64;
 #pragma unroll
         for (int k = 0; k < kAttnBN / 16; ++k)
@@ -243,39 +301,49 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
           // MN-major: LBO = next 16-column chunk, SBO = next 8 kv rows)
           ptx::umma_bf16_ts(tmem_base + 256 + 128 * t, pt + 8 * k,
                             ptx::desc_mnmajor_sw32(vb + k * 16 * 32, kAttnBN * 32, 256),
-                            idesc_o, (i | k) != 0);
+                            idesc_o, !(first && k == 0));
       };
 
-      ptx::mbar_wait(&k_full[0], 0);
-      ptx::tc_fence_after();
+      int g = 0;
+      int sgi = 0;
+      for (; sgi < nseg; ++sgi) {
+        const int4 sg4 = segs[sgi];
+        const Seg sg{sg4.x, sg4.y, sg4.z};
+        ptx::mbar_wait(q_full, sgi & 1);
+        if (g < 256) attn_trace(prm, 4096 + 8 * g + 6);
+        ptx::mbar_wait(&k_full[g % S], (g / S) & 1);
+        ptx::tc_fence_after();
 #pragma unroll
-      for (int t = 0; t < NT; ++t) issue_s(t, 0);
-      ptx::umma_commit(&k_empty[0]);
-      for (int i = 0; i < nblk; ++i) {
-        const int s = i % S;
-        const bool more = i + 1 < nblk;
-        attn_trace(prm, 4096 + 8 * i + 0);
-        ptx::mbar_wait(&v_full[s], (i / S) & 1);
-        attn_trace(prm, 4096 + 8 * i + 1);
+        for (int t = 0; t < NT; ++t) issue_s(t, g);
+        ptx::umma_commit(&k_empty[g % S]);
+        if (sg.n == 1) ptx::umma_commit(q_empty);
+        for (int i = 0; i < sg.n; ++i, ++g) {
+          const int s = g % S;
+          const bool more = i + 1 < sg.n;
+          if (g < 256) attn_trace(prm, 4096 + 8 * g + 0);
+          ptx::mbar_wait(&v_full[s], (g / S) & 1);
+          if (g < 256) attn_trace(prm, 4096 + 8 * g + 1);
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          ptx::mbar_wait(&p_full[t], i & 1);
-          attn_trace(prm, 4096 + 8 * i + 2 + 2 * t);
-          ptx::tc_fence_after();
-          issue_pv(t, i);
-          if (more) {
-            if (t == 0) {
-              ptx::mbar_wait(&k_full[(i + 1) % S], ((i + 1) / S) & 1);
-              ptx::tc_fence_after();
+          for (int t = 0; t < NT; ++t) {
+            ptx::mbar_wait(&p_full[t], g & 1);
+            if (g < 256) attn_trace(prm, 4096 + 8 * g + 2 + 2 * t);
+            ptx::tc_fence_after();
+            issue_pv(t, g, i == 0);
+            if (more) {
+              if (t == 0) {
+                ptx::mbar_wait(&k_full[(g + 1) % S], ((g + 1) / S) & 1);
+                ptx::tc_fence_after();
+              }
+              issue_s(t, g + 1);
+              if (g < 256) attn_trace(prm, 4096 + 8 * g + 3 + 2 * t);
+            } else {
+              ptx::umma_commit(&o_done[t]);
             }
-            issue_s(t, i + 1);
-            attn_trace(prm, 4096 + 8 * i + 3 + 2 * t);
-          } else {
-            ptx::umma_commit(&o_done[t]);
           }
+          ptx::umma_commit(&v_empty[s]);
+          if (more) ptx::umma_commit(&k_empty[(g + 1) % S]);
+          if (i + 2 == sg.n) ptx::umma_commit(q_empty);  // last S of the segment issued
         }
-        ptx::umma_commit(&v_empty[s]);
-        if (more) ptx::umma_commit(&k_empty[(i + 1) % S]);
       }
     }
   } else {
@@ -289,18 +357,27 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     const uint32_t tmem_p = tmem_s + 64;
     const uint32_t tmem_o = tmem_base + 256 + 128 * t + lane_off;
     const float sc = prm.scale_log2;
-    float m_ref = -INFINITY;  // running (lazy) max, scaled log2 domain
-    float l_sum = 0.f;
     // Warpgroup 0 takes the first exp turn.
     constexpr bool pp = NT == 2 && kPingPong;
     if (pp && t == 1) ptx::named_bar_arrive(1, 256);
-    for (int i = 0; i < nblk; ++i) {
-      const int kv0 = (blk_begin + i) * kAttnBN;
+    int g = 0;
+    int sgi = 0;
+    // fused merge: this warp's head-partial flag is released one block after
+    // its stores were issued, so the release does not stall on their acks
+    int* pending_flag = nullptr;
+    for (; sgi < nseg; ++sgi) {
+    const int4 sg4 = segs[sgi];
+    const Seg sg{sg4.x, sg4.y, sg4.z};
+    float m_ref = -INFINITY;  // running (lazy) max, scaled log2 domain
+    float l_sum = 0.f;
+    for (int i = 0; i < sg.n; ++i, ++g) {
+      const int kv0 = (sg.b0 + i) * kAttnBN;
       // S_{t,i} complete; so is PV_{t,i-1} (issued before it), hence O_t is
       // stable until P_{t,i} is published.
-      attn_trace(prm, 2048 * t + 8 * i + 0);
-      ptx::mbar_wait(&s_full[t], i & 1);
-      attn_trace(prm, 2048 * t + 8 * i + 1);
+      const bool tr = g < 256;
+      if (tr) attn_trace(prm, 2048 * t + 8 * g + 0);
+      ptx::mbar_wait(&s_full[t], g & 1);
+      if (tr) attn_trace(prm, 2048 * t + 8 * g + 1);
       ptx::tc_fence_after();
       uint32_t sr[kAttnBN];
 #pragma unroll
@@ -331,9 +408,9 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       // Optional ping-pong of the exp-heavy section between the two softmax
       // warpgroups (named barriers 1/2). Off by default: letting both
       // warpgroups exponentiate concurrently measured 4 % faster at dh 72.
-      attn_trace(prm, 2048 * t + 8 * i + 2);
+      if (tr) attn_trace(prm, 2048 * t + 8 * g + 2);
       if (pp) ptx::named_bar_sync(1 + t, 256);
-      attn_trace(prm, 2048 * t + 8 * i + 3);
+      if (tr) attn_trace(prm, 2048 * t + 8 * g + 3);
       if (i > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
@@ -376,7 +453,12 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[t]);
-      attn_trace(prm, 2048 * t + 8 * i + 4);
+      if (pending_flag) {
+        __syncwarp();
+        if (lane == 0) ptx::st_release_gpu(pending_flag, 1);
+        pending_flag = nullptr;
+      }
+      if (tr) attn_trace(prm, 2048 * t + 8 * g + 4);
       // Row sum off the critical path (the PV MMA is already running).
       float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
@@ -389,17 +471,18 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
       a0 = ptx::fadd2(ptx::fadd2(a0, a1), ptx::fadd2(a2, a3));
       l_sum = l_sum * alpha + (a0.x + a0.y);
       m_ref = m_new;
-      attn_trace(prm, 2048 * t + 8 * i + 5);
+      if (tr) attn_trace(prm, 2048 * t + 8 * g + 5);
     }
-    // Balance the ping-pong: warpgroup 0 consumes warpgroup 1's last hand-off.
-    if (pp && t == 0) ptx::named_bar_sync(1, 256);
 
-    // Epilogue: wait for the last PV, read O, normalise, store.
-    ptx::mbar_wait(&o_done[t], 0);
+    // Segment epilogue: wait for the last PV, read O, normalise, store.
+    ptx::mbar_wait(&o_done[t], sgi & 1);
+    if (g - 1 < 256) attn_trace(prm, 2048 * t + 8 * (g - 1) + 6);
     ptx::tc_fence_after();
+    const int head = sg.x / prm.nq;
+    const int qt = sg.x - head * prm.nq;
     const int lrow = qt * (NT * kAttnBM) + t * kAttnBM + trow;  // row within the launch
     const bool row_ok = lrow < prm.rows;
-    if (prm.kv_splits == 1) {
+    if (sg.n == B) {
       const float inv_l = 1.0f / l_sum;
       __nv_bfloat16* orow =
           prm.out + size_t(prm.row0 + lrow) * prm.hs + size_t(head) * prm.dh;
@@ -432,68 +515,196 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
           }
         }
       }
-    } else {
-      const size_t prow = (size_t(split) * prm.heads + head) * prm.rows_pad + lrow;
-      float* po = prm.part_o + prow * DHP;
-#pragma unroll
-      for (int c = 0; c < kChunks; ++c) {
-        uint32_t r[16];
-        ptx::tmem_ld16(tmem_o + 16 * c, r);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 16; e += 4)
-          *reinterpret_cast<float4*>(po + 16 * c + e) =
-              make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
-                          __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+    } else if (rev && sg.b0 > 0) {
+      // fused merge: tail of a cut item + its head, published by the same
+      // warp of CTA c-1 (per-warp flag; this warp consumes and clears it)
+      const int c = int(blockIdx.x);
+      const int wflag = (c - 1) * kAttnFlagsPerCta + (warp - 4);
+      if (lane == 0) {
+        while (ptx::ld_acquire_gpu(prm.flags + wflag) == 0) __nanosleep(32);
+        prm.flags[wflag] = 0;  // the next launch is stream-ordered after this one
       }
-      prm.part_ml[prow * 2 + 0] = m_ref;
-      prm.part_ml[prow * 2 + 1] = l_sum;
+      __syncwarp();
+      const int prow = t * kAttnBM + trow;
+      const size_t sbase = size_t(2 * (c - 1) + 1);
+      const float m2 = prm.part_ml[(sbase * 2 + 0) * (NT * kAttnBM) + prow];
+      const float l2 = prm.part_ml[(sbase * 2 + 1) * (NT * kAttnBM) + prow];
+      const float mm = fmaxf(m_ref, m2);
+      const float w1 = ptx::ex2_approx(m_ref - mm), w2 = ptx::ex2_approx(m2 - mm);
+      const float inv_l = 1.0f / (w1 * l_sum + w2 * l2);
+      const float a1 = w1 * inv_l, a2 = w2 * inv_l;
+      const float* po = prm.part_o + sbase * DHP * (NT * kAttnBM) + prow;
+      __nv_bfloat16* orow =
+          prm.out + size_t(prm.row0 + lrow) * prm.hs + size_t(head) * prm.dh;
+#pragma unroll
+      for (int c2 = 0; c2 < kChunks; ++c2) {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem_o + 16 * c2, r);
+        float pv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pv[j] = po[size_t(16 * c2 + j) * (NT * kAttnBM)];
+        ptx::tmem_wait_ld();
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = a1 * __uint_as_float(r[j]) + a2 * pv[j];
+        if (row_ok) {
+          if ((prm.dh % 8 == 0) && (prm.hs % 8 == 0)) {
+#pragma unroll
+            for (int e = 0; e < 16; e += 8) {
+              const int d = 16 * c2 + e;
+              if (d < prm.dh) {
+                uint4 v;
+                v.x = ptx::pack_bf16x2(o[e], o[e + 1]);
+                v.y = ptx::pack_bf16x2(o[e + 2], o[e + 3]);
+                v.z = ptx::pack_bf16x2(o[e + 4], o[e + 5]);
+                v.w = ptx::pack_bf16x2(o[e + 6], o[e + 7]);
+                *reinterpret_cast<uint4*>(orow + d) = v;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int d = 16 * c2 + e;
+              if (d < prm.dh) orow[d] = __float2bfloat16_rn(o[e]);
+            }
+          }
+        }
+      }
+    } else {
+      // cut item: partial into slot 2c (first segment) or 2c + 1 (last; the
+      // head of a cut item in fused mode). Column-major [slot][d][row]: each
+      // warp store is one contiguous 128-byte line.
+      const int slot = 2 * int(blockIdx.x) + (sgi == 0 && !rev ? 0 : 1);
+      const int prow = t * kAttnBM + trow;
+      float* po = prm.part_o + size_t(slot) * DHP * (NT * kAttnBM) + prow;
+      const int ep = 12288 + 64 * t + 8 * (sgi & 7);  // debug probes (CTA 0)
+      uint32_t r[kChunks][16];
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) ptx::tmem_ld16(tmem_o + 16 * c, r[c]);
+      ptx::tmem_wait_ld();
+      attn_trace(prm, ep + 0);
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) po[size_t(16 * c + e) * (NT * kAttnBM)] = __uint_as_float(r[c][e]);
+      attn_trace(prm, ep + 1);
+      prm.part_ml[(size_t(slot) * 2 + 0) * (NT * kAttnBM) + prow] = m_ref;
+      prm.part_ml[(size_t(slot) * 2 + 1) * (NT * kAttnBM) + prow] = l_sum;
+      // publish this warp's rows of the head partial to CTA c+1
+      if (rev) pending_flag = prm.flags + int(blockIdx.x) * kAttnFlagsPerCta + (warp - 4);
     }
+    // O_t is read: the next segment's first PV (after its P_{t,0}) may overwrite it
+    if (g - 1 < 256) attn_trace(prm, 2048 * t + 8 * (g - 1) + 7);
+    }
+    if (pending_flag) {
+      __syncwarp();
+      if (lane == 0) ptx::st_release_gpu(pending_flag, 1);
+    }
+    // Balance the ping-pong: warpgroup 0 consumes warpgroup 1's last hand-off.
+    if (pp && t == 0) ptx::named_bar_sync(1, 256);
   }
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (cta_trace) prm.trace[8192 + 4 * blockIdx.x + 2] = ptx::globaltimer();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem_base);
   }
 }
 
-// Merge kv splits in ascending split order (deterministic).
-// One thread per (query row, head, 16-column chunk).
-template <int DHP>
-__global__ void attn_combine_kernel(AttnParams prm) {
-  // prm.rows_pad rows per (split, head) block of the partial buffers
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int chunks = DHP / 16;
-  const int total = prm.rows * prm.heads * chunks;
-  if (idx >= total) return;
-  const int c = idx % chunks;
-  const int head = (idx / chunks) % prm.heads;
-  const int r = idx / (chunks * prm.heads);
-  float m = -INFINITY;
-  for (int sp = 0; sp < prm.kv_splits; ++sp) {
-    const size_t prow = (size_t(sp) * prm.heads + head) * prm.rows_pad + r;
-    m = fmaxf(m, prm.part_ml[prow * 2]);
+// Merge the partials of every cut item in CTA order (deterministic).
+// blockIdx.x + 1 = interior range boundary c; the first boundary inside an
+// item merges it, over CTAs c-1 .. (last CTA whose range meets the item).
+// blockIdx.y = 256-element slice of the item's (row, 16-column chunk)
+// elements; each thread issues all its partials' loads before reducing (the
+// merge is L2-latency bound, not bandwidth bound).
+constexpr int kAttnMaxParts = 8;  // attn_grid keeps every item within 8 CTAs
+
+template <int DHP, int NT>
+__global__ void __launch_bounds__(256)
+    attn_streamk_combine_kernel(AttnParams prm) {
+  __shared__ int s_slot[kAttnMaxParts];
+  __shared__ int s_np;
+  ptx::pdl_wait();
+  ptx::pdl_launch();
+  const int c = int(blockIdx.x) + 1;
+  const long long B = prm.blocks;
+  const long long s = attn_unit_start(prm, c);
+  if (s % B == 0) return;  // boundary on an item edge
+  const int x = int(s / B);
+  const long long x0 = (long long)x * B, x1 = x0 + B;
+  if (attn_unit_start(prm, c - 1) > x0) return;  // an earlier boundary merges this item
+  if (threadIdx.x == 0) {
+    int np = 0;
+    for (int k = c - 1; k < prm.grid && np < kAttnMaxParts; ++k) {
+      const long long st = attn_unit_start(prm, k);
+      if (st >= x1) break;
+      s_slot[np++] = 2 * k + (st >= x0 ? 0 : 1);
+    }
+    s_np = np;
   }
+  __syncthreads();
+  const int np = s_np;
+  constexpr int kChunks = DHP / 16;
+  const int e = int(blockIdx.y) * 256 + int(threadIdx.x);
+  if (e >= NT * kAttnBM * kChunks) return;
+  const int r = e % (NT * kAttnBM);  // row within the item (consecutive threads: rows)
+  const int cc = e / (NT * kAttnBM);
+  const int head = x / prm.nq;
+  const int qt = x - head * prm.nq;
+  const int lrow = qt * (NT * kAttnBM) + r;
+  if (lrow >= prm.rows) return;
+  constexpr int R = NT * kAttnBM;
+  float2 ml[kAttnMaxParts];
+#pragma unroll
+  for (int p = 0; p < kAttnMaxParts; ++p)
+    if (p < np)
+      ml[p] = make_float2(prm.part_ml[(size_t(s_slot[p]) * 2 + 0) * R + r],
+                          prm.part_ml[(size_t(s_slot[p]) * 2 + 1) * R + r]);
+  float m = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < kAttnMaxParts; ++p)
+    if (p < np) m = fmaxf(m, ml[p].x);
   float acc[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
   float l = 0.f;
-  for (int sp = 0; sp < prm.kv_splits; ++sp) {
-    const size_t prow = (size_t(sp) * prm.heads + head) * prm.rows_pad + r;
-    const float w = ptx::ex2_approx(prm.part_ml[prow * 2] - m);
-    l += w * prm.part_ml[prow * 2 + 1];
-    const float* po = prm.part_o + prow * DHP + 16 * c;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] += w * po[e];
+  for (int p = 0; p < kAttnMaxParts; ++p) {
+    if (p < np) {
+      const float w = ptx::ex2_approx(ml[p].x - m);
+      l += w * ml[p].y;
+      const float* po = prm.part_o + (size_t(s_slot[p]) * DHP + 16 * cc) * R + r;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = po[size_t(j) * R];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] += w * v[j];
+    }
   }
   const float inv_l = 1.0f / l;
-  __nv_bfloat16* orow = prm.out + size_t(prm.row0 + r) * prm.hs + size_t(head) * prm.dh;
+  __nv_bfloat16* orow = prm.out + size_t(prm.row0 + lrow) * prm.hs + size_t(head) * prm.dh;
+  const bool vec = (prm.dh % 8 == 0) && (prm.hs % 8 == 0);
+  if (vec) {
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const int d = 16 * c + e;
-    if (d < prm.dh) orow[d] = __float2bfloat16_rn(acc[e] * inv_l);
+    for (int j = 0; j < 16; j += 8) {
+      const int d = 16 * cc + j;
+      if (d < prm.dh) {
+        uint4 v;
+        v.x = ptx::pack_bf16x2(acc[j] * inv_l, acc[j + 1] * inv_l);
+        v.y = ptx::pack_bf16x2(acc[j + 2] * inv_l, acc[j + 3] * inv_l);
+        v.z = ptx::pack_bf16x2(acc[j + 4] * inv_l, acc[j + 5] * inv_l);
+        v.w = ptx::pack_bf16x2(acc[j + 6] * inv_l, acc[j + 7] * inv_l);
+        *reinterpret_cast<uint4*>(orow + d) = v;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int d = 16 * cc + j;
+      if (d < prm.dh) orow[d] = __float2bfloat16_rn(acc[j] * inv_l);
+    }
   }
 }
 

@@ -55,18 +55,21 @@ extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
 }
 
 namespace {
-unsigned long long* g_attn_trace = nullptr;  // device buffer, 8192 slots
+// device buffer: 8192 clock64 slots of CTA 0, then 4 per CTA (globaltimer at
+// entry / after griddepcontrol.wait / exit, SM id) for up to 1024 CTAs
+constexpr int kTraceSlots = 8192 + 4 * 1024 + 1024;  // + epilogue probes of CTA 0
+unsigned long long* g_attn_trace = nullptr;
 }
 
 // Debug-only: record the clock64 timeline of CTA (0,0,0) of the next
 // pf_debug_attention launches into `host` (8192 slots) when enabled.
 extern "C" int pf_debug_attention_trace(int enable, unsigned long long* host) {
   if (enable && !g_attn_trace) {
-    cudaMalloc(reinterpret_cast<void**>(&g_attn_trace), 8192 * 8);
-    cudaMemset(g_attn_trace, 0, 8192 * 8);
+    cudaMalloc(reinterpret_cast<void**>(&g_attn_trace), kTraceSlots * 8);
+    cudaMemset(g_attn_trace, 0, kTraceSlots * 8);
   }
   if (host && g_attn_trace)
-    cudaMemcpy(host, g_attn_trace, 8192 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(host, g_attn_trace, kTraceSlots * 8, cudaMemcpyDeviceToHost);
   if (!enable && g_attn_trace) {
     cudaFree(g_attn_trace);
     g_attn_trace = nullptr;
@@ -84,6 +87,7 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
   const int dhp = (dh + 15) / 16 * 16;
   pf::bf16 *qp = nullptr, *kp = nullptr, *vp = nullptr;
   float* work = nullptr;
+  int* flags = nullptr;
   const size_t n = size_t(heads) * P * dhp;
   cudaMallocAsync(reinterpret_cast<void**>(&qp), n * 2, s);
   cudaMallocAsync(reinterpret_cast<void**>(&kp), n * 2, s);
@@ -113,12 +117,12 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
     pf::AttnLaunch a{dhp, P, rows, row0, heads, dh, hs, float(1.0 / std::sqrt(double(dh))),
                      static_cast<pf::bf16*>(out), nullptr, 0, g_attn_trace};
     const int sms = pf::device_sm_count(dev);
-    const int splits = pf::attn_splits(a, sms);
-    if (splits > 1) {
-      a.work_floats = pf::attn_work_floats(dhp, heads, rows, splits);
-      cudaMallocAsync(reinterpret_cast<void**>(&work), a.work_floats * 4, s);
-      a.work = work;
-    }
+    a.work_floats = pf::attn_work_floats(dhp, sms);
+    cudaMallocAsync(reinterpret_cast<void**>(&work), a.work_floats * 4, s);
+    a.work = work;
+    cudaMallocAsync(reinterpret_cast<void**>(&flags), size_t(sms) * pf::kAttnFlagsPerCta * sizeof(int), s);
+    cudaMemsetAsync(flags, 0, size_t(sms) * pf::kAttnFlagsPerCta * sizeof(int), s);
+    a.flags = flags;
     err = int(pf::attention(tq, tk, tv, a, sms, s));
   }
   cudaStreamSynchronize(s);
@@ -126,6 +130,7 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
   cudaFreeAsync(kp, s);
   cudaFreeAsync(vp, s);
   if (work) cudaFreeAsync(work, s);
+  if (flags) cudaFreeAsync(flags, s);
   cudaStreamSynchronize(s);
   if (!err) err = int(cudaGetLastError());
   return err;

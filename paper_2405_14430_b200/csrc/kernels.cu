@@ -774,23 +774,31 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
 }
 
 // ============================================================== attention
-int attn_splits(const AttnLaunch& a, int sm_count) {
-  const int rows_per_cta = attn_tiles_per_cta(a.dhp) * kAttnBM;
-  const int ctas = ((a.rows + rows_per_cta - 1) / rows_per_cta) * a.heads;
-  const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
-  if (ctas >= sm_count || blocks < 2) return 1;
-  int splits = (sm_count + ctas - 1) / ctas;
-  if (splits > blocks) splits = blocks;
-  if (splits > 16) splits = 16;
-  const int per = (blocks + splits - 1) / splits;
-  return (blocks + per - 1) / per;
+// Persistent CTAs of the stream-K attention schedule (attn_sm100.cuh): one
+// per SM, or fewer so that every CTA owns at least two kv blocks.
+// PF_ATTN_ONE_ITEM_PER_CTA=1 restores one CTA per item (no cut items).
+int attn_grid(const AttnLaunch& a, int sm_count) {
+  static const bool per_item = [] {
+    const char* e = std::getenv("PF_ATTN_ONE_ITEM_PER_CTA");
+    return e && e[0] == '1';
+  }();
+  const int rows_per_item = attn_tiles_per_cta(a.dhp) * kAttnBM;
+  const long long items = (long long)((a.rows + rows_per_item - 1) / rows_per_item) * a.heads;
+  const long long units = items * ((a.P + kAttnBN - 1) / kAttnBN);
+  if (per_item) return int(items);
+  const long long blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  long long g = sm_count;
+  if (units < 2 * g) g = std::max(1LL, units / 2);
+  // every item meets at most kAttnMaxParts CTAs: range >= blocks / (parts - 2)
+  g = std::min(g, std::max(1LL, units * (kAttnMaxParts - 2) / blocks));
+  // at most kAttnMaxSegs segments per CTA: range <= (segs - 3) items; beyond
+  // that many items, one CTA per item
+  if (items > g * (kAttnMaxSegs - 3)) return int(items);
+  return int(g);
 }
 
-size_t attn_work_floats(int dhp, int heads, int rows, int splits) {
-  if (splits <= 1) return 0;
-  const int rows_per_cta = attn_tiles_per_cta(dhp) * kAttnBM;
-  const size_t rows_pad = size_t((rows + rows_per_cta - 1) / rows_per_cta) * rows_per_cta;
-  return size_t(splits) * heads * rows_pad * (dhp + 2);
+size_t attn_work_floats(int dhp, int sm_count) {
+  return size_t(2) * sm_count * attn_tiles_per_cta(dhp) * kAttnBM * (dhp + 2);
 }
 
 namespace {
@@ -800,9 +808,6 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
                         cudaStream_t stream) {
   constexpr int NT = attn_tiles_per_cta(DHP);
   using L = AttnSmem<DHP, NT>;
-  const int q_ctas = (a.rows + NT * kAttnBM - 1) / (NT * kAttnBM);
-  const int blocks = (a.P + kAttnBN - 1) / kAttnBN;
-  const int splits = attn_splits(a, sm_count);
   AttnParams prm;
   prm.P = a.P;
   prm.q_stride = a.q_stride > 0 ? a.q_stride : a.P;
@@ -814,37 +819,43 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   prm.dh = a.dh;
   prm.hs = a.hs;
   prm.scale_log2 = a.scale * 1.4426950408889634f;
-  prm.kv_splits = splits;
-  prm.blocks_per_split = (blocks + splits - 1) / splits;
+  prm.nq = (a.rows + NT * kAttnBM - 1) / (NT * kAttnBM);
+  prm.blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  prm.units = (long long)prm.nq * a.heads * prm.blocks;
+  prm.grid = attn_grid(a, sm_count);
   prm.out = a.out;
-  prm.rows_pad = q_ctas * NT * kAttnBM;
   prm.part_o = nullptr;
   prm.part_ml = nullptr;
   prm.trace = a.trace;
-
-  if (splits > 1) {
-    const size_t need = attn_work_floats(DHP, a.heads, a.rows, splits);
-    if (!a.work || a.work_floats < need) return cudaErrorInvalidValue;
+  const bool cut = prm.units % prm.grid != 0 || (prm.units / prm.grid) % prm.blocks != 0;
+  static const bool no_fuse = [] {
+    const char* e = std::getenv("PF_ATTN_SEPARATE_MERGE");
+    return e && e[0] == '1';
+  }();
+  prm.flags = a.flags;
+  prm.fused = (cut && prm.grid >= 2 && a.flags && !no_fuse &&
+               prm.units / prm.grid >= prm.blocks) ? 1 : 0;
+  if (cut) {
+    const size_t slots = size_t(2) * prm.grid * NT * kAttnBM;
+    if (!a.work || a.work_floats < slots * (DHP + 2)) return cudaErrorInvalidValue;
     prm.part_o = a.work;
-    prm.part_ml = a.work + size_t(splits) * a.heads * prm.rows_pad * DHP;
+    prm.part_ml = a.work + slots * DHP;
   }
-  dim3 grid(q_ctas, a.heads, splits);
   auto go = [&](auto kern) {
     cudaError_t e2 = ensure_smem_attr<decltype(kern)::value>(L::kTotal);
     if (e2 != cudaSuccess) return e2;
-    return launch_pdl(decltype(kern)::value, grid, dim3(L::kThreads), L::kTotal, stream, q, k,
-                      v, a.k2 ? *a.k2 : k, a.v2 ? *a.v2 : v, prm);
+    return launch_pdl(decltype(kern)::value, dim3(prm.grid), dim3(L::kThreads), L::kTotal,
+                      stream, q, k, v, a.k2 ? *a.k2 : k, a.v2 ? *a.v2 : v, prm);
   };
   // Two softmax warpgroups exponentiate concurrently (no ping-pong) with 2 of
   // every 8 four-column groups on the FMA-pipe exp2: measured best of the
   // ping-pong / poly-ratio / f16x2-exp variants at C2 (119 vs 123.5 us).
   cudaError_t e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT>),
                                             &attn_fwd_kernel<DHP, NT>>{});
-  if (e != cudaSuccess || splits == 1) return e;
-  const int total = a.rows * a.heads * (DHP / 16);
-  ++launch_counter();
-  attn_combine_kernel<DHP><<<(total + 255) / 256, 256, 0, stream>>>(prm);
-  return cudaGetLastError();
+  if (e != cudaSuccess || !cut || prm.grid < 2 || prm.fused) return e;
+  const unsigned slices = unsigned((NT * kAttnBM * (DHP / 16) + 255) / 256);
+  return launch_pdl(attn_streamk_combine_kernel<DHP, NT>, dim3(prm.grid - 1, slices), dim3(256),
+                    0, stream, prm);
 }
 }  // namespace
 

@@ -128,6 +128,9 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                  cudaStream_t stream);
 
 // Attention of query rows [row0, row0+rows) against all P kv rows.
+// stream-K attention: one merge flag per softmax warp of each CTA
+constexpr int kAttnFlagsPerCta = 8;
+
 struct AttnLaunch {
   // P: kv rows per head (buffer height); Q rows per head = q_stride (0 -> P)
   int dhp, P, rows, row0, heads, dh, hs;
@@ -142,9 +145,13 @@ struct AttnLaunch {
   int fresh_lo = 0, fresh_hi = 0;
   const CUtensorMap* k2 = nullptr;
   const CUtensorMap* v2 = nullptr;
+  // [sm_count * kAttnFlagsPerCta] zero-initialised flags for the in-kernel merge of cut items
+  // (left zero after every launch); null -> merge in a separate kernel
+  int* flags = nullptr;
 };
-int attn_splits(const AttnLaunch& a, int sm_count);
-size_t attn_work_floats(int dhp, int heads, int rows, int splits);
+int attn_grid(const AttnLaunch& a, int sm_count);
+// partial-result workspace the attention needs on a device with sm_count SMs
+size_t attn_work_floats(int dhp, int sm_count);
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
                       const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                       cudaStream_t stream);

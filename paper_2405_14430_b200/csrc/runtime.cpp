@@ -225,22 +225,11 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
   s.splitk_ws = dalloc<float>(s.splitk_ws_floats);
   s.splitk_counter_cap = 4096;
   s.splitk_counters = dalloc<int>(size_t(s.splitk_counter_cap));
-  // Split-KV workspace sized for the worst case (a single 128-row q tile).
-  {
-    AttnLaunch probe{int(dhp), int(P), 128, 0, int(heads), m.dh, int(hs), 1.f,
-                     nullptr, nullptr, 0};
-    const int splits = attn_splits(probe, s.sm_count);
-    size_t need = 0;
-    // any rows >= 128 use fewer splits per tile; bound by splits * tiles
-    for (int rows = 128; rows <= int(P) + 127; rows += 128) {
-      probe.rows = rows;
-      need = std::max(need, attn_work_floats(int(dhp), int(heads), rows,
-                                             attn_splits(probe, s.sm_count)));
-    }
-    (void)splits;
-    s.attn_work_floats = need;
-    s.attn_work = need ? dalloc<float>(need) : nullptr;
-  }
+  // stream-K attention partials (at most two cut segments per CTA)
+  s.attn_work_floats = attn_work_floats(int(dhp), s.sm_count);
+  s.attn_work = dalloc<float>(s.attn_work_floats);
+  s.attn_flags = dalloc<int>(size_t(s.sm_count) * kAttnFlagsPerCta);
+  PF_CUDA_CHECK(cudaMemset(s.attn_flags, 0, size_t(s.sm_count) * kAttnFlagsPerCta * sizeof(int)));
   s.tm_hb = tmap(s.hb, hs, P, hs * 2, 64, 128, 128);
   if (!encode_tmap_f32_2d(&s.tm_h32, s.h32, hs, P, hs * 4, 32, 128, 128))
     throw CudaError("cuTensorMapEncodeTiled failed for the residual stream");
@@ -378,7 +367,7 @@ void Engine::free_stage(Stage& s) {
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
-  dfree(s.attn_work); dfree(s.flag); dfree(s.splitk_ws); dfree(s.splitk_counters);
+  dfree(s.attn_work); dfree(s.attn_flags); dfree(s.flag); dfree(s.splitk_ws); dfree(s.splitk_counters);
   dfree(s.zeros); dfree(s.text); dfree(s.x); dfree(s.cb);
   if (s.eps_owned) dfree(s.eps);
   for (cudaEvent_t e : s.ev_eps) cudaEventDestroy(e);
@@ -474,6 +463,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   AttnLaunch a{m.dhp, int(m.P), rows, row0, m.heads, m.dh, m.hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
+  a.flags = s.attn_flags;
   if (kv) {
     a.k2 = kv->tm_k2;
     a.v2 = kv->tm_v2;
@@ -1026,6 +1016,7 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
   AttnLaunch a{m.dhp, Pt, rows, row0, m.heads, m.dh, hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
+  a.flags = s.attn_flags;
   prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (joint)");
   prof_end(s);
@@ -1099,6 +1090,7 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
   AttnLaunch a{m.dhp, Pt, rows, row0, m.heads, m.dh, hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
+  a.flags = s.attn_flags;
   prof_begin(s, kAttention, 4 * r * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (single)");
   prof_end(s);
@@ -1888,6 +1880,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   AttnLaunch a{m.dhp, int(m.P), rows, row0, m.heads, m.dh, hs,
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
+  a.flags = s.attn_flags;
   prof_begin(s, kAttention, 4 * r * P * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
   prof_end(s);
@@ -1924,6 +1917,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   AttnLaunch ca{m.dhp, m.T, rows, row0, m.heads, m.dh, hs,
                 float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                 s.attn_work_floats};
+  ca.flags = s.attn_flags;
   ca.q_stride = int(m.P);
   prof_begin(s, kCrossAttention, 4 * r * T * dhs, 0);
   check(attention(s.tm_q, L.tm_kc, L.tm_vc, ca, s.sm_count, s.stream), "cross attention");

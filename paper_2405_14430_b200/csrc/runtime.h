@@ -140,6 +140,7 @@ struct Stage {
   bf16* z = nullptr;      // [P x mlp]
   float* attn_work = nullptr;
   size_t attn_work_floats = 0;
+  int* attn_flags = nullptr;  // [sm_count] stream-K merge flags (zero between launches)
   int* flag = nullptr;    // first non-finite (ordinal), INT_MAX if none
   float* splitk_ws = nullptr;    // split-K partial tiles (skinny GEMMs)
   size_t splitk_ws_floats = 0;

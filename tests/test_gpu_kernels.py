@@ -89,6 +89,9 @@ def _attn_ref(q, k, v, heads, rows, row0):
     (4096, 16, 1152, 512, 1024, 3.0),  # PixArt patch, dh = 72, split-KV
     (4096, 16, 1152, 4096, 0, 3.0),    # PixArt full sequence
     (520, 2, 256, 136, 384, 2.0),   # ragged P / rows, dh = 128
+    (6144, 24, 1536, 6144, 0, 2.0),  # stream-K, in-kernel merge, dh = 64
+    (5000, 16, 1152, 4600, 200, 2.0),  # stream-K in-kernel merge, ragged P and rows
+    (3000, 12, 768, 3000, 0, 2.0),  # stream-K, separate merge kernel
 ])
 def test_attention_matches_fp32(P, heads, hs, rows, row0, scale):
     g = torch.Generator(device="cuda").manual_seed(P + hs + rows)
@@ -100,3 +103,17 @@ def test_attention_matches_fp32(P, heads, hs, rows, row0, scale):
     assert err < 2e-2, err
     rel = ((out - ref).norm() / ref.norm()).item()
     assert rel < 1e-2, rel
+
+
+def test_stream_k_attention_reruns_bitwise():
+    # the in-kernel merge flags must be left zero after every launch: reruns
+    # of a full-size (fused-merge) configuration are bitwise identical
+    import numpy as np
+    import paper_2405_14430_b200 as pf
+    x0 = pf.make_initial_latent(0, 4096, 1152)
+    with pf.ToyDiTCuda(0, 2, 1152, 16, 4.0, 4096, 1) as m:
+        m.set_graphs(False)
+        outs = [m.run_pipefusion(x0, 3, 1, 1, 0.1).final_x for _ in range(3)]
+        m.set_graphs(True)
+        outs += [m.run_pipefusion(x0, 3, 1, 1, 0.1).final_x for _ in range(2)]
+    assert all(np.array_equal(o, outs[0]) for o in outs)

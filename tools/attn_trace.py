@@ -31,22 +31,44 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 print("debug_attention call (incl. repack) us:", e0.elapsed_time(e1) / 10 * 1e3)
-buf = (ctypes.c_ulonglong * 8192)()
+buf = (ctypes.c_ulonglong * (8192 + 4096 + 1024))()
 lib.pf_debug_attention_trace(1, None)
 run()
 torch.cuda.synchronize()
 lib.pf_debug_attention_trace(1, buf)
 lib.pf_debug_attention_trace(0, None)
-a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+allb = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+a = allb[:8192]
+cta = allb[8192:12288].reshape(1024, 4)
+cta = cta[cta[:, 0] > 0]
+if len(cta):
+    t0 = cta[:, 0].min()
+    ent, go, end = (cta[:, 0] - t0) / 1e3, (cta[:, 1] - t0) / 1e3, (cta[:, 2] - t0) / 1e3
+    dur = end - go
+    print(f"CTAs {len(cta)}: entry max {ent.max():.1f} us, after-wait max {go.max():.1f}, "
+          f"end min/median/max {end.min():.1f}/{np.median(end):.1f}/{end.max():.1f} us; "
+          f"duration min/median/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f}")
+    order = np.argsort(dur)
+    print("slowest CTAs (idx, sm, dur us):", [(int(i), int(cta[i, 3]), round(float(dur[i]), 1)) for i in order[-8:]])
+    print("fastest CTAs:", [(int(i), int(cta[i, 3]), round(float(dur[i]), 1)) for i in order[:8]])
 base = a[a > 0].min()
 t = np.where(a > 0, a - base, -1)
-nblk = (P + 127) // 128
-res = {"softmax0": t[0:8 * nblk].reshape(nblk, 8)[:, :6].tolist(),
-       "softmax1": t[2048:2048 + 8 * nblk].reshape(nblk, 8)[:, :6].tolist(),
-       "mma": t[4096:4096 + 8 * nblk].reshape(nblk, 8)[:, :6].tolist(),
-       "tma": t[6144:6144 + 8 * nblk].reshape(nblk, 8)[:, :3].tolist()}
+nblk = int(((t[0:2048].reshape(256, 8)[:, 1]) >= 0).sum())  # blocks CTA 0 processed
+res = {"softmax0": t[0:8 * nblk].reshape(nblk, 8).tolist(),
+       "softmax1": t[2048:2048 + 8 * nblk].reshape(nblk, 8).tolist(),
+       "mma": t[4096:4096 + 8 * nblk].reshape(nblk, 8).tolist(),
+       "tma": t[6144:6144 + 8 * nblk].reshape(nblk, 8)[:, :4].tolist()}
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/attn_trace.json").write_text(json.dumps(res))
-for i in range(min(nblk, 12)):
-    print(i, "sm0", res["softmax0"][i], "sm1", res["softmax1"][i], "mma", res["mma"][i][:6], "tma", res["tma"][i])
-print("last", res["softmax0"][-1], res["softmax1"][-1])
+s1 = [r[1] for r in res["softmax0"]]
+print("CTA 0 blocks:", nblk, "s_full-ready deltas (clk):", np.diff(s1).tolist())
+print("first/last", res["softmax0"][0], res["softmax0"][-1])
+
+for i in range(nblk):
+    if res["softmax0"][i][6] >= 0 or res["mma"][i][6] >= 0 or res["tma"][i][3] >= 0:
+        print("boundary/seg-start", i, "sm0", res["softmax0"][i], "sm1", res["softmax1"][i][6:],
+              "mma", res["mma"][i], "tma", res["tma"][i])
+
+ep = allb[12288:12288 + 128]
+epr = np.where(ep > 0, ep - base, -1).reshape(2, 8, 8)
+print("epilogue probes wg0:", epr[0][:3].tolist(), "wg1:", epr[1][:3].tolist())
