@@ -35,6 +35,9 @@ int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
  * host (8192 uint64, may be NULL) receives the current contents; enable=0
  * frees it. */
 int pf_debug_attention_trace(int enable, unsigned long long* host);
+// Per-CTA timeline (8 slots x 256 CTAs, globaltimer ns) of the 1-SM GEMM
+// kernel launches that follow; debug instrumentation, not part of the product.
+int pf_debug_gemm_trace(int enable, unsigned long long* host);
 
 #ifdef __cplusplus
 }

@@ -109,6 +109,10 @@ struct AttnParams {
   int* flags;          // [grid][kAttnFlagsPerCta] head partial published, per softmax
                        // warp (fused merge; cleared by the reading warp)
   int fused;           // merge cut items in-kernel (every range >= one item)
+  // L2 prefetch of the weights the next kernels stream (the CTAs split every
+  // region; issued by the otherwise idle warp 3 before the PDL wait)
+  const char* pf_ptr[kAttnPrefetchRegions];
+  unsigned long long pf_bytes[kAttnPrefetchRegions];
   // Debug timeline (clock64) of CTA (0,0,0); null in production. Slots:
   // [0, 4096) softmax t: 2048 t + 8 i + event; [4096, 6144) MMA: 8 i + event;
   // [6144, 8192) TMA: 8 i + event.
@@ -213,6 +217,19 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int nseg = *nseg_slot;
   const bool rev = prm.fused != 0;
+  if (warp == 3) {
+    for (int rgn = 0; rgn < kAttnPrefetchRegions; ++rgn) {
+      const unsigned long long bytes = prm.pf_bytes[rgn];
+      if (!bytes) continue;
+      const unsigned long long per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+      const unsigned long long beg = per * blockIdx.x;
+      const unsigned long long end = beg + per < bytes ? beg + per : bytes;
+      constexpr unsigned long long kChunk = 32768;
+      for (unsigned long long off = beg + lane * kChunk; off < end; off += 32 * kChunk)
+        ptx::prefetch_l2_bulk(prm.pf_ptr[rgn] + off,
+                              uint32_t(end - off < kChunk ? end - off : kChunk));
+    }
+  }
   const bool cta_trace = prm.trace && threadIdx.x == 0 && blockIdx.x < 1024;
   if (cta_trace) prm.trace[8192 + 4 * blockIdx.x] = ptx::globaltimer();
   ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete

@@ -54,6 +54,24 @@ extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
                       pf::device_sm_count(dev), static_cast<cudaStream_t>(stream)));
 }
 
+// Debug-only: record the per-CTA timeline of the next 1-SM GEMM launches into
+// a device buffer; `host` (2048 slots) receives it.
+extern "C" int pf_debug_gemm_trace(int enable, unsigned long long* host) {
+  static unsigned long long* buf = nullptr;
+  if (enable && !buf) {
+    cudaMalloc(reinterpret_cast<void**>(&buf), 2048 * 8);
+    cudaMemset(buf, 0, 2048 * 8);
+    pf::set_gemm_trace(buf);
+  }
+  if (host && buf) cudaMemcpy(host, buf, 2048 * 8, cudaMemcpyDeviceToHost);
+  if (!enable && buf) {
+    pf::set_gemm_trace(nullptr);
+    cudaFree(buf);
+    buf = nullptr;
+  }
+  return int(cudaGetLastError());
+}
+
 namespace {
 // device buffer: 8192 clock64 slots of CTA 0, then 4 per CTA (globaltimer at
 // entry / after griddepcontrol.wait / exit, SM id) for up to 1024 CTAs

@@ -23,6 +23,13 @@
 
 namespace pf {
 
+// Debug timeline of the 1-SM GEMM kernel (null in production): 8 slots per
+// CTA (blockIdx.x < 256): globaltimer at entry, after the PDL wait, first
+// stage landed (MMA issuer), last MMA issued, first accumulator ready
+// (epilogue), exit; SM id.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+
+
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;  // 64 bf16 = 128 B = one SW128 atom row
 
@@ -155,6 +162,7 @@ __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tma_a,
                         const __grid_constant__ CUtensorMap tma_b, int rows,
                         int row0, int N, int K, Epi epi, SplitK sk) {
+  const long long t_entry = clock64();
   using L = GemmSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -189,13 +197,42 @@ __global__ void __launch_bounds__(256, 1)
     }
     ptx::fence_barrier_init();
   }
+  const long long t_pre_alloc = clock64();
   if (warp == 2) ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  const long long t_post_alloc = clock64();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned long long* trc = g_gemm_trace && blockIdx.x < 128 ? g_gemm_trace + 16 * blockIdx.x
+                                                              : nullptr;
+  if (trc && threadIdx.x == 0) trc[7] = t_entry;
+  if (trc && threadIdx.x == 0) trc[0] = clock64();
+  if (trc && threadIdx.x == 64) {
+    trc[9] = t_pre_alloc;
+    trc[10] = t_post_alloc;
+  }
+  // The B operand is always a weight matrix (never written by a preceding
+  // kernel): the producer puts the first stages' B tiles in flight before the
+  // PDL wait, overlapping their latency with the predecessor's tail.
+  int preloaded = 0;
+  if (warp == 0 && lane == 0 && int(blockIdx.x) < num_units) {
+    const int split = int(blockIdx.x) % splits;
+    const int nt = (int(blockIdx.x) / splits) / m_tiles;
+    const int kb0 = split * kb_per;
+    preloaded = min(STAGES, min(kblocks, kb0 + kb_per) - kb0);
+    for (int j = 0; j < preloaded; ++j) {
+      ptx::mbar_arrive_expect_tx(&full[j], L::kStageBytes);
+      ptx::tma_load_2d(smem + j * L::kStageBytes + L::kABytes, &tma_b, &full[j],
+                       (kb0 + j) * kGemmBK, nt * BN);
+    }
+  }
   ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
   ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
+  if (trc && threadIdx.x == 0) {
+    trc[1] = clock64();
+    trc[6] = ptx::smid();
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -209,13 +246,19 @@ __global__ void __launch_bounds__(256, 1)
         const int kb0 = split * kb_per;
         const int kb1 = min(kblocks, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          ptx::mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-          ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK,
-                           row0 + mt * kGemmBM);
-          ptx::tma_load_2d(sb, &tma_b, &full[stage], kb * kGemmBK, nt * BN);
+          if (preloaded > 0) {  // B already in flight (first unit, first stages)
+            --preloaded;
+            if (trc && kb == kb0) trc[8] = clock64();
+            ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK, row0 + mt * kGemmBM);
+          } else {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+            ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK,
+                             row0 + mt * kGemmBM);
+            ptx::tma_load_2d(sb, &tma_b, &full[stage], kb * kGemmBK, nt * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -239,6 +282,7 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
+          if (trc && kb == kb0 && unit == int(blockIdx.x)) trc[2] = clock64();
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
           const uint32_t b_base = a_base + L::kABytes;
@@ -258,6 +302,7 @@ __global__ void __launch_bounds__(256, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+      if (trc) trc[3] = clock64();
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
@@ -392,6 +437,7 @@ __global__ void __launch_bounds__(256, 1)
       if constexpr (kNV > 0) stage_colvecs<BN>(epi, colbuf, nt * BN, N, tid);
       ++tile_count;
       ptx::mbar_wait(&tfull[acc], acc_phase);
+      if (trc && tid == 0 && tile_count == 1) trc[4] = clock64();
       ptx::tc_fence_after();
       if constexpr (Epi::kPreload) {
 #pragma unroll
@@ -421,6 +467,7 @@ __global__ void __launch_bounds__(256, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (trc && threadIdx.x == 0) trc[5] = clock64();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
@@ -775,6 +822,17 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // weights (B) in flight before the PDL wait (see gemm_bf16_tn_kernel)
+  int preloaded = 0;
+  if (warp == 0 && lane == 0 && int(blockIdx.x) < num_tiles) {
+    const int nt = int(blockIdx.x) / m_tiles;
+    preloaded = min(STAGES, kblocks);
+    for (int j = 0; j < preloaded; ++j) {
+      ptx::mbar_arrive_expect_tx(&full[j], L::kStageBytes);
+      ptx::tma_load_2d(smem + j * L::kStageBytes + L::kABytes, &tma_b, &full[j],
+                       j * kGemmBK, nt * BN);
+    }
+  }
   ptx::pdl_wait();    // predecessor's outputs (A operand, residual, K/V) complete
   ptx::pdl_launch();  // successor may start its prologue as our CTAs retire
 
@@ -786,12 +844,17 @@ __global__ void __launch_bounds__(256, 1)
         const int mt = tile % m_tiles;
         const int nt = tile / m_tiles;
         for (int kb = 0; kb < kblocks; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          ptx::mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-          ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK, row0 + mt * kGemmBM);
-          ptx::tma_load_2d(sb, &tma_b, &full[stage], kb * kGemmBK, nt * BN);
+          if (preloaded > 0) {
+            --preloaded;
+            ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK, row0 + mt * kGemmBM);
+          } else {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+            ptx::tma_load_2d(sa, &tma_a, &full[stage], kb * kGemmBK, row0 + mt * kGemmBM);
+            ptx::tma_load_2d(sb, &tma_b, &full[stage], kb * kGemmBK, nt * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;

@@ -84,6 +84,12 @@ bool tune_flag(const char* name) {
   return e && e[0] == '1';
 }
 
+// debug: point the 1-SM GEMM kernel's timeline at `buf` (device, 8 x 256
+// slots) or disable it (null)
+cudaError_t set_gemm_trace(unsigned long long* buf) {
+  return cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf));
+}
+
 int64_t& launch_counter() {
   thread_local int64_t count = 0;
   return count;
@@ -833,6 +839,10 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     return e && e[0] == '1';
   }();
   prm.flags = a.flags;
+  for (int i = 0; i < kAttnPrefetchRegions; ++i) {
+    prm.pf_ptr[i] = static_cast<const char*>(a.prefetch[i]);
+    prm.pf_bytes[i] = a.prefetch[i] ? (a.prefetch_bytes[i] & ~size_t(15)) : 0;
+  }
   prm.fused = (cut && prm.grid >= 2 && a.flags && !no_fuse &&
                prm.units / prm.grid >= prm.blocks) ? 1 : 0;
   if (cut) {

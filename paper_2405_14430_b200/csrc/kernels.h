@@ -34,6 +34,7 @@ bool pdl_enabled();
 // Kernel launches issued by the calling thread. Every launch site in the
 // library bumps it; the runtime reports per-run deltas (pf_last_launch_count).
 int64_t& launch_counter();
+cudaError_t set_gemm_trace(unsigned long long* buf);  // debug timeline (gemm_sm100.cuh)
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t stream, Args&&... args) {
@@ -130,6 +131,7 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
 // Attention of query rows [row0, row0+rows) against all P kv rows.
 // stream-K attention: one merge flag per softmax warp of each CTA
 constexpr int kAttnFlagsPerCta = 8;
+constexpr int kAttnPrefetchRegions = 4;
 
 struct AttnLaunch {
   // P: kv rows per head (buffer height); Q rows per head = q_stride (0 -> P)
@@ -148,6 +150,10 @@ struct AttnLaunch {
   // [sm_count * kAttnFlagsPerCta] zero-initialised flags for the in-kernel merge of cut items
   // (left zero after every launch); null -> merge in a separate kernel
   int* flags = nullptr;
+  // weights of the following kernels to pull into L2 during the attention
+  // (16-byte aligned regions; bytes 0 = unused)
+  const void* prefetch[kAttnPrefetchRegions] = {};
+  size_t prefetch_bytes[kAttnPrefetchRegions] = {};
 };
 int attn_grid(const AttnLaunch& a, int sm_count);
 // partial-result workspace the attention needs on a device with sm_count SMs

@@ -464,6 +464,21 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
   a.flags = s.attn_flags;
+  // pull this layer's out-proj / MLP weights and the next layer's (or, after
+  // the stage's last layer, the next patch's first layer's) QKV weights into
+  // L2 while the attention runs: small patches otherwise stream them from HBM
+  // at latency-bound rates
+  if (prefetch_weights_) {
+    const StageLayer& nx = s.layers[size_t(lf + 1 < s.layer_count ? lf + 1 : 0)];
+    a.prefetch[0] = L.wo;
+    a.prefetch_bytes[0] = size_t(m.hs) * m.hs * 2;
+    a.prefetch[1] = L.win;
+    a.prefetch_bytes[1] = size_t(m.mlp) * m.hs * 2;
+    a.prefetch[2] = L.wout;
+    a.prefetch_bytes[2] = size_t(m.hs) * m.mlp * 2;
+    a.prefetch[3] = nx.wqkv;
+    a.prefetch_bytes[3] = size_t(3) * m.hs * m.hs * 2;
+  }
   if (kv) {
     a.k2 = kv->tm_k2;
     a.v2 = kv->tm_v2;

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <tuple>
@@ -373,6 +374,13 @@ class Engine {
   ModelShape shape_;
   std::vector<Stage> stages_;
   int64_t launches_ = 0;
+  // L2 prefetch of the next kernels' weights from the attention kernel.
+  // Opt-in (PF_WEIGHT_PREFETCH=1): measured at C2 M = 8 the GEMMs were not
+  // weight-latency bound (unchanged) and the attention lost 3.5 us per launch.
+  bool prefetch_weights_ = [] {
+    const char* e = std::getenv("PF_WEIGHT_PREFETCH");
+    return e && e[0] == '1';
+  }();
   // ordinal -> (timestep, global layer) for non-finite reporting
   std::vector<std::pair<int, int>> codes_;
 };

@@ -469,6 +469,11 @@ __device__ __forceinline__ uint32_t smid() {
   return r;
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // GPU-scope acquire load / release store (inter-CTA flags)
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
