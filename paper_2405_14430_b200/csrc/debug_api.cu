@@ -33,7 +33,12 @@ extern "C" int pf_debug_gemm(const void* A, const void* B, float* C, int rows,
     return int(cudaErrorInvalidValue);
   if (!pf::make_weight_maps(&tb, static_cast<const pf::bf16*>(B), N, K))
     return int(cudaErrorInvalidValue);
+  CUtensorMap ta_half;
+  if (!pf::encode_tmap_bf16_2d(&ta_half, A, uint64_t(K), uint64_t(total_rows), uint64_t(K) * 2,
+                               64, 64, 128))
+    return int(cudaErrorInvalidValue);
   pf::EpiParams ep;
+  ep.a_half = &ta_half;
   ep.out_f32 = C - size_t(row0) * N;  // epilogue indexes by global row
   ep.ld = N;
   // split-K workspace as the runtime attaches it (skinny problems split K)

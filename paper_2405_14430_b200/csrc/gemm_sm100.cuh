@@ -495,11 +495,21 @@ struct Gemm2SmSmem {
   static_assert(((BN / 2) * 128) % 1024 == 0, "B half must keep 1024-B aligned stages");
 };
 
-template <int BN, int STAGES, class Epi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+// NP = 2: a cluster of two CTA pairs computing N-adjacent tiles of the same
+// 256 rows. Each CTA loads half of its 128-row A tile (a 64-row box,
+// tma_a_half) and multicasts it to itself and its counterpart in the other
+// pair, so every A tile leaves L2 once per cluster instead of once per pair:
+// the layer GEMMs move ~8-9 TB/s of operands L2 -> SM over all SMs, and this
+// cuts that traffic by 25-33 %. A stage may be refilled only when both
+// pairs' MMAs released it: the empty barriers count one multicast commit
+// from each pair. Opt-in (kernels.cu): only 33 4-CTA clusters fit on the
+// 148 SMs, and the lost wave outweighs the ~8 % per-tile gain measured.
+template <int BN, int STAGES, class Epi, int NP = 1>
+__global__ void __cluster_dims__(2 * NP, 1, 1) __launch_bounds__(256, 1)
     gemm2sm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tma_a,
                            const __grid_constant__ CUtensorMap tma_b, int rows, int row0,
-                           int N, int K, Epi epi) {
+                           int N, int K, Epi epi,
+                           const __grid_constant__ CUtensorMap tma_a_half) {
   using L = Gemm2SmSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -512,21 +522,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = ptx::lane_id();
-  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t crank = ptx::cluster_ctarank();
+  const uint32_t rank = crank & 1;          // position in the CTA pair
+  const int pr = int(crank >> 1);           // pair within the cluster (N offset)
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x >> 1;
-  const int nclusters = gridDim.x >> 1;
+  const int cluster = blockIdx.x / (2 * NP);
+  const int nclusters = gridDim.x / (2 * NP);
   const int m_tiles = (rows + 2 * kGemmBM - 1) / (2 * kGemmBM);
-  const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
+  const int n_tiles = (N + BN - 1) / BN;   // NP = 2: even (host checks)
+  const int num_tiles = m_tiles * (n_tiles / NP);
   const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+  const uint16_t pair_mask = uint16_t(0x3u << (2 * pr));
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tma_a);
     ptx::prefetch_tmap(&tma_b);
+    if constexpr (NP == 2) ptx::prefetch_tmap(&tma_a_half);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], NP);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -548,14 +562,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
         const int mt = tile % m_tiles;
-        const int nt = tile / m_tiles;
+        const int nt = (tile / m_tiles) * NP + pr;
         for (int kb = 0; kb < kblocks; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L::kStageBytes);
-          ptx::tma_load_2d_2sm(sa, &tma_a, &full[stage], kb * kGemmBK,
-                               row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM);
+          if constexpr (NP == 2) {
+            // rows [64 pr, +64) of this CTA's A tile, to both pairs
+            ptx::tma_load_2d_2sm_mc(sa + pr * (L::kABytes / 2), &tma_a_half, &full[stage],
+                                    kb * kGemmBK,
+                                    row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM + 64 * pr,
+                                    uint16_t(0x5u << rank));
+          } else {
+            ptx::tma_load_2d_2sm(sa, &tma_a, &full[stage], kb * kGemmBK,
+                                 row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM);
+          }
           ptx::tma_load_2d_2sm(sb, &tma_b, &full[stage], kb * kGemmBK,
                                nt * BN + int(rank) * (BN / 2));
           if (++stage == STAGES) {
@@ -585,26 +607,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           for (int k = 0; k < kGemmBK / 16; ++k)
             ptx::umma2_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
                                ptx::desc_kmajor_sw128(b_base + k * 32), idesc, (kb | k) != 0);
-          ptx::umma2_commit_mc(&empty[stage], 0x3);
+          // the stage's A also holds the other pair's multicast half: release
+          // it to every CTA of the cluster
+          ptx::umma2_commit_mc(&empty[stage], NP == 2 ? uint16_t(0xF) : pair_mask);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::umma2_commit_mc(&tfull[acc], 0x3);
+        ptx::umma2_commit_mc(&tfull[acc], pair_mask);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader0 =
+        ptx::mapa_shared(ptx::smem_u32(&tempty[0]), uint32_t(2 * pr));
     int acc = 0;
     uint32_t acc_phase = 0;
     int tile_count = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
       const int mt = tile % m_tiles;
-      const int nt = tile / m_tiles;
+      const int nt = (tile / m_tiles) * NP + pr;
       const int local_row = mt * 2 * kGemmBM + int(rank) * kGemmBM + 32 * q + int(lane);
       const bool row_ok = local_row < rows;
       float pre[Epi::kPreload ? BN / 32 : 1][32];

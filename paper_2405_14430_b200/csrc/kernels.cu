@@ -470,18 +470,64 @@ cudaError_t launch_gemm(const CUtensorMap& a, const CUtensorMap& b, int rows,
                     sk);
 }
 
+// Co-resident clusters of `kern` (cluster dims compiled in), cached per kernel.
+template <auto kern>
+int max_active_clusters(uint32_t smem, int cluster) {
+  static std::mutex mu;
+  static int cached = -1;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cached < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(cluster));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cached = n;
+  }
+  return cached;
+}
+
 template <int BN, int STAGES, class E>
 cudaError_t launch_gemm2sm(const CUtensorMap& a, const CUtensorMap& b, int rows,
                            int row0, int N, int K, const E& epi, int sm_count,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const CUtensorMap* a_half = nullptr) {
   using L = Gemm2SmSmem<BN, STAGES>;
-  constexpr auto kern = gemm2sm_bf16_tn_kernel<BN, STAGES, E>;
+  const int m_pairs = (rows + 2 * kGemmBM - 1) / (2 * kGemmBM);
+  const int n_tiles = (N + BN - 1) / BN;
+  if (a_half && n_tiles % 2 == 0) {
+    // clusters of two CTA pairs sharing A (see gemm2sm_bf16_tn_kernel)
+    constexpr auto kern4 = gemm2sm_bf16_tn_kernel<BN, STAGES, E, 2>;
+    cudaError_t e = ensure_smem_attr<kern4>(L::kTotal);
+    if (e != cudaSuccess) return e;
+    const int clusters = max_active_clusters<kern4>(L::kTotal, 4);
+    if (tune_flag("PF_VERBOSE"))
+      std::fprintf(stderr, "gemm2sm<%d> 4-CTA clusters: %d active\n", BN, clusters);
+    if (clusters > 0) {
+      const int tiles = m_pairs * (n_tiles / 2);
+      const int grid = 4 * (tiles < clusters ? tiles : clusters);
+      return launch_pdl(kern4, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N,
+                        K, epi, *a_half);
+    }
+  }
+  constexpr auto kern = gemm2sm_bf16_tn_kernel<BN, STAGES, E, 1>;
   cudaError_t e = ensure_smem_attr<kern>(L::kTotal);
   if (e != cudaSuccess) return e;
-  const int tiles = ((rows + 2 * kGemmBM - 1) / (2 * kGemmBM)) * ((N + BN - 1) / BN);
+  const int tiles = m_pairs * n_tiles;
   const int pairs = sm_count / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  return launch_pdl(kern, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N, K, epi);
+  return launch_pdl(kern, dim3(grid), dim3(256), L::kTotal, stream, a, b, rows, row0, N, K, epi,
+                    a);
 }
 
 template <bool kTwoSm, int BN, int STAGES>
@@ -490,7 +536,12 @@ cudaError_t gemm_dispatch(const CUtensorMap& a, const CUtensorMap& b, int rows,
                           int sm_count, cudaStream_t stream, SplitK sk = SplitK{}) {
   auto go = [&](const auto& epi) {
     if constexpr (kTwoSm)
-      return launch_gemm2sm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream);
+      // A multicast over 4-CTA clusters is opt-in (PF_A_MULTICAST=1): measured
+      // at C2 only 33 such clusters are co-resident (132 SMs), the tile waves
+      // then grow from 4 to 5, and the per-tile gain is ~8 % (QKV 40.8 ->
+      // 45.0 us, MLP-in 40.4 -> 47.3 us)
+      return launch_gemm2sm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream,
+                                        tune_flag("PF_A_MULTICAST") ? ep.a_half : nullptr);
     else
       return launch_gemm<BN, STAGES>(a, b, rows, row0, N, K, epi, sm_count, stream, sk);
   };

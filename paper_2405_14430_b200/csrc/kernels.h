@@ -72,6 +72,9 @@ struct EpiParams {
   int code = 0;
   // Residual only: tensor maps over out_f32 (fp32, box 32 x 128, SW128) and
   // out_bf16 (bf16, box 64 x 128, SW128) enable the TMA epilogue.
+  // 64-row box over the A operand (bf16, SW128): enables the 4-CTA-cluster
+  // 2-SM kernel that multicasts A across N-adjacent tile pairs
+  const CUtensorMap* a_half = nullptr;
   const CUtensorMap* tm_h32 = nullptr;
   const CUtensorMap* tm_hb = nullptr;
   // Residual: write the updated rows (fp32 and bf16 copy) to these buffers /

@@ -231,6 +231,7 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
   s.attn_flags = dalloc<int>(size_t(s.sm_count) * kAttnFlagsPerCta);
   PF_CUDA_CHECK(cudaMemset(s.attn_flags, 0, size_t(s.sm_count) * kAttnFlagsPerCta * sizeof(int)));
   s.tm_hb = tmap(s.hb, hs, P, hs * 2, 64, 128, 128);
+  s.tm_hb_half = tmap(s.hb, hs, P, hs * 2, 64, 64, 128);
   if (!encode_tmap_f32_2d(&s.tm_h32, s.h32, hs, P, hs * 4, 32, 128, 128))
     throw CudaError("cuTensorMapEncodeTiled failed for the residual stream");
   s.tm_attn = tmap(s.attn, hs, P, hs * 2, 64, 128, 128);
@@ -456,6 +457,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   qkv.dh = m.dh;
   qkv.dhp = m.dhp;
   qkv.P = int(m.P);
+  qkv.a_half = &s.tm_hb_half;
   prof_begin(s, kGemmQKV, 2 * r * hs * 3 * hs, 0);
   check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * m.hs, m.hs, Epi::QKV, sk(s, qkv),
              s.sm_count, s.stream), "gemm qkv");
@@ -506,6 +508,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   EpiParams th;
   th.out_bf16 = s.z;
   th.ld = m.mlp;
+  th.a_half = &s.tm_hb_half;
   prof_begin(s, kGemmMlpIn, 2 * r * hs * mlp, 0);
   check(gemm(s.tm_hb, L.tm_win, rows, row0, m.mlp, m.hs, Epi::Tanh, sk(s, th),
              s.sm_count, s.stream), "gemm mlp-in");

@@ -148,6 +148,7 @@ struct Stage {
   int* splitk_counters = nullptr;
   int splitk_counter_cap = 0;
   CUtensorMap tm_hb, tm_attn, tm_z, tm_q;
+  CUtensorMap tm_hb_half;  // 64-row boxes over hb (A multicast across cluster pairs)
   CUtensorMap tm_h32;  // fp32 residual stream, box 32 x 128 (TMA epilogue)
   cudaEvent_t ev_fwd = nullptr;  // "rows sent to stage d+1"
   // stage 0 only

@@ -128,6 +128,18 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 // 2-SM TMA load: data lands in this CTA's smem, completion is signalled on
 // the mbarrier of the pair's even CTA (peer bit 24 cleared, as CUTLASS's
 // SM100_TMA_2SM_LOAD does).
+// 2-SM load multicast to the CTAs in `mask` (same smem offset in each); the
+// transaction bytes are signalled on each destination's pair-leader barrier.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* m,
+                                                   uint64_t* bar, int32_t c0, int32_t c1,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+      "bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* m,
                                                 uint64_t* bar, int32_t c0, int32_t c1) {
   asm volatile(

@@ -37,6 +37,7 @@ def _gemm(A, B, rows, row0):
     (4096, 512, 1536, 3456, 1152),  # PixArt patch QKV
     (4096, 4096, 0, 1152, 4608),    # PixArt MLP-out full sequence (2-SM, BN 128)
     (4096, 4096, 0, 4608, 1152),    # PixArt MLP-in (2-SM, BN 256)
+    (4096, 4096, 0, 3456, 1152),    # PixArt QKV (2-SM, BN 192)
     (1024, 1000, 24, 4608, 1152),   # 2-SM with a ragged last row tile
     (512, 300, 100, 96, 64),        # 2-SM with N < BN (B half partly out of range)
     (2048, 256, 1792, 3456, 1152),  # one 2-SM row tile, BN 192 (split-K 2 on 1-SM tiles)
@@ -54,6 +55,17 @@ def test_gemm_matches_fp32(total, rows, row0, N, K):
     err = (C - ref).abs().max().item()
     scale = ref.abs().max().item()
     assert err <= 1e-4 * max(1.0, scale) + 1e-3, (err, scale)
+
+
+@pytest.mark.parametrize("total,rows,row0,N,K", [
+    (4096, 4096, 0, 4608, 1152),
+    (4096, 4096, 0, 3456, 1152),
+    (4096, 3000, 96, 4608, 1152),   # ragged last row tile
+])
+def test_gemm_a_multicast_matches_fp32(monkeypatch, total, rows, row0, N, K):
+    # opt-in 4-CTA clusters (two CTA pairs multicasting the A tile)
+    monkeypatch.setenv("PF_A_MULTICAST", "1")
+    test_gemm_matches_fp32(total, rows, row0, N, K)
 
 
 def _attn(q, k, v, heads, rows, row0):
