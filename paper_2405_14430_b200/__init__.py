@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import sys
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import List, Optional, Sequence
@@ -205,6 +206,22 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
+def _out_buffer(owner, x: np.ndarray) -> np.ndarray:
+    """Result latent for a host-buffer run. Reuses an array this context
+    returned earlier once the caller has dropped every reference to it (views
+    included): first-touch page faults of a fresh 37 MB array cost ~5 ms at
+    C2, more than the device-to-host copy itself."""
+    pool = owner.__dict__.setdefault("_out_pool", [])
+    for a in pool:
+        # references: the pool list, the loop variable, getrefcount's argument
+        if a.shape == x.shape and sys.getrefcount(a) == 3:
+            return a
+    a = np.empty_like(x)
+    if len(pool) < 4:
+        pool.append(a)
+    return a
+
+
 class ToyDiTCuda:
     """A toy DiT resident on B200 stage devices, split into `workers` stages.
 
@@ -352,7 +369,7 @@ class ToyDiTCuda:
         x = _f64c(x_init)
         if x.shape != (self.seq_len, self.hidden_size):
             raise ValidationError("latent width does not match the model hidden size")
-        out = np.empty_like(x)
+        out = _out_buffer(self, x)
         status = self._lib.pf_run_pipefusion(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
                                              patches, warmup, ctypes.c_double(eta),
                                              _dptr(out), ctypes.byref(st))
@@ -365,7 +382,7 @@ class ToyDiTCuda:
                          eta: float) -> ParallelRunResult:
         """ditsim::run_distrifusion (execute.hpp:131-133) on this context's GPU."""
         x = _f64c(x_init)
-        out = np.empty_like(x)
+        out = _out_buffer(self, x)
         per = max(0, steps - warmup)
         cap = workers * per
         ff = (ctypes.c_double * max(1, cap))()
@@ -381,7 +398,7 @@ class ToyDiTCuda:
     def serial_reference(self, x_init, steps: int, eta: float) -> np.ndarray:
         """ditsim::serial_reference (execute.hpp:102-104) on the GPU."""
         x = _f64c(x_init)
-        out = np.empty_like(x)
+        out = _out_buffer(self, x)
         status = self._lib.pf_serial_reference(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
                                                ctypes.c_double(eta), _dptr(out))
         _raise(status, self._err())
