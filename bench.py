@@ -38,6 +38,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# Rank-mode patch lanes (stream-memory-op signal waits on several streams)
+# need more than the default 8 hardware queues; set before CUDA initialises.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -368,6 +368,15 @@ void Engine::free_stage(Stage& s) {
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
+  if (s.lane != 0) use_lane(s, 0);
+  for (Stage::Lane& ln : s.extra) {
+    dfree(ln.attn_work); dfree(ln.attn_flags); dfree(ln.splitk_ws); dfree(ln.splitk_counters);
+    if (ln.stream) cudaStreamDestroy(ln.stream);
+  }
+  for (auto& v : s.ev_attn)
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
+  for (cudaEvent_t e : s.ev_lane)
+    if (e) cudaEventDestroy(e);
   dfree(s.attn_work); dfree(s.attn_flags); dfree(s.flag); dfree(s.splitk_ws); dfree(s.splitk_counters);
   dfree(s.zeros); dfree(s.text); dfree(s.x); dfree(s.cb);
   if (s.eps_owned) dfree(s.eps);
@@ -458,6 +467,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   qkv.dhp = m.dhp;
   qkv.P = int(m.P);
   qkv.a_half = &s.tm_hb_half;
+  if (lane_wait_) PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, lane_wait_, 0));
   prof_begin(s, kGemmQKV, 2 * r * hs * 3 * hs, 0);
   check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * m.hs, m.hs, Epi::QKV, sk(s, qkv),
              s.sm_count, s.stream), "gemm qkv");
@@ -491,6 +501,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
   check(attention(s.tm_q, kv ? *kv->tm_k : L.tm_k, kv ? *kv->tm_v : L.tm_v, a, s.sm_count,
                   s.stream), "attention");
   prof_end(s);
+  if (lane_rec_) PF_CUDA_CHECK(cudaEventRecord(lane_rec_, s.stream));
   EpiParams res;
   res.out_f32 = s.h32;
   res.out_bf16 = s.hb;
@@ -608,6 +619,47 @@ void Engine::send_rows(int from, int row0, int rows, int patch, int t) {
                                     src.stream));
     tl_end(src.stream);
   }
+}
+
+// Extra lanes of a stage (allocated on first use, outside stream capture).
+void Engine::alloc_lanes(Stage& s, int lanes) {
+  if (s.lanes_alloc >= lanes) return;
+  DeviceGuard g(s.device);
+  for (int k = s.lanes_alloc; k < lanes; ++k) {
+    Stage::Lane& ln = s.extra[k];
+    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&ln.stream, cudaStreamNonBlocking));
+    ln.attn_work = dalloc<float>(s.attn_work_floats);
+    ln.attn_flags = dalloc<int>(size_t(s.sm_count) * kAttnFlagsPerCta);
+    PF_CUDA_CHECK(cudaMemset(ln.attn_flags, 0,
+                             size_t(s.sm_count) * kAttnFlagsPerCta * sizeof(int)));
+    ln.splitk_ws = dalloc<float>(s.splitk_ws_floats);
+    ln.splitk_counters = dalloc<int>(size_t(s.splitk_counter_cap));
+    PF_CUDA_CHECK(cudaMemset(ln.splitk_counters, 0, size_t(s.splitk_counter_cap) * sizeof(int)));
+  }
+  for (int k = 0; k < lanes; ++k) {
+    auto& v = s.ev_attn[k];
+    while (v.size() < size_t(s.layer_count)) {
+      cudaEvent_t e;
+      PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      v.push_back(e);
+    }
+    if (!s.ev_lane[k]) PF_CUDA_CHECK(cudaEventCreateWithFlags(&s.ev_lane[k], cudaEventDisableTiming));
+  }
+  s.lanes_alloc = lanes;
+}
+
+void Engine::use_lane(Stage& s, int lane) {
+  if (s.lane == lane) return;
+  auto swap_in = [&](Stage::Lane& ln) {
+    std::swap(s.stream, ln.stream);
+    std::swap(s.attn_work, ln.attn_work);
+    std::swap(s.attn_flags, ln.attn_flags);
+    std::swap(s.splitk_ws, ln.splitk_ws);
+    std::swap(s.splitk_counters, ln.splitk_counters);
+  };
+  if (s.lane != 0) swap_in(s.extra[s.lane]);  // lane 0's resources back in place
+  if (lane != 0) swap_in(s.extra[lane]);
+  s.lane = lane;
 }
 
 // check_pipefusion_args (execute.cpp:97-131), with the layer divisibility
@@ -750,9 +802,27 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
 
   // ---- steady: patch pipeline (execute.cpp:192-212)
   const int steady = steps - warmup;
+  // Lanes (one stage, toy block, M >= 2): patch j runs on lane j % lanes, so
+  // the kernels of consecutive patches overlap; small patches leave most of
+  // the GPU idle in per-kernel latency otherwise. The only cross-patch
+  // dependency inside a stage is the K/V buffer: patch j's QKV GEMM of layer
+  // l overwrites its rows, which the previous patch's layer-l attention
+  // reads (stale), and patch j's attention reads the previous patch's fresh
+  // rows -- so QKV(j, l) waits for ATTN(j-1, l) (ev_attn). Everything else a
+  // patch touches is its own rows or its lane's scratch.
+  const int nl = steady > 0 ? lanes_for(patches) : 1;
+  const bool lanes = nl > 1;
+  if (lanes) {
+    DeviceGuard g(s0.device);
+    PF_CUDA_CHECK(cudaEventRecord(s0.ev_lane[0], s0.stream));
+    for (int k = 1; k < nl; ++k)
+      PF_CUDA_CHECK(cudaStreamWaitEvent(s0.extra[k].stream, s0.ev_lane[0], 0));
+  }
+  int prev_lane = -1;  // lane of the previously enqueued steady patch
   for (int q = 0; q < steady; ++q) {
     const int t = steady - 1 - q;
     for (int j = 0; j < patches; ++j) {
+      if (lanes) use_lane(s0, j % nl);
       const int row0 = j * r;  // image rows of patch j
       // the block's joint rows: the text rows travel with patch 0
       const int brow0 = joint && j > 0 ? J + row0 : 0;
@@ -791,8 +861,13 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
               throw NumericError(os.str());
             }
           }
+          if (lanes) {
+            lane_wait_ = prev_lane >= 0 ? s.ev_attn[prev_lane][size_t(lf)] : nullptr;
+            lane_rec_ = s.ev_attn[j % nl][size_t(lf)];
+          }
           forward(s, lf, joint ? brows : r, joint ? brow0 : row0, t,
                   next_code(t, s.first_layer + lf));
+          lane_wait_ = lane_rec_ = nullptr;
         }
         // fresh_fraction(src[0], t) after the stage (execute.cpp:67-73,164)
         {
@@ -806,6 +881,15 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
         if (d == n - 1 && n > 1)
           PF_CUDA_CHECK(cudaEventRecord(s0.ev_eps[size_t(j)], s.stream));
       }
+      prev_lane = j % nl;
+    }
+  }
+  if (lanes) {  // join the other lanes back into lane 0
+    DeviceGuard g(s0.device);
+    use_lane(s0, 0);
+    for (int k = 1; k < nl; ++k) {
+      PF_CUDA_CHECK(cudaEventRecord(s0.ev_lane[k], s0.extra[k].stream));
+      PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_lane[k], 0));
     }
   }
   if (steady > 0) {
@@ -843,6 +927,7 @@ void Engine::prepare_run(int patches, int steps) {
     s0.eps_owned = true;
   }
   if (n == 1) s0.eps = s0.h32 + size_t(shape_.J()) * shape_.hs;  // image rows of h
+  if (lanes_for(patches) > 1) alloc_lanes(s0, lanes_for(patches));
   if (int(s0.ev_eps.size()) < patches) {
     DeviceGuard g(stages_[size_t(n - 1)].device);
     while (int(s0.ev_eps.size()) < patches) {
@@ -1535,8 +1620,60 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   // joint block: the eps rows of the last rank are image rows (offset by the
   // text rows), which the GEMM's joint-row stores cannot address: copy them
   const bool fused = !copy_send && !(joint && succ_eps_);
+  // Lanes (toy block, fused sends, M >= 2): the ops of patch j run on lane
+  // j % nl, full-sequence ops on lane 0 (lanes fork after / join before
+  // them). Besides the K/V ordering of layer_forward (QKV(j, l) after the
+  // previous patch's ATTN(l)), the signal writes must keep plan order: their
+  // values are absolute message counts that the peers wait on with >=.
+  // A lane blocked in a signal wait (a stream memory operation, invisible to
+  // the driver's dependency tracking) stalls every stream sharing its
+  // hardware queue: lanes here need CUDA_DEVICE_MAX_CONNECTIONS >= 16 (set
+  // before the context is created, as bench.py and the tests do).
+  static const bool enough_queues = [] {
+    const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    return e && std::atoi(e) >= 16;
+  }();
+  const int nl = (fused && enough_queues && m.block == kBlockToy && !profiling_ && !timeline_on_)
+                     ? std::min(lanes_, patches) : 1;
+  if (nl > 1) {
+    alloc_lanes(s, nl);
+    if (!ev_write_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_write_, cudaEventDisableTiming));
+  }
+  bool forked = false, wrote = false;
+  int prev_lane = -1;
+  auto ordered_write = [&](cudaStream_t st, uint32_t* addr, uint32_t value) {
+    if (nl > 1 && wrote) PF_CUDA_CHECK(cudaStreamWaitEvent(st, ev_write_, 0));
+    stream_write(st, addr, value, dev);
+    if (nl > 1) {
+      PF_CUDA_CHECK(cudaEventRecord(ev_write_, st));
+      wrote = true;
+    }
+  };
+  auto join_lanes = [&]() {
+    if (!forked) return;
+    use_lane(s, 0);
+    for (int k = 1; k < nl; ++k) {
+      PF_CUDA_CHECK(cudaEventRecord(s.ev_lane[k], s.extra[k].stream));
+      PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, s.ev_lane[k], 0));
+    }
+    forked = false;
+  };
   for (size_t oi = 0; oi < plan.size(); ++oi) {
     const PlanOp& op = plan[oi];
+    if (nl > 1) {
+      if (op.patch < 0 || op.kind == PlanOp::kLatentUpdate) {
+        join_lanes();
+      } else {
+        if (!forked) {  // lanes start after lane 0's work so far
+          use_lane(s, 0);
+          PF_CUDA_CHECK(cudaEventRecord(s.ev_lane[0], s.stream));
+          for (int k = 1; k < nl; ++k)
+            PF_CUDA_CHECK(cudaStreamWaitEvent(s.extra[k].stream, s.ev_lane[0], 0));
+          forked = true;
+        }
+        use_lane(s, op.patch % nl);
+      }
+    }
     // plan rows are image rows; joint blocks carry the text rows with the
     // full sequence and with patch 0
     const int row0 = op.row0, rows = op.rows;
@@ -1547,8 +1684,8 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         stream_wait_geq(s.stream, sig_, base_in + uint32_t(op.msg), dev);
         break;
       case PlanOp::kAck:
-        stream_write(op.flag && !fused ? send_stream_ : s.stream, pred_sig_ + 1,
-                     base_in + uint32_t(op.msg), dev);
+        ordered_write(op.flag && !fused ? send_stream_ : s.stream, pred_sig_ + 1,
+                      base_in + uint32_t(op.msg));
         break;
       case PlanOp::kPrepare: {
         // this rank's previous send of the same rows must have finished reading h32
@@ -1607,6 +1744,10 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           if (send && send->overlap > 0)  // landing rows free at the successor
             stream_wait_geq(s.stream, sig_ + 1, base_out + uint32_t(send->overlap), dev);
           redirect_ = send ? &peer_out_ : nullptr;
+          if (nl > 1 && op.patch >= 0) {
+            lane_wait_ = prev_lane >= 0 ? s.ev_attn[prev_lane][size_t(lf)] : nullptr;
+            lane_rec_ = s.ev_attn[op.patch % nl][size_t(lf)];
+          }
           if (px) layer_forward_px(s, lf, rows, row0, t, code);
           else if (joint && s.first_layer + lf < m.double_layers)
             layer_forward_joint(s, lf, brows, brow0, code);
@@ -1614,8 +1755,9 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
             layer_forward_single(s, lf, brows, brow0, code);
           else layer_forward(s, lf, rows, row0, code);
           redirect_ = nullptr;
+          lane_wait_ = lane_rec_ = nullptr;
           if (send) {
-            stream_write(s.stream, succ_sig_, base_out + uint32_t(send->msg), dev);
+            ordered_write(s.stream, succ_sig_, base_out + uint32_t(send->msg));
             for (int j = 0; j < patches; ++j)
               if (send->patch < 0 || send->patch == j) {
                 PF_CUDA_CHECK(cudaEventRecord(ev_sent_[size_t(j)], s.stream));
@@ -1628,6 +1770,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           int fresh = 0;
           for (int v : src[0]) fresh += (v == t);
           st.fresh_fraction[0].push_back(double(fresh) / double(patches));
+          prev_lane = op.patch % nl;
         }
         break;
       }
@@ -1656,7 +1799,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           }
         }
         tl_end(send_stream_);
-        stream_write(send_stream_, succ_sig_, base_out + uint32_t(op.msg), dev);
+        ordered_write(send_stream_, succ_sig_, base_out + uint32_t(op.msg));
         for (int j = 0; j < patches; ++j)
           if (op.patch < 0 || op.patch == j) {
             PF_CUDA_CHECK(cudaEventRecord(ev_sent_[size_t(j)], send_stream_));
@@ -1669,6 +1812,8 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   const uint32_t per_run = uint32_t(plan_messages_per_run(steps, patches, warmup));
   msgs_in_base_ += per_run;
   msgs_out_base_ += per_run;
+  if (nl > 1) join_lanes();
+  use_lane(s, 0);
   // join: the caller waits for both streams
   PF_CUDA_CHECK(cudaEventRecord(s.ev_fwd, s.stream));
   PF_CUDA_CHECK(cudaStreamWaitEvent(caller, s.ev_fwd, 0));

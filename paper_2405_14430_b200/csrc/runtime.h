@@ -151,6 +151,22 @@ struct Stage {
   CUtensorMap tm_hb_half;  // 64-row boxes over hb (A multicast across cluster pairs)
   CUtensorMap tm_h32;  // fp32 residual stream, box 32 x 128 (TMA epilogue)
   cudaEvent_t ev_fwd = nullptr;  // "rows sent to stage d+1"
+  // Extra patch lanes (small patches): own stream and the per-launch scratch
+  // concurrent patches must not share. The fields above always hold the
+  // active lane's resources: use_lane() swaps extra[k] in (lane 0's live in
+  // extra[lane] meanwhile).
+  static constexpr int kMaxLanes = 4;
+  struct Lane {
+    cudaStream_t stream = nullptr;
+    float* attn_work = nullptr;
+    int* attn_flags = nullptr;
+    float* splitk_ws = nullptr;
+    int* splitk_counters = nullptr;
+  } extra[kMaxLanes];
+  int lane = 0;
+  int lanes_alloc = 1;
+  std::vector<cudaEvent_t> ev_attn[kMaxLanes];  // per local layer: the lane's last attention
+  cudaEvent_t ev_lane[kMaxLanes] = {};          // lane fork / join
   // stage 0 only
   float* x = nullptr;    // [P x hs] latent
   float* eps = nullptr;  // [P x hs] noise landing buffer (== last stage h32 when N == 1)
@@ -334,6 +350,7 @@ class Engine {
   uint32_t msgs_in_base_ = 0, msgs_out_base_ = 0;
   cudaEvent_t ev_compute_ = nullptr;
   std::vector<cudaEvent_t> ev_sent_;  // per patch: last send of its rows finished
+  cudaEvent_t ev_write_ = nullptr;    // rank mode with lanes: last signal write (in plan order)
   int px_steps_ = 0;  // S of the enqueued run (layout of the per-run PixArt buffers)
   cudaEvent_t ev_start_ = nullptr;
   int stage_of_layer(int layer) const;
@@ -375,6 +392,27 @@ class Engine {
   ModelShape shape_;
   std::vector<Stage> stages_;
   int64_t launches_ = 0;
+  // multi-lane patch schedule (single stage, toy block, M >= 2): patch j runs
+  // on lane j % lanes; layer_forward waits lane_wait_ before its QKV GEMM and
+  // records lane_rec_ after its attention (see enqueue_run)
+  cudaEvent_t lane_wait_ = nullptr;
+  cudaEvent_t lane_rec_ = nullptr;
+  // lanes per stage for M >= 2 (PF_LANES=1..4; PF_ONE_LANE=1 is PF_LANES=1)
+  int lanes_ = [] {
+    const char* one = std::getenv("PF_ONE_LANE");
+    if (one && one[0] == '1') return 1;
+    const char* e = std::getenv("PF_LANES");
+    const int v = e ? std::atoi(e) : 4;
+    return v < 1 ? 1 : (v > Stage::kMaxLanes ? Stage::kMaxLanes : v);
+  }();
+  void use_lane(Stage& s, int lane);
+  void alloc_lanes(Stage& s, int lanes);
+  int lanes_for(int patches) const {
+    if (patches < 2 || stages_.size() != 1 || shape_.block != kBlockToy || profiling_ ||
+        timeline_on_ || rank_mode())
+      return 1;
+    return lanes_ < patches ? lanes_ : patches;
+  }
   // L2 prefetch of the next kernels' weights from the attention kernel.
   // Opt-in (PF_WEIGHT_PREFETCH=1): measured at C2 M = 8 the GEMMs were not
   // weight-latency bound (unchanged) and the attention lost 3.5 us per launch.

@@ -4,6 +4,13 @@ from pathlib import Path
 
 import pytest
 
+# Rank-mode patch lanes wait on peer signals with stream memory operations;
+# several ranks sharing one GPU in one process need more hardware queues than
+# the default 8, or a blocked lane can stall an unrelated stream behind it.
+# Must be set before the CUDA context exists (see paper_2405_14430_b200
+# runtime: rank-mode lanes need >= 16).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
