@@ -797,7 +797,7 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
     }
   }
   if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % kGemmBM == 0 && N % 32 == 0 &&
-      gemm_bn_1sm(N) == 128) {
+      gemm_bn_1sm(N) == 128 && !tune_flag("PF_NO_RESID_TMA")) {
     constexpr int kStages = 4;
     using L = GemmResSmem<kStages>;
     const int tiles = (rows / kGemmBM) * ((N + L::BN - 1) / L::BN);

@@ -1633,7 +1633,8 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
     const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
     return e && std::atoi(e) >= 16;
   }();
-  const int nl = (fused && enough_queues && m.block == kBlockToy && !profiling_ && !timeline_on_)
+  const int nl = (fused && enough_queues && (m.block == kBlockToy || m.block == kBlockPixArt) &&
+                  !profiling_ && !timeline_on_)
                      ? std::min(lanes_, patches) : 1;
   if (nl > 1) {
     alloc_lanes(s, nl);
@@ -2035,6 +2036,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   qkv.ln_cols = hs;
   qkv.c1 = px.foldq + (size_t(lf) * 2 * S + 2 * t) * 3 * hs;
   qkv.c2 = qkv.c1 + 3 * hs;
+  if (lane_wait_) PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, lane_wait_, 0));
   prof_begin(s, kGemmQKV, 2 * r * dhs * 3 * dhs, 0);
   check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * hs, hs, Epi::QKV, sk(s, qkv), s.sm_count, s.stream),
         "gemm qkv");
@@ -2047,6 +2049,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
   prof_begin(s, kAttention, 4 * r * P * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
   prof_end(s);
+  if (lane_rec_) PF_CUDA_CHECK(cudaEventRecord(lane_rec_, s.stream));
   // 3. h += gate1 (attn Wo + bo); raw bf16 copy for the cross-attention query
   EpiParams res;
   res.out_f32 = s.h32;

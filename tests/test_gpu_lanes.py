@@ -13,11 +13,13 @@ import paper_2405_14430_b200 as pf
 pytestmark = pytest.mark.gpu
 
 
-def _run(monkeypatch, lanes, L, hs, heads, p, S, M, W, graphs, reps=1):
+def _run(monkeypatch, lanes, L, hs, heads, p, S, M, W, graphs, reps=1, text=0):
     monkeypatch.delenv("PF_ONE_LANE", raising=False)
     monkeypatch.setenv("PF_LANES", str(lanes))
     x0 = pf.make_initial_latent(1, p, hs)
-    with pf.ToyDiTCuda(0, L, hs, heads, 4.0, p, 1) as m:
+    model = (pf.PixArtCuda(0, L, hs, heads, 4.0, p, text, 1) if text
+             else pf.ToyDiTCuda(0, L, hs, heads, 4.0, p, 1))
+    with model as m:
         m.set_graphs(graphs)
         outs = [m.run_pipefusion(x0, S, M, W, 0.1) for _ in range(reps)]
     return outs
@@ -39,3 +41,14 @@ def test_lanes_equal_one_lane(monkeypatch, L, hs, heads, p, S, M, W, graphs, lan
         assert (r.stats.fresh_patch_reads, r.stats.stale_patch_reads) == \
             (one.stats.fresh_patch_reads, one.stats.stale_patch_reads)
         assert r.stats.per_worker_fresh_fraction == one.stats.per_worker_fresh_fraction
+
+
+@pytest.mark.parametrize("L,hs,heads,p,T,S,M,W", [
+    (3, 128, 4, 512, 8, 4, 4, 1),
+    (2, 1152, 16, 4096, 120, 3, 8, 1),  # PixArt-alpha patch shape
+])
+def test_lanes_pixart_equal_one_lane(monkeypatch, L, hs, heads, p, T, S, M, W):
+    one = _run(monkeypatch, 1, L, hs, heads, p, S, M, W, True, text=T)[0]
+    four = _run(monkeypatch, 4, L, hs, heads, p, S, M, W, True, reps=2, text=T)
+    for r in four:
+        assert np.array_equal(r.final_x, one.final_x)
