@@ -802,7 +802,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
 
   // ---- steady: patch pipeline (execute.cpp:192-212)
   const int steady = steps - warmup;
-  // Lanes (one stage, toy block, M >= 2): patch j runs on lane j % lanes, so
+  // Lanes (one stage, M >= 2): patch j runs on lane j % lanes, so
   // the kernels of consecutive patches overlap; small patches leave most of
   // the GPU idle in per-kernel latency otherwise. The only cross-patch
   // dependency inside a stage is the K/V buffer: patch j's QKV GEMM of layer
@@ -1110,6 +1110,7 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
   qkv.dh = m.dh;
   qkv.dhp = m.dhp;
   qkv.P = Pt;
+  if (lane_wait_) PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, lane_wait_, 0));
   both([&](bool txt, int r0, int n) {
     prof_begin(s, kGemmQKV, 2.0 * n * dhs * 3 * dhs, 0);
     check(gemm(s.tm_hb, txt ? L.tm_t_wqkv : L.tm_wqkv, n, r0, 3 * hs, hs, Epi::QKV,
@@ -1123,6 +1124,7 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
   prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (joint)");
   prof_end(s);
+  if (lane_rec_) PF_CUDA_CHECK(cudaEventRecord(lane_rec_, s.stream));
   EpiParams res;
   res.out_f32 = s.h32;
   res.out_bf16 = s.hb;
@@ -1179,6 +1181,7 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
   qkv.dh = m.dh;
   qkv.dhp = m.dhp;
   qkv.P = Pt;
+  if (lane_wait_) PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, lane_wait_, 0));
   prof_begin(s, kGemmQKV, 2 * r * dhs * 3 * dhs, 0);
   check(gemm(s.tm_hb, L.tm_wqkv, rows, row0, 3 * hs, hs, Epi::QKV, sk(s, qkv), s.sm_count,
              s.stream), "gemm qkv (single)");
@@ -1197,6 +1200,7 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
   prof_begin(s, kAttention, 4 * r * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (single)");
   prof_end(s);
+  if (lane_rec_) PF_CUDA_CHECK(cudaEventRecord(lane_rec_, s.stream));
   EpiParams res;
   res.out_f32 = s.h32;
   res.out_bf16 = s.hb;
@@ -1620,7 +1624,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   // joint block: the eps rows of the last rank are image rows (offset by the
   // text rows), which the GEMM's joint-row stores cannot address: copy them
   const bool fused = !copy_send && !(joint && succ_eps_);
-  // Lanes (toy block, fused sends, M >= 2): the ops of patch j run on lane
+  // Lanes (fused sends, M >= 2): the ops of patch j run on lane
   // j % nl, full-sequence ops on lane 0 (lanes fork after / join before
   // them). Besides the K/V ordering of layer_forward (QKV(j, l) after the
   // previous patch's ATTN(l)), the signal writes must keep plan order: their
@@ -1633,8 +1637,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
     const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
     return e && std::atoi(e) >= 16;
   }();
-  const int nl = (fused && enough_queues && (m.block == kBlockToy || m.block == kBlockPixArt) &&
-                  !profiling_ && !timeline_on_)
+  const int nl = (fused && enough_queues && !profiling_ && !timeline_on_)
                      ? std::min(lanes_, patches) : 1;
   if (nl > 1) {
     alloc_lanes(s, nl);

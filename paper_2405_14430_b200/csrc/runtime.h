@@ -408,8 +408,7 @@ class Engine {
   void use_lane(Stage& s, int lane);
   void alloc_lanes(Stage& s, int lanes);
   int lanes_for(int patches) const {
-    if (patches < 2 || stages_.size() != 1 || shape_.block == kBlockJoint || profiling_ ||
-        timeline_on_ || rank_mode())
+    if (patches < 2 || stages_.size() != 1 || profiling_ || timeline_on_ || rank_mode())
       return 1;
     return lanes_ < patches ? lanes_ : patches;
   }

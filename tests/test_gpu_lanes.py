@@ -13,12 +13,16 @@ import paper_2405_14430_b200 as pf
 pytestmark = pytest.mark.gpu
 
 
-def _run(monkeypatch, lanes, L, hs, heads, p, S, M, W, graphs, reps=1, text=0):
+def _run(monkeypatch, lanes, L, hs, heads, p, S, M, W, graphs, reps=1, text=0, joint=None):
     monkeypatch.delenv("PF_ONE_LANE", raising=False)
     monkeypatch.setenv("PF_LANES", str(lanes))
     x0 = pf.make_initial_latent(1, p, hs)
-    model = (pf.PixArtCuda(0, L, hs, heads, 4.0, p, text, 1) if text
-             else pf.ToyDiTCuda(0, L, hs, heads, 4.0, p, 1))
+    if joint is not None:
+        model = pf.JointDiTCuda(0, L, hs, heads, 4.0, p, text, 1, double_layers=joint)
+    elif text:
+        model = pf.PixArtCuda(0, L, hs, heads, 4.0, p, text, 1)
+    else:
+        model = pf.ToyDiTCuda(0, L, hs, heads, 4.0, p, 1)
     with model as m:
         m.set_graphs(graphs)
         outs = [m.run_pipefusion(x0, S, M, W, 0.1) for _ in range(reps)]
@@ -50,5 +54,16 @@ def test_lanes_equal_one_lane(monkeypatch, L, hs, heads, p, S, M, W, graphs, lan
 def test_lanes_pixart_equal_one_lane(monkeypatch, L, hs, heads, p, T, S, M, W):
     one = _run(monkeypatch, 1, L, hs, heads, p, S, M, W, True, text=T)[0]
     four = _run(monkeypatch, 4, L, hs, heads, p, S, M, W, True, reps=2, text=T)
+    for r in four:
+        assert np.array_equal(r.final_x, one.final_x)
+
+
+@pytest.mark.parametrize("L,D,hs,heads,p,T,S,M", [
+    (4, 2, 128, 4, 512, 24, 4, 4),     # double + single stream layers, text rows with patch 0
+    (3, 3, 1536, 24, 4096, 333, 3, 8),  # SD3-medium-shaped joint blocks
+])
+def test_lanes_joint_equal_one_lane(monkeypatch, L, D, hs, heads, p, T, S, M):
+    one = _run(monkeypatch, 1, L, hs, heads, p, S, M, 1, True, text=T, joint=D)[0]
+    four = _run(monkeypatch, 4, L, hs, heads, p, S, M, 1, True, reps=2, text=T, joint=D)
     for r in four:
         assert np.array_equal(r.final_x, one.final_x)
