@@ -844,6 +844,17 @@ int attn_grid(const AttnLaunch& a, int sm_count) {
   const long long units = items * ((a.P + kAttnBN - 1) / kAttnBN);
   if (per_item) return int(items);
   const long long blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  // Small patches (fewer than sm_count / 2 items): exactly two CTAs per item,
+  // the head half's partial merged in-kernel by the tail half's CTA -- no
+  // separate merge launch, and the SMs left free serve the other patch lanes
+  // (PF_ATTN_HALVES=0 keeps the full-grid stream-K schedule)
+  static const bool halves = [] {
+    const char* e = std::getenv("PF_ATTN_HALVES");
+    return !(e && e[0] == '0');
+  }();
+  if (halves && a.flags && blocks >= 4 && blocks % 2 == 0 && 2 * items <= sm_count &&
+      units / sm_count < blocks)
+    return int(2 * items);
   long long g = sm_count;
   if (units < 2 * g) g = std::max(1LL, units / 2);
   // every item meets at most kAttnMaxParts CTAs: range >= blocks / (parts - 2)
@@ -894,8 +905,11 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.pf_ptr[i] = static_cast<const char*>(a.prefetch[i]);
     prm.pf_bytes[i] = a.prefetch[i] ? (a.prefetch_bytes[i] & ~size_t(15)) : 0;
   }
+  // in-kernel merge when every item meets at most two CTAs, each holding a
+  // head or a tail: ranges of at least one item, or exactly half an item
+  const bool halves = prm.units % prm.grid == 0 && 2 * (prm.units / prm.grid) == prm.blocks;
   prm.fused = (cut && prm.grid >= 2 && a.flags && !no_fuse &&
-               prm.units / prm.grid >= prm.blocks) ? 1 : 0;
+               (prm.units / prm.grid >= prm.blocks || halves)) ? 1 : 0;
   if (cut) {
     const size_t slots = size_t(2) * prm.grid * NT * kAttnBM;
     if (!a.work || a.work_floats < slots * (DHP + 2)) return cudaErrorInvalidValue;

@@ -98,7 +98,7 @@ def _attn_ref(q, k, v, heads, rows, row0):
     (256, 4, 128, 64, 128, 3.0),    # tiny config patch, dh = 32
     (256, 4, 128, 256, 0, 3.0),
     (1024, 8, 512, 1024, 0, 4.0),   # dh = 64
-    (4096, 16, 1152, 512, 1024, 3.0),  # PixArt patch, dh = 72, split-KV
+    (4096, 16, 1152, 512, 1024, 3.0),  # PixArt patch, dh = 72, two CTAs per item (halves)
     (4096, 16, 1152, 4096, 0, 3.0),    # PixArt full sequence
     (520, 2, 256, 136, 384, 2.0),   # ragged P / rows, dh = 128
     (6144, 24, 1536, 6144, 0, 2.0),  # stream-K, in-kernel merge, dh = 64
@@ -112,7 +112,9 @@ def test_attention_matches_fp32(P, heads, hs, rows, row0, scale):
     out = _attn(q, k, v, heads, rows, row0)[row0:row0 + rows].float()
     ref = _attn_ref(q, k, v, heads, rows, row0)
     err = (out - ref).abs().max().item()
-    assert err < 2e-2, err
+    # outputs reach |x| ~ scale: the bf16 output ulp there is scale * 2^-7
+    # (0.031 at scale 4); P is rounded to bf16 before PV as well
+    assert err < max(2e-2, 0.75 * scale * 2 ** -7), err
     rel = ((out - ref).norm() / ref.norm()).item()
     assert rel < 1e-2, rel
 
