@@ -131,3 +131,26 @@ def test_stream_k_attention_reruns_bitwise():
         m.set_graphs(True)
         outs += [m.run_pipefusion(x0, 3, 1, 1, 0.1).final_x for _ in range(2)]
     assert all(np.array_equal(o, outs[0]) for o in outs)
+
+
+def test_residual_split_k_opt_in(monkeypatch):
+    # opt-in split-K of skinny long-K residual GEMMs (workspace partials +
+    # resid_reduce_kernel), one lane: same result as the unsplit GEMMs up to
+    # fp32 summation order, and deterministic
+    import numpy as np
+    import paper_2405_14430_b200 as pf
+    monkeypatch.setenv("PF_LANES", "1")
+    x0 = pf.make_initial_latent(0, 4096, 1152)
+
+    def run(split):
+        if split:
+            monkeypatch.setenv("PF_RESID_SPLITK", "1")
+        else:
+            monkeypatch.delenv("PF_RESID_SPLITK", raising=False)
+        with pf.ToyDiTCuda(0, 2, 1152, 16, 4.0, 4096, 1) as m:
+            return [m.run_pipefusion(x0, 3, 8, 1, 0.1).final_x for _ in range(2)]
+
+    a, b = run(False), run(True)
+    assert np.array_equal(b[0], b[1])
+    rel = float(np.linalg.norm(a[0] - b[0]) / np.linalg.norm(a[0]))
+    assert rel <= 1e-3, rel
