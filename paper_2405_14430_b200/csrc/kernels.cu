@@ -860,6 +860,12 @@ int attn_grid(const AttnLaunch& a, int sm_count) {
   if (halves && a.flags && blocks >= 4 && blocks % 2 == 0 && 2 * items <= sm_count &&
       units / sm_count < blocks)
     return int(2 * items);
+  // A patch (fewer rows than the K/V buffer, M >= 2: patch lanes run other
+  // patches concurrently) whose items fit in one wave: one CTA per item; the
+  // stream-K cuts and their merge cost more than the SMs the other lanes
+  // fill (C2 M = 2: 0.165 vs 0.172 s). Decided by shape only, so every
+  // stage count and lane count picks the same schedule (bitwise-equal runs).
+  if (a.rows < a.P && items <= sm_count) return int(items);
   long long g = sm_count;
   if (units < 2 * g) g = std::max(1LL, units / 2);
   // every item meets at most kAttnMaxParts CTAs: range >= blocks / (parts - 2)

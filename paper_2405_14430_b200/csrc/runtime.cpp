@@ -75,11 +75,8 @@ CUtensorMap tmap(const void* base, uint64_t inner, uint64_t outer,
 }
 
 // The stage's split-K workspace attached to a GEMM's epilogue parameters
-// (split-K itself is opt-in, kernels.cu). Not while patch lanes run
-// concurrently: split-K spreads a skinny GEMM over idle SMs, which the other
-// lanes already use.
+// (skinny residual split-K itself is opt-in, kernels.cu).
 EpiParams sk(const Stage& s, EpiParams ep) {
-  if (s.concurrent) return ep;
   ep.splitk_ws = s.splitk_ws;
   ep.splitk_ws_floats = s.splitk_ws_floats;
   ep.splitk_counters = s.splitk_counters;
@@ -823,7 +820,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       PF_CUDA_CHECK(cudaStreamWaitEvent(s0.extra[k].stream, s0.ev_lane[0], 0));
   }
   int prev_lane = -1;  // lane of the previously enqueued steady patch
-  s0.concurrent = lanes;
   for (int q = 0; q < steady; ++q) {
     const int t = steady - 1 - q;
     for (int j = 0; j < patches; ++j) {
@@ -889,7 +885,6 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       prev_lane = j % nl;
     }
   }
-  s0.concurrent = false;
   if (lanes) {  // join the other lanes back into lane 0
     DeviceGuard g(s0.device);
     use_lane(s0, 0);
@@ -1683,7 +1678,6 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         }
         use_lane(s, op.patch % nl);
       }
-      s.concurrent = forked;
     }
     // plan rows are image rows; joint blocks carry the text rows with the
     // full sequence and with patch 0
@@ -1825,7 +1819,6 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   msgs_out_base_ += per_run;
   if (nl > 1) join_lanes();
   use_lane(s, 0);
-  s.concurrent = false;
   // join: the caller waits for both streams
   PF_CUDA_CHECK(cudaEventRecord(s.ev_fwd, s.stream));
   PF_CUDA_CHECK(cudaStreamWaitEvent(caller, s.ev_fwd, 0));

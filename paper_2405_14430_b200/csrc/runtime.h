@@ -165,7 +165,6 @@ struct Stage {
   } extra[kMaxLanes];
   int lane = 0;
   int lanes_alloc = 1;
-  bool concurrent = false;  // patch lanes active: no split-K (see sk())
   std::vector<cudaEvent_t> ev_attn[kMaxLanes];  // per local layer: the lane's last attention
   cudaEvent_t ev_lane[kMaxLanes] = {};          // lane fork / join
   // stage 0 only
