@@ -414,6 +414,16 @@ class ToyDiTCuda:
         _raise(status, self._err())
         return h, k, v
 
+    def run_distrifusion_device(self, x_dev_ptr: int, steps: int, workers: int,
+                                warmup: int, eta: float, stream_ptr: int = 0) -> StalenessStats:
+        """Enqueue a DistriFusion run on a device fp32 latent (in place); asynchronous."""
+        st = _Stats(0, 0, None, 0)
+        status = self._lib.pf_run_distrifusion_device(
+            self._ctx, ctypes.c_void_p(x_dev_ptr), steps, workers, warmup,
+            ctypes.c_double(eta), ctypes.c_void_p(stream_ptr), ctypes.byref(st))
+        _raise(status, self._err())
+        return StalenessStats(st.fresh_patch_reads, st.stale_patch_reads, [])
+
     def run_pipefusion_device(self, x_dev_ptr: int, steps: int, patches: int,
                               warmup: int, eta: float, stream_ptr: int = 0) -> StalenessStats:
         """Enqueue a run on a device fp32 latent (in place); asynchronous."""

@@ -1305,6 +1305,13 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
     return kv;
   };
   const size_t hs = size_t(m.hs);
+  // Workers of one steady step are independent (each writes only its own
+  // shard's rows of this step's K/V buffer and reads the others' rows of the
+  // previous step's), so they run on the stage's patch lanes, forked at the
+  // start of the step and joined at its end (the next step reads every
+  // shard of this step's buffer and overwrites the one this step read).
+  const int nl = lanes_for(workers);
+  if (nl > 1) alloc_lanes(s, nl);
   for (int step = 0; step < steps; ++step) {
     const int t = steps - 1 - step;
     if (step < warmup) {
@@ -1321,8 +1328,14 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
       }
       check(latent_update(x_dev, s.h32, eta, size_t(m.P) * hs, s.stream), "latent_update");
     } else {
+      if (nl > 1) {
+        PF_CUDA_CHECK(cudaEventRecord(s.ev_lane[0], s.stream));
+        for (int k = 1; k < nl; ++k)
+          PF_CUDA_CHECK(cudaStreamWaitEvent(s.extra[k].stream, s.ev_lane[0], 0));
+      }
       for (int i = 0; i < workers; ++i) {
         const int row0 = i * r;
+        if (nl > 1) use_lane(s, i % nl);
         check(patch_prepare(x_dev, nullptr, s.cb, s.h32, s.hb, row0, r, m.hs, 0.f, false,
                             s.stream), "patch_prepare");
         for (int l = 0; l < s.layer_count; ++l) {
@@ -1336,6 +1349,13 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
         st.fresh_fraction[size_t(i)].push_back(1.0 / double(workers));
         check(latent_update(x_dev + size_t(row0) * hs, s.h32 + size_t(row0) * hs, eta,
                             size_t(r) * hs, s.stream), "latent_update");
+      }
+      if (nl > 1) {
+        use_lane(s, 0);
+        for (int k = 1; k < nl; ++k) {
+          PF_CUDA_CHECK(cudaEventRecord(s.ev_lane[k], s.extra[k].stream));
+          PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, s.ev_lane[k], 0));
+        }
       }
     }
     prev = 1 - prev;  // install: this step's buffer becomes the previous step's

@@ -67,3 +67,16 @@ def test_lanes_joint_equal_one_lane(monkeypatch, L, D, hs, heads, p, T, S, M):
     four = _run(monkeypatch, 4, L, hs, heads, p, S, M, 1, True, reps=2, text=T, joint=D)
     for r in four:
         assert np.array_equal(r.final_x, one.final_x)
+
+
+@pytest.mark.parametrize("workers,L,S,W", [(4, 2, 4, 1), (2, 3, 3, 0)])
+def test_distrifusion_lanes_equal_one_lane(monkeypatch, workers, L, S, W):
+    x0 = pf.make_initial_latent(2, 4096, 1152)
+    res = []
+    for lanes in (1, 4):
+        monkeypatch.setenv("PF_LANES", str(lanes))
+        with pf.ToyDiTCuda(0, L, 1152, 16, 4.0, 4096, 1) as m:
+            res.append([m.run_distrifusion(x0, S, workers, W, 0.1) for _ in range(2)])
+    for r in res[1]:
+        assert np.array_equal(r.final_x, res[0][0].final_x)
+        assert r.stats.per_worker_fresh_fraction == res[0][0].stats.per_worker_fresh_fraction
