@@ -1,2 +1,3 @@
-for M in 8; do timeout 300 python tools/enqueue_probe.py $M 2>&1 | tail -1; done
-which perf 2>/dev/null; ls /usr/bin/*perf* 2>/dev/null | head -3
+timeout 300 python tools/enqueue_probe.py 8 2>&1 | tail -1
+PF_NO_PDL=1 timeout 300 python tools/enqueue_probe.py 8 2>&1 | tail -1
+PF_LANES=1 timeout 300 python tools/enqueue_probe.py 8 2>&1 | tail -1
