@@ -1,0 +1,30 @@
+"""compute-sanitizer workload for the stream-K attention schedules (fused
+in-kernel merge, halves, one CTA per item, separate merge kernel), patch
+lanes and the opt-in residual split-K. Sanitizer input, not a test."""
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2405_14430_b200 as pf  # noqa: E402
+
+lib = pf.load_library()
+s = torch.cuda.current_stream().cuda_stream
+for P, heads, hs, rows, row0 in [(4096, 16, 1152, 4096, 0), (4096, 16, 1152, 512, 1024),
+                                 (4096, 16, 1152, 2048, 0), (3000, 12, 768, 3000, 0)]:
+    q, k, v = [(torch.rand(P, hs, device="cuda") - 0.5).to(torch.bfloat16) for _ in range(3)]
+    out = torch.zeros(P, hs, dtype=torch.bfloat16, device="cuda")
+    assert lib.pf_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), P,
+                                  rows, row0, heads, hs, s) == 0
+    torch.cuda.synchronize()
+x0 = pf.make_initial_latent(0, 512, 128)
+with pf.ToyDiTCuda(0, 2, 128, 4, 4.0, 512, 1) as m:
+    a = m.run_pipefusion(x0, 3, 4, 1, 0.1)
+os.environ["PF_RESID_SPLITK"] = "1"
+os.environ["PF_LANES"] = "1"
+with pf.ToyDiTCuda(0, 1, 1152, 16, 4.0, 1024, 1) as m:
+    b = m.run_pipefusion(pf.make_initial_latent(0, 1024, 1152), 2, 8, 1, 0.1)
+print("ok", np.isfinite(a.final_x).all(), np.isfinite(b.final_x).all())
