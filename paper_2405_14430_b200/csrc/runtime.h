@@ -155,7 +155,7 @@ struct Stage {
   // concurrent patches must not share. The fields above always hold the
   // active lane's resources: use_lane() swaps extra[k] in (lane 0's live in
   // extra[lane] meanwhile).
-  static constexpr int kMaxLanes = 4;
+  static constexpr int kMaxLanes = 8;
   struct Lane {
     cudaStream_t stream = nullptr;
     float* attn_work = nullptr;
@@ -397,7 +397,8 @@ class Engine {
   // records lane_rec_ after its attention (see enqueue_run)
   cudaEvent_t lane_wait_ = nullptr;
   cudaEvent_t lane_rec_ = nullptr;
-  // lanes per stage for M >= 2 (PF_LANES=1..4; PF_ONE_LANE=1 is PF_LANES=1)
+  // lanes per stage for M >= 2 (PF_LANES=1..8, default 4 -- 6 and 8 measured no
+  // faster at C2 M = 8; PF_ONE_LANE=1 is PF_LANES=1)
   int lanes_ = [] {
     const char* one = std::getenv("PF_ONE_LANE");
     if (one && one[0] == '1') return 1;
