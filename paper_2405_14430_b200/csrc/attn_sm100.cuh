@@ -31,6 +31,12 @@
 // computed first and published (partial + release flag), and the tail
 // (CTA c's first segment) is computed last and merged with it in the
 // epilogue -- the flag is long set by then, and no CTA waits on a later one.
+// The same in-kernel merge serves "halves" grids (exactly two CTAs per item,
+// one head and one tail, used for small patches), and patches whose items
+// fit one wave run one CTA per item (no cuts); attn_grid (kernels.cu) picks
+// the schedule from the shape only. Partials are stored column-major
+// ([slot][d][row]: one 128-byte line per warp store), and each softmax warp
+// releases its own flag one KV block after its stores were issued.
 // Roles (384 threads):
 //   warp 0        TMA producer: Q tiles once, then K_i and V_i in two rings
 //   warp 1        MMA issuer: S_{t,i} = Q_t K_i^T (SS: both operands in smem)
@@ -52,9 +58,10 @@
 // (MUFU ~80 % busy inside it, idle during max / row sum). A variant with
 // double-buffered 64-column S buffers per tile (S_{j+1} computed during the
 // softmax of S_j) was 8 % slower: the softmax is not waiting on the MMA.
-// Merging the kv splits inside the kernel (the last-arriving CTA of each
-// query tile group) instead of attn_combine_kernel was 1.75x slower at
-// 512-row patches: the merge then runs on one CTA per (tiles, head).
+// Before the stream-K schedule, merging uniform kv splits inside the kernel
+// (the last-arriving CTA of each query tile group) was 1.75x slower than a
+// separate merge kernel at 512-row patches: the merge then ran on one CTA
+// per (tiles, head) at the end of the critical path.
 #pragma once
 
 #include "kernels.h"  // kAttnFlagsPerCta
