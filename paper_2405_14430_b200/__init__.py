@@ -45,6 +45,7 @@ EXPORTED_SYMBOLS = [
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
     "pf_version", "pf_make_initial_latent", "pf_set_graphs", "pf_set_profiling", "pf_kernel_profile",
     "pf_debug_gemm", "pf_debug_attention", "pf_debug_attention_trace", "pf_debug_gemm_trace",
+    "pf_debug_attn_schedule",
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
@@ -152,6 +153,7 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_debug_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
     lib.pf_debug_attention_trace.argtypes = [i32, vp]
     lib.pf_debug_gemm_trace.argtypes = [i32, vp]
+    lib.pf_debug_attn_schedule.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(ctypes.c_longlong)]
     if path is None:
         _lib = lib
     return lib

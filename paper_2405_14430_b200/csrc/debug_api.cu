@@ -77,6 +77,24 @@ extern "C" int pf_debug_gemm_trace(int enable, unsigned long long* host) {
   return int(cudaGetLastError());
 }
 
+// Host-only: the stream-K attention schedule the library picks for a launch
+// (no GPU needed). out = {nq, blocks, units, grid, cut, fused}.
+extern "C" int pf_debug_attn_schedule(int P, int rows, int heads, int dhp, int sm_count,
+                                      long long* out) {
+  if (!out || P <= 0 || rows <= 0 || heads <= 0 || dhp <= 0 || sm_count <= 0) return 1;
+  static int dummy_flags = 0;
+  pf::AttnLaunch a{dhp, P, rows, 0, heads, dhp, heads * dhp, 1.f, nullptr, nullptr, 0};
+  a.flags = &dummy_flags;  // the runtime always provides merge flags
+  const pf::AttnSchedule sc = pf::attn_schedule(a, sm_count);
+  out[0] = sc.nq;
+  out[1] = sc.blocks;
+  out[2] = sc.units;
+  out[3] = sc.grid;
+  out[4] = sc.cut ? 1 : 0;
+  out[5] = sc.fused ? 1 : 0;
+  return 0;
+}
+
 namespace {
 // device buffer: 8192 clock64 slots of CTA 0, then 4 per CTA (globaltimer at
 // entry / after griddepcontrol.wait / exit, SM id) for up to 1024 CTAs

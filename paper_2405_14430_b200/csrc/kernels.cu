@@ -876,6 +876,26 @@ int attn_grid(const AttnLaunch& a, int sm_count) {
   return int(g);
 }
 
+AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count) {
+  static const bool no_fuse = [] {
+    const char* e = std::getenv("PF_ATTN_SEPARATE_MERGE");
+    return e && e[0] == '1';
+  }();
+  const int rows_per_item = attn_tiles_per_cta(a.dhp) * kAttnBM;
+  AttnSchedule sc;
+  sc.nq = (a.rows + rows_per_item - 1) / rows_per_item;
+  sc.blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  sc.units = (long long)sc.nq * a.heads * sc.blocks;
+  sc.grid = attn_grid(a, sm_count);
+  sc.cut = sc.units % sc.grid != 0 || (sc.units / sc.grid) % sc.blocks != 0;
+  // in-kernel merge when every item meets at most two CTAs, each holding a
+  // head or a tail: ranges of at least one item, or exactly half an item
+  const bool halves = sc.units % sc.grid == 0 && 2 * (sc.units / sc.grid) == sc.blocks;
+  sc.fused = sc.cut && sc.grid >= 2 && a.flags && !no_fuse &&
+             (sc.units / sc.grid >= sc.blocks || halves);
+  return sc;
+}
+
 size_t attn_work_floats(int dhp, int sm_count) {
   return size_t(2) * sm_count * attn_tiles_per_cta(dhp) * kAttnBM * (dhp + 2);
 }
@@ -898,29 +918,22 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   prm.dh = a.dh;
   prm.hs = a.hs;
   prm.scale_log2 = a.scale * 1.4426950408889634f;
-  prm.nq = (a.rows + NT * kAttnBM - 1) / (NT * kAttnBM);
-  prm.blocks = (a.P + kAttnBN - 1) / kAttnBN;
-  prm.units = (long long)prm.nq * a.heads * prm.blocks;
-  prm.grid = attn_grid(a, sm_count);
+  const AttnSchedule sc = attn_schedule(a, sm_count);
+  prm.nq = sc.nq;
+  prm.blocks = sc.blocks;
+  prm.units = sc.units;
+  prm.grid = sc.grid;
   prm.out = a.out;
   prm.part_o = nullptr;
   prm.part_ml = nullptr;
   prm.trace = a.trace;
-  const bool cut = prm.units % prm.grid != 0 || (prm.units / prm.grid) % prm.blocks != 0;
-  static const bool no_fuse = [] {
-    const char* e = std::getenv("PF_ATTN_SEPARATE_MERGE");
-    return e && e[0] == '1';
-  }();
+  const bool cut = sc.cut;
   prm.flags = a.flags;
   for (int i = 0; i < kAttnPrefetchRegions; ++i) {
     prm.pf_ptr[i] = static_cast<const char*>(a.prefetch[i]);
     prm.pf_bytes[i] = a.prefetch[i] ? (a.prefetch_bytes[i] & ~size_t(15)) : 0;
   }
-  // in-kernel merge when every item meets at most two CTAs, each holding a
-  // head or a tail: ranges of at least one item, or exactly half an item
-  const bool halves = prm.units % prm.grid == 0 && 2 * (prm.units / prm.grid) == prm.blocks;
-  prm.fused = (cut && prm.grid >= 2 && a.flags && !no_fuse &&
-               (prm.units / prm.grid >= prm.blocks || halves)) ? 1 : 0;
+  prm.fused = sc.fused ? 1 : 0;
   if (cut) {
     const size_t slots = size_t(2) * prm.grid * NT * kAttnBM;
     if (!a.work || a.work_floats < slots * (DHP + 2)) return cudaErrorInvalidValue;

@@ -159,6 +159,15 @@ struct AttnLaunch {
   size_t prefetch_bytes[kAttnPrefetchRegions] = {};
 };
 int attn_grid(const AttnLaunch& a, int sm_count);
+// The attention launch's schedule (host only): query-tile groups per head,
+// KV blocks per item, units, persistent CTAs, whether items are cut and
+// whether the cut items are merged in-kernel.
+struct AttnSchedule {
+  int nq = 0, blocks = 0, grid = 0;
+  long long units = 0;
+  bool cut = false, fused = false;
+};
+AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count);
 // partial-result workspace the attention needs on a device with sm_count SMs
 size_t attn_work_floats(int dhp, int sm_count);
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
