@@ -95,12 +95,17 @@ int64_t& launch_counter() {
   return count;
 }
 
+bool& pdl_thread_off() {
+  thread_local bool off = false;
+  return off;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PF_NO_PDL");
     return !(e && e[0] == '1');
   }();
-  return on;
+  return on && !pdl_thread_off();
 }
 
 int device_sm_count(int device) {

@@ -31,6 +31,10 @@ int device_sm_count(int device);
 // ptx::pdl_wait() before its first dependent memory access). PF_NO_PDL=1 in
 // the environment turns the attribute off (plain stream serialisation).
 bool pdl_enabled();
+// Per-thread switch: launches enqueued by this thread skip PDL while set
+// (patch lanes: early-launched CTAs waiting on their predecessor would hold
+// SMs the other lanes could use).
+bool& pdl_thread_off();
 // Kernel launches issued by the calling thread. Every launch site in the
 // library bumps it; the runtime reports per-run deltas (pf_last_launch_count).
 int64_t& launch_counter();

@@ -25,6 +25,22 @@ namespace pf {
 
 namespace {
 
+// Patch lanes run without programmatic dependent launch: an early-launched
+// grid waiting on its predecessor holds SMs the other lanes could use
+// (C2 M = 8: 0.201 vs 0.207 s; PF_LANES_PDL=1 keeps PDL). Scoped, per thread.
+struct PdlOff {
+  bool prev;
+  explicit PdlOff(bool lanes) : prev(pdl_thread_off()) { set(lanes); }
+  void set(bool lanes) {
+    static const bool keep = [] {
+      const char* e = std::getenv("PF_LANES_PDL");
+      return e && e[0] == '1';
+    }();
+    pdl_thread_off() = lanes && !keep;
+  }
+  ~PdlOff() { pdl_thread_off() = prev; }
+};
+
 // Counts the kernels a run enqueues (launch_counter() delta over its scope).
 struct LaunchTally {
   int64_t& out;
@@ -820,6 +836,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       PF_CUDA_CHECK(cudaStreamWaitEvent(s0.extra[k].stream, s0.ev_lane[0], 0));
   }
   int prev_lane = -1;  // lane of the previously enqueued steady patch
+  PdlOff pdl_off(lanes);
   for (int q = 0; q < steady; ++q) {
     const int t = steady - 1 - q;
     for (int j = 0; j < patches; ++j) {
@@ -885,6 +902,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       prev_lane = j % nl;
     }
   }
+  pdl_off.set(false);
   if (lanes) {  // join the other lanes back into lane 0
     DeviceGuard g(s0.device);
     use_lane(s0, 0);
@@ -1666,6 +1684,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   }
   bool forked = false, wrote = false;
   int prev_lane = -1;
+  PdlOff pdl_off(false);
   auto ordered_write = [&](cudaStream_t st, uint32_t* addr, uint32_t value) {
     if (nl > 1 && wrote) PF_CUDA_CHECK(cudaStreamWaitEvent(st, ev_write_, 0));
     stream_write(st, addr, value, dev);
@@ -1698,6 +1717,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         }
         use_lane(s, op.patch % nl);
       }
+      pdl_off.set(forked);
     }
     // plan rows are image rows; joint blocks carry the text rows with the
     // full sequence and with patch 0
