@@ -32,9 +32,9 @@
 // (CTA c's first segment) is computed last and merged with it in the
 // epilogue -- the flag is long set by then, and no CTA waits on a later one.
 // The same in-kernel merge serves "halves" grids (exactly two CTAs per item,
-// one head and one tail, used for small patches), and patches whose items
-// fit one wave run one CTA per item (no cuts); attn_grid (kernels.cu) picks
-// the schedule from the shape only. Partials are stored column-major
+// one head and one tail, for full sequences with few items), and patches
+// whose items fit one wave run one CTA per item (no cuts); attn_grid
+// (kernels.cu) picks the schedule from the shape only. Partials are stored column-major
 // ([slot][d][row]: one 128-byte line per warp store), and each softmax warp
 // releases its own flag one KV block after its stores were issued.
 // Roles (384 threads):

@@ -854,9 +854,15 @@ int attn_grid(const AttnLaunch& a, int sm_count) {
   const long long units = items * ((a.P + kAttnBN - 1) / kAttnBN);
   if (per_item) return int(items);
   const long long blocks = (a.P + kAttnBN - 1) / kAttnBN;
-  // Small patches (fewer than sm_count / 2 items): exactly two CTAs per item,
-  // the head half's partial merged in-kernel by the tail half's CTA -- no
-  // separate merge launch, and the SMs left free serve the other patch lanes
+  // A patch (fewer rows than the K/V buffer, M >= 2: patch lanes run other
+  // patches concurrently) whose items fit in one wave: one CTA per item; the
+  // stream-K cuts and their merges cost more than the SMs the other lanes
+  // fill (C2 M = 2 / 4 / 8: 0.172 / 0.188 / 0.204 s with cut schedules vs
+  // 0.166 / 0.177 / 0.200 s). Decided by shape only, so every stage count and
+  // lane count picks the same schedule (bitwise-equal runs).
+  if (a.rows < a.P && items <= sm_count) return int(items);
+  // A full sequence with fewer items than half the SMs: exactly two CTAs per
+  // item, the head half's partial merged in-kernel by the tail half's CTA
   // (PF_ATTN_HALVES=0 keeps the full-grid stream-K schedule)
   static const bool halves = [] {
     const char* e = std::getenv("PF_ATTN_HALVES");
@@ -865,12 +871,6 @@ int attn_grid(const AttnLaunch& a, int sm_count) {
   if (halves && a.flags && blocks >= 4 && blocks % 2 == 0 && 2 * items <= sm_count &&
       units / sm_count < blocks)
     return int(2 * items);
-  // A patch (fewer rows than the K/V buffer, M >= 2: patch lanes run other
-  // patches concurrently) whose items fit in one wave: one CTA per item; the
-  // stream-K cuts and their merge cost more than the SMs the other lanes
-  // fill (C2 M = 2: 0.165 vs 0.172 s). Decided by shape only, so every
-  // stage count and lane count picks the same schedule (bitwise-equal runs).
-  if (a.rows < a.P && items <= sm_count) return int(items);
   long long g = sm_count;
   if (units < 2 * g) g = std::max(1LL, units / 2);
   // every item meets at most kAttnMaxParts CTAs: range >= blocks / (parts - 2)

@@ -5,8 +5,8 @@ CTAs as one head segment and one tail segment (what the kernel's flag protocol
 handles); otherwise cut items meet at most kAttnMaxParts = 8 CTAs (the merge
 kernel's bound) and CTAs hold at most kAttnMaxSegs = 64 segments; schedules of
 C2 shapes are the documented ones (full sequence: stream-K over 148 SMs with
-in-kernel merge; 512-row patches: two CTAs per item; 2048-row patches: one
-CTA per item).
+in-kernel merge; patches: one CTA per item; a small full sequence: two CTAs
+per item).
 """
 import ctypes
 
@@ -78,5 +78,6 @@ def test_schedule_invariants(P, rows, heads, dhp, sms):
 
 def test_c2_schedules():
     assert schedule(4096, 4096, 16, 80)[3:] == (148, True, True)   # stream-K, merged in-kernel
-    assert schedule(4096, 512, 16, 80)[3:] == (64, True, True)     # two CTAs per item
+    assert schedule(4096, 512, 16, 80)[3:] == (32, False, False)    # one CTA per item
+    assert schedule(1024, 1024, 8, 64)[3:] == (64, True, True)     # full sequence, two CTAs per item
     assert schedule(4096, 2048, 16, 80)[3:] == (128, False, False)  # one CTA per item

@@ -97,8 +97,8 @@ def _attn_ref(q, k, v, heads, rows, row0):
     (32, 4, 16, 32, 0, 1.0),        # dh = 4
     (256, 4, 128, 64, 128, 3.0),    # tiny config patch, dh = 32
     (256, 4, 128, 256, 0, 3.0),
-    (1024, 8, 512, 1024, 0, 4.0),   # dh = 64
-    (4096, 16, 1152, 512, 1024, 3.0),  # PixArt patch, dh = 72, two CTAs per item (halves)
+    (1024, 8, 512, 1024, 0, 4.0),   # dh = 64, two CTAs per item (halves, in-kernel merge)
+    (4096, 16, 1152, 512, 1024, 3.0),  # PixArt patch, dh = 72, one CTA per item
     (4096, 16, 1152, 4096, 0, 3.0),    # PixArt full sequence
     (520, 2, 256, 136, 384, 2.0),   # ragged P / rows, dh = 128
     (6144, 24, 1536, 6144, 0, 2.0),  # stream-K, in-kernel merge, dh = 64
