@@ -142,6 +142,10 @@ pf_status pf_create_joint_rank(uint64_t seed, const pf_model_desc* desc, int tex
 size_t pf_peer_blob_size(void);
 pf_status pf_export_peer(pf_ctx* ctx, void* blob, size_t capacity);
 pf_status pf_connect_peers(pf_ctx* ctx, const void* pred_blob, const void* succ_blob);
+/* pf_connect_peers plus every other rank's signal page: blobs[r] is rank r's
+ * blob (all `world` of them). With it a failing rank closes the run for all
+ * ranks, not only its neighbours (see pf_rank_reset). */
+pf_status pf_connect_world(pf_ctx* ctx, const void* const* blobs, int world);
 /* rank / world of a context (0 / 1 for a single-process context) */
 int pf_rank(const pf_ctx* ctx);
 int pf_world(const pf_ctx* ctx);
@@ -151,6 +155,22 @@ int pf_world(const pf_ctx* ctx);
  * op count (ops may be NULL to query it), or -1 on invalid arguments. */
 int64_t pf_rank_plan(int rank, int world, int steps, int patches, int warmup, int64_t seq_len,
                      int32_t* ops, int64_t capacity);
+
+/* Channel close in rank mode (Channel::close, channel.hpp:26-57; close_all on
+ * a worker failure, execute.cpp:246-251,345-374). A rank whose run fails
+ * (an error while it enqueues its plan) returns that error, after marking
+ * the run closed in every connected rank's signal page and playing the rest
+ * of its plan's message protocol without compute, so no peer blocks. The
+ * peers' pf_run_pipefusion / pf_synchronize then return PF_NUMERIC "channel
+ * closed mid-run" (their own non-finite activation, the root cause, is
+ * reported first when present); the next run works normally. A rank whose
+ * waits see no progress for PF_RANK_TIMEOUT_S seconds (default 600: a peer
+ * died or never ran) releases its own and its neighbours' waits and fails
+ * the same way; the message counters of the ranks then disagree, so every
+ * later run fails until pf_rank_reset has been called on every rank (with a
+ * host barrier before and after it). pf_rank_broken: 1 in that state. */
+pf_status pf_rank_reset(pf_ctx* ctx);
+int pf_rank_broken(const pf_ctx* ctx);
 
 void pf_destroy(pf_ctx* ctx);
 
@@ -199,6 +219,30 @@ pf_status pf_serial_reference(pf_ctx* ctx, const double* x_init,
                               pf_layout layout, int steps, double eta,
                               double* x_out);
 
+/* ditsim::serial_reference(toy, x_init, steps, eta, keep_trajectory) --
+ * execute.hpp:98-104, toy_model.cpp:201-214, with the trajectory:
+ * `trajectory` (NULL = keep_trajectory false) receives (steps + 1)
+ * matrices of seq_len x hidden_size in `layout`, matrix k at
+ * trajectory + k * seq_len * hidden_size: k = 0 the initial latent, k the
+ * latent after k update steps (SerialResult::trajectory). Single-process
+ * contexts only for a trajectory. */
+pf_status pf_serial_reference_ex(pf_ctx* ctx, const double* x_init, pf_layout layout,
+                                 int steps, double eta, double* x_out, double* trajectory);
+
+/* ditsim::auto_warmup(toy, x_init, steps, eta, threshold) -- execute.hpp:141-147,
+ * toy_model.cpp:230-249: synchronous steps until ||x_k - x_{k-1}|| /
+ * ||x_{k-1}|| < threshold; *warmup = k (or steps), *threshold_met = 1/0.
+ * The norms are fp64 reductions on the GPU. Single-process contexts. */
+pf_status pf_auto_warmup(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps,
+                         double eta, double threshold, int* warmup, int* threshold_met);
+
+/* ditsim::divergence(a, b) = ||a - b||_F / ||b||_F -- execute.hpp:136-137,
+ * toy_model.cpp:216-228 (fp64, on ctx's stage-0 GPU; the norm is
+ * layout-independent). PF_VALIDATION with the reference's messages on a shape
+ * mismatch or a zero reference. */
+pf_status pf_divergence(pf_ctx* ctx, const double* a, int64_t a_rows, int64_t a_cols,
+                        const double* b, int64_t b_rows, int64_t b_cols, double* out);
+
 /* ditsim::toy_layer_forward(layer, heads, h, k_buf, v_buf, row0) --
  * execute.hpp:75-77, toy_model.cpp:169-177, for unit parity: rows
  * [row0, row0+rows) of h pass through global layer `layer` against the given
@@ -224,7 +268,10 @@ pf_status pf_make_initial_latent(uint64_t seed, int64_t seq_len, int hidden_size
 /* CUDA graphs (default on): the first run of a given (latent buffer,
  * steps, patches, warmup, eta, stream) is captured into a CUDA graph and
  * later runs replay it -- one graph launch per image. Disabled automatically
- * while profiling, on the legacy default stream, and across several devices. */
+ * while profiling, on the legacy default stream, and for single-process
+ * contexts whose stages span several devices. In rank mode every rank
+ * captures its own plan; the signal waits / writes become graph memory-op
+ * nodes whose message counts are re-based before each replay. */
 pf_status pf_set_graphs(pf_ctx* ctx, int enabled);
 
 /* Per-kernel CUDA-event profile (no reference analogue). When enabled, every

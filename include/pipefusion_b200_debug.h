@@ -43,6 +43,16 @@ int pf_debug_gemm_trace(int enable, unsigned long long* host);
 // blocks per item, units, persistent CTAs, items cut (0/1), merged in-kernel (0/1)}.
 int pf_debug_attn_schedule(int P, int rows, int heads, int dhp, int sm_count, long long* out);
 
+/* Failure injection for the channel-close tests (rank mode): ctx's next runs
+ * throw when its plan loop reaches op `op` (-1 disables), after which the
+ * rank closes the pipeline (pf_rank_reset reopens it). ctx is a pf_ctx*.
+ * Returns a pf_status value. */
+struct pf_ctx;
+int pf_debug_fail_at(struct pf_ctx* ctx, int op);
+/* Makes global layer `layer`'s out-projection weight NaN (non-finite
+ * activations from that layer on). Returns a pf_status value. */
+int pf_debug_poison_layer(struct pf_ctx* ctx, int layer);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ __all__ = [
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
     "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda", "rank_plan",
     "PLAN_KINDS", "connect_ranks", "connect_distributed", "trace_json", "JointDiTCuda",
+    "SerialResult", "AutoWarmupResult", "root_cause", "reset_distributed",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
@@ -45,7 +46,8 @@ EXPORTED_SYMBOLS = [
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
     "pf_version", "pf_make_initial_latent", "pf_set_graphs", "pf_set_profiling", "pf_kernel_profile",
     "pf_debug_gemm", "pf_debug_attention", "pf_debug_attention_trace", "pf_debug_gemm_trace",
-    "pf_debug_attn_schedule",
+    "pf_debug_attn_schedule", "pf_serial_reference_ex", "pf_auto_warmup", "pf_divergence",
+    "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_debug_fail_at", "pf_debug_poison_layer",
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
@@ -112,9 +114,18 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
                                        ctypes.POINTER(vp)]
     lib.pf_create_pixart_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32,
                                           i32, i32, ctypes.POINTER(vp)]
+    lib.pf_serial_reference_ex.argtypes = [vp, dptr, i32, i32, dbl, dptr, dptr]
+    lib.pf_auto_warmup.argtypes = [vp, dptr, i32, i32, dbl, dbl, ctypes.POINTER(i32),
+                                   ctypes.POINTER(i32)]
+    lib.pf_divergence.argtypes = [vp, dptr, i64, i64, dptr, i64, i64, dptr]
+    lib.pf_rank_reset.argtypes = [vp]
+    lib.pf_rank_broken.argtypes = [vp]
+    lib.pf_debug_fail_at.argtypes = [vp, i32]
+    lib.pf_debug_poison_layer.argtypes = [vp, i32]
     lib.pf_peer_blob_size.restype = ctypes.c_size_t
     lib.pf_export_peer.argtypes = [vp, vp, ctypes.c_size_t]
     lib.pf_connect_peers.argtypes = [vp, vp, vp]
+    lib.pf_connect_world.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p), i32]
     lib.pf_rank.argtypes = [vp]
     lib.pf_world.argtypes = [vp]
     lib.pf_rank_plan.argtypes = [i32, i32, i32, i32, i32, i64, ctypes.POINTER(ctypes.c_int32),
@@ -193,6 +204,53 @@ class StalenessStats:
 
 
 @dataclass
+class SerialResult:
+    """ditsim::SerialResult (execute.hpp:93-98): trajectory[0] is the initial
+    latent, trajectory[k] the latent after k update steps."""
+    final_x: np.ndarray
+    trajectory: List[np.ndarray] = field(default_factory=list)
+    timestep: int = -1
+
+
+@dataclass
+class AutoWarmupResult:
+    """ditsim::AutoWarmupResult (execute.hpp:139-142)."""
+    warmup: int = 0
+    threshold_met: bool = False
+
+
+_NONFINITE = "non-finite activation at timestep "
+_CLOSED = "channel closed mid-run"
+
+
+def root_cause(errors: Sequence[Optional[BaseException]]) -> Optional[BaseException]:
+    """The error a failed multi-rank run reports, given each rank's error in
+    rank order (None = that rank succeeded): the reference prefers a root
+    cause over the "channel closed mid-run" cascade (execute.cpp:357-374).
+    Ranks here detect non-finite activations after the run, so a NaN that
+    travelled on to later stages is reported by several ranks: the earliest
+    in execution order (highest timestep, then lowest layer) is the root."""
+    first = next((e for e in errors if e is not None), None)
+    roots = [e for e in errors if e is not None and not str(e).startswith(_CLOSED)]
+    if not roots:
+        return first
+    nonfinite = []
+    for e in roots:
+        m = str(e)
+        if isinstance(e, NumericError) and m.startswith(_NONFINITE):
+            try:
+                t, layer = m[len(_NONFINITE):].split(", layer ")
+                nonfinite.append((-int(t), int(layer), e))
+            except ValueError:
+                pass
+    parsed = {id(v[2]) for v in nonfinite}
+    others = [e for e in roots if id(e) not in parsed]
+    if others:  # a failure other than a travelling NaN: first in rank order
+        return others[0]
+    return min(nonfinite, key=lambda v: v[:2])[2]
+
+
+@dataclass
 class ParallelRunResult:
     """ditsim::ParallelRunResult (execute.hpp:116-119); final timestep is -1."""
     final_x: np.ndarray
@@ -208,20 +266,18 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
-def _out_buffer(owner, x: np.ndarray) -> np.ndarray:
-    """Result latent for a host-buffer run. Reuses an array this context
-    returned earlier once the caller has dropped every reference to it (views
-    included): first-touch page faults of a fresh 37 MB array cost ~5 ms at
-    C2, more than the device-to-host copy itself."""
-    pool = owner.__dict__.setdefault("_out_pool", [])
-    for a in pool:
-        # references: the pool list, the loop variable, getrefcount's argument
-        if a.shape == x.shape and sys.getrefcount(a) == 3:
-            return a
-    a = np.empty_like(x)
-    if len(pool) < 4:
-        pool.append(a)
-    return a
+def _out_buffer(x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Result latent for a host-buffer run: the caller's `out` (float64,
+    C-contiguous, x's shape; reusing one array across runs avoids the
+    first-touch page faults of a fresh 37 MB array, ~5 ms at C2) or a new
+    array. The library never keeps or reuses a returned array itself."""
+    if out is None:
+        return np.empty_like(x)
+    if (not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != x.shape
+            or not out.flags.c_contiguous or not out.flags.writeable):
+        raise ValidationError("out must be a writeable C-contiguous float64 array of the "
+                              "latent's shape")
+    return out
 
 
 class ToyDiTCuda:
@@ -304,6 +360,12 @@ class ToyDiTCuda:
     def connect_peers(self, pred: bytes, succ: bytes) -> None:
         _raise(self._lib.pf_connect_peers(self._ctx, pred, succ), self._err())
 
+    def connect_world(self, blobs: Sequence[bytes]) -> None:
+        """Connect to the neighbours and open every rank's signal page
+        (pf_connect_world): a failing rank then closes the run for all."""
+        arr = (ctypes.c_char_p * len(blobs))(*blobs)
+        _raise(self._lib.pf_connect_world(self._ctx, arr, len(blobs)), self._err())
+
     @classmethod
     def from_weights(cls, layer_mats, condition_bias, heads: int, seq_len: int,
                      workers: int = 1, devices=None) -> "ToyDiTCuda":
@@ -351,9 +413,35 @@ class ToyDiTCuda:
         return int(self._lib.pf_last_launch_count(self._ctx))
 
     # ---------------------------------------------------------------- runs
+    def _rank_status(self, status: int) -> None:
+        """Raise this rank's error; with a process group attached
+        (connect_distributed), every rank raises the run's root cause
+        (root_cause) so all ranks report the same failure."""
+        group = getattr(self, "_group", False)  # set by connect_distributed
+        if self.world <= 1 or group is False:
+            _raise(status, self._err())
+            return
+        import torch.distributed as dist
+        mine = None if status == PF_OK else (status, self._err())
+        allv = [None] * self.world
+        dist.all_gather_object(allv, mine, group=group)
+        errs = []
+        for v in allv:
+            if v is None:
+                errs.append(None)
+                continue
+            try:
+                _raise(*v)
+            except Exception as e:  # noqa: BLE001 - rebuilt per rank
+                errs.append(e)
+        err = root_cause(errs)
+        if err is not None:
+            raise err
+
     def run_pipefusion(self, x_init, steps: int, patches: int, warmup: int,
-                       eta: float) -> ParallelRunResult:
-        """ditsim::run_pipefusion (execute.hpp:124-127) on the GPU stages."""
+                       eta: float, out: Optional[np.ndarray] = None) -> ParallelRunResult:
+        """ditsim::run_pipefusion (execute.hpp:124-127) on the GPU stages.
+        `out`: optional float64 array receiving the final latent."""
         per = max(0, patches * (steps - warmup))
         stages = 1 if self.world > 1 else self.workers
         cap = stages * per
@@ -364,18 +452,18 @@ class ToyDiTCuda:
             status = self._lib.pf_run_pipefusion(self._ctx, None, PF_ROW_MAJOR, steps, patches,
                                                  warmup, ctypes.c_double(eta), None,
                                                  ctypes.byref(st))
-            _raise(status, self._err())
+            self._rank_status(status)
             return ParallelRunResult(None, StalenessStats(st.fresh_patch_reads,
                                                           st.stale_patch_reads,
                                                           [list(ff[:per])]))
         x = _f64c(x_init)
         if x.shape != (self.seq_len, self.hidden_size):
             raise ValidationError("latent width does not match the model hidden size")
-        out = _out_buffer(self, x)
+        out = _out_buffer(x, out)
         status = self._lib.pf_run_pipefusion(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
                                              patches, warmup, ctypes.c_double(eta),
                                              _dptr(out), ctypes.byref(st))
-        _raise(status, self._err())
+        self._rank_status(status)
         fr = [list(ff[d * per:(d + 1) * per]) for d in range(stages)]
         return ParallelRunResult(out, StalenessStats(st.fresh_patch_reads,
                                                      st.stale_patch_reads, fr))
@@ -384,7 +472,7 @@ class ToyDiTCuda:
                          eta: float) -> ParallelRunResult:
         """ditsim::run_distrifusion (execute.hpp:131-133) on this context's GPU."""
         x = _f64c(x_init)
-        out = _out_buffer(self, x)
+        out = _out_buffer(x)
         per = max(0, steps - warmup)
         cap = workers * per
         ff = (ctypes.c_double * max(1, cap))()
@@ -397,14 +485,62 @@ class ToyDiTCuda:
         return ParallelRunResult(out, StalenessStats(st.fresh_patch_reads,
                                                      st.stale_patch_reads, fr))
 
-    def serial_reference(self, x_init, steps: int, eta: float) -> np.ndarray:
-        """ditsim::serial_reference (execute.hpp:102-104) on the GPU."""
+    def serial_reference(self, x_init, steps: int, eta: float, keep_trajectory: bool = False):
+        """ditsim::serial_reference (execute.hpp:102-104) on the GPU: the final
+        latent, or with keep_trajectory a SerialResult holding the S + 1
+        latents of the trajectory (pf_serial_reference_ex)."""
         x = _f64c(x_init)
-        out = _out_buffer(self, x)
-        status = self._lib.pf_serial_reference(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
-                                               ctypes.c_double(eta), _dptr(out))
+        out = _out_buffer(x)
+        if not keep_trajectory:
+            status = self._lib.pf_serial_reference(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
+                                                   ctypes.c_double(eta), _dptr(out))
+            _raise(status, self._err())
+            return out
+        traj = np.empty((max(steps, 0) + 1,) + x.shape)
+        status = self._lib.pf_serial_reference_ex(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
+                                                  ctypes.c_double(eta), _dptr(out),
+                                                  _dptr(traj))
         _raise(status, self._err())
-        return out
+        return SerialResult(out, list(traj))
+
+    def auto_warmup(self, x_init, steps: int, eta: float, threshold: float) -> AutoWarmupResult:
+        """ditsim::auto_warmup (execute.hpp:141-147) on the GPU."""
+        x = _f64c(x_init)
+        w, met = ctypes.c_int(0), ctypes.c_int(0)
+        status = self._lib.pf_auto_warmup(self._ctx, _dptr(x), PF_ROW_MAJOR, steps,
+                                          ctypes.c_double(eta), ctypes.c_double(threshold),
+                                          ctypes.byref(w), ctypes.byref(met))
+        _raise(status, self._err())
+        return AutoWarmupResult(w.value, bool(met.value))
+
+    def divergence(self, a, b) -> float:
+        """ditsim::divergence (execute.hpp:136-137): ||a - b|| / ||b||, fp64 on the GPU."""
+        a, b = _f64c(a), _f64c(b)
+        a2 = a.reshape(a.shape[0], -1) if a.ndim else a.reshape(1, 1)
+        b2 = b.reshape(b.shape[0], -1) if b.ndim else b.reshape(1, 1)
+        out = ctypes.c_double()
+        status = self._lib.pf_divergence(self._ctx, _dptr(a2), a2.shape[0], a2.shape[1],
+                                         _dptr(b2), b2.shape[0], b2.shape[1], ctypes.byref(out))
+        _raise(status, self._err())
+        return out.value
+
+    # ---------------------------------------------------------------- rank mode
+    def rank_reset(self) -> None:
+        """Reopen a pipeline the watchdog closed (pf_rank_reset); call on every
+        rank between two host barriers (reset_distributed does that)."""
+        _raise(self._lib.pf_rank_reset(self._ctx), self._err())
+
+    @property
+    def rank_broken(self) -> bool:
+        return bool(self._lib.pf_rank_broken(self._ctx))
+
+    def debug_fail_at(self, op: int) -> None:
+        """Test hook: this rank's next runs throw at plan op `op` (-1: off)."""
+        _raise(self._lib.pf_debug_fail_at(self._ctx, op), self._err())
+
+    def debug_poison_layer(self, layer: int) -> None:
+        """Test hook: layer `layer`'s out-projection produces NaN."""
+        _raise(self._lib.pf_debug_poison_layer(self._ctx, layer), self._err())
 
     def layer_forward(self, layer: int, h, k_buf, v_buf, row0: int):
         """ditsim::toy_layer_forward (execute.hpp:75-77); returns (h, k, v)."""
@@ -535,19 +671,29 @@ def rank_plan(rank: int, world: int, steps: int, patches: int, warmup: int,
 def connect_ranks(stages: Sequence[ToyDiTCuda]) -> None:
     """Connect the rank-mode contexts of one process (stages[d] = rank d)."""
     blobs = [s.export_peer() for s in stages]
-    n = len(stages)
-    for d, s in enumerate(stages):
-        s.connect_peers(blobs[(d - 1) % n], blobs[(d + 1) % n])
+    for s in stages:
+        s.connect_world(blobs)
 
 
-def connect_distributed(stage: ToyDiTCuda, group=None) -> None:
+def connect_distributed(stage: ToyDiTCuda, group=None, agree_on_errors: bool = True) -> None:
     """Connect this process's rank-mode context to its neighbours, exchanging
-    peer blobs over torch.distributed (any backend; gloo is enough)."""
+    peer blobs over torch.distributed (any backend; gloo is enough). With
+    agree_on_errors, host-buffer runs (run_pipefusion) all-gather each rank's
+    status afterwards and every rank raises the run's root cause."""
     import torch.distributed as dist
     blobs = [None] * stage.world
     dist.all_gather_object(blobs, stage.export_peer(), group=group)
-    d, n = stage.rank, stage.world
-    stage.connect_peers(blobs[(d - 1) % n], blobs[(d + 1) % n])
+    stage.connect_world(blobs)
+    stage._group = group if agree_on_errors else False
+
+
+def reset_distributed(stage: ToyDiTCuda, group=None) -> None:
+    """Reopen a pipeline closed by a failed run: barrier, pf_rank_reset on
+    every rank, barrier."""
+    import torch.distributed as dist
+    dist.barrier(group=group)
+    stage.rank_reset()
+    dist.barrier(group=group)
 
 
 def trace_json(spans: Sequence[dict]) -> dict:

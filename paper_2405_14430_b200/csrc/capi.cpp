@@ -3,11 +3,14 @@
 
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
+#include "pipefusion_b200_debug.h"
 #include "runtime.h"
 
 struct pf_ctx {
@@ -206,6 +209,19 @@ pf_status pf_connect_peers(pf_ctx* ctx, const void* pred_blob, const void* succ_
     std::memcpy(&pred, pred_blob, sizeof(pred));
     std::memcpy(&succ, succ_blob, sizeof(succ));
     ctx->engine->connect_peers(pred, succ);
+  });
+}
+
+pf_status pf_connect_world(pf_ctx* ctx, const void* const* blobs, int world) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (!blobs || world < 1) throw pf::ValidationError("NULL peer blobs");
+    std::vector<pf::PeerBlob> v(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+      if (!blobs[r]) throw pf::ValidationError("NULL peer blob");
+      std::memcpy(&v[size_t(r)], blobs[r], sizeof(pf::PeerBlob));
+    }
+    ctx->engine->connect_world(v);
   });
 }
 
@@ -561,6 +577,177 @@ pf_status pf_serial_reference(pf_ctx* ctx, const double* x_init, pf_layout layou
   // W = S with one patch: every step is a full-sequence synchronous forward
   // with freshly written K/V, which is serial_reference (toy_model.cpp:201-214).
   return pf_run_pipefusion(ctx, x_init, layout, steps, 1, steps, eta, x_out, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Device buffer freed on scope exit.
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) {
+    if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess) {
+      cudaGetLastError();
+      throw pf::CudaError("cudaMalloc failed");
+    }
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct DeviceScope {
+  int prev = 0;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceScope() { cudaSetDevice(prev); }
+};
+
+// W = S full-sequence steps with the engine's serial tap attached: every step
+// is toy_forward on the whole latent with freshly written K/V, i.e.
+// serial_reference (toy_model.cpp:201-214). The tap collects what
+// keep_trajectory and auto_warmup need on the device.
+void serial_tapped(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps, double eta,
+                   pf::Engine::SerialTap& tap) {
+  pf::Engine& eng = *ctx->engine;
+  if (eng.rank_mode())
+    throw pf::ValidationError("serial trajectory / auto_warmup need a single-process context");
+  upload_x(ctx, x_init, layout);
+  const pf::Stage& s0 = eng.stage(0);
+  struct Untap { pf::Engine& e; ~Untap() { e.set_serial_tap(nullptr); } } untap{eng};
+  eng.set_serial_tap(&tap);
+  eng.run(ctx->x_scratch, steps, 1, steps, float(eta), s0.stream, nullptr);
+  eng.finish(s0.stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+pf_status pf_serial_reference_ex(pf_ctx* ctx, const double* x_init, pf_layout layout,
+                                 int steps, double eta, double* x_out, double* trajectory) {
+  if (!ctx) return PF_VALIDATION;
+  if (!trajectory) return pf_serial_reference(ctx, x_init, layout, steps, eta, x_out);
+  return guarded(&ctx->last_error, [&] {
+    if (steps < 1) throw pf::ValidationError("serial_reference needs steps >= 1");
+    if (!x_init || !x_out) throw pf::ValidationError("NULL latent pointer");
+    const pf::ModelShape& m = ctx->engine->shape();
+    const size_t n = size_t(m.P) * m.hs;
+    DeviceScope dev(ctx->engine->stage(0).device);
+    DevBuf traj(size_t(steps + 1) * n * sizeof(float));
+    pf::Engine::SerialTap tap;
+    tap.traj = traj.as<float>();
+    serial_tapped(ctx, x_init, layout, steps, eta, tap);
+    const pf::Stage& s0 = ctx->engine->stage(0);
+    for (int k = 0; k <= steps; ++k) {
+      cudaError_t e = pf::latent_to_f64(tap.traj + size_t(k) * n, ctx->x64_scratch, m.P, m.hs,
+                                        layout == PF_COL_MAJOR, s0.stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(trajectory + size_t(k) * n, ctx->x64_scratch, n * 8,
+                            cudaMemcpyDeviceToHost, s0.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s0.stream);
+      if (e != cudaSuccess)
+        throw pf::CudaError(std::string("trajectory download: ") + cudaGetErrorString(e));
+    }
+    std::memcpy(x_out, trajectory + size_t(steps) * n, n * sizeof(double));
+  });
+}
+
+pf_status pf_auto_warmup(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps,
+                         double eta, double threshold, int* warmup, int* threshold_met) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (steps < 1) throw pf::ValidationError("auto_warmup needs steps >= 1");
+    if (!x_init || !warmup) throw pf::ValidationError("NULL pointer");
+    DeviceScope dev(ctx->engine->stage(0).device);
+    DevBuf sums(size_t(2 * steps) * sizeof(double));
+    DevBuf work(pf::sumsq_work_bytes());
+    pf::Engine::SerialTap tap;
+    tap.sums = sums.as<double>();
+    tap.work = work.p;
+    std::string failure;
+    try {
+      serial_tapped(ctx, x_init, layout, steps, eta, tap);
+    } catch (const pf::NumericError& e) {
+      failure = e.what();  // raised below unless an earlier step met the threshold
+    }
+    std::vector<double> h(size_t(2 * steps));
+    if (cudaMemcpy(h.data(), tap.sums, h.size() * sizeof(double), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+      throw pf::CudaError("auto_warmup: reading the step norms failed");
+    // toy_model.cpp:236-248: relative = ||x_k - x_{k-1}|| / ||x_{k-1}||
+    for (int k = 1; k <= steps; ++k) {
+      const double xx = h[size_t(2 * (k - 1))], dd = h[size_t(2 * (k - 1) + 1)];
+      if (!std::isfinite(xx) || !std::isfinite(dd)) break;  // the step that failed
+      const double denom = std::sqrt(xx), change = std::sqrt(dd);
+      const double relative =
+          denom > 0.0 ? change / denom
+                      : (change == 0.0 ? 0.0 : std::numeric_limits<double>::infinity());
+      if (relative < threshold) {
+        *warmup = k;
+        if (threshold_met) *threshold_met = 1;
+        return;
+      }
+    }
+    if (!failure.empty()) throw pf::NumericError(failure);
+    *warmup = steps;
+    if (threshold_met) *threshold_met = 0;
+  });
+}
+
+pf_status pf_divergence(pf_ctx* ctx, const double* a, int64_t a_rows, int64_t a_cols,
+                        const double* b, int64_t b_rows, int64_t b_cols, double* out) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    if (a_rows != b_rows || a_cols != b_cols) {
+      std::ostringstream os;
+      os << "divergence shape mismatch: " << a_rows << "x" << a_cols << " vs " << b_rows << "x"
+         << b_cols;
+      throw pf::ValidationError(os.str());
+    }
+    if (!a || !b || !out) throw pf::ValidationError("NULL pointer");
+    const size_t n = size_t(a_rows) * size_t(a_cols);
+    const pf::Stage& s0 = ctx->engine->stage(0);
+    DeviceScope dev(s0.device);
+    DevBuf da(n * 8), db(n * 8), work(pf::sumsq_work_bytes()), res(2 * sizeof(double));
+    cudaError_t e = cudaMemcpyAsync(da.p, a, n * 8, cudaMemcpyHostToDevice, s0.stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, s0.stream);
+    if (e == cudaSuccess)
+      e = pf::sumsq_diff(da.as<double>(), db.as<double>(), n, work.p, res.as<double>(),
+                         s0.stream);
+    double h[2] = {0, 0};
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h, res.p, sizeof(h), cudaMemcpyDeviceToHost, s0.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s0.stream);
+    if (e != cudaSuccess) throw pf::CudaError(std::string("divergence: ") + cudaGetErrorString(e));
+    // toy_model.cpp:216-228
+    const double denom = std::sqrt(h[1]);
+    if (denom == 0.0) throw pf::ValidationError("divergence undefined against a zero reference");
+    *out = std::sqrt(h[0]) / denom;
+  });
+}
+
+pf_status pf_rank_reset(pf_ctx* ctx) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] { ctx->engine->rank_reset(); });
+}
+
+int pf_rank_broken(const pf_ctx* ctx) { return ctx && ctx->engine->rank_broken() ? 1 : 0; }
+
+int pf_debug_fail_at(pf_ctx* ctx, int op) {
+  if (!ctx) return PF_VALIDATION;
+  ctx->engine->debug_fail_at(op);
+  return PF_OK;
+}
+
+int pf_debug_poison_layer(pf_ctx* ctx, int layer) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] { ctx->engine->debug_poison_layer(layer); });
 }
 
 pf_status pf_layer_forward(pf_ctx* ctx, int layer, double* h, int64_t rows,

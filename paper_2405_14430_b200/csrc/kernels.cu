@@ -1120,6 +1120,83 @@ cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+namespace {
+// Deterministic fp64 pair of sums of squares (fixed grid, fixed reduction
+// order: reruns and stage counts give identical bits).
+constexpr int kSumBlocks = 296, kSumThreads = 256;
+
+template <class T>
+__device__ void sumsq_pair_block(double a, double b, double2* part) {
+  __shared__ double sa[kSumThreads], sb[kSumThreads];
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = kSumThreads / 2; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) {
+      sa[threadIdx.x] += sa[threadIdx.x + w];
+      sb[threadIdx.x] += sb[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(sa[0], sb[0]);
+}
+
+// part[blk] = (sum x^2, sum (eta e)^2) over fp32 x, e
+__global__ void sumsq_latent_kernel(const float* __restrict__ x, const float* __restrict__ e,
+                                    double eta, size_t n, double2* __restrict__ part) {
+  double a = 0.0, b = 0.0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double xv = x[i], d = eta * double(e[i]);
+    a += xv * xv;
+    b += d * d;
+  }
+  sumsq_pair_block<float>(a, b, part);
+}
+
+// part[blk] = (sum (a - b)^2, sum b^2) over fp64 a, b
+__global__ void sumsq_diff_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                  size_t n, double2* __restrict__ part) {
+  double u = 0.0, v = 0.0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double d = a[i] - b[i];
+    u += d * d;
+    v += b[i] * b[i];
+  }
+  sumsq_pair_block<double>(u, v, part);
+}
+
+__global__ void sumsq_finish_kernel(const double2* __restrict__ part, int n, double* out) {
+  double2 acc = make_double2(0.0, 0.0);
+  for (int i = 0; i < n; ++i) {  // fixed order
+    acc.x += part[i].x;
+    acc.y += part[i].y;
+  }
+  out[0] = acc.x;
+  out[1] = acc.y;
+}
+}  // namespace
+
+size_t sumsq_work_bytes() { return size_t(kSumBlocks) * sizeof(double2); }
+
+cudaError_t sumsq_latent(const float* x, const float* eps, double eta, size_t n, void* work,
+                         double* out, cudaStream_t stream) {
+  launch_counter() += 2;
+  sumsq_latent_kernel<<<kSumBlocks, kSumThreads, 0, stream>>>(x, eps, eta, n,
+                                                               static_cast<double2*>(work));
+  sumsq_finish_kernel<<<1, 1, 0, stream>>>(static_cast<double2*>(work), kSumBlocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t sumsq_diff(const double* a, const double* b, size_t n, void* work, double* out,
+                       cudaStream_t stream) {
+  launch_counter() += 2;
+  sumsq_diff_kernel<<<kSumBlocks, kSumThreads, 0, stream>>>(a, b, n, static_cast<double2*>(work));
+  sumsq_finish_kernel<<<1, 1, 0, stream>>>(static_cast<double2*>(work), kSumBlocks, out);
+  return cudaGetLastError();
+}
+
 cudaError_t reset_flag(int* flag, cudaStream_t stream) {
   ++launch_counter();
   reset_flag_kernel<<<1, 1, 0, stream>>>(flag);

@@ -215,6 +215,16 @@ cudaError_t px_patch_prepare(float* x, const float* eps, const float* cb, const 
                              float* h32, bf16* hb, float2* stats, int stats_ld, int row0,
                              int rows, int hs, float eta, bool update, cudaStream_t stream);
 
+// Deterministic fp64 reductions (fixed grid and order), for auto_warmup and
+// divergence (toy_model.cpp:216-249). `work`: sumsq_work_bytes() of scratch.
+// out[0] = sum x^2, out[1] = sum (eta eps)^2  over n fp32 elements
+size_t sumsq_work_bytes();
+cudaError_t sumsq_latent(const float* x, const float* eps, double eta, size_t n, void* work,
+                         double* out, cudaStream_t stream);
+// out[0] = sum (a - b)^2, out[1] = sum b^2  over n fp64 elements
+cudaError_t sumsq_diff(const double* a, const double* b, size_t n, void* work, double* out,
+                       cudaStream_t stream);
+
 // Device-side finite-check flag reset: *flag = INT_MAX
 cudaError_t reset_flag(int* flag, cudaStream_t stream);
 

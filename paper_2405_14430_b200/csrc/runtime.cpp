@@ -5,8 +5,12 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <chrono>
 #include <mutex>
+#include <random>
 #include <sstream>
+#include <thread>
+#include <type_traits>
 
 #include <unistd.h>
 
@@ -108,6 +112,67 @@ void check(cudaError_t e, const char* what) {
   }
 }
 
+// Graph nodes of captured stream memory operations (batch mem-op nodes):
+// enumerated once after capture, their values patched before a replay.
+struct GraphMemOps {
+  CUresult (*node_type)(CUgraphNode, CUgraphNodeType*) = nullptr;
+  CUresult (*get)(CUgraphNode, CUDA_BATCH_MEM_OP_NODE_PARAMS*) = nullptr;
+  CUresult (*exec_set)(CUgraphExec, CUgraphNode, const CUDA_BATCH_MEM_OP_NODE_PARAMS*) = nullptr;
+};
+
+const GraphMemOps& graph_memops() {
+  static GraphMemOps g;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    auto get = [](const char* name, auto& fn) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+    };
+    get("cuGraphNodeGetType", g.node_type);
+    get("cuGraphBatchMemOpNodeGetParams", g.get);
+    get("cuGraphExecBatchMemOpNodeSetParams", g.exec_set);
+  });
+  if (!g.node_type || !g.get || !g.exec_set)
+    throw CudaError("graph batch memory-operation entry points are unavailable");
+  return g;
+}
+
+// Per-process identity for PeerBlob: hostname + boot id, and a random nonce.
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ULL) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ULL;
+  return h;
+}
+uint64_t host_identity() {
+  static const uint64_t id = [] {
+    char host[256] = {0};
+    gethostname(host, sizeof(host) - 1);
+    std::string boot;
+    if (FILE* f = std::fopen("/proc/sys/kernel/random/boot_id", "r")) {
+      char buf[64] = {0};
+      if (std::fgets(buf, sizeof(buf), f)) boot = buf;
+      std::fclose(f);
+    }
+    return fnv1a(boot, fnv1a(host));
+  }();
+  return id;
+}
+uint64_t process_nonce() {
+  static const uint64_t n = [] {
+    std::random_device rd;
+    return (uint64_t(rd()) << 32) ^ uint64_t(rd()) ^ uint64_t(getpid());
+  }();
+  return n;
+}
+
+constexpr uint32_t kAbortSpan = 1u << 30;  // abort value = run base + kAbortSpan
+
+// stream memory operations (rank mode), defined with the rank-mode code
+void stream_wait_geq(cudaStream_t st, const uint32_t* addr, uint32_t value, int device);
+void stream_write(cudaStream_t st, uint32_t* addr, uint32_t value, int device);
+
 }  // namespace
 
 void validate_shape(const ModelShape& s) {
@@ -204,11 +269,13 @@ Engine::~Engine() {
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t e : ev_sent_) cudaEventDestroy(e);
     if (ev_compute_) cudaEventDestroy(ev_compute_);
+    for (cudaEvent_t e : ev_write_)
+      if (e) cudaEventDestroy(e);
     if (send_stream_) cudaStreamDestroy(send_stream_);
+    if (abort_stream_) cudaStreamDestroy(abort_stream_);
     dfree(sig_);
   }
-  for (auto& kv : graphs_)
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  drop_graphs();
   for (size_t d = 0; d < prof_pool_.size() && d < stages_.size(); ++d) {
     DeviceGuard g(stages_[d].device);
     for (cudaEvent_t e : prof_pool_[d]) cudaEventDestroy(e);
@@ -330,11 +397,15 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
 }
 
 // Per-run PixArt buffers, sized for `steps` timesteps (outside any capture).
-static void px_alloc_run(Stage& s, const ModelShape& m, int steps) {
+// Growing them frees the old buffers, which captured graphs of earlier runs
+// still reference: those graphs are dropped first.
+void Engine::px_alloc_run(Stage& s, int steps) {
+  const ModelShape& m = shape_;
   PxStage& px = s.px;
   if (steps <= px.steps_cap) return;
   DeviceGuard g(s.device);
-  if (s.stream) cudaStreamSynchronize(s.stream);
+  cudaDeviceSynchronize();  // a replayed graph may still read the old buffers
+  drop_graphs();
   for (float* p : {px.sinus, px.e1, px.temb, px.tv, px.mod, px.foldq, px.foldm}) dfree(p);
   dfree(px.fold_aq);
   dfree(px.fold_am);
@@ -357,6 +428,14 @@ static void px_alloc_run(Stage& s, const ModelShape& m, int steps) {
   px.foldq = dalloc<float>(nl * 2 * S * 3 * hs);
   px.foldm = dalloc<float>(nl * 2 * S * size_t(m.mlp));
   px.steps_cap = steps;
+}
+
+void Engine::drop_graphs() {
+  for (auto& kv : graphs_) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  graphs_.clear();
 }
 
 void Engine::free_stage(Stage& s) {
@@ -776,6 +855,12 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
   float* h32_img = s0.h32 + size_t(J) * m.hs;  // image row 0 of the activations
   bf16* hb_img = s0.hb + size_t(J) * m.hs;
 
+  const size_t n_lat = size_t(m.P) * m.hs;
+  if (tap_ && tap_->traj) {
+    DeviceGuard g(s0.device);
+    PF_CUDA_CHECK(cudaMemcpyAsync(tap_->traj, x_dev, n_lat * 4, cudaMemcpyDeviceToDevice,
+                                  s0.stream));
+  }
   // ---- warmup: synchronous full-sequence steps (execute.cpp:181-190)
   for (int w = 0; w < warmup; ++w) {
     const int t = steps - 1 - w;
@@ -812,9 +897,15 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[0], 0));
     }
     DeviceGuard g(s0.device);
+    if (tap_ && tap_->sums)  // auto_warmup's ||x|| and ||x_next - x|| (toy_model.cpp:238-241)
+      check(sumsq_latent(x_dev, s0.eps, double(eta), n_lat, tap_->work, tap_->sums + 2 * w,
+                         s0.stream), "sumsq_latent");
     prof_begin(s0, kSampler, 0, double(m.P) * m.hs * 12);
     check(latent_update(x_dev, s0.eps, eta, size_t(m.P) * m.hs, s0.stream), "latent_update");
     prof_end(s0);
+    if (tap_ && tap_->traj)
+      PF_CUDA_CHECK(cudaMemcpyAsync(tap_->traj + size_t(w + 1) * n_lat, x_dev, n_lat * 4,
+                                    cudaMemcpyDeviceToDevice, s0.stream));
   }
 
   // ---- steady: patch pipeline (execute.cpp:192-212)
@@ -837,6 +928,24 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
   }
   int prev_lane = -1;  // lane of the previously enqueued steady patch
   PdlOff pdl_off(lanes);
+  // On a throw mid-loop: clear the lane hand-off events and leave the stage
+  // on lane 0 with every lane joined (errors ignored: the run is abandoned).
+  struct LaneUnwind {
+    Engine* e;
+    Stage& s;
+    int nl;
+    bool armed = true;
+    ~LaneUnwind() {
+      if (!armed) return;
+      e->lane_wait_ = e->lane_rec_ = nullptr;
+      e->use_lane(s, 0);
+      for (int k = 1; k < nl; ++k) {
+        cudaEventRecord(s.ev_lane[k], s.extra[k].stream);
+        cudaStreamWaitEvent(s.stream, s.ev_lane[k], 0);
+      }
+      cudaGetLastError();
+    }
+  } lane_unwind{this, s0, nl};
   for (int q = 0; q < steady; ++q) {
     const int t = steady - 1 - q;
     for (int j = 0; j < patches; ++j) {
@@ -903,6 +1012,7 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     }
   }
   pdl_off.set(false);
+  lane_unwind.armed = false;
   if (lanes) {  // join the other lanes back into lane 0
     DeviceGuard g(s0.device);
     use_lane(s0, 0);
@@ -935,7 +1045,7 @@ void Engine::prepare_run(int patches, int steps) {
   const int n = stage_count();
   Stage& s0 = stages_[0];
   if (shape_.block == kBlockPixArt && steps >= 1)
-    for (Stage& s : stages_) px_alloc_run(s, shape_, steps);
+    for (Stage& s : stages_) px_alloc_run(s, steps);
   if (!ev_start_) {
     DeviceGuard g(s0.device);
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
@@ -960,13 +1070,14 @@ void Engine::prepare_run(int patches, int steps) {
 void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
                  cudaStream_t caller, RunStats* stats) {
   if (rank_mode()) {
-    enqueue_rank_run(x_dev, steps, patches, warmup, eta, caller, stats);
+    run_rank(x_dev, steps, patches, warmup, eta, caller, stats);
     return;
   }
   if (patches >= 1) prepare_run(patches, steps);
   bool single_device = true;
   for (const Stage& s : stages_) single_device &= s.device == stages_[0].device;
-  if (!graphs_enabled_ || profiling_ || timeline_on_ || caller == nullptr || !single_device) {
+  if (!graphs_enabled_ || profiling_ || timeline_on_ || caller == nullptr || !single_device ||
+      tap_) {
     enqueue_run(x_dev, steps, patches, warmup, eta, caller, stats);
     return;
   }
@@ -1004,23 +1115,245 @@ void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
 void Engine::finish(cudaStream_t caller) {
   {
     DeviceGuard g(stages_[0].device);
-    PF_CUDA_CHECK(cudaStreamSynchronize(caller));
-    if (send_stream_) PF_CUDA_CHECK(cudaStreamSynchronize(send_stream_));
+    wait_stream(caller);
+    if (send_stream_) wait_stream(send_stream_);
   }
   int first = INT_MAX;
   for (Stage& s : stages_) {
     DeviceGuard g(s.device);
-    PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
+    wait_stream(s.stream);
     int f = INT_MAX;
     PF_CUDA_CHECK(cudaMemcpy(&f, s.flag, sizeof(int), cudaMemcpyDeviceToHost));
     first = std::min(first, f);
   }
+  // the root cause (this rank's own non-finite activation) is preferred over
+  // the cascade (a neighbour closed the channel), as execute.cpp:357-374
   if (first != INT_MAX && first >= 0 && size_t(first) < codes_.size()) {
     std::ostringstream os;
     os << "non-finite activation at timestep " << codes_[size_t(first)].first
        << ", layer " << codes_[size_t(first)].second;
     throw NumericError(os.str());
   }
+  if (rank_mode() && run_epoch_ > 0) {
+    if (broken_) throw NumericError("channel closed mid-run (no progress from a peer rank)");
+    uint32_t aborted = 0;
+    DeviceGuard g(stages_[0].device);
+    PF_CUDA_CHECK(cudaMemcpy(&aborted, sig_ + 2, sizeof(aborted), cudaMemcpyDeviceToHost));
+    if (aborted == run_epoch_) throw NumericError("channel closed mid-run");
+  }
+}
+
+void Engine::wait_stream(cudaStream_t st) {
+  if (!rank_mode()) {
+    PF_CUDA_CHECK(cudaStreamSynchronize(st));
+    return;
+  }
+  // Watchdog: a peer that died or stopped enqueueing leaves this rank's
+  // signal waits blocked forever. After rank_timeout_s_ without completion,
+  // release them (own pages) and the neighbours' (the pipeline is closed).
+  using clock = std::chrono::steady_clock;
+  auto t0 = clock::now();
+  bool aborted = false;
+  int spins = 0;
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) PF_CUDA_CHECK(e);
+    const double waited = std::chrono::duration<double>(clock::now() - t0).count();
+    if (waited > rank_timeout_s_) {
+      if (aborted) throw NumericError("channel closed mid-run (stream did not drain after abort)");
+      watchdog_abort();
+      aborted = true;
+      t0 = clock::now();
+    }
+    if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+void Engine::prepare_rank_run(int patches, int steps) {
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  if (shape_.block == kBlockPixArt) px_alloc_run(s, steps);
+  while (int(ev_sent_.size()) < patches) {
+    cudaEvent_t e;
+    PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_sent_.push_back(e);
+  }
+  if (!ev_start_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+  for (cudaEvent_t& e : ev_write_)
+    if (!e) PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int nl = std::min(lanes_, patches);
+  if (nl > 1) alloc_lanes(s, nl);
+}
+
+void Engine::run_rank(float* x_dev, int steps, int patches, int warmup, float eta,
+                      cudaStream_t caller, RunStats* stats) {
+  if (!connected_) throw ValidationError("rank-mode engine is not connected to its peers");
+  if (broken_)
+    throw NumericError("channel closed mid-run (an earlier run of this pipeline was aborted; "
+                       "call pf_rank_reset on every rank)");
+  // identical on every rank: fails everywhere before anything is enqueued
+  validate_run(steps, patches, warmup);
+  ++run_epoch_;
+  DeviceGuard g(stages_[0].device);
+  const bool graph = graphs_enabled_ && !profiling_ && !timeline_on_ && caller != nullptr &&
+                     fail_at_op_ < 0;
+  try {
+    if (!graph) {
+      enqueue_rank_run(x_dev, steps, patches, warmup, eta, caller, stats);
+      return;
+    }
+    if (rank_ == 0 && !x_dev) throw ValidationError("NULL latent pointer");
+    prepare_rank_run(patches, steps);
+    const GraphMemOps& gm = graph_memops();
+    uint32_t eta_bits;
+    std::memcpy(&eta_bits, &eta, sizeof(eta_bits));
+    const GraphKey key{x_dev, steps, patches, warmup, eta_bits, caller};
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+      // Capture this rank's plan once. The signal waits / writes become
+      // batch mem-op nodes whose values hold the capture-time base; later
+      // replays patch them to their own base (message counters never reset).
+      GraphEntry e;
+      const uint32_t in0 = msgs_in_base_, out0 = msgs_out_base_;
+      PF_CUDA_CHECK(cudaStreamBeginCapture(caller, cudaStreamCaptureModeThreadLocal));
+      cudaGraph_t graph_h = nullptr;
+      try {
+        enqueue_rank_run(x_dev, steps, patches, warmup, eta, caller, &e.stats);
+      } catch (...) {
+        // nothing of the plan was executed: close the run and play the
+        // message protocol without compute, then report the root cause
+        const std::exception_ptr failure = std::current_exception();
+        cudaStreamEndCapture(caller, &graph_h);
+        if (graph_h) cudaGraphDestroy(graph_h);
+        cudaGetLastError();
+        msgs_in_base_ = in0;
+        msgs_out_base_ = out0;
+        close_channels();
+        enqueue_rank_run(x_dev, steps, patches, warmup, eta, caller, nullptr, true);
+        std::rethrow_exception(failure);
+      }
+      PF_CUDA_CHECK(cudaStreamEndCapture(caller, &graph_h));
+      msgs_in_base_ = in0;  // the capture executed nothing
+      msgs_out_base_ = out0;
+      e.graph = graph_h;
+      e.base = in0;
+      e.launches = launches_;
+      e.codes = codes_;
+      size_t n = 0;
+      PF_CUDA_CHECK(cudaGraphGetNodes(graph_h, nullptr, &n));
+      std::vector<cudaGraphNode_t> nodes(n);
+      PF_CUDA_CHECK(cudaGraphGetNodes(graph_h, nodes.data(), &n));
+      for (cudaGraphNode_t nd : nodes) {
+        CUgraphNodeType t;
+        if (gm.node_type(reinterpret_cast<CUgraphNode>(nd), &t) != CUDA_SUCCESS)
+          throw CudaError("cuGraphNodeGetType failed");
+        if (t != CU_GRAPH_NODE_TYPE_BATCH_MEM_OP) continue;
+        CUDA_BATCH_MEM_OP_NODE_PARAMS prm;
+        if (gm.get(reinterpret_cast<CUgraphNode>(nd), &prm) != CUDA_SUCCESS)
+          throw CudaError("cuGraphBatchMemOpNodeGetParams failed");
+        GraphEntry::MemOpNode mn;
+        mn.node = nd;
+        for (unsigned k = 0; k < prm.count; ++k) {
+          const CUstreamBatchMemOpParams& op = prm.paramArray[k];
+          uint32_t v = 0;
+          if (op.operation == CU_STREAM_MEM_OP_WAIT_VALUE_32) v = op.waitValue.value;
+          else if (op.operation == CU_STREAM_MEM_OP_WRITE_VALUE_32) v = op.writeValue.value;
+          else throw CudaError("unexpected memory operation in a captured rank plan");
+          mn.delta.push_back(v - in0);
+        }
+        e.memops.push_back(std::move(mn));
+      }
+      PF_CUDA_CHECK(cudaGraphInstantiate(&e.exec, graph_h, 0));
+      it = graphs_.emplace(key, std::move(e)).first;
+    }
+    GraphEntry& e = it->second;
+    if (e.base != msgs_in_base_) {
+      for (GraphEntry::MemOpNode& mn : e.memops) {
+        CUDA_BATCH_MEM_OP_NODE_PARAMS prm;
+        if (gm.get(reinterpret_cast<CUgraphNode>(mn.node), &prm) != CUDA_SUCCESS)
+          throw CudaError("cuGraphBatchMemOpNodeGetParams failed");
+        std::vector<CUstreamBatchMemOpParams> ops(prm.paramArray, prm.paramArray + prm.count);
+        for (size_t k = 0; k < ops.size(); ++k) {
+          const uint32_t v = msgs_in_base_ + mn.delta[k];
+          if (ops[k].operation == CU_STREAM_MEM_OP_WAIT_VALUE_32) ops[k].waitValue.value = v;
+          else ops[k].writeValue.value = v;
+        }
+        prm.paramArray = ops.data();
+        if (gm.exec_set(reinterpret_cast<CUgraphExec>(e.exec),
+                        reinterpret_cast<CUgraphNode>(mn.node), &prm) != CUDA_SUCCESS)
+          throw CudaError("cuGraphExecBatchMemOpNodeSetParams failed");
+      }
+      e.base = msgs_in_base_;
+    }
+    run_base_ = msgs_in_base_;
+    PF_CUDA_CHECK(cudaGraphLaunch(e.exec, caller));
+    const uint32_t per_run = uint32_t(plan_messages_per_run(steps, patches, warmup));
+    msgs_in_base_ += per_run;
+    msgs_out_base_ += per_run;
+    launches_ = e.launches;
+    codes_ = e.codes;
+    if (stats) *stats = e.stats;
+  } catch (const ValidationError&) {
+    if (rank_ == 0 && !x_dev) {  // rank 0 alone: the peers are waiting for it
+      close_channels();
+      enqueue_rank_run(nullptr, steps, patches, warmup, eta, caller, nullptr, true);
+    }
+    throw;
+  }
+}
+
+void Engine::close_channels() {
+  if (!rank_mode() || !connected_) return;
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  std::vector<uint32_t*> pages = world_sig_;
+  if (pages.empty()) pages = {pred_sig_, succ_sig_};
+  pages.push_back(sig_);
+  for (uint32_t* page : pages)
+    if (page) stream_write(abort_stream_, page + 2, run_epoch_, s.device);
+  PF_CUDA_CHECK(cudaStreamSynchronize(abort_stream_));
+}
+
+void Engine::watchdog_abort() {
+  if (!rank_mode() || !connected_) return;
+  broken_ = true;
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  const int dev = s.device;
+  close_channels();
+  // every wait of this run (own and neighbours') passes: >= base + kAbortSpan
+  const uint32_t release = run_base_ + kAbortSpan;
+  stream_write(abort_stream_, sig_, release, dev);
+  stream_write(abort_stream_, sig_ + 1, release, dev);
+  if (succ_sig_) stream_write(abort_stream_, succ_sig_, release, dev);
+  if (pred_sig_) stream_write(abort_stream_, pred_sig_ + 1, release, dev);
+  cudaStreamSynchronize(abort_stream_);
+  cudaGetLastError();
+}
+
+void Engine::rank_reset() {
+  if (!rank_mode()) return;
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  PF_CUDA_CHECK(cudaDeviceSynchronize());
+  PF_CUDA_CHECK(cudaMemset(sig_, 0, 64 * sizeof(uint32_t)));
+  PF_CUDA_CHECK(cudaDeviceSynchronize());
+  msgs_in_base_ = msgs_out_base_ = 0;
+  run_epoch_ = 0;
+  run_base_ = 0;
+  broken_ = false;
+}
+
+void Engine::debug_poison_layer(int layer) {
+  const int d = stage_of_layer(layer);
+  if (d < 0) throw ValidationError("layer index out of range");
+  Stage& s = stages_[size_t(d)];
+  DeviceGuard g(s.device);
+  const bf16 nan = __float2bfloat16_rn(NAN);
+  bf16* w = s.layers[size_t(layer - s.first_layer)].wo;
+  PF_CUDA_CHECK(cudaMemcpy(w, &nan, sizeof(nan), cudaMemcpyHostToDevice));
+  drop_graphs();
 }
 
 void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0,
@@ -1070,7 +1403,7 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
   if (m.block == kBlockPixArt) {
     if (steps < 1 || t < 0 || t >= steps)
       throw ValidationError("timestep index outside [0, steps)");
-    px_alloc_run(s, m, steps);
+    px_alloc_run(s, steps);
     px_conditioning(s, steps);
     const int lf = layer - s.first_layer;
     const float* scale1 = s.px.mod + (size_t(lf) * steps + t) * 6 * hs + hs;
@@ -1458,6 +1791,7 @@ void stream_write(cudaStream_t st, uint32_t* addr, uint32_t value, int device) {
     throw CudaError("cuStreamWriteValue32 failed");
 }
 
+
 }  // namespace
 
 Engine::Engine(const ModelShape& shape_in, int device, int rank, int world)
@@ -1489,7 +1823,10 @@ Engine::Engine(const ModelShape& shape_in, int device, int rank, int world)
     alloc_stage(s, first, last - first, rank == 0);
     DeviceGuard g(device);
     PF_CUDA_CHECK(cudaStreamCreateWithFlags(&send_stream_, cudaStreamNonBlocking));
+    PF_CUDA_CHECK(cudaStreamCreateWithFlags(&abort_stream_, cudaStreamNonBlocking));
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_compute_, cudaEventDisableTiming));
+    // signal page: [0] messages delivered here, [1] acknowledgements from the
+    // successor, [2] epoch of a run a neighbour aborted (0: none)
     sig_ = dalloc<uint32_t>(64);
     if (rank == 0 && world > 1) {
       s.eps = dalloc<float>(size_t(shape_.P) * shape_.hs);
@@ -1511,6 +1848,8 @@ PeerBlob Engine::export_peer() {
   b.device = s.device;
   b.block = shape_.block;
   b.pid = int64_t(getpid());
+  b.host_id = host_identity();
+  b.nonce = process_nonce();
   std::memset(&b.h_h32, 0, sizeof(b.h_h32));
   std::memset(&b.h_hb, 0, sizeof(b.h_hb));
   std::memset(&b.h_stats, 0, sizeof(b.h_stats));
@@ -1540,9 +1879,15 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
     throw ValidationError("peer blobs do not belong to this rank's neighbours");
   Stage& s = stages_[0];
   DeviceGuard g(s.device);
-  const int64_t me = int64_t(getpid());
+  for (const PeerBlob* b : {&pred, &succ})
+    if (b->host_id != host_identity()) {
+      std::ostringstream os;
+      os << "peer rank " << b->rank << " lives on another host: stage boundaries need peer "
+         << "memory (CUDA IPC over NVLink) within one node";
+      throw ValidationError(os.str());
+    }
   auto open = [&](const PeerBlob& b, const cudaIpcMemHandle_t& h, uint64_t raw) -> void* {
-    if (b.pid == me) {
+    if (b.nonce == process_nonce() && b.pid == int64_t(getpid())) {
       // same process: UVA pointer; enable peer access when on another device
       if (b.device != s.device) {
         int ok = 0;
@@ -1593,11 +1938,36 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
   connected_ = true;
 }
 
+void Engine::connect_world(const std::vector<PeerBlob>& blobs) {
+  if (!rank_mode()) throw ValidationError("connect_world needs a rank-mode engine");
+  if (int(blobs.size()) != world_) throw ValidationError("connect_world needs one blob per rank");
+  for (int r = 0; r < world_; ++r)
+    if (blobs[size_t(r)].rank != r) throw ValidationError("peer blobs are not in rank order");
+  connect_peers(blobs[size_t((rank_ - 1 + world_) % world_)], blobs[size_t((rank_ + 1) % world_)]);
+  Stage& s = stages_[0];
+  DeviceGuard g(s.device);
+  world_sig_.clear();
+  for (int r = 0; r < world_; ++r) {
+    if (r == rank_) continue;
+    const PeerBlob& b = blobs[size_t(r)];
+    if (r == (rank_ + 1) % world_) { world_sig_.push_back(succ_sig_); continue; }
+    if (r == (rank_ - 1 + world_) % world_) { world_sig_.push_back(pred_sig_); continue; }
+    if (b.nonce == process_nonce() && b.pid == int64_t(getpid())) {
+      world_sig_.push_back(reinterpret_cast<uint32_t*>(b.p_sig));
+    } else {
+      void* p = nullptr;
+      PF_CUDA_CHECK(cudaIpcOpenMemHandle(&p, b.h_sig, cudaIpcMemLazyEnablePeerAccess));
+      ipc_opened_.push_back(p);
+      world_sig_.push_back(static_cast<uint32_t*>(p));
+    }
+  }
+}
+
 // One rank's share of run_pipefusion (rank_plan.h): its stage's layers on the
 // compute stream, boundary transfers on the send stream, and the message
 // protocol as stream-ordered waits/writes on the peers' signal pages.
 void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, float eta,
-                              cudaStream_t caller, RunStats* stats) {
+                              cudaStream_t caller, RunStats* stats, bool skip_all) {
   const ModelShape& m = shape_;
   if (!connected_) throw ValidationError("rank-mode engine is not connected to its peers");
   validate_run(steps, patches, warmup);
@@ -1608,16 +1978,9 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   const bool px = m.block == kBlockPixArt;
   const int r = int(m.P / patches);
   const size_t hs = size_t(m.hs);
-  if (px) px_alloc_run(s, m, steps);
-  if (int(ev_sent_.size()) < patches) {
-    while (int(ev_sent_.size()) < patches) {
-      cudaEvent_t e;
-      PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      ev_sent_.push_back(e);
-    }
-  }
-  if (!ev_start_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+  prepare_rank_run(patches, steps);
   std::vector<bool> sent_before(size_t(patches), false);
+  run_base_ = msgs_in_base_;
 
   RunStats local;
   RunStats& st = stats ? *stats : local;
@@ -1678,19 +2041,20 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   }();
   const int nl = (fused && enough_queues && !profiling_ && !timeline_on_)
                      ? std::min(lanes_, patches) : 1;
-  if (nl > 1) {
-    alloc_lanes(s, nl);
-    if (!ev_write_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_write_, cudaEventDisableTiming));
-  }
-  bool forked = false, wrote = false;
+  if (nl > 1) alloc_lanes(s, nl);
+  bool forked = false, wrote[2] = {false, false};
   int prev_lane = -1;
   PdlOff pdl_off(false);
-  auto ordered_write = [&](cudaStream_t st, uint32_t* addr, uint32_t value) {
-    if (nl > 1 && wrote) PF_CUDA_CHECK(cudaStreamWaitEvent(st, ev_write_, 0));
+  // Signal writes of one counter keep plan order across lanes (chain 0:
+  // acknowledgements to the predecessor, chain 1: message counts to the
+  // successor); the two counters are independent, so acks of a lane never
+  // wait for another lane's compute.
+  auto ordered_write = [&](int chain, cudaStream_t st, uint32_t* addr, uint32_t value) {
+    if (nl > 1 && wrote[chain]) PF_CUDA_CHECK(cudaStreamWaitEvent(st, ev_write_[chain], 0));
     stream_write(st, addr, value, dev);
     if (nl > 1) {
-      PF_CUDA_CHECK(cudaEventRecord(ev_write_, st));
-      wrote = true;
+      PF_CUDA_CHECK(cudaEventRecord(ev_write_[chain], st));
+      wrote[chain] = true;
     }
   };
   auto join_lanes = [&]() {
@@ -1702,9 +2066,23 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
     }
     forked = false;
   };
-  for (size_t oi = 0; oi < plan.size(); ++oi) {
-    const PlanOp& op = plan[oi];
-    if (nl > 1) {
+  // Channel close (execute.cpp:345-348): when an op throws, this rank closes
+  // the run -- the abort word of every rank's signal page is set -- and
+  // finishes its plan in skip mode: the message protocol only (receive
+  // waits, acknowledgements, message counts), no compute. Every peer's wait
+  // of the run is then satisfied exactly as in a good run, so the counters
+  // stay consistent for the next run, and the peers report "channel closed
+  // mid-run" from finish(). The op that threw is redone in skip mode (its
+  // signal values are absolute, so a repeated write or wait is harmless).
+  bool skip = skip_all;
+  std::exception_ptr failure;
+  auto do_op = [&](size_t oi, const PlanOp& op) {
+    if (!skip && int(oi) == fail_at_op_) {
+      std::ostringstream os;
+      os << "injected failure at plan op " << oi << " of rank " << rank_;
+      throw NumericError(os.str());
+    }
+    if (nl > 1 && !skip) {
       if (op.patch < 0 || op.kind == PlanOp::kLatentUpdate) {
         join_lanes();
       } else {
@@ -1729,10 +2107,11 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         stream_wait_geq(s.stream, sig_, base_in + uint32_t(op.msg), dev);
         break;
       case PlanOp::kAck:
-        ordered_write(op.flag && !fused ? send_stream_ : s.stream, pred_sig_ + 1,
+        ordered_write(0, op.flag && !fused ? send_stream_ : s.stream, pred_sig_ + 1,
                       base_in + uint32_t(op.msg));
         break;
       case PlanOp::kPrepare: {
+        if (skip) break;
         // this rank's previous send of the same rows must have finished reading h32
         for (int j = 0; j < patches; ++j)
           if ((op.patch < 0 || op.patch == j) && sent_before[size_t(j)])
@@ -1752,11 +2131,21 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         break;
       }
       case PlanOp::kLatentUpdate:
+        if (skip) break;
         prof_begin(s, kSampler, 0, double(m.P) * hs * 12);
         check(latent_update(x_dev, s.eps, eta, size_t(m.P) * hs, s.stream), "latent_update");
         prof_end(s);
         break;
       case PlanOp::kCompute: {
+        if (skip) {  // the fused send's protocol part only
+          if (fused && oi + 1 < plan.size() && plan[oi + 1].kind == PlanOp::kSend) {
+            const PlanOp& sn = plan[oi + 1];
+            if (sn.overlap > 0)
+              stream_wait_geq(s.stream, sig_ + 1, base_out + uint32_t(sn.overlap), dev);
+            ordered_write(1, s.stream, succ_sig_, base_out + uint32_t(sn.msg));
+          }
+          break;
+        }
         const int t = op.t;
         if (rank_ != 0) tl_begin(rank_, 0, op.patch, t, s.stream);
         for (int lf = 0; lf < s.layer_count; ++lf) {
@@ -1802,7 +2191,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           redirect_ = nullptr;
           lane_wait_ = lane_rec_ = nullptr;
           if (send) {
-            ordered_write(s.stream, succ_sig_, base_out + uint32_t(send->msg));
+            ordered_write(1, s.stream, succ_sig_, base_out + uint32_t(send->msg));
             for (int j = 0; j < patches; ++j)
               if (send->patch < 0 || send->patch == j) {
                 PF_CUDA_CHECK(cudaEventRecord(ev_sent_[size_t(j)], s.stream));
@@ -1821,6 +2210,12 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
       }
       case PlanOp::kSend: {
         if (fused) break;  // stored by the last MLP-out GEMM, signalled after it
+        if (skip) {
+          if (op.overlap > 0)
+            stream_wait_geq(s.stream, sig_ + 1, base_out + uint32_t(op.overlap), dev);
+          ordered_write(1, s.stream, succ_sig_, base_out + uint32_t(op.msg));
+          break;
+        }
         PF_CUDA_CHECK(cudaEventRecord(ev_compute_, s.stream));
         PF_CUDA_CHECK(cudaStreamWaitEvent(send_stream_, ev_compute_, 0));
         if (op.overlap > 0)
@@ -1844,7 +2239,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           }
         }
         tl_end(send_stream_);
-        ordered_write(send_stream_, succ_sig_, base_out + uint32_t(op.msg));
+        ordered_write(1, send_stream_, succ_sig_, base_out + uint32_t(op.msg));
         for (int j = 0; j < patches; ++j)
           if (op.patch < 0 || op.patch == j) {
             PF_CUDA_CHECK(cudaEventRecord(ev_sent_[size_t(j)], send_stream_));
@@ -1852,6 +2247,21 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
           }
         break;
       }
+    }
+  };
+  for (size_t oi = 0; oi < plan.size(); ++oi) {
+    try {
+      do_op(oi, plan[oi]);
+    } catch (...) {
+      if (skip) throw;  // the protocol itself failed (CUDA error): nothing left to do
+      failure = std::current_exception();
+      skip = true;
+      redirect_ = nullptr;
+      lane_wait_ = lane_rec_ = nullptr;
+      join_lanes();
+      pdl_off.set(false);
+      close_channels();
+      do_op(oi, plan[oi]);
     }
   }
   const uint32_t per_run = uint32_t(plan_messages_per_run(steps, patches, warmup));
@@ -1864,6 +2274,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
   PF_CUDA_CHECK(cudaStreamWaitEvent(caller, s.ev_fwd, 0));
   PF_CUDA_CHECK(cudaEventRecord(ev_compute_, send_stream_));
   PF_CUDA_CHECK(cudaStreamWaitEvent(caller, ev_compute_, 0));
+  if (failure) std::rethrow_exception(failure);
 }
 
 // ============================================================== PixArt block

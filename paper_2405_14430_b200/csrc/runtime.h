@@ -218,6 +218,9 @@ struct PeerBlob {
   uint32_t magic = 0x50465042;  // "PFPB"
   int32_t rank = 0, world = 1, device = 0, block = 0;
   int64_t pid = 0;
+  // host identity (hostname + boot id) and a random per-process nonce: PIDs
+  // alone collide across PID namespaces / containers / hosts
+  uint64_t host_id = 0, nonce = 0;
   cudaIpcMemHandle_t h_h32, h_hb, h_stats, h_eps, h_sig;
   uint64_t p_h32 = 0, p_hb = 0, p_stats = 0, p_eps = 0, p_sig = 0;
 };
@@ -263,8 +266,32 @@ class Engine {
   bool owns_layer(int layer) const { return stage_of_layer(layer) >= 0; }
   PeerBlob export_peer();
   void connect_peers(const PeerBlob& pred, const PeerBlob& succ);
+  // skip_all: the message protocol only, no compute (a rank that failed
+  // before anything of its plan was enqueued, e.g. during graph capture)
   void enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, float eta,
-                        cudaStream_t caller, RunStats* stats);
+                        cudaStream_t caller, RunStats* stats, bool skip_all = false);
+  // Channel close (the reference's Channel::close, channel.hpp:26-57, and
+  // close_all on a worker failure, execute.cpp:246-251,345-374). A rank
+  // whose run throws sets the abort word (the run's epoch) in the signal page
+  // of every rank it knows (all ranks after connect_world, else its two
+  // neighbours) and finishes its plan in skip mode (message protocol only),
+  // so no peer blocks; the peers' finish() raises "channel closed mid-run",
+  // and the next run starts from consistent counters.
+  void close_channels();
+  // Watchdog (finish() saw no progress for rank_timeout_s_, e.g. a peer
+  // died): release this rank's own and its neighbours' waits with values
+  // past every message of the run. The counters no longer agree afterwards:
+  // the pipeline stays closed until rank_reset() on every rank.
+  void watchdog_abort();
+  void rank_reset();
+  // Also open every rank's signal page (blobs[r] of rank r) so a failing
+  // rank can close the run for all of them; connects the neighbours too.
+  void connect_world(const std::vector<PeerBlob>& blobs);
+  bool rank_broken() const { return broken_; }
+  // test hook: throw from the plan loop when reaching op `op` (-1: off)
+  void debug_fail_at(int op) { fail_at_op_ = op; }
+  // test hook: make global layer `layer`'s out-projection produce NaN
+  void debug_poison_layer(int layer);
 
   const ModelShape& shape() const { return shape_; }
   int stage_count() const { return int(stages_.size()); }
@@ -281,6 +308,17 @@ class Engine {
   void run(float* x_dev, int steps, int patches, int warmup, float eta,
            cudaStream_t caller, RunStats* stats);
   void set_graphs(bool on) { graphs_enabled_ = on; }
+  // serial_reference(keep_trajectory) / auto_warmup taps on the warmup
+  // (full-sequence) steps of the next runs (single-process engines, no graph
+  // replay while set): per warmup step w, sums[2w], sums[2w+1] = ||x||^2,
+  // ||eta eps||^2 before the update (device fp64), and traj + (w+1) n = x
+  // after it (traj = x at the start); n = seq_len * hidden_size.
+  struct SerialTap {
+    double* sums = nullptr;
+    float* traj = nullptr;
+    void* work = nullptr;  // sumsq_work_bytes()
+  };
+  void set_serial_tap(const SerialTap* t) { tap_ = t; }
   // Synchronise every stage and raise deferred numeric errors.
   void finish(cudaStream_t caller);
 
@@ -318,6 +356,8 @@ class Engine {
   void layer_forward_joint(Stage& s, int lf, int rows, int row0, int code);
   void layer_forward_single(Stage& s, int lf, int rows, int row0, int code);
   void px_conditioning(Stage& s, int steps);
+  void px_alloc_run(Stage& s, int steps);
+  void drop_graphs();
   void px_patch_prepare(float* x_dev, bool update, int row0, int rows, int t, float eta);
   void send_rows(int from, int row0, int rows, int patch, int t);
   void prepare_run(int patches, int steps);
@@ -332,6 +372,7 @@ class Engine {
   float* succ_eps_ = nullptr;      // last rank: rank 0's eps buffer
   uint32_t* succ_sig_ = nullptr;   // successor's signal page
   uint32_t* pred_sig_ = nullptr;   // predecessor's signal page
+  std::vector<uint32_t*> world_sig_;  // every other rank's signal page (connect_world)
   std::vector<void*> ipc_opened_;
   bool connected_ = false;
   // Fused stage-boundary send: the stage's last MLP-out GEMM stores its rows
@@ -350,7 +391,26 @@ class Engine {
   uint32_t msgs_in_base_ = 0, msgs_out_base_ = 0;
   cudaEvent_t ev_compute_ = nullptr;
   std::vector<cudaEvent_t> ev_sent_;  // per patch: last send of its rows finished
-  cudaEvent_t ev_write_ = nullptr;    // rank mode with lanes: last signal write (in plan order)
+  // rank mode with lanes: last signal write per counter (acks to the
+  // predecessor, message counts to the successor), each chain in plan order
+  cudaEvent_t ev_write_[2] = {nullptr, nullptr};
+  cudaStream_t abort_stream_ = nullptr;
+  uint32_t run_epoch_ = 0;     // rank runs started (same on every rank)
+  uint32_t run_base_ = 0;      // message base of the run in flight
+  bool broken_ = false;        // watchdog abort: counters no longer agree
+  int fail_at_op_ = -1;
+  double rank_timeout_s_ = [] {
+    const char* e = std::getenv("PF_RANK_TIMEOUT_S");
+    const double v = e ? std::atof(e) : 600.0;
+    return v > 0 ? v : 600.0;
+  }();
+  // rank mode: enqueue or replay the captured graph of this rank's plan
+  void run_rank(float* x_dev, int steps, int patches, int warmup, float eta,
+                cudaStream_t caller, RunStats* stats);
+  void prepare_rank_run(int patches, int steps);
+  // wait for a stream; in rank mode with a watchdog that aborts the pipeline
+  // when no progress is made for rank_timeout_s_
+  void wait_stream(cudaStream_t st);
   int px_steps_ = 0;  // S of the enqueued run (layout of the per-run PixArt buffers)
   cudaEvent_t ev_start_ = nullptr;
   int stage_of_layer(int layer) const;
@@ -370,10 +430,21 @@ class Engine {
     RunStats stats;
     int64_t launches = 0;
     std::vector<std::pair<int, int>> codes;
+    // rank mode: the captured graph's stream memory operations (signal
+    // waits / writes). Their values are message counts relative to the
+    // run's base, patched before a replay whose base differs.
+    cudaGraph_t graph = nullptr;
+    struct MemOpNode {
+      void* node = nullptr;  // CUgraphNode of `graph`
+      std::vector<uint32_t> delta;  // value - base, per op of the batch
+    };
+    std::vector<MemOpNode> memops;
+    uint32_t base = 0;  // base the exec's values currently hold
   };
   using GraphKey = std::tuple<float*, int, int, int, uint32_t, cudaStream_t>;
   std::map<GraphKey, GraphEntry> graphs_;
   bool graphs_enabled_ = true;
+  const SerialTap* tap_ = nullptr;
 
   bool profiling_ = false;
   bool timeline_on_ = false;

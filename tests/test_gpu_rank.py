@@ -144,3 +144,183 @@ def test_same_process_ranks_joint(D, N):
     outs, stats = _same_process_ranks(seed, L, hs, heads, p, N, 4, 2, 1, x0, text=T, joint=D)
     assert np.array_equal(outs[0], ref.final_x)
     assert stats[0] == (ref.stats.fresh_patch_reads, ref.stats.stale_patch_reads)
+
+
+# ----------------------------------------------------------------- graph replay
+@pytest.mark.parametrize("N,M", [(2, 4), (4, 8)])
+def test_rank_graph_replay_equals_enqueue(N, M):
+    """Each rank captures its plan once; replays re-base the signal values.
+    Three replays (bases 0, R, 2R) equal three graph-less runs bit for bit."""
+    import torch
+    seed, L, hs, heads, p, S, W = 0, 4, 128, 4, 256, 4, 1
+    x0 = pf.make_initial_latent(0, p, hs)
+    res = {}
+    for graphs in (False, True):
+        ranks = [pf.ToyDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, r, N, 0) for r in range(N)]
+        pf.connect_ranks(ranks)
+        for m in ranks:
+            m.set_graphs(graphs)
+        streams = [torch.cuda.Stream() for _ in ranks]
+        outs = []
+        x0t = torch.from_numpy(x0.astype(np.float32)).cuda()
+        x = torch.empty_like(x0t)
+        for _ in range(3):
+            x.copy_(x0t)
+            torch.cuda.synchronize()
+            for r, m in enumerate(ranks):
+                m.run_pipefusion_device(x.data_ptr() if r == 0 else 0, S, M, W, 0.1,
+                                        streams[r].cuda_stream)
+            for r, m in enumerate(ranks):
+                m.synchronize(streams[r].cuda_stream)
+            outs.append(x.double().cpu().numpy())
+        for m in ranks:
+            m.close()
+        res[graphs] = outs
+    for a, b in zip(res[False], res[True]):
+        assert np.array_equal(a, b)
+    assert all(np.array_equal(res[True][0], o) for o in res[True][1:])
+
+
+# ----------------------------------------------------------------- channel close
+def _ranks(N, p=256, hs=128, L=4, heads=4):
+    ranks = [pf.ToyDiTCuda.rank_stage(0, L, hs, heads, 4.0, p, r, N, 0) for r in range(N)]
+    pf.connect_ranks(ranks)
+    return ranks
+
+
+def _run_all(ranks, x0, S, M, W, graphs=True):
+    """Enqueue every rank, then wait on each; returns (x, per-rank error)."""
+    import torch
+    streams = [torch.cuda.Stream() for _ in ranks]
+    x = torch.from_numpy(x0.astype(np.float32)).cuda()
+    torch.cuda.synchronize()
+    errs = [None] * len(ranks)
+    for r, m in enumerate(ranks):
+        m.set_graphs(graphs)
+        try:
+            m.run_pipefusion_device(x.data_ptr() if r == 0 else 0, S, M, W, 0.1,
+                                    streams[r].cuda_stream)
+        except (pf.NumericError, pf.ValidationError) as e:
+            errs[r] = e
+    for r, m in enumerate(ranks):
+        try:
+            m.synchronize(streams[r].cuda_stream)
+        except pf.NumericError as e:
+            errs[r] = errs[r] or e
+    return x.double().cpu().numpy(), errs
+
+
+@pytest.mark.parametrize("fail_rank,op", [(1, 5), (1, 40), (0, 12), (2, 25)])
+def test_thrown_error_closes_every_channel(fail_rank, op):
+    """A rank that throws mid-plan (execute.cpp:345-348 close_all) closes the
+    run: every rank returns, the others report "channel closed mid-run", the
+    root cause wins (execute.cpp:357-374), and the next run is bit-exact."""
+    N, p, hs, S, M, W = 3, 256, 128, 4, 4, 1
+    x0 = pf.make_initial_latent(0, p, hs)
+    ref = _single(0, 4, hs, 4, p, N, S, M, W, x0)
+    ranks = _ranks(N)
+    ranks[fail_rank].debug_fail_at(op)
+    _, errs = _run_all(ranks, x0, S, M, W)
+    assert "injected failure" in str(errs[fail_rank])
+    for r in range(N):
+        if r != fail_rank:
+            assert str(errs[r]) == "channel closed mid-run", (r, errs[r])
+        assert not ranks[r].rank_broken
+    assert "injected failure" in str(pf.root_cause(errs))
+    # the failing rank played its message protocol to the end: the counters
+    # agree and the next run (graphs on and off) is bit-exact, no reset needed
+    ranks[fail_rank].debug_fail_at(-1)
+    for graphs in (True, False):
+        x, errs = _run_all(ranks, x0, S, M, W, graphs=graphs)
+        assert errs == [None] * N
+        assert np.array_equal(x, ref.final_x)
+    for m in ranks:
+        m.close()
+
+
+def test_nan_root_cause_is_the_first_non_finite_layer():
+    """A NaN born in rank 1's layer reaches rank 0 a step later; every rank
+    returns, and the root cause is rank 1's (earliest timestep)."""
+    N, p, hs, S, M, W = 2, 256, 128, 4, 4, 1
+    x0 = pf.make_initial_latent(0, p, hs)
+    ranks = _ranks(N)
+    ranks[1].debug_poison_layer(3)
+    _, errs = _run_all(ranks, x0, S, M, W)
+    assert all(isinstance(e, pf.NumericError) for e in errs), errs
+    assert str(errs[1]) == "non-finite activation at timestep 3, layer 3"
+    assert str(pf.root_cause(errs)) == "non-finite activation at timestep 3, layer 3"
+    for m in ranks:
+        m.close()
+
+
+def test_watchdog_releases_a_rank_whose_peer_never_runs(monkeypatch):
+    monkeypatch.setenv("PF_RANK_TIMEOUT_S", "2")
+    import torch
+    N, p, hs, S, M, W = 2, 256, 128, 3, 2, 1
+    x0 = pf.make_initial_latent(0, p, hs)
+    ranks = _ranks(N)
+    x = torch.from_numpy(x0.astype(np.float32)).cuda()
+    st = torch.cuda.Stream()
+    ranks[0].run_pipefusion_device(x.data_ptr(), S, M, W, 0.1, st.cuda_stream)  # rank 1 idle
+    with pytest.raises(pf.NumericError, match="channel closed mid-run"):
+        ranks[0].synchronize(st.cuda_stream)
+    assert ranks[0].rank_broken
+    with pytest.raises(pf.NumericError, match="channel closed mid-run"):
+        ranks[0].run_pipefusion_device(x.data_ptr(), S, M, W, 0.1, st.cuda_stream)
+    for m in ranks:
+        m.rank_reset()
+    ref = _single(0, 4, hs, 4, p, N, S, M, W, x0)
+    x, errs = _run_all(ranks, x0, S, M, W)
+    assert errs == [None] * N and np.array_equal(x, ref.final_x)
+    for m in ranks:
+        m.close()
+
+
+def _proc_fail(rank, world, port, cfg, q):
+    try:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        seed, L, hs, heads, p, S, M, W = cfg
+        m = pf.ToyDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, rank, world, 0)
+        pf.connect_distributed(m)
+        if rank == 1:
+            m.debug_fail_at(9)
+        x0 = pf.make_initial_latent(0, p, hs)
+        try:
+            m.run_pipefusion(x0 if rank == 0 else None, S, M, W, 0.1)
+            out = "no error"
+        except pf.NumericError as e:
+            out = str(e)
+        # the next run needs no reset: bitwise equal to a fresh single context
+        m.debug_fail_at(-1)
+        res = m.run_pipefusion(x0 if rank == 0 else None, S, M, W, 0.1)
+        dist.barrier()
+        m.close()
+        q.put((rank, out, res.final_x))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "exception " + repr(e), None))
+
+
+def test_process_per_rank_failure_reports_root_cause_everywhere():
+    seed, L, hs, heads, p, S, M, W = 0, 4, 128, 4, 256, 4, 4, 1
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    cfg = (seed, L, hs, heads, p, S, M, W)
+    procs = [ctx.Process(target=_proc_fail, args=(r, world, port, cfg, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = {}
+    for _ in range(world):
+        r, msg, x = q.get(timeout=300)
+        got[r] = (msg, x)
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in range(world):
+        assert got[r][0].startswith("injected failure at plan op 9 of rank 1"), got[r][0]
+    x0 = pf.make_initial_latent(0, p, hs)
+    ref = _single(seed, L, hs, heads, p, world, S, M, W, x0)
+    assert np.array_equal(got[0][1], ref.final_x)
