@@ -237,9 +237,9 @@ pf_status pf_auto_warmup(pf_ctx* ctx, const double* x_init, pf_layout layout, in
                          double eta, double threshold, int* warmup, int* threshold_met);
 
 /* ditsim::divergence(a, b) = ||a - b||_F / ||b||_F -- execute.hpp:136-137,
- * toy_model.cpp:216-228 (fp64, on ctx's stage-0 GPU; the norm is
- * layout-independent). PF_VALIDATION with the reference's messages on a shape
- * mismatch or a zero reference. */
+ * toy_model.cpp:216-228 (fp64 on ctx's stage-0 GPU, or on device 0 when ctx
+ * is NULL; the norm is layout-independent). PF_VALIDATION with the
+ * reference's messages on a shape mismatch or a zero reference. */
 pf_status pf_divergence(pf_ctx* ctx, const double* a, int64_t a_rows, int64_t a_cols,
                         const double* b, int64_t b_rows, int64_t b_cols, double* out);
 
@@ -296,6 +296,9 @@ pf_status pf_kernel_profile(pf_ctx* ctx, int kind, double* total_ms,
  * caller stream; returns the span count (spans may be NULL) or -1. */
 pf_status pf_set_timeline(pf_ctx* ctx, int enabled);
 int64_t pf_timeline(pf_ctx* ctx, double* spans, int64_t capacity);
+
+/* Number of visible CUDA devices (0 when there is none or no driver). */
+int pf_device_count(void);
 
 /* Introspection for tests and benchmarks. */
 int pf_stage_count(const pf_ctx* ctx);

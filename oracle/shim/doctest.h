@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -75,6 +76,12 @@ inline void fail(const char* file, int line, const char* expr) {
     if (!(__VA_ARGS__)) doctest::detail::fail(__FILE__, __LINE__, #__VA_ARGS__); \
   } while (0)
 #define CHECK_FALSE(...) CHECK(!(__VA_ARGS__))
+#define MESSAGE(...)                                                        \
+  do {                                                                      \
+    std::ostringstream _os;                                                 \
+    _os << __VA_ARGS__;                                                     \
+    std::printf("%s:%d: %s\n", __FILE__, __LINE__, _os.str().c_str());     \
+  } while (0)
 #define REQUIRE(...)                                                        \
   do {                                                                      \
     ++doctest::detail::checks();                                            \

@@ -47,7 +47,7 @@ EXPORTED_SYMBOLS = [
     "pf_version", "pf_make_initial_latent", "pf_set_graphs", "pf_set_profiling", "pf_kernel_profile",
     "pf_debug_gemm", "pf_debug_attention", "pf_debug_attention_trace", "pf_debug_gemm_trace",
     "pf_debug_attn_schedule", "pf_serial_reference_ex", "pf_auto_warmup", "pf_divergence",
-    "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_debug_fail_at", "pf_debug_poison_layer",
+    "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_device_count", "pf_debug_fail_at", "pf_debug_poison_layer",
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",

@@ -654,6 +654,8 @@ pf_status pf_serial_reference_ex(pf_ctx* ctx, const double* x_init, pf_layout la
       if (e != cudaSuccess)
         throw pf::CudaError(std::string("trajectory download: ") + cudaGetErrorString(e));
     }
+    // trajectory[0] is the caller's latent itself (not its fp32 image)
+    std::memcpy(trajectory, x_init, n * sizeof(double));
     std::memcpy(x_out, trajectory + size_t(steps) * n, n * sizeof(double));
   });
 }
@@ -700,10 +702,18 @@ pf_status pf_auto_warmup(pf_ctx* ctx, const double* x_init, pf_layout layout, in
   });
 }
 
+int pf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 pf_status pf_divergence(pf_ctx* ctx, const double* a, int64_t a_rows, int64_t a_cols,
                         const double* b, int64_t b_rows, int64_t b_cols, double* out) {
-  if (!ctx) return PF_VALIDATION;
-  return guarded(&ctx->last_error, [&] {
+  return guarded(ctx ? &ctx->last_error : &g_create_error, [&] {
     if (a_rows != b_rows || a_cols != b_cols) {
       std::ostringstream os;
       os << "divergence shape mismatch: " << a_rows << "x" << a_cols << " vs " << b_rows << "x"
@@ -712,18 +722,18 @@ pf_status pf_divergence(pf_ctx* ctx, const double* a, int64_t a_rows, int64_t a_
     }
     if (!a || !b || !out) throw pf::ValidationError("NULL pointer");
     const size_t n = size_t(a_rows) * size_t(a_cols);
-    const pf::Stage& s0 = ctx->engine->stage(0);
-    DeviceScope dev(s0.device);
+    // ctx's stage-0 GPU and stream; without a context device 0's default stream
+    const int device = ctx ? ctx->engine->stage(0).device : 0;
+    cudaStream_t stream = ctx ? ctx->engine->stage(0).stream : nullptr;
+    DeviceScope dev(device);
     DevBuf da(n * 8), db(n * 8), work(pf::sumsq_work_bytes()), res(2 * sizeof(double));
-    cudaError_t e = cudaMemcpyAsync(da.p, a, n * 8, cudaMemcpyHostToDevice, s0.stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, s0.stream);
+    cudaError_t e = cudaMemcpyAsync(da.p, a, n * 8, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess)
-      e = pf::sumsq_diff(da.as<double>(), db.as<double>(), n, work.p, res.as<double>(),
-                         s0.stream);
+      e = pf::sumsq_diff(da.as<double>(), db.as<double>(), n, work.p, res.as<double>(), stream);
     double h[2] = {0, 0};
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(h, res.p, sizeof(h), cudaMemcpyDeviceToHost, s0.stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s0.stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, res.p, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) throw pf::CudaError(std::string("divergence: ") + cudaGetErrorString(e));
     // toy_model.cpp:216-228
     const double denom = std::sqrt(h[1]);
