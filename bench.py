@@ -30,8 +30,11 @@ pipeline stage d (its L/N layers) on GPU LOCAL_RANK, and stage-boundary
 activations / the returned eps go straight into the neighbour's landing
 buffers over peer memory (NVLink, CUDA IPC; rank_plan.h). Each rank times
 its own stream with CUDA events; the reported time is the max over ranks.
-Without torchrun, --gpus N drives N devices from one process (one stream
-per stage).
+Without torchrun, `--gpus N` (N > 1) launches the same N processes itself
+(one per GPU, RANK/WORLD_SIZE/LOCAL_RANK set, rendezvous on 127.0.0.1) and
+relays rank 0's line, so the plain command times the same rank-mode path
+(per-rank CUDA-graph replay, patch lanes) as the torchrun launch.
+`--single-process` keeps the older one-process multi-device engine (tests).
 """
 from __future__ import annotations
 
@@ -246,6 +249,13 @@ def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
     return {
         "value": per_sample * samples_per_image, "unit": UNIT, "cores": cores,
         "kind": "reference",
+        # the reference's own N=1 path (Backend::Inline, execute.cpp:694) is
+        # one host thread; spreading sampled units over `cores` threads makes
+        # `value` a throughput-equivalent figure about `cores` x kinder to the CPU
+        "single_thread_value": per_sample * cores * samples_per_image,
+        "semantics": (f"units spread over {cores} host threads (throughput-equivalent); the "
+                      "reference's own N=1 run is single-threaded (execute.cpp:694), see "
+                      "single_thread_value"),
         "sample": (f"{done} toy_layer_forward units of {sample_rows} query rows x "
                    f"{kvp}-row K/V at hs={c['hs']} heads={c['heads']} (reference "
                    f"toy_model.cpp, fp64, {cores} threads in {wall:.1f}s); extrapolated "
@@ -275,6 +285,10 @@ def run_ours(args, c, world, rank):
         if px:
             model = pf.PixArtCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"],
                                              c["T"], rank, world, local)
+        elif c.get("block") == "joint":
+            model = pf.JointDiTCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"],
+                                               c["T"], rank, world, local,
+                                               double_layers=c.get("D"))
         else:
             model = pf.ToyDiTCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], rank,
                                              world, local)
@@ -318,13 +332,18 @@ def run_ours(args, c, world, rank):
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
+            h0 = time.perf_counter()
             for _ in range(args.steps):
                 one_image()
+            host_ms = (time.perf_counter() - h0) * 1e3
             ev1.record(stream)
             model.synchronize(sp)
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1)
     clock_info = clocks.summary()
+    # host time to enqueue (or replay) one image vs its device time, per rank
+    enqueue = {"host_ms_per_image": gather_ranks(host_ms / args.steps, world),
+               "device_ms_per_image": gather_ranks(ms / args.steps, world)}
     ms = max_over_ranks(ms, world)
     barrier(world)
 
@@ -350,9 +369,24 @@ def run_ours(args, c, world, rank):
     prof = model.kernel_profile()
     model.set_profiling(False)
     barrier(world)
+    all_launches = gather_ranks(launches, world)
     if rank != 0:
         return None
     finite = bool(np.isfinite(out.final_x).all())
+    nvlink = None
+    bb = boundary_bytes(c, world, M)
+    if bb is not None:
+        # the boundary stores are fused into the last MLP-out GEMM of each
+        # stage, so the link is timed per image: bytes on the busiest boundary
+        # over the image time, against one direction of one GPU's NVLink 5
+        link_peak = 900.0
+        busiest = max(bb)
+        gbs = busiest / sec_per_image / 1e9
+        nvlink = {"bytes_per_image_per_boundary": bb, "achieved_gbs": gbs,
+                  "peak_gbs": link_peak, "frac": gbs / link_peak,
+                  "ideal_ms_per_image": busiest / (link_peak * 1e9) * 1e3,
+                  "note": "fp32 + bf16 activation rows per message, fp32 eps back to "
+                          "rank 0; peak = NVLink 5 per direction (nominal)"}
     # ---- per-kernel CUDA-event profile of one extra image
     gemm_kinds = ["gemm_qkv", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out", "gemm_cross_q",
                   "gemm_cross_out"]
@@ -376,11 +410,17 @@ def run_ours(args, c, world, rank):
     gemm_fl = sum(prof[k]["flops"] for k in gemm_kinds)
     d = prof[dom]
     achieved = d["flops"] / d["launches"] / (d["ms"] / d["launches"] * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
+        # dram__bytes_read + dram__bytes_write per launch of this config's
+        # dominant kernel, from an ncu --set full capture of the same config
+        # and patch count (null when that capture does not exist)
         try:
-            traffic = json.loads(tf.read_text()).get(dom)
+            t = json.loads(tf.read_text())
+            ent = t.get("configs", {}).get(f"{args.config}_m{M}", {})
+            traffic = ent.get(dom)
+            traffic_src = ent.get("source") if traffic is not None else None
         except Exception:
             traffic = None
     total_flops = flops_per_image(c, mlp)
@@ -406,11 +446,18 @@ def run_ours(args, c, world, rank):
                 "api": "pf_run_pipefusion (C ABI, fp64 host latent in/out)"},
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved,
                      "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,
-                     "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": f"{peak_kind} bf16 sustained",
+                     "measured_in": ("a separate profiled image: every kernel bracketed by "
+                                     "CUDA events on its stream, one lane, no graph replay "
+                                     "(value runs graphs" + (" and patch lanes" if M > 1
+                                                             else "") + ")"),
                      "gemm_all_frac": (gemm_fl / (gemm_ms * 1e-3) / 1e12) / peak_tf},
         "kernels": kernels,
-        "gpu_launches": launches * args.steps,
-        "gpu_launches_note": ("rank 0's kernels" if world > 1 else "all stages"),
+        "gpu_launches": sum(all_launches) * args.steps,
+        "gpu_launches_note": ("summed over the ranks" if world > 1 else "all stages"),
+        "enqueue": enqueue,
+        "nvlink": nvlink,
         "clocks": clock_info,
         "finite": finite,
         "model_build_s": t_build,
@@ -424,6 +471,42 @@ def barrier(world):
         dist.barrier()
 
 
+def gather_ranks(v, world):
+    """[v of rank 0, v of rank 1, ...] (every rank gets the list)."""
+    if world <= 1:
+        return [v]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, v)
+    return out
+
+
+def boundary_bytes(c, world, M):
+    """Bytes one image moves over each stage boundary (rank d -> d+1) and
+    from the last rank back to rank 0, from the rank plans (pf_rank_plan):
+    activations travel as fp32 rows plus their bf16 copy (the next stage's
+    GEMM operand), PixArt adds per-row LayerNorm partial stats (hs/32 float2),
+    the returned eps is fp32 only. Per SURVEY 8(d) / costmodel.cpp:117-123."""
+    if world <= 1:
+        return None
+    import paper_2405_14430_b200 as pf
+    hs, p = c["hs"], c["p"]
+    per_rank = []
+    for d in range(world):
+        plan = pf.rank_plan(d, world, c["S"], M, c["W"], p)
+        sends = plan[plan[:, 0] == 2]  # kind 2 = send
+        rows = int(sends[:, 4].sum())
+        last = d == world - 1
+        if c.get("block") == "joint" and not last:
+            # the text rows ride along with the full sequence and patch 0
+            rows += c["T"] * int((sends[:, 2] <= 0).sum())
+        b = rows * hs * 4 + (0 if last else rows * hs * 2)
+        if c.get("block") == "pixart" and not last:
+            b += rows * (hs // 32) * 8
+        per_rank.append(b)
+    return per_rank
+
+
 def max_over_ranks(v, world):
     if world <= 1:
         return v
@@ -432,6 +515,42 @@ def max_over_ranks(v, world):
     t = torch.tensor([v], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def spawn_ranks(args):
+    """`--gpus N` without torchrun: start one bench process per GPU (the same
+    environment torchrun would give them) and relay rank 0's JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    n = args.gpus
+    import tempfile
+    procs = []
+    out = tempfile.TemporaryFile()
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), GROUP_RANK="0", MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), CUDA_DEVICE_MAX_CONNECTIONS="32")
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve())]
+                                      + sys.argv[1:], env=env,
+                                      stdout=out if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    while any(pr.poll() is None for pr in procs):
+        failed = [pr for pr in procs if pr.poll() not in (None, 0)]
+        if failed:  # one rank died: the others would wait for it forever
+            rc = failed[0].returncode
+            for pr in procs:
+                if pr.poll() is None:
+                    pr.kill()
+            break
+        time.sleep(0.2)
+    for pr in procs:
+        rc = rc or pr.wait()
+    out.seek(0)
+    sys.stdout.write(out.read().decode(errors="replace"))
+    sys.stdout.flush()
+    return rc
 
 
 def main():
@@ -444,10 +563,14 @@ def main():
     ap.add_argument("--patches", type=int, default=0, help="M (default: N)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--single-process", action="store_true",
+                    help="--gpus N from one process (multi-device engine, no rank mode)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world == 1 and args.gpus > 1 and args.impl == "ours" and not args.single_process:
+        sys.exit(spawn_ranks(args))
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

@@ -76,6 +76,20 @@ typedef struct pf_ctx pf_ctx;
 pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
                         const int* devices, int n_stages, pf_ctx** out);
 
+/* Arithmetic of the toy block. PF_PRECISION_BF16 (pf_create_toy's) is the
+ * product path: bf16 tcgen05 GEMM / attention operands, fp32 accumulation
+ * and residual stream. PF_PRECISION_FP32 is a parity mode -- fp32 weights,
+ * activations and K/V buffers on CUDA-core kernels, same executor, schedule
+ * and K/V update order -- that anchors full-depth runs against the fp64
+ * reference where bf16 rounding alone would exceed the tolerance (SURVEY
+ * 8(c) T2). Toy block only; no DistriFusion. */
+typedef enum { PF_PRECISION_BF16 = 0, PF_PRECISION_FP32 = 1 } pf_precision;
+pf_status pf_create_toy_ex(uint64_t seed, const pf_model_desc* desc, int precision,
+                           const int* devices, int n_stages, pf_ctx** out);
+pf_status pf_create_toy_rank_ex(uint64_t seed, const pf_model_desc* desc, int precision,
+                                int rank, int world, int device, pf_ctx** out);
+int pf_precision_of(const pf_ctx* ctx);
+
 /* Create an executor from caller-owned fp64 weights: 6 matrices per layer in
  * ToyDiTLayer order (w_q, w_k, w_v, w_o [hs x hs], w_mlp_in [hs x mlp],
  * w_mlp_out [mlp x hs]), i.e. weights[6*l + i], plus condition_bias [hs].

@@ -47,7 +47,8 @@ EXPORTED_SYMBOLS = [
     "pf_version", "pf_make_initial_latent", "pf_set_graphs", "pf_set_profiling", "pf_kernel_profile",
     "pf_debug_gemm", "pf_debug_attention", "pf_debug_attention_trace", "pf_debug_gemm_trace",
     "pf_debug_attn_schedule", "pf_serial_reference_ex", "pf_auto_warmup", "pf_divergence",
-    "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_device_count", "pf_debug_fail_at", "pf_debug_poison_layer",
+    "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_device_count", "pf_debug_fail_at",
+    "pf_debug_poison_layer", "pf_create_toy_ex", "pf_create_toy_rank_ex", "pf_precision_of",
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
@@ -55,6 +56,10 @@ KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_m
 
 PF_OK, PF_NUMERIC, PF_VALIDATION, PF_CUDA = 0, 1, 2, 3
 PF_ROW_MAJOR, PF_COL_MAJOR = 0, 1
+
+
+PRECISION_BF16 = 0  # pf_precision (include/pipefusion_b200.h)
+PRECISION_FP32 = 1
 
 
 class ValidationError(ValueError):
@@ -112,6 +117,11 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
     lib.pf_create_toy_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
                                        ctypes.POINTER(vp)]
+    lib.pf_create_toy_ex.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32,
+                                     ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_create_toy_rank_ex.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32,
+                                          i32, i32, ctypes.POINTER(vp)]
+    lib.pf_precision_of.argtypes = [vp]
     lib.pf_create_pixart_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32,
                                           i32, i32, ctypes.POINTER(vp)]
     lib.pf_serial_reference_ex.argtypes = [vp, dptr, i32, i32, dbl, dptr, dptr]
@@ -290,7 +300,9 @@ class ToyDiTCuda:
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, workers: int = 1,
                  devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0,
-                 _rank=None, _joint=None):
+                 _rank=None, _joint=None, precision: int = 0):
+        """precision: PRECISION_BF16 (the product path) or PRECISION_FP32
+        (parity mode: fp32 CUDA-core kernels, same executor; toy block)."""
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         self.layers, self.hidden_size, self.heads = layers, hidden_size, heads
@@ -311,8 +323,9 @@ class ToyDiTCuda:
                                                      _text_tokens, rank, workers, device,
                                                      ctypes.byref(self._ctx))
             else:
-                st = self._lib.pf_create_toy_rank(ctypes.c_uint64(seed), ctypes.byref(desc), rank,
-                                                  workers, device, ctypes.byref(self._ctx))
+                st = self._lib.pf_create_toy_rank_ex(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                                     precision, rank, workers, device,
+                                                     ctypes.byref(self._ctx))
             if st != PF_OK:
                 _raise(st, self._lib.pf_last_error(None).decode())
             return
@@ -329,8 +342,9 @@ class ToyDiTCuda:
                                             _text_tokens, dev_arr, workers,
                                             ctypes.byref(self._ctx))
         elif _weights is None:
-            st = self._lib.pf_create_toy(ctypes.c_uint64(seed), ctypes.byref(desc),
-                                         dev_arr, workers, ctypes.byref(self._ctx))
+            st = self._lib.pf_create_toy_ex(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                            precision, dev_arr, workers,
+                                            ctypes.byref(self._ctx))
         else:
             mats, cb = _weights
             keep = [_f64c(m) for m in mats]
@@ -343,13 +357,14 @@ class ToyDiTCuda:
 
     @classmethod
     def rank_stage(cls, seed: int, layers: int, hidden_size: int, heads: int, mlp_ratio: float,
-                   seq_len: int, rank: int, world: int, device: int = 0) -> "ToyDiTCuda":
+                   seq_len: int, rank: int, world: int, device: int = 0,
+                   precision: int = 0) -> "ToyDiTCuda":
         """One process (or context) per stage: stage `rank` of `world` on
         `device` (the reference's worker thread d of run_pipefusion_threads).
         Connect the ranks with connect_ranks / connect_distributed."""
         obj = cls.__new__(cls)
         ToyDiTCuda.__init__(obj, seed, layers, hidden_size, heads, mlp_ratio, seq_len, world,
-                            None, _rank=(rank, device))
+                            None, _rank=(rank, device), precision=precision)
         return obj
 
     def export_peer(self) -> bytes:
@@ -408,6 +423,11 @@ class ToyDiTCuda:
             c = self._lib.pf_stage_layer_count(self._ctx, d)
             out.append(range(f, f + c))
         return out
+
+    @property
+    def precision(self) -> int:
+        """PRECISION_BF16 or PRECISION_FP32 (pf_precision_of)."""
+        return int(self._lib.pf_precision_of(self._ctx))
 
     def last_launch_count(self) -> int:
         return int(self._lib.pf_last_launch_count(self._ctx))

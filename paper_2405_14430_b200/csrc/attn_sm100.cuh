@@ -137,7 +137,10 @@ __host__ __device__ __forceinline__ long long attn_unit_start(const AttnParams& 
 // kPoly: bit (g & 7) set -> 4-element group g of a score row takes the
 // FMA-pipe exp2 polynomial instead of MUFU.EX2. kPingPong: serialise the two
 // softmax warpgroups' exp sections (named barriers 1/2).
-template <int DHP, int NT, int kPoly = 0x88, bool kPingPong = false>
+// kSumCol: V column dh (< DHP) is 1.0 in every kv row, so O column dh
+// accumulates the softmax row sum in the PV MMA (of the bf16 P it multiplies
+// V with) and the softmax warps skip their per-element row sum.
+template <int DHP, int NT, int kPoly = 0x88, bool kPingPong = false, bool kSumCol = false>
 __global__ void __launch_bounds__(128 + 128 * NT, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
@@ -416,16 +419,18 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
         for (int e = 0; e < kAttnBN; ++e)
           if (e >= valid) s[e] = -INFINITY;
       }
+      // row max with three-input FMNMX3: 8 chains over 16 columns each
+      static_assert(kAttnBN == 128, "row-max chains");
       float bm[8];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) bm[a] = s[a];
+      for (int a = 0; a < 8; ++a) {
+        bm[a] = ptx::fmax3(s[a], s[a + 8], s[a + 16]);
 #pragma unroll
-      for (int e = 8; e < kAttnBN; e += 8)
-#pragma unroll
-        for (int a = 0; a < 8; ++a) bm[a] = fmaxf(bm[a], s[e + a]);
-      const float bmax =
-          fmaxf(fmaxf(fmaxf(bm[0], bm[1]), fmaxf(bm[2], bm[3])),
-                fmaxf(fmaxf(bm[4], bm[5]), fmaxf(bm[6], bm[7]))) * sc;
+        for (int e = 24; e < 120; e += 16) bm[a] = ptx::fmax3(bm[a], s[e + a], s[e + 8 + a]);
+        bm[a] = fmaxf(bm[a], s[120 + a]);
+      }
+      const float bmax = fmaxf(ptx::fmax3(bm[0], bm[1], bm[2]),
+                               ptx::fmax3(bm[3], ptx::fmax3(bm[4], bm[5], bm[6]), bm[7])) * sc;
       const bool need = bmax > m_ref + 8.0f;
       const float m_new = need ? bmax : m_ref;
       const float alpha = need ? ptx::ex2_approx(m_ref - m_new) : 1.0f;  // 0 on first block
@@ -483,17 +488,19 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
         pending_flag = nullptr;
       }
       if (tr) attn_trace(prm, 2048 * t + 8 * g + 4);
-      // Row sum off the critical path (the PV MMA is already running).
-      float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+      if constexpr (!kSumCol) {
+        // Row sum off the critical path (the PV MMA is already running).
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
-      for (int e = 0; e < kAttnBN; e += 8) {
-        a0 = ptx::fadd2(a0, make_float2(s[e], s[e + 1]));
-        a1 = ptx::fadd2(a1, make_float2(s[e + 2], s[e + 3]));
-        a2 = ptx::fadd2(a2, make_float2(s[e + 4], s[e + 5]));
-        a3 = ptx::fadd2(a3, make_float2(s[e + 6], s[e + 7]));
+        for (int e = 0; e < kAttnBN; e += 8) {
+          a0 = ptx::fadd2(a0, make_float2(s[e], s[e + 1]));
+          a1 = ptx::fadd2(a1, make_float2(s[e + 2], s[e + 3]));
+          a2 = ptx::fadd2(a2, make_float2(s[e + 4], s[e + 5]));
+          a3 = ptx::fadd2(a3, make_float2(s[e + 6], s[e + 7]));
+        }
+        a0 = ptx::fadd2(ptx::fadd2(a0, a1), ptx::fadd2(a2, a3));
+        l_sum = l_sum * alpha + (a0.x + a0.y);
       }
-      a0 = ptx::fadd2(ptx::fadd2(a0, a1), ptx::fadd2(a2, a3));
-      l_sum = l_sum * alpha + (a0.x + a0.y);
       m_ref = m_new;
       if (tr) attn_trace(prm, 2048 * t + 8 * g + 5);
     }
@@ -502,6 +509,17 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     ptx::mbar_wait(&o_done[t], sgi & 1);
     if (g - 1 < 256) attn_trace(prm, 2048 * t + 8 * (g - 1) + 6);
     ptx::tc_fence_after();
+    if constexpr (kSumCol) {  // the row sum is O column dh (rescaled with O)
+      uint32_t r[16];
+      ptx::tmem_ld16(tmem_o + 16 * (prm.dh / 16), r);
+      ptx::tmem_wait_ld();
+      const int cd = prm.dh % 16;
+      float lv = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j == cd) lv = __uint_as_float(r[j]);
+      l_sum = lv;
+    }
     const int head = sg.x / prm.nq;
     const int qt = sg.x - head * prm.nq;
     const int lrow = qt * (NT * kAttnBM) + t * kAttnBM + trow;  // row within the launch

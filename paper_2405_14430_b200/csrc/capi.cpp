@@ -164,14 +164,39 @@ pf_status pf_create_toy(uint64_t seed, const pf_model_desc* desc,
 
 pf_status pf_create_toy_rank(uint64_t seed, const pf_model_desc* desc, int rank, int world,
                              int device, pf_ctx** out) {
+  return pf_create_toy_rank_ex(seed, desc, PF_PRECISION_BF16, rank, world, device, out);
+}
+
+pf_status pf_create_toy_rank_ex(uint64_t seed, const pf_model_desc* desc, int precision,
+                                int rank, int world, int device, pf_ctx** out) {
   if (out) *out = nullptr;
   return guarded(&g_create_error, [&] {
     if (!out) throw pf::ValidationError("output pointer is NULL");
     auto ctx = std::make_unique<pf_ctx>();
-    ctx->engine = std::make_unique<pf::Engine>(shape_of(desc), device, rank, world);
+    pf::ModelShape s = shape_of(desc);
+    s.precision = precision;
+    ctx->engine = std::make_unique<pf::Engine>(s, device, rank, world);
     load_toy(*ctx->engine, seed);
     *out = ctx.release();
   });
+}
+
+pf_status pf_create_toy_ex(uint64_t seed, const pf_model_desc* desc, int precision,
+                           const int* devices, int n_stages, pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.precision = precision;
+    ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    load_toy(*ctx->engine, seed);
+    *out = ctx.release();
+  });
+}
+
+int pf_precision_of(const pf_ctx* ctx) {
+  return ctx && ctx->engine ? ctx->engine->shape().precision : -1;
 }
 
 pf_status pf_create_pixart_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,

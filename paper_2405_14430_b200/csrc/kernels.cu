@@ -954,8 +954,30 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   // Two softmax warpgroups exponentiate concurrently (no ping-pong) with 2 of
   // every 8 four-column groups on the FMA-pipe exp2: measured best of the
   // ping-pong / poly-ratio / f16x2-exp variants at C2 (119 vs 123.5 us).
-  cudaError_t e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT>),
-                                            &attn_fwd_kernel<DHP, NT>>{});
+  // With a row-sum column in V (padded head dims), PF_ATTN_POLY selects the
+  // share of FMA-pipe exp2 (hex mask over 8 four-column groups; A/B runs).
+  static const int poly = [] {
+    const char* e = std::getenv("PF_ATTN_POLY");
+    return e ? int(std::strtol(e, nullptr, 16)) : 0x88;
+  }();
+  cudaError_t e;
+  if (a.v_sum_col && a.dh < DHP) {
+    if (DHP != 80 || poly == 0x88)
+      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, true>),
+                                    &attn_fwd_kernel<DHP, NT, 0x88, false, true>>{});
+    else if (poly == 0xAA)
+      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0xAA, false, true>),
+                                    &attn_fwd_kernel<DHP, NT, 0xAA, false, true>>{});
+    else if (poly == 0x92)
+      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x92, false, true>),
+                                    &attn_fwd_kernel<DHP, NT, 0x92, false, true>>{});
+    else
+      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, true>),
+                                    &attn_fwd_kernel<DHP, NT, 0x88, false, true>>{});
+  } else {
+    e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT>),
+                                  &attn_fwd_kernel<DHP, NT>>{});
+  }
   if (e != cudaSuccess || !cut || prm.grid < 2 || prm.fused) return e;
   const unsigned slices = unsigned((NT * kAttnBM * (DHP / 16) + 255) / 256);
   return launch_pdl(attn_streamk_combine_kernel<DHP, NT>, dim3(prm.grid - 1, slices), dim3(256),
@@ -1111,6 +1133,21 @@ cudaError_t latent_to_f64(const float* src, double* dst, int64_t rows, int cols,
   ++launch_counter();
   latent_to_f64_kernel<<<ew_grid(size_t(rows) * cols / 4 + 1), 256, 0, stream>>>(
       src, dst, rows, cols, col_major ? 1 : 0);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void v_ones_col_kernel(bf16* v, size_t rows, int dhp, int dh) {
+  for (size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x; r < rows;
+       r += size_t(gridDim.x) * blockDim.x)
+    v[r * dhp + dh] = __float2bfloat16_rn(1.0f);
+}
+}  // namespace
+
+cudaError_t v_ones_col(bf16* v, size_t rows, int dhp, int dh, cudaStream_t stream) {
+  if (dh >= dhp || rows == 0) return cudaSuccess;
+  ++launch_counter();
+  v_ones_col_kernel<<<ew_grid(rows), 256, 0, stream>>>(v, rows, dhp, dh);
   return cudaGetLastError();
 }
 

@@ -161,6 +161,10 @@ struct AttnLaunch {
   // (16-byte aligned regions; bytes 0 = unused)
   const void* prefetch[kAttnPrefetchRegions] = {};
   size_t prefetch_bytes[kAttnPrefetchRegions] = {};
+  // every V row (k/v, k2/v2) holds 1.0 in padding column dh (dh < dhp,
+  // v_ones_col): the PV MMA then produces the softmax row sum in O column dh
+  // and the softmax warps skip their per-element sum
+  bool v_sum_col = false;
 };
 int attn_grid(const AttnLaunch& a, int sm_count);
 // The attention launch's schedule (host only): query-tile groups per head,
@@ -192,6 +196,9 @@ cudaError_t latent_from_f64(const double* src, float* dst, int64_t rows, int col
                             cudaStream_t stream);
 cudaError_t latent_to_f64(const float* src, double* dst, int64_t rows, int cols, bool col_major,
                           cudaStream_t stream);
+// V buffers [rows][dhp] with dh < dhp: column dh = 1 (the attention's
+// row-sum column, AttnLaunch::v_sum_col); the other padding columns stay 0
+cudaError_t v_ones_col(bf16* v, size_t rows, int dhp, int dh, cudaStream_t stream);
 // hb[i] = bf16(h32[i]), i < n
 cudaError_t to_bf16(const float* h32, bf16* hb, size_t n, cudaStream_t stream);
 // ---- PixArt block conditioning (pixart.cu) ----
@@ -224,6 +231,18 @@ cudaError_t sumsq_latent(const float* x, const float* eps, double eta, size_t n,
 // out[0] = sum (a - b)^2, out[1] = sum b^2  over n fp64 elements
 cudaError_t sumsq_diff(const double* a, const double* b, size_t n, void* work, double* out,
                        cudaStream_t stream);
+
+// ---- fp32 parity mode (parity_f32.cu; CUDA cores, test infrastructure) ----
+// C[M x N] (ldc) <- A[M x K] (lda) . B[K x N] (ldb), all fp32 row-major:
+//   kF32Store: C = acc;  kF32Residual: C += acc (non-finite -> atomicMin(flag, code));
+//   kF32Tanh: C = tanh(acc)
+enum F32Epi : int { kF32Store = 0, kF32Residual = 1, kF32Tanh = 2 };
+cudaError_t gemm_f32(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M,
+                     int N, int K, int epi, int* flag, int code, cudaStream_t stream);
+// rows query rows of q [rows x hs] against k, v [P x hs] (row-major, head h =
+// columns [h dh, (h+1) dh)) -> out [rows x hs]
+cudaError_t attention_f32(const float* q, const float* k, const float* v, float* out, int rows,
+                          int P, int heads, int dh, int hs, float scale, cudaStream_t stream);
 
 // Device-side finite-check flag reset: *flag = INT_MAX
 cudaError_t reset_flag(int* flag, cudaStream_t stream);

@@ -198,6 +198,10 @@ void validate_shape(const ModelShape& s) {
     throw ValidationError("joint block needs at least one text token");
   if (s.block == kBlockJoint && (s.double_layers < 0 || s.double_layers > s.layers))
     throw ValidationError("double-stream layer count must lie in [0, layers]");
+  if (s.precision != kPrecBf16 && s.precision != kPrecFp32)
+    throw ValidationError("unknown precision");
+  if (s.precision == kPrecFp32 && s.block != kBlockToy)
+    throw ValidationError("the fp32 parity mode supports the toy block only");
   if (s.block == kBlockPixArt) {
     if (s.hs % 32 != 0)
       throw ValidationError("PixArt block needs hidden_size divisible by 32");
@@ -336,6 +340,17 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
       throw CudaError("cuTensorMapEncodeTiled failed for a weight matrix");
     L.tm_k = tmap(L.k, dhp, heads * P, dhp * 2, 16, 128, 32);
     L.tm_v = tmap(L.v, dhp, heads * P, dhp * 2, 16, 128, 32);
+    check(v_ones_col(L.v, heads * P, int(dhp), m.dh, nullptr), "v_ones_col");
+    if (m.precision == kPrecFp32) {
+      L.w32 = dalloc<float>(4 * hs * hs + 2 * hs * mlp);
+      L.k32 = dalloc<float>(P * hs);
+      L.v32 = dalloc<float>(P * hs);
+    }
+  }
+  if (m.precision == kPrecFp32) {
+    s.q32 = dalloc<float>(P * hs);
+    s.attn32 = dalloc<float>(P * hs);
+    s.z32 = dalloc<float>(P * mlp);
   }
   s.zeros = dalloc<float>(hs);
   if (is_first) {
@@ -374,6 +389,7 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
       L.woc = dalloc<bf16>(hs * hs);
       L.kc = dalloc<bf16>(kvc_rows * dhp);
       L.vc = dalloc<bf16>(kvc_rows * dhp);
+      check(v_ones_col(L.vc, kvc_rows, int(dhp), m.dh, nullptr), "v_ones_col");
       if (!make_weight_maps(&L.tm_wqc, L.wqc, int(hs), int(hs)) ||
           !make_weight_maps(&L.tm_wkvc, L.wkvc, int(2 * hs), int(hs)) ||
           !make_weight_maps(&L.tm_woc, L.woc, int(hs), int(hs)))
@@ -445,6 +461,7 @@ void Engine::free_stage(Stage& s) {
   for (StageLayer& L : s.layers) {
     dfree(L.wqkv); dfree(L.wo); dfree(L.win); dfree(L.wout);
     dfree(L.k); dfree(L.v);
+    dfree(L.w32); dfree(L.k32); dfree(L.v32);
   }
   for (StageLayer& L : s.layers) {
     for (float* p : {L.bqkv, L.bo, L.bqc, L.bkvc, L.boc, L.b1, L.b2}) dfree(p);
@@ -464,6 +481,7 @@ void Engine::free_stage(Stage& s) {
   }
   s.layers.clear();
   dfree(s.h32); dfree(s.hb); dfree(s.q); dfree(s.attn); dfree(s.z);
+  dfree(s.q32); dfree(s.attn32); dfree(s.z32);
   if (s.lane != 0) use_lane(s, 0);
   for (Stage::Lane& ln : s.extra) {
     dfree(ln.attn_work); dfree(ln.attn_flags); dfree(ln.splitk_ws); dfree(ln.splitk_counters);
@@ -523,6 +541,18 @@ void Engine::load_layer(int layer, const HostMatrix (&w)[6]) {
   Stage& s = stages_[size_t(d)];
   StageLayer& L = s.layers[size_t(layer - s.first_layer)];
   upload_toy_weights(s.device, shape_.hs, shape_.mlp, w, L.wqkv, L.wo, L.win, L.wout);
+  if (L.w32) {  // fp32 parity mode: x.W orientation, row-major
+    const size_t hs = size_t(shape_.hs), mlp = size_t(shape_.mlp);
+    std::vector<float> f(4 * hs * hs + 2 * hs * mlp);
+    size_t off = 0;
+    for (int i = 0; i < 6; ++i) {
+      for (int r = 0; r < w[i].rows; ++r)
+        for (int c = 0; c < w[i].cols; ++c) f[off + size_t(r) * w[i].cols + c] = float(w[i].at(r, c));
+      off += size_t(w[i].rows) * size_t(w[i].cols);
+    }
+    DeviceGuard g(s.device);
+    PF_CUDA_CHECK(cudaMemcpy(L.w32, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+  }
 }
 
 void Engine::load_layer_joint(int layer, const HostMatrix (&w)[12]) {
@@ -547,11 +577,65 @@ void Engine::load_condition_bias(const double* cb) {
   PF_CUDA_CHECK(cudaMemcpy(s.cb, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
 }
 
+// fp32 parity mode of the toy layer (same order as toy_model.cpp:169-177):
+// Q, K, V projections with K/V written into rows [row0, row0+rows) of the
+// full buffers before attending, attention over all P rows, out-proj
+// residual, tanh MLP, MLP residual -- on the fp32 residual stream h32.
+void Engine::layer_forward_f32(Stage& s, int lf, int rows, int row0, int code) {
+  const ModelShape& m = shape_;
+  StageLayer& L = s.layers[size_t(lf)];
+  const int hs = m.hs, mlp = m.mlp;
+  const size_t o = size_t(row0) * size_t(hs), hh = size_t(hs) * size_t(hs);
+  const float* h = s.h32 + o;
+  const float *wq = L.w32, *wk = wq + hh, *wv = wk + hh, *wo = wv + hh, *win = wo + hh,
+              *wout = win + size_t(hs) * size_t(mlp);
+  const double r = rows, dhs = hs, dmlp = mlp, P = double(m.P);
+  if (lane_wait_) PF_CUDA_CHECK(cudaStreamWaitEvent(s.stream, lane_wait_, 0));
+  prof_begin(s, kGemmQKV, 2 * r * dhs * 3 * dhs, 0);
+  check(gemm_f32(h, hs, wq, hs, s.q32 + o, hs, rows, hs, hs, kF32Store, nullptr, 0, s.stream),
+        "gemm q (fp32)");
+  check(gemm_f32(h, hs, wk, hs, L.k32 + o, hs, rows, hs, hs, kF32Store, nullptr, 0, s.stream),
+        "gemm k (fp32)");
+  check(gemm_f32(h, hs, wv, hs, L.v32 + o, hs, rows, hs, hs, kF32Store, nullptr, 0, s.stream),
+        "gemm v (fp32)");
+  prof_end(s);
+  prof_begin(s, kAttention, 4 * r * P * dhs, 0);
+  check(attention_f32(s.q32 + o, L.k32, L.v32, s.attn32 + o, rows, int(m.P), m.heads, m.dh, hs,
+                      float(1.0 / std::sqrt(double(m.dh))), s.stream),
+        "attention (fp32)");
+  prof_end(s);
+  if (lane_rec_) PF_CUDA_CHECK(cudaEventRecord(lane_rec_, s.stream));
+  prof_begin(s, kGemmOut, 2 * r * dhs * dhs, 0);
+  check(gemm_f32(s.attn32 + o, hs, wo, hs, s.h32 + o, hs, rows, hs, hs, kF32Residual, s.flag,
+                 code, s.stream),
+        "gemm out-proj (fp32)");
+  prof_end(s);
+  prof_begin(s, kGemmMlpIn, 2 * r * dhs * dmlp, 0);
+  check(gemm_f32(s.h32 + o, hs, win, mlp, s.z32 + size_t(row0) * mlp, mlp, rows, mlp, hs,
+                 kF32Tanh, nullptr, 0, s.stream),
+        "gemm mlp-in (fp32)");
+  prof_end(s);
+  float* dst = redirect_ ? redirect_->h32 : s.h32;
+  if (dst != s.h32)  // rank mode, last layer: residual base then the successor's rows
+    PF_CUDA_CHECK(cudaMemcpyAsync(dst + o, s.h32 + o, size_t(rows) * hs * 4,
+                                  cudaMemcpyDefault, s.stream));
+  prof_begin(s, kGemmMlpOut, 2 * r * dhs * dmlp, 0);
+  check(gemm_f32(s.z32 + size_t(row0) * mlp, mlp, wout, hs, dst + o, hs, rows, hs, mlp,
+                 kF32Residual, s.flag, code, s.stream),
+        "gemm mlp-out (fp32)");
+  prof_end(s);
+}
+
 // One toy DiT layer over rows [row0, row0+rows) (toy_model.cpp:169-177):
 // fused QKV projection writing this block's K/V rows into the full buffers,
 // attention over all P rows, out-proj residual, tanh MLP, MLP residual.
 void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const KvView* kv) {
   const ModelShape& m = shape_;
+  if (m.precision == kPrecFp32) {
+    if (kv) throw ValidationError("the fp32 parity mode does not run DistriFusion");
+    layer_forward_f32(s, lf, rows, row0, code);
+    return;
+  }
   StageLayer& L = s.layers[size_t(lf)];
   const double r = rows, hs = m.hs, mlp = m.mlp, P = double(m.P);
   EpiParams qkv;
@@ -572,6 +656,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
   a.flags = s.attn_flags;
+  a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
   // pull this layer's out-proj / MLP weights and the next layer's (or, after
   // the stage's last layer, the next patch's first layer's) QKV weights into
   // L2 while the attention runs: small patches otherwise stream them from HBM
@@ -825,6 +910,13 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       for (StageLayer& L : s.layers) {
         PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
         PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kv, s.stream));
+        check(v_ones_col(L.v, kv / (size_t(m.dhp) * sizeof(bf16)), m.dhp, m.dh, s.stream),
+              "v_ones_col");
+        if (L.k32) {
+          const size_t n32 = size_t(m.rows_total()) * size_t(m.hs) * sizeof(float);
+          PF_CUDA_CHECK(cudaMemsetAsync(L.k32, 0, n32, s.stream));
+          PF_CUDA_CHECK(cudaMemsetAsync(L.v32, 0, n32, s.stream));
+        }
       }
     }
   }
@@ -1390,7 +1482,46 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
       kd[(size_t(head) * P + r) * m.dhp + dd] = __float2bfloat16_rn(float(k_buf[idx(r, c, P)]));
       vd[(size_t(head) * P + r) * m.dhp + dd] = __float2bfloat16_rn(float(v_buf[idx(r, c, P)]));
     }
+  if (m.dh < m.dhp)  // the attention's row-sum column (AttnLaunch::v_sum_col)
+    for (int64_t r = 0; r < int64_t(m.heads) * P; ++r)
+      vd[size_t(r) * m.dhp + m.dh] = __float2bfloat16_rn(1.0f);
   DeviceGuard g(s.device);
+  if (m.precision == kPrecFp32) {  // parity mode: fp32 row-major K/V
+    std::vector<float> k32(size_t(P) * hs), v32(size_t(P) * hs);
+    for (int64_t r = 0; r < P; ++r)
+      for (int c = 0; c < hs; ++c) {
+        k32[size_t(r) * hs + c] = float(k_buf[idx(r, c, P)]);
+        v32[size_t(r) * hs + c] = float(v_buf[idx(r, c, P)]);
+      }
+    PF_CUDA_CHECK(cudaMemcpy(s.h32 + row0 * hs, h32.data(), h32.size() * 4,
+                             cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(L.k32, k32.data(), k32.size() * 4, cudaMemcpyHostToDevice));
+    PF_CUDA_CHECK(cudaMemcpy(L.v32, v32.data(), v32.size() * 4, cudaMemcpyHostToDevice));
+    LaunchTally tally(launches_);
+    check(reset_flag(s.flag, s.stream), "reset_flag");
+    codes_.assign(1, {0, layer});
+    layer_forward(s, layer - s.first_layer, int(rows), int(row0), 0);
+    PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
+    PF_CUDA_CHECK(cudaMemcpy(h32.data(), s.h32 + row0 * hs, h32.size() * 4,
+                             cudaMemcpyDeviceToHost));
+    PF_CUDA_CHECK(cudaMemcpy(k32.data(), L.k32, k32.size() * 4, cudaMemcpyDeviceToHost));
+    PF_CUDA_CHECK(cudaMemcpy(v32.data(), L.v32, v32.size() * 4, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < rows; ++r)
+      for (int c = 0; c < hs; ++c) h[idx(r, c, rows)] = double(h32[size_t(r) * hs + c]);
+    for (int64_t r = 0; r < P; ++r)
+      for (int c = 0; c < hs; ++c) {
+        k_buf[idx(r, c, P)] = double(k32[size_t(r) * hs + c]);
+        v_buf[idx(r, c, P)] = double(v32[size_t(r) * hs + c]);
+      }
+    int f = INT_MAX;
+    PF_CUDA_CHECK(cudaMemcpy(&f, s.flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (f != INT_MAX) {
+      std::ostringstream os;
+      os << "non-finite activation at timestep 0, layer " << layer;
+      throw NumericError(os.str());
+    }
+    return;
+  }
   PF_CUDA_CHECK(cudaMemcpyAsync(s.h32 + row0 * hs, h32.data(), h32.size() * 4,
                                 cudaMemcpyHostToDevice, s.stream));
   PF_CUDA_CHECK(cudaMemcpyAsync(s.hb + row0 * hs, hb.data(), hb.size() * 2,
@@ -1473,6 +1604,7 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
   a.flags = s.attn_flags;
+  a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
   prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (joint)");
   prof_end(s);
@@ -1549,6 +1681,7 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
   a.flags = s.attn_flags;
+  a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
   prof_begin(s, kAttention, 4 * r * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (single)");
   prof_end(s);
@@ -1617,6 +1750,7 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
       PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
       L.k2 = dalloc<bf16>(kvn);
       L.v2 = dalloc<bf16>(kvn);
+      check(v_ones_col(L.v2, kvn / size_t(m.dhp), m.dhp, m.dh, nullptr), "v_ones_col");
       L.tm_k2 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
       L.tm_v2 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
     }
@@ -1641,6 +1775,7 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
     for (StageLayer& L : s.layers) {
       PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kvn * sizeof(bf16), s.stream));
       PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kvn * sizeof(bf16), s.stream));
+      check(v_ones_col(L.v, kvn / size_t(m.dhp), m.dhp, m.dh, s.stream), "v_ones_col");
     }
   auto view = [&](StageLayer& L, int fresh_lo, int fresh_hi) {
     const int nxt = 1 - prev;
@@ -2007,6 +2142,13 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
     for (StageLayer& L : s.layers) {
       PF_CUDA_CHECK(cudaMemsetAsync(L.k, 0, kv, s.stream));
       PF_CUDA_CHECK(cudaMemsetAsync(L.v, 0, kv, s.stream));
+      check(v_ones_col(L.v, kv / (size_t(m.dhp) * sizeof(bf16)), m.dhp, m.dh, s.stream),
+            "v_ones_col");
+      if (L.k32) {
+        const size_t n32 = size_t(m.rows_total()) * size_t(m.hs) * sizeof(float);
+        PF_CUDA_CHECK(cudaMemsetAsync(L.k32, 0, n32, s.stream));
+        PF_CUDA_CHECK(cudaMemsetAsync(L.v32, 0, n32, s.stream));
+      }
     }
   }
   if (px) px_conditioning(s, steps);
@@ -2501,6 +2643,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
                float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                s.attn_work_floats};
   a.flags = s.attn_flags;
+  a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
   prof_begin(s, kAttention, 4 * r * P * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
   prof_end(s);
@@ -2539,6 +2682,7 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
                 float(1.0 / std::sqrt(double(m.dh))), s.attn, s.attn_work,
                 s.attn_work_floats};
   ca.flags = s.attn_flags;
+  ca.v_sum_col = m.dh < m.dhp;
   ca.q_stride = int(m.P);
   prof_begin(s, kCrossAttention, 4 * r * T * dhs, 0);
   check(attention(s.tm_q, L.tm_kc, L.tm_vc, ca, s.sm_count, s.stream), "cross attention");

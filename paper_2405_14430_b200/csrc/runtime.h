@@ -58,6 +58,10 @@ struct ModelShape {
   // their own), the rest single-stream parallel blocks (Flux-style: shared
   // weights over all joint rows, attention and MLP both read the block input)
   int double_layers = 0;
+  // kPrecBf16: the product path (bf16 tcgen05 operands, fp32 accumulation);
+  // kPrecFp32: parity mode (toy block only): fp32 weights, activations and
+  // K/V buffers, CUDA-core kernels (parity_f32.cu), same executor
+  int precision = 0;
   // joint-row offset of image row 0 and rows of the activation / K/V buffers
   int64_t J() const { return block == 2 ? T : 0; }
   int64_t rows_total() const { return P + J(); }
@@ -65,6 +69,8 @@ struct ModelShape {
 
 constexpr int kBlockToy = 0;
 constexpr int kBlockPixArt = 1;
+constexpr int kPrecBf16 = 0;
+constexpr int kPrecFp32 = 1;
 // SD3-style joint-attention block (MMDiT double stream, toy arithmetic per
 // stream): T text rows precede the P image rows in every activation and K/V
 // buffer ("joint rows"); text rows are recomputed with patch 0 of every step.
@@ -106,6 +112,9 @@ struct StageLayer {
   WeightMaps tm_wqc, tm_wkvc, tm_woc;
   bf16 *kc = nullptr, *vc = nullptr;
   CUtensorMap tm_kc, tm_vc;
+  // fp32 parity mode: w32 = [Wq | Wk | Wv | Wo] (4 x [hs x hs]), Win [hs x mlp],
+  // Wout [mlp x hs], x.W orientation row-major; K/V [P x hs] row-major
+  float *w32 = nullptr, *k32 = nullptr, *v32 = nullptr;
 };
 
 // PixArt per-stage conditioning state (adaLN-single and the LayerNorm fold).
@@ -135,6 +144,7 @@ struct Stage {
   cudaStream_t stream = nullptr;
   std::vector<StageLayer> layers;
   float* h32 = nullptr;   // [P x hs] residual stream (landing buffer)
+  float *q32 = nullptr, *attn32 = nullptr, *z32 = nullptr;  // fp32 parity mode
   bf16* hb = nullptr;     // [P x hs] bf16 operand copy of h32
   bf16* q = nullptr;      // [heads][P][dhp]
   bf16* attn = nullptr;   // [P x hs]
@@ -352,6 +362,7 @@ class Engine {
   };
   void layer_forward(Stage& s, int lf, int rows, int row0, int code,
                      const KvView* kv = nullptr);
+  void layer_forward_f32(Stage& s, int lf, int rows, int row0, int code);
   void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
   void layer_forward_joint(Stage& s, int lf, int rows, int row0, int code);
   void layer_forward_single(Stage& s, int lf, int rows, int row0, int code);
@@ -480,7 +491,8 @@ class Engine {
   void use_lane(Stage& s, int lane);
   void alloc_lanes(Stage& s, int lanes);
   int lanes_for(int patches) const {
-    if (patches < 2 || stages_.size() != 1 || profiling_ || timeline_on_ || rank_mode())
+    if (patches < 2 || stages_.size() != 1 || profiling_ || timeline_on_ || rank_mode() ||
+        shape_.precision != kPrecBf16)
       return 1;
     return lanes_ < patches ? lanes_ : patches;
   }

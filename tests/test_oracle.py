@@ -199,3 +199,42 @@ def test_c1_survey_values():
                        [0.32449335502956572, 0.24827867908782209, -0.39906740005157071],
                        rtol=0, atol=1e-15)
     assert float(s4["x_pipefusion"].sum()) == pytest.approx(271.39910203039642, rel=1e-12)
+
+
+# ------------------------------------------------------ 4. numpy restatement pinned
+def test_np_oracle_layer_forward_matches_reference(ref):
+    """oracle/np_oracle.layer_forward (the vectorised fp64 checker the C2 / C3
+    layer-unit GPU tests use at widths where the scalar restatement is too
+    slow) against the reference's own toy_layer_forward (oracle/_ref) at
+    hs=128: equal up to summation order."""
+    from oracle import np_oracle
+    hs, heads, p, rows, row0 = 128, 4, 256, 64, 64
+    m = ref.build_toy_model(3, 2, hs, heads, 4.0)
+    weights, _ = m.weights()
+    rng = np.random.default_rng(11)
+    h = rng.uniform(-1, 1, (rows, hs))
+    k = rng.uniform(-1, 1, (p, hs))
+    v = rng.uniform(-1, 1, (p, hs))
+    for layer in range(2):
+        rh, rk, rv = m.layer_forward(layer, h, k, v, row0)
+        nk, nv = k.copy(), v.copy()
+        nh = np_oracle.layer_forward(weights[layer], heads, h.copy(), nk, nv, row0)
+        assert np.abs(nh - rh).max() <= 1e-12 * np.abs(rh).max()
+        assert np.abs(nk - rk).max() <= 1e-12 and np.abs(nv - rv).max() <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c2s_s1_w0", "c2s_s2_w1", "c2s_s4_w1"])
+def test_c2_short_horizon_fixture_stats(rs, name):
+    """The C2-shape fixtures (tests/golden/make_golden_c2.py) carry the
+    staleness stats of their (p, M, S, W): they do not depend on the model's
+    width or depth per layer, so a small model of the same depth reproduces
+    them exactly; the latent is finite and of the C2 shape."""
+    g = np.load(GOLDEN / f"{name}.npz")
+    c = eval(str(g["config"]))  # noqa: S307 - our own fixture
+    assert g["x_pipefusion"].shape == (c["p"], c["hs"])
+    assert np.isfinite(g["x_pipefusion"]).all()
+    m = rs.build_toy_model(0, c["L"], 8, 2)
+    x0 = rs.make_initial_latent(0, c["p"], 8)
+    _, (fresh, stale, ff) = m.run_pipefusion(x0, c["S"], 1, c["M"], c["W"], c["eta"])
+    assert (fresh, stale) == (int(g["fresh"]), int(g["stale"]))
+    assert np.array_equal(np.asarray(ff), g["fresh_fraction"])
