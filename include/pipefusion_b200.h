@@ -130,6 +130,26 @@ pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout la
 /* 0 = toy block, 1 = PixArt block, 2 = joint block, -1 = NULL context. */
 int pf_block_kind(const pf_ctx* ctx);
 
+/* MMDiT block variants (BASELINE configs 4 and 5; no reference analogue --
+ * spec: oracle/mmdit_oracle.py). Layers [0, double_layers) are SD3 / Flux
+ * double-stream joint blocks (per-stream adaLN-Zero modulation, LayerNorm,
+ * QK RMSNorm, GELU MLP; text and image rows attend over one joint K/V
+ * buffer), the rest Flux single-stream parallel blocks; rope != 0 adds the
+ * Flux axial RoPE. Every parameter (and the text tokens) is generated on the
+ * device from `seed` with the counter-based stream of the spec, so a 12B
+ * Flux model needs no host copy. Same executor and schedule as
+ * pf_create_toy; text rows as pf_create_joint. */
+pf_status pf_create_mmdit(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                          int double_layers, int rope, const int* devices, int n_stages,
+                          pf_ctx** out);
+pf_status pf_create_mmdit_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                               int double_layers, int rope, int rank, int world, int device,
+                               pf_ctx** out);
+/* Device bytes of the context's parameters (weights, biases, modulation)
+ * and of its K/V buffers, summed over its stages (rank mode: this rank's). */
+size_t pf_stage_param_bytes(const pf_ctx* ctx);
+size_t pf_stage_kv_bytes(const pf_ctx* ctx);
+
 /* ---- One process per GPU ("rank mode") ----
  * The reference runs one worker thread per stage exchanging PatchMsg values
  * over bounded channels (run_pipefusion_threads, execute.cpp:231-385). In rank

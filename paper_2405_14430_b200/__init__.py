@@ -28,7 +28,8 @@ __all__ = [
     "StalenessStats", "ParallelRunResult", "ToyDiTCuda", "EXPORTED_SYMBOLS",
     "mlp_hidden_of", "make_initial_latent", "KERNEL_KINDS", "PixArtCuda", "rank_plan",
     "PLAN_KINDS", "connect_ranks", "connect_distributed", "trace_json", "JointDiTCuda",
-    "SerialResult", "AutoWarmupResult", "root_cause", "reset_distributed",
+    "SerialResult", "AutoWarmupResult", "root_cause", "reset_distributed", "MMDiTCuda",
+    "PRECISION_BF16", "PRECISION_FP32",
 ]
 
 LIB_PATH = Path(__file__).resolve().parent / "libpipefusion_b200.so"
@@ -49,6 +50,7 @@ EXPORTED_SYMBOLS = [
     "pf_debug_attn_schedule", "pf_serial_reference_ex", "pf_auto_warmup", "pf_divergence",
     "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_device_count", "pf_debug_fail_at",
     "pf_debug_poison_layer", "pf_create_toy_ex", "pf_create_toy_rank_ex", "pf_precision_of",
+    "pf_create_mmdit", "pf_create_mmdit_rank", "pf_stage_param_bytes", "pf_stage_kv_bytes",
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
@@ -114,6 +116,14 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_create_joint_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
                                          i32, i32, ctypes.POINTER(vp)]
     lib.pf_block_kind.argtypes = [vp]
+    lib.pf_create_mmdit.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
+                                    ctypes.POINTER(i32), i32, ctypes.POINTER(vp)]
+    lib.pf_create_mmdit_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
+                                         i32, i32, i32, ctypes.POINTER(vp)]
+    lib.pf_stage_param_bytes.argtypes = [vp]
+    lib.pf_stage_param_bytes.restype = ctypes.c_size_t
+    lib.pf_stage_kv_bytes.argtypes = [vp]
+    lib.pf_stage_kv_bytes.restype = ctypes.c_size_t
     lib.pf_layer_forward_t.argtypes = [vp, i32, i32, i32, dptr, i64, i64, dptr, dptr, i32]
     lib.pf_create_toy_rank.argtypes = [ctypes.c_uint64, ctypes.POINTER(_Desc), i32, i32, i32,
                                        ctypes.POINTER(vp)]
@@ -300,7 +310,7 @@ class ToyDiTCuda:
     def __init__(self, seed: int, layers: int, hidden_size: int, heads: int,
                  mlp_ratio: float, seq_len: int, workers: int = 1,
                  devices: Optional[Sequence[int]] = None, _weights=None, _text_tokens=0,
-                 _rank=None, _joint=None, precision: int = 0):
+                 _rank=None, _joint=None, precision: int = 0, _mmdit=None):
         """precision: PRECISION_BF16 (the product path) or PRECISION_FP32
         (parity mode: fp32 CUDA-core kernels, same executor; toy block)."""
         self._lib = load_library()
@@ -314,7 +324,11 @@ class ToyDiTCuda:
             # rank mode: this context holds stage `rank` of `workers` on `device`
             rank, device = _rank
             self.rank, self.world = rank, workers
-            if _joint is not None:
+            if _mmdit is not None:
+                st = self._lib.pf_create_mmdit_rank(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                                    _text_tokens, _mmdit[0], _mmdit[1], rank,
+                                                    workers, device, ctypes.byref(self._ctx))
+            elif _joint is not None:
                 st = self._lib.pf_create_joint_rank(ctypes.c_uint64(seed), ctypes.byref(desc),
                                                     _text_tokens, _joint, rank, workers, device,
                                                     ctypes.byref(self._ctx))
@@ -333,7 +347,11 @@ class ToyDiTCuda:
         if len(devs) != workers:
             raise ValidationError("devices must list one CUDA device per worker")
         dev_arr = (ctypes.c_int * max(1, workers))(*devs)
-        if _joint is not None:
+        if _mmdit is not None:
+            st = self._lib.pf_create_mmdit(ctypes.c_uint64(seed), ctypes.byref(desc),
+                                           _text_tokens, _mmdit[0], _mmdit[1], dev_arr, workers,
+                                           ctypes.byref(self._ctx))
+        elif _joint is not None:
             st = self._lib.pf_create_joint(ctypes.c_uint64(seed), ctypes.byref(desc),
                                            _text_tokens, _joint, dev_arr, workers,
                                            ctypes.byref(self._ctx))
@@ -423,6 +441,14 @@ class ToyDiTCuda:
             c = self._lib.pf_stage_layer_count(self._ctx, d)
             out.append(range(f, f + c))
         return out
+
+    def param_bytes(self) -> int:
+        """Device bytes of this context's parameters (pf_stage_param_bytes)."""
+        return int(self._lib.pf_stage_param_bytes(self._ctx))
+
+    def kv_bytes(self) -> int:
+        """Device bytes of this context's K/V buffers (pf_stage_kv_bytes)."""
+        return int(self._lib.pf_stage_kv_bytes(self._ctx))
 
     @property
     def precision(self) -> int:
@@ -768,6 +794,43 @@ class JointDiTCuda(ToyDiTCuda):
         return obj
 
     def set_text(self, y) -> None:
+        y = _f64c(y)
+        _raise(self._lib.pf_set_text(self._ctx, _dptr(y), y.shape[0], PF_ROW_MAJOR),
+               self._err())
+
+
+class MMDiTCuda(ToyDiTCuda):
+    """MMDiT blocks (pf_create_mmdit): `double_layers` SD3 / Flux double-stream
+    joint blocks, then Flux single-stream blocks; `rope` adds the Flux axial
+    RoPE. Parameters and text tokens are generated on the device from `seed`
+    (oracle/mmdit_oracle.py MMDiT holds the same values)."""
+
+    def __init__(self, seed: int, layers: int, hidden_size: int, heads: int, mlp_ratio: float,
+                 seq_len: int, text_tokens: int, workers: int = 1,
+                 devices: Optional[Sequence[int]] = None, double_layers: Optional[int] = None,
+                 rope: bool = False):
+        self.text_tokens = text_tokens
+        self.double_layers = layers if double_layers is None else double_layers
+        self.rope = bool(rope)
+        super().__init__(seed, layers, hidden_size, heads, mlp_ratio, seq_len, workers,
+                         devices, _text_tokens=text_tokens,
+                         _mmdit=(self.double_layers, int(self.rope)))
+
+    @classmethod
+    def rank_stage(cls, seed: int, layers: int, hidden_size: int, heads: int, mlp_ratio: float,
+                   seq_len: int, text_tokens: int, rank: int, world: int, device: int = 0,
+                   double_layers: Optional[int] = None, rope: bool = False) -> "MMDiTCuda":
+        obj = cls.__new__(cls)
+        obj.text_tokens = text_tokens
+        obj.double_layers = layers if double_layers is None else double_layers
+        obj.rope = bool(rope)
+        ToyDiTCuda.__init__(obj, seed, layers, hidden_size, heads, mlp_ratio, seq_len, world,
+                            None, _text_tokens=text_tokens, _rank=(rank, device),
+                            _mmdit=(obj.double_layers, int(obj.rope)))
+        return obj
+
+    def set_text(self, y) -> None:
+        """Replace the text tokens [text_tokens x hidden] (pf_set_text)."""
         y = _f64c(y)
         _raise(self._lib.pf_set_text(self._ctx, _dptr(y), y.shape[0], PF_ROW_MAJOR),
                self._err())

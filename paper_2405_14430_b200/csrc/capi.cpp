@@ -369,7 +369,7 @@ pf_status pf_set_text(pf_ctx* ctx, const double* y, int64_t tokens, pf_layout la
   if (!ctx) return PF_VALIDATION;
   return guarded(&ctx->last_error, [&] {
     const pf::ModelShape& m = ctx->engine->shape();
-    if (m.block != pf::kBlockPixArt && m.block != pf::kBlockJoint)
+    if (m.block != pf::kBlockPixArt && !m.joint_rows())
       throw pf::ValidationError("model has no text conditioning");
     if (!y) throw pf::ValidationError("NULL text pointer");
     if (tokens != m.T) throw pf::ValidationError("text token count does not match the model");
@@ -396,6 +396,50 @@ pf_status pf_create_joint(uint64_t seed, const pf_model_desc* desc, int text_tok
     load_joint(*ctx->engine, seed, text_tokens, double_layers);
     *out = ctx.release();
   });
+}
+
+pf_status pf_create_mmdit(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                          int double_layers, int rope, const int* devices, int n_stages,
+                          pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.block = pf::kBlockMMDiT;
+    s.T = text_tokens;
+    s.double_layers = double_layers;
+    s.rope = rope ? 1 : 0;
+    ctx->engine = std::make_unique<pf::Engine>(s, device_list(devices, n_stages));
+    ctx->engine->mm_generate(seed);
+    *out = ctx.release();
+  });
+}
+
+pf_status pf_create_mmdit_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,
+                               int double_layers, int rope, int rank, int world, int device,
+                               pf_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded(&g_create_error, [&] {
+    if (!out) throw pf::ValidationError("output pointer is NULL");
+    auto ctx = std::make_unique<pf_ctx>();
+    pf::ModelShape s = shape_of(desc);
+    s.block = pf::kBlockMMDiT;
+    s.T = text_tokens;
+    s.double_layers = double_layers;
+    s.rope = rope ? 1 : 0;
+    ctx->engine = std::make_unique<pf::Engine>(s, device, rank, world);
+    ctx->engine->mm_generate(seed);
+    *out = ctx.release();
+  });
+}
+
+size_t pf_stage_param_bytes(const pf_ctx* ctx) {
+  return ctx && ctx->engine ? ctx->engine->param_bytes() : 0;
+}
+
+size_t pf_stage_kv_bytes(const pf_ctx* ctx) {
+  return ctx && ctx->engine ? ctx->engine->kv_bytes() : 0;
 }
 
 pf_status pf_create_joint_rank(uint64_t seed, const pf_model_desc* desc, int text_tokens,

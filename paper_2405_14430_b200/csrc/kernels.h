@@ -222,6 +222,23 @@ cudaError_t px_patch_prepare(float* x, const float* eps, const float* cb, const 
                              float* h32, bf16* hb, float2* stats, int stats_ld, int row0,
                              int rows, int hs, float eta, bool update, cudaStream_t stream);
 
+// ---- MMDiT blocks (mmdit.cu; spec oracle/mmdit_oracle.py) ----
+// key of tensor `tid` of a model seeded with `seed` (splitmix64 stream)
+uint64_t mm_tensor_key(uint64_t seed, uint64_t tid);
+// parameter tensor [K x N] (x.W orientation) -> kind 0: bf16 [N x K] (K-major),
+// 1: fp32 [K x N] * scale, 2: fp32 1 + 0.1 u (gains), 3: fp32 [N x K] * scale
+cudaError_t mm_fill(void* dst, uint64_t key, int64_t K, int64_t N, float scale, int kind,
+                    cudaStream_t stream);
+// out[s][n] (row pitch ld_out) = in[s] . W[n] + b[n], W bf16 [N x K], s < S
+cudaError_t mm_gemv_bf16(const float* in, int S, int K, const bf16* W, const float* b, int N,
+                         float* out, int ld_out, cudaStream_t stream);
+// QK-norm (+ Flux RoPE) in place on joint rows [row0, row0+rows) of the
+// head-major q [heads][q_rows][dhp] and k [heads][k_rows][dhp]
+cudaError_t mm_qk_norm_rope(bf16* q, bf16* k, int heads, int q_rows, int k_rows, int dhp, int dh,
+                            int row0, int rows, int J, const float* gq_img, const float* gk_img,
+                            const float* gq_txt, const float* gk_txt, bool rope, int side,
+                            cudaStream_t stream);
+
 // Deterministic fp64 reductions (fixed grid and order), for auto_warmup and
 // divergence (toy_model.cpp:216-249). `work`: sumsq_work_bytes() of scratch.
 // out[0] = sum x^2, out[1] = sum (eta eps)^2  over n fp32 elements

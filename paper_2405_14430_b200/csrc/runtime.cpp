@@ -1,5 +1,6 @@
 // PipeFusion runtime (see runtime.h for the mapping onto the reference).
 #include "runtime.h"
+#include "runtime_internal.h"
 
 #include <algorithm>
 #include <climits>
@@ -15,17 +16,6 @@
 #include <unistd.h>
 
 namespace pf {
-
-#define PF_CUDA_CHECK(expr)                                                  \
-  do {                                                                       \
-    cudaError_t _e = (expr);                                                 \
-    if (_e != cudaSuccess) {                                                 \
-      std::ostringstream _os;                                                \
-      _os << "CUDA error " << cudaGetErrorString(_e) << " at " << __FILE__   \
-          << ":" << __LINE__ << " (" #expr ")";                              \
-      throw CudaError(_os.str());                                            \
-    }                                                                        \
-  } while (0)
 
 namespace {
 
@@ -53,18 +43,6 @@ struct LaunchTally {
   ~LaunchTally() { out = launch_counter() - base; }
 };
 
-struct DeviceGuard {
-  int prev = 0;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    if (cur != prev) cudaSetDevice(prev);
-  }
-};
 
 template <class T>
 T* dalloc(size_t n) {
@@ -94,23 +72,7 @@ CUtensorMap tmap(const void* base, uint64_t inner, uint64_t outer,
   return m;
 }
 
-// The stage's split-K workspace attached to a GEMM's epilogue parameters
-// (skinny residual split-K itself is opt-in, kernels.cu).
-EpiParams sk(const Stage& s, EpiParams ep) {
-  ep.splitk_ws = s.splitk_ws;
-  ep.splitk_ws_floats = s.splitk_ws_floats;
-  ep.splitk_counters = s.splitk_counters;
-  ep.splitk_counter_cap = s.splitk_counter_cap;
-  return ep;
-}
 
-void check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    std::ostringstream os;
-    os << "CUDA error " << cudaGetErrorString(e) << " launching " << what;
-    throw CudaError(os.str());
-  }
-}
 
 // Graph nodes of captured stream memory operations (batch mem-op nodes):
 // enumerated once after capture, their values patched before a replay.
@@ -192,16 +154,22 @@ void validate_shape(const ModelShape& s) {
     throw ValidationError("CUDA backend needs hidden_size and mlp hidden size divisible by 8");
   if (s.P % 8 != 0) throw ValidationError("CUDA backend needs seq_len divisible by 8");
   if (s.hs / s.heads > 128) throw ValidationError("CUDA backend supports head dim <= 128");
-  if (s.block != kBlockToy && s.block != kBlockPixArt && s.block != kBlockJoint)
+  if (s.block != kBlockToy && s.block != kBlockPixArt && s.block != kBlockJoint &&
+      s.block != kBlockMMDiT)
     throw ValidationError("unknown block kind");
-  if (s.block == kBlockJoint && s.T < 1)
+  if (s.joint_rows() && s.T < 1)
     throw ValidationError("joint block needs at least one text token");
-  if (s.block == kBlockJoint && (s.double_layers < 0 || s.double_layers > s.layers))
+  if (s.joint_rows() && (s.double_layers < 0 || s.double_layers > s.layers))
     throw ValidationError("double-stream layer count must lie in [0, layers]");
   if (s.precision != kPrecBf16 && s.precision != kPrecFp32)
     throw ValidationError("unknown precision");
   if (s.precision == kPrecFp32 && s.block != kBlockToy)
     throw ValidationError("the fp32 parity mode supports the toy block only");
+  if (s.block == kBlockMMDiT) {
+    if (s.hs % 64 != 0) throw ValidationError("MMDiT block needs hidden_size divisible by 64");
+    if (s.rope && s.dh % 32 != 0)
+      throw ValidationError("RoPE needs a head dim divisible by 32 (axes dh/8, 7dh/16, 7dh/16)");
+  }
   if (s.block == kBlockPixArt) {
     if (s.hs % 32 != 0)
       throw ValidationError("PixArt block needs hidden_size divisible by 32");
@@ -356,7 +324,7 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
   if (is_first) {
     s.x = dalloc<float>(size_t(m.P) * hs);
     s.cb = dalloc<float>(hs);
-    if (m.block == kBlockJoint) s.text = dalloc<float>(size_t(m.T) * hs);
+    if (m.joint_rows()) s.text = dalloc<float>(size_t(m.T) * hs);
   }
   if (m.block == kBlockJoint) {
     for (int lf = 0; lf < count; ++lf) {
@@ -373,6 +341,7 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
         throw CudaError("cuTensorMapEncodeTiled failed for a text-stream weight");
     }
   }
+  if (m.block == kBlockMMDiT) mm_alloc_stage(s);
   if (m.block == kBlockPixArt) {
     const size_t T = size_t(m.T), Tpad = (T + 127) / 128 * 128;
     const size_t kvc_rows = heads * T + 128;  // + one TMA box of zero rows
@@ -463,6 +432,7 @@ void Engine::free_stage(Stage& s) {
     dfree(L.k); dfree(L.v);
     dfree(L.w32); dfree(L.k32); dfree(L.v32);
   }
+  if (shape_.block == kBlockMMDiT) mm_free_stage(s);
   for (StageLayer& L : s.layers) {
     for (float* p : {L.bqkv, L.bo, L.bqc, L.bkvc, L.boc, L.b1, L.b2}) dfree(p);
     dfree(L.k2); dfree(L.v2);
@@ -777,9 +747,9 @@ void Engine::send_rows(int from, int row0, int rows, int patch, int t) {
                                   cudaMemcpyDefault, src.stream));
     PF_CUDA_CHECK(cudaMemcpyAsync(dst.hb + off, src.hb + off, cnt * 2,
                                   cudaMemcpyDefault, src.stream));
-    if (shape_.block == kBlockPixArt) {
-      // LayerNorm partial sums of the rows ([hs/32][P] float2)
-      const size_t pitch = size_t(shape_.P) * sizeof(float2);
+    if (shape_.ln_stats()) {
+      // LayerNorm partial sums of the rows ([hs/32][P + T] float2)
+      const size_t pitch = size_t(shape_.rows_total()) * sizeof(float2);
       PF_CUDA_CHECK(cudaMemcpy2DAsync(dst.px.stats + row0, pitch, src.px.stats + row0, pitch,
                                       size_t(rows) * sizeof(float2), size_t(shape_.hs / 32),
                                       cudaMemcpyDefault, src.stream));
@@ -924,15 +894,18 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     codes_.emplace_back(t, layer);
     return int(codes_.size()) - 1;
   };
-  if (px)
+  const bool mm = m.block == kBlockMMDiT;
+  if (px || mm)
     for (Stage& s : stages_) {
       DeviceGuard g(s.device);
-      px_conditioning(s, steps);
+      if (px) px_conditioning(s, steps);
+      else mm_conditioning(s, steps);
     }
-  const bool joint = m.block == kBlockJoint;
+  const bool joint = m.joint_rows();
   const int J = int(m.J());  // joint block: text rows [0, J) precede the image rows
   auto forward = [&](Stage& s, int lf, int rows, int row0, int t, int code) {
     if (px) layer_forward_px(s, lf, rows, row0, t, code);
+    else if (mm) layer_forward_mm(s, lf, rows, row0, t, code);
     else if (joint && s.first_layer + lf < m.double_layers)
       layer_forward_joint(s, lf, rows, row0, code);
     else if (joint)
@@ -940,7 +913,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
     else layer_forward(s, lf, rows, row0, code);
   };
   // joint block: the text stream re-enters from the text tokens every step
-  auto text_prepare = [&]() {
+  auto text_prepare = [&](int t) {
+    if (mm) {
+      mm_text_prepare(s0, t);
+      return;
+    }
     check(patch_prepare(s0.text, nullptr, s0.zeros, s0.h32, s0.hb, 0, J, m.hs, 0.f, false,
                         s0.stream), "text rows");
   };
@@ -960,9 +937,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
       DeviceGuard g(s0.device);
       tl_begin(0, 0, -1, t, s0.stream);
       prof_begin(s0, kSampler, 0, double(m.P) * m.hs * (4 + 4 + 2));
-      if (joint) text_prepare();
+      if (joint) text_prepare(t);
       if (px)
         px_patch_prepare(x_dev, false, 0, int(m.P), t, 0.f);
+      else if (mm)
+        mm_patch_prepare(s0, x_dev, false, 0, int(m.P), t, 0.f);
       else
         check(patch_prepare(x_dev, nullptr, s0.cb, h32_img, hb_img, 0, int(m.P), m.hs,
                             0.f, false, s0.stream), "patch_prepare");
@@ -1052,9 +1031,11 @@ void Engine::enqueue_run(float* x_dev, int steps, int patches, int warmup,
           PF_CUDA_CHECK(cudaStreamWaitEvent(s0.stream, s0.ev_eps[size_t(j)], 0));
         tl_begin(0, 0, j, t, s0.stream);
         prof_begin(s0, kSampler, 0, double(r) * m.hs * (q > 0 ? 4 + 4 + 4 + 4 + 2 : 4 + 4 + 2));
-        if (joint && j == 0) text_prepare();
+        if (joint && j == 0) text_prepare(t);
         if (px)
           px_patch_prepare(x_dev, q > 0, row0, r, t, eta);
+        else if (mm)
+          mm_patch_prepare(s0, x_dev, q > 0, row0, r, t, eta);
         else
           check(patch_prepare(x_dev, s0.eps, s0.cb, h32_img, hb_img, row0, r, m.hs, eta,
                               q > 0, s0.stream), "patch_prepare");
@@ -1138,6 +1119,8 @@ void Engine::prepare_run(int patches, int steps) {
   Stage& s0 = stages_[0];
   if (shape_.block == kBlockPixArt && steps >= 1)
     for (Stage& s : stages_) px_alloc_run(s, steps);
+  if (shape_.block == kBlockMMDiT && steps >= 1)
+    for (Stage& s : stages_) mm_alloc_run(s, steps);
   if (!ev_start_) {
     DeviceGuard g(s0.device);
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
@@ -1266,6 +1249,7 @@ void Engine::prepare_rank_run(int patches, int steps) {
   Stage& s = stages_[0];
   DeviceGuard g(s.device);
   if (shape_.block == kBlockPixArt) px_alloc_run(s, steps);
+  if (shape_.block == kBlockMMDiT) mm_alloc_run(s, steps);
   while (int(ev_sent_.size()) < patches) {
     cudaEvent_t e;
     PF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1452,7 +1436,7 @@ void Engine::layer_forward_host(int layer, double* h, int64_t rows, int64_t row0
                                 double* k_buf, double* v_buf, bool col_major, int t,
                                 int steps) {
   const ModelShape& m = shape_;
-  if (m.block == kBlockJoint)
+  if (m.joint_rows())
     throw ValidationError("single-layer entry point not available for the joint block");
   const int d = stage_of_layer(layer);
   if (d < 0) throw ValidationError("layer index out of range");
@@ -2046,7 +2030,7 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
   } else {
     succ_h32_ = static_cast<float*>(open(succ, succ.h_h32, succ.p_h32));
     succ_hb_ = static_cast<bf16*>(open(succ, succ.h_hb, succ.p_hb));
-    if (shape_.block == kBlockPixArt)
+    if (shape_.ln_stats())
       succ_stats_ = static_cast<float2*>(open(succ, succ.h_stats, succ.p_stats));
   }
   // tensor maps over the successor's buffers for the fused send (the last
@@ -2151,7 +2135,9 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
       }
     }
   }
+  const bool mm = m.block == kBlockMMDiT;
   if (px) px_conditioning(s, steps);
+  if (mm) mm_conditioning(s, steps);
 
   const uint32_t base_in = msgs_in_base_, base_out = msgs_out_base_;
   const auto plan = build_rank_plan(rank_, world_, steps, patches, warmup, m.P);
@@ -2163,7 +2149,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
     const char* e = std::getenv("PF_RANK_COPY");
     return e && e[0] == '1';
   }();
-  const bool joint = m.block == kBlockJoint;
+  const bool joint = m.joint_rows();
   const int J = int(m.J());
   // joint block: the eps rows of the last rank are image rows (offset by the
   // text rows), which the GEMM's joint-row stores cannot address: copy them
@@ -2261,11 +2247,16 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
         tl_begin(rank_, 0, op.patch, op.t, s.stream);
         prof_begin(s, kSampler, 0, double(rows) * hs * (op.flag ? 18 : 10));
         if (joint && op.patch <= 0) {  // the text stream re-enters each step
-          check(patch_prepare(s.text, nullptr, s.zeros, s.h32, s.hb, 0, J, m.hs, 0.f, false,
-                              s.stream), "text rows");
+          if (mm)
+            mm_text_prepare(s, op.t);
+          else
+            check(patch_prepare(s.text, nullptr, s.zeros, s.h32, s.hb, 0, J, m.hs, 0.f, false,
+                                s.stream), "text rows");
         }
         if (px)
           px_patch_prepare(x_dev, op.flag != 0, row0, rows, op.t, eta);
+        else if (mm)
+          mm_patch_prepare(s, x_dev, op.flag != 0, row0, rows, op.t, eta);
         else
           check(patch_prepare(x_dev, s.eps, s.cb, s.h32 + size_t(J) * hs, s.hb + size_t(J) * hs,
                               row0, rows, m.hs, eta, op.flag != 0, s.stream), "patch_prepare");
@@ -2325,6 +2316,7 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
             lane_rec_ = s.ev_attn[op.patch % nl][size_t(lf)];
           }
           if (px) layer_forward_px(s, lf, rows, row0, t, code);
+          else if (mm) layer_forward_mm(s, lf, brows, brow0, t, code);
           else if (joint && s.first_layer + lf < m.double_layers)
             layer_forward_joint(s, lf, brows, brow0, code);
           else if (joint)
@@ -2373,11 +2365,12 @@ void Engine::enqueue_rank_run(float* x_dev, int steps, int patches, int warmup, 
                                         cudaMemcpyDefault, send_stream_));
           PF_CUDA_CHECK(cudaMemcpyAsync(succ_hb_ + off, s.hb + off, cnt * 2, cudaMemcpyDefault,
                                         send_stream_));
-          if (px) {
-            const size_t pitch = size_t(m.P) * sizeof(float2);
-            PF_CUDA_CHECK(cudaMemcpy2DAsync(succ_stats_ + row0, pitch, s.px.stats + row0, pitch,
-                                            size_t(rows) * sizeof(float2), size_t(m.hs / 32),
-                                            cudaMemcpyDefault, send_stream_));
+          if (m.ln_stats()) {
+            const size_t pitch = size_t(m.rows_total()) * sizeof(float2);
+            PF_CUDA_CHECK(cudaMemcpy2DAsync(succ_stats_ + brow0, pitch, s.px.stats + brow0,
+                                            pitch, size_t(brows) * sizeof(float2),
+                                            size_t(m.hs / 32), cudaMemcpyDefault,
+                                            send_stream_));
           }
         }
         tl_end(send_stream_);
@@ -2527,7 +2520,7 @@ void Engine::load_px_globals(const double* const* gw) {
 }
 
 void Engine::set_text(const double* y) {
-  if (shape_.block == kBlockJoint) {
+  if (shape_.joint_rows()) {
     Stage& s0 = stages_[0];
     if (!s0.text) return;  // rank mode, rank > 0: text enters the pipeline on rank 0
     std::vector<float> t(size_t(shape_.T) * shape_.hs);

@@ -62,8 +62,15 @@ struct ModelShape {
   // kPrecFp32: parity mode (toy block only): fp32 weights, activations and
   // K/V buffers, CUDA-core kernels (parity_f32.cu), same executor
   int precision = 0;
+  // MMDiT block: Flux axial RoPE on q / k (0: none, SD3-style)
+  int rope = 0;
   // joint-row offset of image row 0 and rows of the activation / K/V buffers
-  int64_t J() const { return block == 2 ? T : 0; }
+  // (joint and MMDiT blocks: T text rows first)
+  bool joint_rows() const { return block == 2 || block == 3; }
+  // blocks whose GEMMs consume LayerNorm statistics of the residual stream
+  // (PixArt, MMDiT): the stats travel with the rows across stage boundaries
+  bool ln_stats() const { return block == 1 || block == 3; }
+  int64_t J() const { return joint_rows() ? T : 0; }
   int64_t rows_total() const { return P + J(); }
 };
 
@@ -75,6 +82,12 @@ constexpr int kPrecFp32 = 1;
 // stream): T text rows precede the P image rows in every activation and K/V
 // buffer ("joint rows"); text rows are recomputed with patch 0 of every step.
 constexpr int kBlockJoint = 2;
+// MMDiT blocks (oracle/mmdit_oracle.py): SD3-style double-stream joint blocks
+// (per-stream adaLN-Zero, LayerNorm, QK RMSNorm, GELU MLP) for layers
+// [0, double_layers), Flux-style single-stream parallel blocks after them;
+// optional Flux RoPE. Joint rows as kBlockJoint; conditioning and LayerNorm
+// folding through the PixArt machinery (PxStage, stats [hs/32][P + T]).
+constexpr int kBlockMMDiT = 3;
 constexpr int kPxFreq = 256;  // sinusoidal timestep features
 
 // Host fp64 source of one layer's weights, in the reference's orientation
@@ -112,6 +125,13 @@ struct StageLayer {
   WeightMaps tm_wqc, tm_wkvc, tm_woc;
   bf16 *kc = nullptr, *vc = nullptr;
   CUtensorMap tm_kc, tm_vc;
+  // MMDiT: text-stream biases (double layers), adaLN-Zero modulation
+  // weights (bf16 [6hs x hs] double / [3hs x hs] single, per stream) and
+  // biases, QK-norm gains [dh] per stream
+  float *t_bqkv = nullptr, *t_bo = nullptr, *t_b1 = nullptr, *t_b2 = nullptr;
+  bf16 *wmod = nullptr, *t_wmod = nullptr;
+  float *bmod = nullptr, *t_bmod = nullptr;
+  float *gq = nullptr, *gk = nullptr, *t_gq = nullptr, *t_gk = nullptr;
   // fp32 parity mode: w32 = [Wq | Wk | Wv | Wo] (4 x [hs x hs]), Win [hs x mlp],
   // Wout [mlp x hs], x.W orientation row-major; K/V [P x hs] row-major
   float *w32 = nullptr, *k32 = nullptr, *v32 = nullptr;
@@ -186,6 +206,11 @@ struct Stage {
   float* text = nullptr;   // joint block: [T x hs] text tokens (fp32), stage 0
   std::vector<cudaEvent_t> ev_eps;  // per patch, recorded by the last stage
   PxStage px;
+  // MMDiT: modulation weights of the global layer after this stage's last
+  // (its scale1 shapes the bf16 operand this stage hands over); per stream
+  bf16 *mm_next_wmod[2] = {nullptr, nullptr};
+  float *mm_next_bmod[2] = {nullptr, nullptr};
+  float* mm_bcond = nullptr;  // bt2 + y_pooled (MMDiT conditioning bias)
 };
 
 // Kernel kinds for the optional per-launch CUDA-event profile.
@@ -255,6 +280,9 @@ class Engine {
   // t_embedder / t_block weights (x.W orientation): wt1 [256 x hs], bt1,
   // wt2 [hs x hs], bt2, wt0 [hs x 6hs], bt0.
   void load_px_globals(const double* const* g);
+  // MMDiT: generate every parameter of this engine's stages on the device
+  // from `seed` (oracle/mmdit_oracle.py MMDiT), text tokens included
+  void mm_generate(uint64_t seed);
   // Text tokens y [T x hs] (row-major fp64) used by every stage's cross-attention.
   void set_text(const double* y);
   // Joint block: one layer's 12 matrices, image stream (w_q, w_k, w_v, w_o,
@@ -363,6 +391,23 @@ class Engine {
   void layer_forward(Stage& s, int lf, int rows, int row0, int code,
                      const KvView* kv = nullptr);
   void layer_forward_f32(Stage& s, int lf, int rows, int row0, int code);
+  // MMDiT (runtime_mmdit.cpp)
+  void mm_alloc_stage(Stage& s);
+  void mm_free_stage(Stage& s);
+  void mm_alloc_run(Stage& s, int steps);
+  void mm_conditioning(Stage& s, int steps);
+  void mm_patch_prepare(Stage& s0, float* x_dev, bool update, int row0, int rows, int t,
+                        float eta);
+  void mm_text_prepare(Stage& s0, int t);
+  void layer_forward_mm(Stage& s, int lf, int rows, int row0, int t, int code);
+  bool mm_double(int global_layer) const { return global_layer < shape_.double_layers; }
+
+ public:
+  // device bytes of this engine's parameters / K/V buffers (all its stages)
+  size_t param_bytes() const;
+  size_t kv_bytes() const;
+
+ private:
   void layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int code);
   void layer_forward_joint(Stage& s, int lf, int rows, int row0, int code);
   void layer_forward_single(Stage& s, int lf, int rows, int row0, int code);
