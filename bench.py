@@ -75,14 +75,20 @@ CONFIGS = {
     "c3px": dict(name="PixArt-alpha DiT block variant 2048px (28 layers, hidden 1152, 16 heads, "
                       "16384 tokens, 120 text tokens), 20 steps, 1 warmup",
                  L=28, hs=1152, heads=16, p=16384, S=20, W=1, block="pixart", T=120),
-    "c4": dict(name="SD3-medium-shaped joint-attention DiT 1024px (24 blocks, hidden 1536, "
-                    "24 heads, 4096 image + 333 text tokens in one K/V buffer; toy arithmetic "
-                    "per stream), 20 steps, 1 warmup",
-               L=24, hs=1536, heads=24, p=4096, S=20, W=1, block="joint", T=333),
-    "c5": dict(name="Flux.1-shaped DiT 2048px (19 double-stream + 38 single-stream blocks, "
-                    "hidden 3072, 24 heads, 16384 image + 512 text tokens, ~8.6B toy-block "
-                    "parameters), 28 steps, 1 warmup",
-               L=57, hs=3072, heads=24, p=16384, S=28, W=1, block="joint", T=512, D=19),
+    "c4": dict(name="SD3-medium-shaped MMDiT 1024px (24 double-stream joint blocks, hidden "
+                    "1536, 24 heads, 4096 image + 333 text tokens in one K/V buffer; adaLN-Zero, "
+                    "LayerNorm, QK RMSNorm, GELU MLP), 20 steps, 1 warmup",
+               L=24, hs=1536, heads=24, p=4096, S=20, W=1, block="mmdit", T=333, D=24,
+               rope=False),
+    "c5": dict(name="Flux.1-shaped MMDiT 2048px (19 double-stream + 38 single-stream blocks, "
+                    "hidden 3072, 24 heads, 16384 image + 512 text tokens, axial RoPE, QK "
+                    "RMSNorm, ~11.9B parameters), 28 steps, 1 warmup",
+               L=57, hs=3072, heads=24, p=16384, S=28, W=1, block="mmdit", T=512, D=19,
+               rope=True),
+    "c4toy": dict(name="SD3-medium-shaped joint-attention DiT 1024px (24 blocks, hidden 1536, "
+                       "24 heads, 4096 image + 333 text tokens; toy arithmetic per stream), "
+                       "20 steps, 1 warmup",
+                  L=24, hs=1536, heads=24, p=4096, S=20, W=1, block="joint", T=333),
     "c1": dict(name="tiny DiT (4 layers, hidden 128, 4 heads, 256 tokens), 5 steps, 1 warmup",
                L=4, hs=128, heads=4, p=256, S=5, W=1),
     "cref": dict(name="reference_execute.cfg (4 layers, hidden 32, 4 heads, 64 tokens), 20 "
@@ -94,7 +100,7 @@ def flops_per_image(c, mlp):
     """The reference's ComputeModel (simulate.cpp:30-44) for mlp_ratio 4:
     S * L * (24 p hs^2 + 4 p^2 hs); generalised to mlp = 4 hs."""
     p, hs = c["p"], c["hs"]
-    if c.get("block") == "joint":
+    if c.get("block") in ("joint", "mmdit"):
         # both streams' GEMMs over their rows and joint attention over p + T
         # rows, per step and layer; the text rows run once per step
         pt = p + c["T"]
@@ -211,6 +217,37 @@ def cpu_port_baseline_pixart(c, budget_s=20.0, sample_rows=32):
                        f"{wall:.1f}s); extrapolated x{samples_per_image:.0f} units/image")}
 
 
+def cpu_port_baseline_mmdit(c, budget_s=20.0, sample_rows=32):
+    """MMDiT blocks: no reference path exists, so the CPU baseline is the fp64
+    spec (oracle/mmdit_oracle.py, numpy) on sampled 32-row units of one block
+    of the true width (a double block for SD3, a single block for Flux's
+    majority) against the full joint K/V buffer, extrapolated."""
+    from oracle import mmdit_oracle as mo
+    single = c["D"] < c["L"] - c["D"]
+    m = mo.MMDiT(0, 1, c["hs"], c["heads"], 4 * c["hs"], c["T"], c["p"], 0 if single else 1,
+                 rope=c["rope"])
+    pt = c["p"] + c["T"]
+    rng = np.random.default_rng(0)
+    k = rng.uniform(-1, 1, (pt, c["hs"]))
+    v = rng.uniform(-1, 1, (pt, c["hs"]))
+    done, t0 = 0, time.perf_counter()
+    while True:
+        h = np.random.default_rng(done).uniform(-1, 1, (sample_rows, c["hs"]))
+        row0 = c["T"] + (done * sample_rows) % c["p"]
+        mo.layer_forward(m, 0, c["S"] - 1, c["S"], h, k, v, row0)
+        done += 1
+        if time.perf_counter() - t0 > budget_s * 0.5 or done >= 64:
+            break
+    wall = time.perf_counter() - t0
+    units = c["S"] * c["L"] * (pt / sample_rows)
+    cores = os.cpu_count() or 1
+    return {"value": wall / done * units, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"{done} {'single' if single else 'double'}-stream block units of "
+                       f"{sample_rows} rows x {pt}-row joint K/V (oracle/mmdit_oracle.py, "
+                       f"numpy fp64, BLAS threads up to {cores}) in {wall:.1f}s; extrapolated "
+                       f"x{units:.0f} units/image")}
+
+
 def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
     """Time the reference's own toy_layer_forward (oracle/_ref, built from
     /root/reference) at the true shape on `sample_rows` query rows against a
@@ -218,6 +255,8 @@ def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
     extrapolate to one image: S * L * (p / sample_rows) samples."""
     if c.get("block") == "pixart":
         return cpu_port_baseline_pixart(c, budget_s, sample_rows)
+    if c.get("block") == "mmdit":
+        return cpu_port_baseline_mmdit(c, budget_s, sample_rows)
     from concurrent.futures import ThreadPoolExecutor
     from oracle import loader
     if not loader.REFERENCE_LIB.exists():
@@ -289,6 +328,10 @@ def run_ours(args, c, world, rank):
             model = pf.JointDiTCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"],
                                                c["T"], rank, world, local,
                                                double_layers=c.get("D"))
+        elif c.get("block") == "mmdit":
+            model = pf.MMDiTCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"],
+                                            rank, world, local, double_layers=c["D"],
+                                            rope=c["rope"])
         else:
             model = pf.ToyDiTCuda.rank_stage(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], rank,
                                              world, local)
@@ -303,6 +346,9 @@ def run_ours(args, c, world, rank):
         elif c.get("block") == "joint":
             model = pf.JointDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n,
                                     devices, double_layers=c.get("D"))
+        elif c.get("block") == "mmdit":
+            model = pf.MMDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], n,
+                                 devices, double_layers=c["D"], rope=c["rope"])
         else:
             model = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], n, devices)
     t_build = time.perf_counter() - t_build
@@ -370,6 +416,8 @@ def run_ours(args, c, world, rank):
     model.set_profiling(False)
     barrier(world)
     all_launches = gather_ranks(launches, world)
+    mem = {"param_bytes_per_stage": gather_ranks(model.param_bytes(), world),
+           "kv_bytes_per_stage": gather_ranks(model.kv_bytes(), world)}
     if rank != 0:
         return None
     finite = bool(np.isfinite(out.final_x).all())
@@ -461,6 +509,7 @@ def run_ours(args, c, world, rank):
         "clocks": clock_info,
         "finite": finite,
         "model_build_s": t_build,
+        "memory": mem,
     }
     return line
 

@@ -72,3 +72,19 @@ for i in range(nblk):
 ep = allb[12288:12288 + 128]
 epr = np.where(ep > 0, ep - base, -1).reshape(2, 8, 8)
 print("epilogue probes wg0:", epr[0][:3].tolist(), "wg1:", epr[1][:3].tolist())
+
+# per-phase means over CTA 0's steady blocks (clk): S wait, load+max, exp+P store, row sum
+for name in ("softmax0", "softmax1"):
+    arr = np.array(res[name][2:nblk - 1], dtype=np.int64)
+    if len(arr) == 0:
+        continue
+    ok = (arr[:, :6] >= 0).all(axis=1)
+    arr = arr[ok]
+    d = lambda a, b: float(np.mean(arr[:, b] - arr[:, a]))
+    per = float(np.mean(np.diff(arr[:, 1])))
+    print(f"{name}: period {per:.0f} clk | wait S {d(0, 1):.0f} | load+max {d(1, 2):.0f} | "
+          f"pp {d(2, 3):.0f} | exp+store {d(3, 4):.0f} | sum {d(4, 5):.0f}")
+mm = np.array(res["mma"][2:nblk - 1], dtype=np.int64)
+if len(mm):
+    print("mma: wait V", float(np.mean(mm[:, 1] - mm[:, 0])), "wait P0",
+          float(np.mean(mm[:, 2] - mm[:, 1])), "issue0->P1", float(np.mean(mm[:, 4] - mm[:, 3])))
