@@ -366,6 +366,11 @@ def run_ours(args, c, world, rank):
         model.run_pipefusion_device(x_dev.data_ptr() if holds_x else 0, c["S"], M, c["W"], 0.1,
                                     sp)
 
+    # rank mode: every rank builds its CUDA graph before any rank replays one
+    # (pf_prepare_pipefusion_device), then the ranks start together
+    model.prepare_pipefusion_device(x_dev.data_ptr() if holds_x else 0, c["S"], M, c["W"], 0.1,
+                                    sp)
+    barrier(world)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             one_image()

@@ -237,6 +237,16 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
  * workers share its GPU. CUDA constraint: seq_len / workers divisible by
  * 128 (workers > 1). stats->fresh_fraction receives workers x (steps-warmup)
  * values, worker-major. */
+/* Rank mode: capture and instantiate this rank's CUDA graph for exactly these
+ * arguments (latent pointer and stream included) without running it; the
+ * next pf_run_pipefusion_device with the same arguments replays it. Ranks of
+ * one process sharing a device replay graphs only when every rank prepared
+ * them first (otherwise their runs are enqueued op by op): instantiating a
+ * graph while a peer's replay waits on this rank can block. No-op outside
+ * rank mode. */
+pf_status pf_prepare_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps, int patches,
+                                       int warmup, double eta, void* stream);
+
 pf_status pf_run_distrifusion(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps,
                               int workers, int warmup, double eta, double* x_out,
                               pf_stats* stats);

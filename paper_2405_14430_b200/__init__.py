@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = [
     "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_device_count", "pf_debug_fail_at",
     "pf_debug_poison_layer", "pf_create_toy_ex", "pf_create_toy_rank_ex", "pf_precision_of",
     "pf_create_mmdit", "pf_create_mmdit_rank", "pf_stage_param_bytes", "pf_stage_kv_bytes",
+    "pf_prepare_pipefusion_device",
 ]
 
 KERNEL_KINDS = ["gemm_qkv", "attention", "gemm_out_proj", "gemm_mlp_in", "gemm_mlp_out",
@@ -167,6 +168,7 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_run_pipefusion_device.argtypes = [vp, vp, i32, i32, i32, dbl, vp,
                                              ctypes.POINTER(_Stats)]
     lib.pf_synchronize.argtypes = [vp, vp]
+    lib.pf_prepare_pipefusion_device.argtypes = [vp, vp, i32, i32, i32, dbl, vp]
     lib.pf_serial_reference.argtypes = [vp, dptr, i32, i32, dbl, dptr]
     lib.pf_layer_forward.argtypes = [vp, i32, dptr, i64, i64, dptr, dptr, i32]
     for name in ("pf_stage_count",):
@@ -617,6 +619,15 @@ class ToyDiTCuda:
             ctypes.c_double(eta), ctypes.c_void_p(stream_ptr), ctypes.byref(st))
         _raise(status, self._err())
         return StalenessStats(st.fresh_patch_reads, st.stale_patch_reads, [])
+
+    def prepare_pipefusion_device(self, x_dev_ptr: int, steps: int, patches: int, warmup: int,
+                                  eta: float, stream_ptr: int = 0) -> None:
+        """Rank mode: build this rank's CUDA graph for these arguments without
+        running it (pf_prepare_pipefusion_device); call on every rank before
+        the first run when ranks share a device in one process."""
+        _raise(self._lib.pf_prepare_pipefusion_device(
+            self._ctx, ctypes.c_void_p(x_dev_ptr or None), steps, patches, warmup,
+            ctypes.c_double(eta), ctypes.c_void_p(stream_ptr or None)), self._err())
 
     def set_graphs(self, enabled: bool) -> None:
         self._lib.pf_set_graphs(self._ctx, 1 if enabled else 0)

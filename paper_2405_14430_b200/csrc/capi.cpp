@@ -597,6 +597,15 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
   });
 }
 
+pf_status pf_prepare_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps, int patches,
+                                       int warmup, double eta, void* stream) {
+  if (!ctx) return PF_VALIDATION;
+  return guarded(&ctx->last_error, [&] {
+    ctx->engine->prepare_graph(x_dev, steps, patches, warmup, float(eta),
+                               static_cast<cudaStream_t>(stream));
+  });
+}
+
 pf_status pf_run_distrifusion(pf_ctx* ctx, const double* x_init, pf_layout layout, int steps,
                               int workers, int warmup, double eta, double* x_out,
                               pf_stats* stats) {

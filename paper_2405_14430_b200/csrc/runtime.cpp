@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <chrono>
@@ -389,7 +390,7 @@ void Engine::px_alloc_run(Stage& s, int steps) {
   PxStage& px = s.px;
   if (steps <= px.steps_cap) return;
   DeviceGuard g(s.device);
-  cudaDeviceSynchronize();  // a replayed graph may still read the old buffers
+  sync_own();  // a replayed graph may still read the old buffers
   drop_graphs();
   for (float* p : {px.sinus, px.e1, px.temb, px.tv, px.mod, px.foldq, px.foldm}) dfree(p);
   dfree(px.fold_aq);
@@ -1182,6 +1183,8 @@ void Engine::run(float* x_dev, int steps, int patches, int warmup, float eta,
   }
   DeviceGuard g(stages_[0].device);
   PF_CUDA_CHECK(cudaGraphLaunch(it->second.exec, caller));
+  if (!ev_replayed_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_replayed_, cudaEventDisableTiming));
+  PF_CUDA_CHECK(cudaEventRecord(ev_replayed_, caller));
   launches_ = it->second.launches;
   codes_ = it->second.codes;
   if (stats) *stats = it->second.stats;
@@ -1263,24 +1266,39 @@ void Engine::prepare_rank_run(int patches, int steps) {
 }
 
 void Engine::run_rank(float* x_dev, int steps, int patches, int warmup, float eta,
-                      cudaStream_t caller, RunStats* stats) {
+                      cudaStream_t caller, RunStats* stats, bool launch) {
   if (!connected_) throw ValidationError("rank-mode engine is not connected to its peers");
   if (broken_)
     throw NumericError("channel closed mid-run (an earlier run of this pipeline was aborted; "
                        "call pf_rank_reset on every rank)");
   // identical on every rank: fails everywhere before anything is enqueued
   validate_run(steps, patches, warmup);
-  ++run_epoch_;
+  if (launch) ++run_epoch_;
   DeviceGuard g(stages_[0].device);
-  const bool graph = graphs_enabled_ && !profiling_ && !timeline_on_ && caller != nullptr &&
-                     fail_at_op_ < 0;
+  bool graph = graphs_enabled_ && !profiling_ && !timeline_on_ && caller != nullptr &&
+               fail_at_op_ < 0;
+  uint32_t eta_bits0;
+  std::memcpy(&eta_bits0, &eta, sizeof(eta_bits0));
+  if (graph && launch && shared_device_peer_ &&
+      !graphs_.count(GraphKey{x_dev, steps, patches, warmup, eta_bits0, caller}))
+    graph = false;  // not prepared up front: enqueue (see connect_peers)
+  if (!launch && !graph) return;
+  static const bool dbg = [] {
+    const char* e = std::getenv("PF_RANK_DEBUG");
+    return e && e[0] == '1';
+  }();
+  auto trace = [&](const char* what) {
+    if (dbg) std::fprintf(stderr, "[rank %d] %s\n", rank_, what);
+  };
   try {
     if (!graph) {
       enqueue_rank_run(x_dev, steps, patches, warmup, eta, caller, stats);
       return;
     }
     if (rank_ == 0 && !x_dev) throw ValidationError("NULL latent pointer");
+    trace("prepare");
     prepare_rank_run(patches, steps);
+    trace("prepared");
     const GraphMemOps& gm = graph_memops();
     uint32_t eta_bits;
     std::memcpy(&eta_bits, &eta, sizeof(eta_bits));
@@ -1310,6 +1328,7 @@ void Engine::run_rank(float* x_dev, int steps, int patches, int warmup, float et
         std::rethrow_exception(failure);
       }
       PF_CUDA_CHECK(cudaStreamEndCapture(caller, &graph_h));
+      trace("captured");
       msgs_in_base_ = in0;  // the capture executed nothing
       msgs_out_base_ = out0;
       e.graph = graph_h;
@@ -1341,9 +1360,11 @@ void Engine::run_rank(float* x_dev, int steps, int patches, int warmup, float et
         e.memops.push_back(std::move(mn));
       }
       PF_CUDA_CHECK(cudaGraphInstantiate(&e.exec, graph_h, 0));
+      trace("instantiated");
       it = graphs_.emplace(key, std::move(e)).first;
     }
     GraphEntry& e = it->second;
+    if (!launch) return;  // prepare_graph: built, not replayed
     if (e.base != msgs_in_base_) {
       for (GraphEntry::MemOpNode& mn : e.memops) {
         CUDA_BATCH_MEM_OP_NODE_PARAMS prm;
@@ -1363,7 +1384,12 @@ void Engine::run_rank(float* x_dev, int steps, int patches, int warmup, float et
       e.base = msgs_in_base_;
     }
     run_base_ = msgs_in_base_;
+    trace("launch");
     PF_CUDA_CHECK(cudaGraphLaunch(e.exec, caller));
+    if (!ev_replayed_)
+      PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_replayed_, cudaEventDisableTiming));
+    PF_CUDA_CHECK(cudaEventRecord(ev_replayed_, caller));
+    trace("launched");
     const uint32_t per_run = uint32_t(plan_messages_per_run(steps, patches, warmup));
     msgs_in_base_ += per_run;
     msgs_out_base_ += per_run;
@@ -1405,6 +1431,18 @@ void Engine::watchdog_abort() {
   if (succ_sig_) stream_write(abort_stream_, succ_sig_, release, dev);
   if (pred_sig_) stream_write(abort_stream_, pred_sig_ + 1, release, dev);
   cudaStreamSynchronize(abort_stream_);
+  cudaGetLastError();
+}
+
+void Engine::sync_own() {
+  for (Stage& s : stages_) {
+    DeviceGuard g(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    for (int k = 1; k < s.lanes_alloc; ++k)
+      if (s.extra[k].stream) cudaStreamSynchronize(s.extra[k].stream);
+  }
+  if (send_stream_) cudaStreamSynchronize(send_stream_);
+  if (ev_replayed_) cudaEventSynchronize(ev_replayed_);
   cudaGetLastError();
 }
 
@@ -1998,6 +2036,14 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
     throw ValidationError("peer blobs do not belong to this rank's neighbours");
   Stage& s = stages_[0];
   DeviceGuard g(s.device);
+  // A neighbour in this process on this device: instantiating a CUDA graph
+  // while a peer's replay waits on this rank's signals can block the host
+  // (measured on B200 with 4 patch lanes), so graphs are used only once
+  // they were built up front by prepare_graph on every rank (run_rank).
+  shared_device_peer_ = false;
+  for (const PeerBlob* b : {&pred, &succ})
+    if (b->nonce == process_nonce() && b->pid == int64_t(getpid()) && b->device == s.device)
+      shared_device_peer_ = true;
   for (const PeerBlob* b : {&pred, &succ})
     if (b->host_id != host_identity()) {
       std::ostringstream os;

@@ -346,6 +346,13 @@ class Engine {
   void run(float* x_dev, int steps, int patches, int warmup, float eta,
            cudaStream_t caller, RunStats* stats);
   void set_graphs(bool on) { graphs_enabled_ = on; }
+  // Rank mode: capture and instantiate this rank's graph for the run's
+  // arguments without launching it. Ranks sharing one device in one process
+  // replay graphs only after every rank prepared them (see connect_peers).
+  void prepare_graph(float* x_dev, int steps, int patches, int warmup, float eta,
+                     cudaStream_t caller) {
+    if (rank_mode()) run_rank(x_dev, steps, patches, warmup, eta, caller, nullptr, false);
+  }
   // serial_reference(keep_trajectory) / auto_warmup taps on the warmup
   // (full-sequence) steps of the next runs (single-process engines, no graph
   // replay while set): per warmup step w, sums[2w], sums[2w+1] = ||x||^2,
@@ -462,13 +469,19 @@ class Engine {
   }();
   // rank mode: enqueue or replay the captured graph of this rank's plan
   void run_rank(float* x_dev, int steps, int patches, int warmup, float eta,
-                cudaStream_t caller, RunStats* stats);
+                cudaStream_t caller, RunStats* stats, bool launch = true);
+  bool shared_device_peer_ = false;  // a neighbour rank in this process on this device
   void prepare_rank_run(int patches, int steps);
   // wait for a stream; in rank mode with a watchdog that aborts the pipeline
   // when no progress is made for rank_timeout_s_
   void wait_stream(cudaStream_t st);
   int px_steps_ = 0;  // S of the enqueued run (layout of the per-run PixArt buffers)
   cudaEvent_t ev_start_ = nullptr;
+  // recorded on the caller stream after every graph replay: sync_own() waits
+  // for this engine's work only (ranks sharing a device must not wait for
+  // each other's device-wide work, which may wait on them in turn)
+  cudaEvent_t ev_replayed_ = nullptr;
+  void sync_own();
   int stage_of_layer(int layer) const;
 
   struct ProfRec {

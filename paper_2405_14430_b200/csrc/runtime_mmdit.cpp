@@ -195,7 +195,7 @@ void Engine::mm_alloc_run(Stage& s, int steps) {
   PxStage& px = s.px;
   if (steps <= px.steps_cap) return;
   DeviceGuard g(s.device);
-  cudaDeviceSynchronize();  // a replayed graph may still read the old buffers
+  sync_own();  // a replayed graph may still read the old buffers
   drop_graphs();
   for (float* p : {px.sinus, px.e1, px.temb, px.tv, px.mod, px.foldq, px.foldm}) mm_free(p);
   mm_free(px.fold_aq);

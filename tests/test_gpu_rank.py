@@ -45,8 +45,14 @@ def _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0, text=0, runs=1, j
     # one caller stream per rank: a shared caller stream would chain the ranks'
     # joins and forks (rank 1 would wait for rank 0, which waits for rank 1)
     streams = [torch.cuda.Stream() for _ in ranks]
+    x = torch.from_numpy(x0.astype(np.float32)).cuda()
+    # ranks sharing the device replay CUDA graphs only once all of them built
+    # theirs (pf_prepare_pipefusion_device)
+    for r, m in enumerate(ranks):
+        m.prepare_pipefusion_device(x.data_ptr() if r == 0 else 0, S, M, W, 0.1,
+                                    streams[r].cuda_stream)
     for _ in range(runs):
-        x = torch.from_numpy(x0.astype(np.float32)).cuda()
+        x.copy_(torch.from_numpy(x0.astype(np.float32)))
         torch.cuda.synchronize()
         st = []
         # enqueue every rank before waiting on any: the ranks depend on each other
@@ -164,6 +170,10 @@ def test_rank_graph_replay_equals_enqueue(N, M):
         outs = []
         x0t = torch.from_numpy(x0.astype(np.float32)).cuda()
         x = torch.empty_like(x0t)
+        if graphs:
+            for r, m in enumerate(ranks):
+                m.prepare_pipefusion_device(x.data_ptr() if r == 0 else 0, S, M, W, 0.1,
+                                            streams[r].cuda_stream)
         for _ in range(3):
             x.copy_(x0t)
             torch.cuda.synchronize()

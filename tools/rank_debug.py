@@ -16,6 +16,7 @@ import torch  # noqa: E402
 import paper_2405_14430_b200 as pf  # noqa: E402
 
 N, M, S, W, graphs, runs = (int(a) for a in sys.argv[1:7])
+warm = len(sys.argv) > 7 and sys.argv[7] == "warm"  # one graph-less run first
 L, hs, heads, p = 4, 128, 4, 256
 x0 = pf.make_initial_latent(0, p, hs)
 with pf.ToyDiTCuda(0, L, hs, heads, 4.0, p, N) as m:
@@ -23,7 +24,7 @@ with pf.ToyDiTCuda(0, L, hs, heads, 4.0, p, N) as m:
 ranks = [pf.ToyDiTCuda.rank_stage(0, L, hs, heads, 4.0, p, r, N, 0) for r in range(N)]
 pf.connect_ranks(ranks)
 for m in ranks:
-    m.set_graphs(bool(graphs))
+    m.set_graphs(bool(graphs) and not warm)
 streams = [torch.cuda.Stream() for _ in ranks]
 x = torch.from_numpy(x0.astype(np.float32)).cuda()
 for it in range(runs):
@@ -39,3 +40,6 @@ for it in range(runs):
         print(f"run {it}: rank {r} done ({time.time() - t0:.2f}s)", flush=True)
     got = x.double().cpu().numpy()
     print(f"run {it}: {'OK' if np.array_equal(got, ref) else 'MISMATCH'}", flush=True)
+    if warm:
+        for m in ranks:
+            m.set_graphs(bool(graphs))
