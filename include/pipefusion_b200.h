@@ -239,11 +239,11 @@ pf_status pf_run_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps,
  * values, worker-major. */
 /* Rank mode: capture and instantiate this rank's CUDA graph for exactly these
  * arguments (latent pointer and stream included) without running it; the
- * next pf_run_pipefusion_device with the same arguments replays it. Ranks of
- * one process sharing a device replay graphs only when every rank prepared
- * them first (otherwise their runs are enqueued op by op): instantiating a
- * graph while a peer's replay waits on this rank can block. No-op outside
- * rank mode. */
+ * next pf_run_pipefusion_device with the same arguments replays it. Call it
+ * on every rank (then a host barrier) before the first run: instantiating a
+ * graph while a peer's replay already waits on this rank can block. Ranks of
+ * one process sharing a device never replay graphs (their runs are enqueued
+ * op by op). No-op outside rank mode. */
 pf_status pf_prepare_pipefusion_device(pf_ctx* ctx, float* x_dev, int steps, int patches,
                                        int warmup, double eta, void* stream);
 

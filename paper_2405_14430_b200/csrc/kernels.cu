@@ -954,30 +954,29 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
   // Two softmax warpgroups exponentiate concurrently (no ping-pong) with 2 of
   // every 8 four-column groups on the FMA-pipe exp2: measured best of the
   // ping-pong / poly-ratio / f16x2-exp variants at C2 (119 vs 123.5 us).
-  // With a row-sum column in V (padded head dims), PF_ATTN_POLY selects the
-  // share of FMA-pipe exp2 (hex mask over 8 four-column groups; A/B runs).
-  static const int poly = [] {
-    const char* e = std::getenv("PF_ATTN_POLY");
-    return e ? int(std::strtol(e, nullptr, 16)) : 0x88;
+  // With a row-sum column in V (padded head dims) the softmax skips its row
+  // sum. PF_ATTN_VAR (A/B runs, head dim 80 only): 1 ping-pong of the two
+  // softmax warpgroups' exp sections, 2 all-MUFU exp2, 3 ping-pong + all-MUFU.
+  static const int var = [] {
+    const char* e = std::getenv("PF_ATTN_VAR");
+    return e ? std::atoi(e) : 0;
   }();
-  cudaError_t e;
-  if (a.v_sum_col && a.dh < DHP) {
-    if (DHP != 80 || poly == 0x88)
-      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, true>),
-                                    &attn_fwd_kernel<DHP, NT, 0x88, false, true>>{});
-    else if (poly == 0xAA)
-      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0xAA, false, true>),
-                                    &attn_fwd_kernel<DHP, NT, 0xAA, false, true>>{});
-    else if (poly == 0x92)
-      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x92, false, true>),
-                                    &attn_fwd_kernel<DHP, NT, 0x92, false, true>>{});
-    else
-      e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, true>),
-                                    &attn_fwd_kernel<DHP, NT, 0x88, false, true>>{});
-  } else {
-    e = go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT>),
-                                  &attn_fwd_kernel<DHP, NT>>{});
-  }
+  auto pick = [&](auto sumcol) {
+    constexpr bool SC = decltype(sumcol)::value;
+    if (DHP == 80 && var == 1)
+      return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, true, SC>),
+                                       &attn_fwd_kernel<DHP, NT, 0x88, true, SC>>{});
+    if (DHP == 80 && var == 2)
+      return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x00, false, SC>),
+                                       &attn_fwd_kernel<DHP, NT, 0x00, false, SC>>{});
+    if (DHP == 80 && var == 3)
+      return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x00, true, SC>),
+                                       &attn_fwd_kernel<DHP, NT, 0x00, true, SC>>{});
+    return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, SC>),
+                                     &attn_fwd_kernel<DHP, NT, 0x88, false, SC>>{});
+  };
+  const cudaError_t e = (a.v_sum_col && a.dh < DHP) ? pick(std::true_type{})
+                                                     : pick(std::false_type{});
   if (e != cudaSuccess || !cut || prm.grid < 2 || prm.fused) return e;
   const unsigned slices = unsigned((NT * kAttnBM * (DHP / 16) + 255) / 256);
   return launch_pdl(attn_streamk_combine_kernel<DHP, NT>, dim3(prm.grid - 1, slices), dim3(256),

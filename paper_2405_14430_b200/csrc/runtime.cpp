@@ -1277,11 +1277,7 @@ void Engine::run_rank(float* x_dev, int steps, int patches, int warmup, float et
   DeviceGuard g(stages_[0].device);
   bool graph = graphs_enabled_ && !profiling_ && !timeline_on_ && caller != nullptr &&
                fail_at_op_ < 0;
-  uint32_t eta_bits0;
-  std::memcpy(&eta_bits0, &eta, sizeof(eta_bits0));
-  if (graph && launch && shared_device_peer_ &&
-      !graphs_.count(GraphKey{x_dev, steps, patches, warmup, eta_bits0, caller}))
-    graph = false;  // not prepared up front: enqueue (see connect_peers)
+  if (shared_device_peer_) graph = false;  // see connect_peers
   if (!launch && !graph) return;
   static const bool dbg = [] {
     const char* e = std::getenv("PF_RANK_DEBUG");
@@ -2036,10 +2032,13 @@ void Engine::connect_peers(const PeerBlob& pred, const PeerBlob& succ) {
     throw ValidationError("peer blobs do not belong to this rank's neighbours");
   Stage& s = stages_[0];
   DeviceGuard g(s.device);
-  // A neighbour in this process on this device: instantiating a CUDA graph
-  // while a peer's replay waits on this rank's signals can block the host
-  // (measured on B200 with 4 patch lanes), so graphs are used only once
-  // they were built up front by prepare_graph on every rank (run_rank).
+  // A neighbour in this process on this device (tests on one GPU): such
+  // ranks enqueue their plans op by op instead of replaying CUDA graphs.
+  // Measured on B200: instantiating a graph while a peer's replay waits on
+  // this rank's signals blocks the host, and several in-process replays
+  // with patch lanes can map their waiting branches onto shared hardware
+  // queues and stall each other. One rank per GPU (or per process) is the
+  // deployment shape and replays graphs.
   shared_device_peer_ = false;
   for (const PeerBlob* b : {&pred, &succ})
     if (b->nonce == process_nonce() && b->pid == int64_t(getpid()) && b->device == s.device)

@@ -347,8 +347,8 @@ class Engine {
            cudaStream_t caller, RunStats* stats);
   void set_graphs(bool on) { graphs_enabled_ = on; }
   // Rank mode: capture and instantiate this rank's graph for the run's
-  // arguments without launching it. Ranks sharing one device in one process
-  // replay graphs only after every rank prepared them (see connect_peers).
+  // arguments without launching it (ranks sharing a device in one process
+  // never use graphs, see connect_peers).
   void prepare_graph(float* x_dev, int steps, int patches, int warmup, float eta,
                      cudaStream_t caller) {
     if (rank_mode()) run_rank(x_dev, steps, patches, warmup, eta, caller, nullptr, false);

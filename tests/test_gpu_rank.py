@@ -153,42 +153,73 @@ def test_same_process_ranks_joint(D, N):
 
 
 # ----------------------------------------------------------------- graph replay
-@pytest.mark.parametrize("N,M", [(2, 4), (4, 8)])
-def test_rank_graph_replay_equals_enqueue(N, M):
-    """Each rank captures its plan once; replays re-base the signal values.
-    Three replays (bases 0, R, 2R) equal three graph-less runs bit for bit."""
-    import torch
-    seed, L, hs, heads, p, S, W = 0, 4, 128, 4, 256, 4, 1
-    x0 = pf.make_initial_latent(0, p, hs)
-    res = {}
-    for graphs in (False, True):
-        ranks = [pf.ToyDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, r, N, 0) for r in range(N)]
-        pf.connect_ranks(ranks)
-        for m in ranks:
-            m.set_graphs(graphs)
-        streams = [torch.cuda.Stream() for _ in ranks]
-        outs = []
+def _proc_graphs(rank, world, port, cfg, q):
+    """One rank per process (the deployment shape): three graph-less runs,
+    then three CUDA-graph replays (prepared on every rank first)."""
+    try:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        seed, L, hs, heads, p, S, M, W = cfg
+        m = pf.ToyDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, rank, world, 0)
+        pf.connect_distributed(m)
+        x0 = pf.make_initial_latent(0, p, hs)
         x0t = torch.from_numpy(x0.astype(np.float32)).cuda()
         x = torch.empty_like(x0t)
-        if graphs:
-            for r, m in enumerate(ranks):
-                m.prepare_pipefusion_device(x.data_ptr() if r == 0 else 0, S, M, W, 0.1,
-                                            streams[r].cuda_stream)
-        for _ in range(3):
-            x.copy_(x0t)
-            torch.cuda.synchronize()
-            for r, m in enumerate(ranks):
-                m.run_pipefusion_device(x.data_ptr() if r == 0 else 0, S, M, W, 0.1,
-                                        streams[r].cuda_stream)
-            for r, m in enumerate(ranks):
-                m.synchronize(streams[r].cuda_stream)
-            outs.append(x.double().cpu().numpy())
-        for m in ranks:
-            m.close()
-        res[graphs] = outs
-    for a, b in zip(res[False], res[True]):
+        st = torch.cuda.Stream()
+        outs = {}
+        for graphs in (False, True):
+            m.set_graphs(graphs)
+            m.prepare_pipefusion_device(x.data_ptr() if rank == 0 else 0, S, M, W, 0.1,
+                                        st.cuda_stream)
+            dist.barrier()
+            res = []
+            for _ in range(3):
+                x.copy_(x0t)
+                torch.cuda.synchronize()
+                m.run_pipefusion_device(x.data_ptr() if rank == 0 else 0, S, M, W, 0.1,
+                                        st.cuda_stream)
+                m.synchronize(st.cuda_stream)
+                res.append(x.double().cpu().numpy())
+                dist.barrier()
+            outs[graphs] = res
+        launches = m.last_launch_count()
+        dist.barrier()
+        m.close()
+        q.put((rank, outs, launches))
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, "exception " + repr(e), 0))
+
+
+@pytest.mark.parametrize("N,M", [(2, 4), (4, 8)])
+def test_rank_graph_replay_equals_enqueue(N, M):
+    """Each rank process captures its plan once; replays re-base the signal
+    values. Three replays (bases R, 2R, 3R after three enqueued runs) equal
+    the enqueued runs bit for bit (ranks share the test box's one GPU)."""
+    cfg = (0, 4, 128, 4, 256, 4, M, 1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_proc_graphs, args=(r, N, port, cfg, q)) for r in range(N)]
+    for pr in procs:
+        pr.start()
+    got = {}
+    for _ in range(N):
+        r, outs, launches = q.get(timeout=600)
+        got[r] = (outs, launches)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert not isinstance(got[0][0], str), got[0][0]
+    enq, rep = got[0][0][False], got[0][0][True]
+    for a, b in zip(enq, rep):
         assert np.array_equal(a, b)
-    assert all(np.array_equal(res[True][0], o) for o in res[True][1:])
+    assert all(np.array_equal(enq[0], o) for o in enq[1:] + rep)
+    x0 = pf.make_initial_latent(0, 256, 128)
+    ref = _single(0, 4, 128, 4, 256, N, 4, M, 1, x0)
+    assert np.array_equal(enq[0], ref.final_x)
+    assert all(got[r][1] > 0 for r in range(N))
 
 
 # ----------------------------------------------------------------- channel close
