@@ -90,7 +90,7 @@ def test_mmdit_memory_is_sharded_across_stages():
     """Layer sharding: each of N rank-mode stages holds 1/N of
     the layers' parameters and K/V buffers (plus the next stage's first
     modulation matrix)."""
-    L, hs, heads, p, T, D = 8, 128, 4, 256, 16, 4
+    L, hs, heads, p, T, D = 8, 128, 4, 256, 16, 8  # equal layers: equal shares
     with pf.MMDiTCuda(1, L, hs, heads, 4.0, p, T, 1, double_layers=D) as m:
         full_p, full_kv = m.param_bytes(), m.kv_bytes()
     ranks = [pf.MMDiTCuda.rank_stage(1, L, hs, heads, 4.0, p, T, r, 4, 0, double_layers=D)

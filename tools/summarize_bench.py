@@ -4,7 +4,8 @@ import sys
 
 for f in sys.argv[1:]:
     try:
-        d = json.load(open(f))
+        lines = [ln for ln in open(f).read().splitlines() if ln.strip().startswith("{")]
+        d = json.loads(lines[-1])
     except Exception as e:  # noqa: BLE001
         print(f, "unreadable:", e)
         continue
