@@ -75,11 +75,15 @@ constexpr int kAttnBN = 128;   // kv rows per block
 constexpr int kAttnMaxSegs = 64;  // segments per CTA (attn_grid keeps within)
 
 // NT query tiles (of 128 rows) per CTA share every K/V tile.
-template <int DHP, int NT>
+// kW softmax warps per query-row quadrant of a tile (1: one thread per row
+// owns all 128 scores of a KV block; 2: two warps split the block's columns
+// and exchange their partial row maxima through shared memory).
+template <int DHP, int NT, int kW = 1>
 struct AttnSmem {
   static constexpr uint32_t kTileBytes = kAttnBM * DHP * 2;  // Q, K or V tile
   static constexpr uint32_t kTileAlloc = (kTileBytes + 1023) & ~1023u;
-  static constexpr uint32_t kBudget = 232448 - 1024 - 512 - 16 * kAttnMaxSegs;
+  static constexpr uint32_t kXBytes = kW == 2 ? 2 * NT * 4 * 2 * 32 * 4 : 0;  // max exchange
+  static constexpr uint32_t kBudget = 232448 - 1024 - 512 - 16 * kAttnMaxSegs - kXBytes;
   static constexpr int kStagesMax = int((kBudget - NT * kTileAlloc) / (2 * kTileAlloc));
   static constexpr int kStages = kStagesMax > 4 ? 4 : kStagesMax;
   static constexpr uint32_t kQOff = 0;
@@ -87,8 +91,9 @@ struct AttnSmem {
   static constexpr uint32_t kVOff = kKOff + kStages * kTileAlloc;
   static constexpr uint32_t kBarOff = kVOff + kStages * kTileAlloc;
   static constexpr uint32_t kSegOff = kBarOff + 512;  // int4 segment table
-  static constexpr uint32_t kTotal = kSegOff + 16 * kAttnMaxSegs + 1024;
-  static constexpr int kThreads = 128 + 128 * NT;
+  static constexpr uint32_t kXOff = kSegOff + 16 * kAttnMaxSegs;  // [2][NT][4][2][32] fp32
+  static constexpr uint32_t kTotal = kXOff + kXBytes + 1024;
+  static constexpr int kThreads = 128 + 128 * NT * kW;
   static_assert(DHP % 16 == 0 && DHP <= 128, "head dim padding");
   static_assert(kStages >= 2, "attention smem budget");
   static_assert(kTotal <= 232448, "attention smem budget");
@@ -140,16 +145,18 @@ __host__ __device__ __forceinline__ long long attn_unit_start(const AttnParams& 
 // kSumCol: V column dh (< DHP) is 1.0 in every kv row, so O column dh
 // accumulates the softmax row sum in the PV MMA (of the bf16 P it multiplies
 // V with) and the softmax warps skip their per-element row sum.
-template <int DHP, int NT, int kPoly = 0x88, bool kPingPong = false, bool kSumCol = false>
-__global__ void __launch_bounds__(128 + 128 * NT, 1)
+template <int DHP, int NT, int kPoly = 0x88, bool kPingPong = false, bool kSumCol = false,
+          int kW = 1>
+__global__ void __launch_bounds__(128 + 128 * NT * kW, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_k2,
                     const __grid_constant__ CUtensorMap tm_v2, AttnParams prm) {
-  using L = AttnSmem<DHP, NT>;
+  using L = AttnSmem<DHP, NT, kW>;
   constexpr int S = L::kStages;
   constexpr int kChunks = DHP / 16;
+  static_assert(kW == 1 || (kW == 2 && kSumCol && !kPingPong), "split softmax needs kSumCol");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
     }
     for (int t = 0; t < NT; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&p_full[t], 128 * kW);
       ptx::mbar_init(&o_done[t], 1);
     }
     ptx::fence_barrier_init();
@@ -372,6 +379,233 @@ __global__ void __launch_bounds__(128 + 128 * NT, 1)
           if (i + 2 == sg.n) ptx::umma_commit(q_empty);  // last S of the segment issued
         }
       }
+    }
+  } else if constexpr (kW == 2) {
+    ptx::setmaxnreg_inc<104>();
+    // ------------------------------------------------ softmax, two warps per row
+    // Warps 4 + 8 t + 4 h + q own rows 32 q .. 32 q + 31 of tile t (TMEM lane
+    // quadrant q) and KV columns [64 h, 64 h + 64) of each block: half the
+    // scores per thread, twice the warps per SM sub-partition to overlap the
+    // MUFU exp2 with the FMA-pipe polynomial and the TMEM traffic. The two
+    // warps of a row quadrant exchange partial block maxima through shared
+    // memory (double-buffered by block parity) and agree on every rescale
+    // decision; O's column chunks, the epilogue stores and the merge partials
+    // are split between them (chunk c belongs to half c % 2). The row sum is
+    // O column dh (kSumCol).
+    const int idx = warp - 4;
+    const int t = idx >> 3;
+    const int half = (idx >> 2) & 1;
+    const int q = warp & 3;
+    const int trow = 32 * q + int(lane);
+    const uint32_t lane_off = uint32_t(32 * q) << 16;
+    const uint32_t tmem_s = tmem_base + 128 * t + lane_off;
+    const uint32_t tmem_p = tmem_s + 64;
+    const uint32_t tmem_o = tmem_base + 256 + 128 * t + lane_off;
+    const float sc = prm.scale_log2;
+    float* xmax = reinterpret_cast<float*>(smem + L::kXOff);
+    const uint32_t bar_id = uint32_t(3 + 4 * t + q);
+    int g = 0;
+    int sgi = 0;
+    int* pending_flag = nullptr;
+    for (; sgi < nseg; ++sgi) {
+      const int4 sg4 = segs[sgi];
+      const Seg sg{sg4.x, sg4.y, sg4.z};
+      float m_ref = -INFINITY;
+      for (int i = 0; i < sg.n; ++i, ++g) {
+        const int kv0 = (sg.b0 + i) * kAttnBN + 64 * half;
+        const bool tr = g < 256;
+        if (tr) attn_trace(prm, 2048 * t + 8 * g + 0);
+        ptx::mbar_wait(&s_full[t], g & 1);
+        if (tr) attn_trace(prm, 2048 * t + 8 * g + 1);
+        ptx::tc_fence_after();
+        uint32_t sr[64];
+        ptx::tmem_ld32(tmem_s + 64 * half, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        ptx::tmem_ld32(tmem_s + 64 * half + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        ptx::tmem_wait_ld();
+        float* s = reinterpret_cast<float*>(sr);
+        if (kv0 + 64 > prm.P) {
+          const int valid = prm.P - kv0;
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e >= valid) s[e] = -INFINITY;
+        }
+        float bm[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          bm[a] = ptx::fmax3(s[a], s[a + 8], s[a + 16]);
+          bm[a] = ptx::fmax3(bm[a], s[a + 24], s[a + 32]);
+          bm[a] = ptx::fmax3(bm[a], s[a + 40], s[a + 48]);
+          bm[a] = fmaxf(bm[a], s[a + 56]);
+        }
+        const float pm = fmaxf(ptx::fmax3(bm[0], bm[1], bm[2]),
+                               ptx::fmax3(bm[3], ptx::fmax3(bm[4], bm[5], bm[6]), bm[7]));
+        // exchange with the other half (the barrier also orders this warp's
+        // P stores after the other warp's score loads of the shared columns)
+        float* xs = xmax + ((size_t(g & 1) * NT + t) * 4 + q) * 64;
+        xs[32 * half + int(lane)] = pm;
+        ptx::named_bar_sync(bar_id, 64);
+        const float po = xs[32 * (half ^ 1) + int(lane)];
+        const float bmax = (half == 0 ? fmaxf(pm, po) : fmaxf(po, pm)) * sc;
+        const bool need = bmax > m_ref + 8.0f;
+        const float m_new = need ? bmax : m_ref;
+        const float alpha = need ? ptx::ex2_approx(m_ref - m_new) : 1.0f;
+        if (tr) attn_trace(prm, 2048 * t + 8 * g + 2);
+        if (i > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+          for (int c = half; c < kChunks; c += 2) {
+            uint32_t r[16];
+            ptx::tmem_ld16(tmem_o + 16 * c, r);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            ptx::tmem_st16(tmem_o + 16 * c, r);
+          }
+        }
+        if (tr) attn_trace(prm, 2048 * t + 8 * g + 3);
+        const float2 sc2 = make_float2(sc, sc);
+        const float2 nm2 = make_float2(-m_new, -m_new);
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {  // 32 scores -> 16 packed bf16 pairs per store
+          uint32_t pk[16];
+#pragma unroll
+          for (int gg = 0; gg < 8; ++gg) {
+            const int e = 32 * hq + 4 * gg;
+            const int grp = 8 * hq + gg;
+            const float2 x0 = ptx::ffma2(make_float2(s[e], s[e + 1]), sc2, nm2);
+            const float2 x1 = ptx::ffma2(make_float2(s[e + 2], s[e + 3]), sc2, nm2);
+            float2 p0, p1;
+            if ((kPoly >> (grp & 7)) & 1) {
+              p0 = ptx::ex2_poly2(x0);
+              p1 = ptx::ex2_poly2(x1);
+            } else {
+              p0 = make_float2(ptx::ex2_approx(x0.x), ptx::ex2_approx(x0.y));
+              p1 = make_float2(ptx::ex2_approx(x1.x), ptx::ex2_approx(x1.y));
+            }
+            pk[2 * gg] = ptx::pack_bf16x2(p0.x, p0.y);
+            pk[2 * gg + 1] = ptx::pack_bf16x2(p1.x, p1.y);
+          }
+          ptx::tmem_st16(tmem_p + 32 * half + 16 * hq, pk);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[t]);
+        if (pending_flag) {
+          __syncwarp();
+          if (lane == 0) ptx::st_release_gpu(pending_flag, 1);
+          pending_flag = nullptr;
+        }
+        if (tr) attn_trace(prm, 2048 * t + 8 * g + 4);
+        m_ref = m_new;
+        if (tr) attn_trace(prm, 2048 * t + 8 * g + 5);
+      }
+
+      // Segment epilogue: this warp's column chunks of O.
+      ptx::mbar_wait(&o_done[t], sgi & 1);
+      ptx::tc_fence_after();
+      float l_sum;
+      {
+        uint32_t r[16];
+        ptx::tmem_ld16(tmem_o + 16 * (prm.dh / 16), r);
+        ptx::tmem_wait_ld();
+        const int cd = prm.dh % 16;
+        float lv = 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j == cd) lv = __uint_as_float(r[j]);
+        l_sum = lv;
+      }
+      const int head = sg.x / prm.nq;
+      const int qt = sg.x - head * prm.nq;
+      const int lrow = qt * (NT * kAttnBM) + t * kAttnBM + trow;
+      const bool row_ok = lrow < prm.rows;
+      const bool vec = (prm.dh % 8 == 0) && (prm.hs % 8 == 0);
+      __nv_bfloat16* orow = prm.out + size_t(prm.row0 + lrow) * prm.hs + size_t(head) * prm.dh;
+      auto store16 = [&](int c, const float (&o)[16]) {
+        if (!row_ok) return;
+        if (vec) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 8) {
+            const int d = 16 * c + e;
+            if (d < prm.dh) {
+              uint4 v;
+              v.x = ptx::pack_bf16x2(o[e], o[e + 1]);
+              v.y = ptx::pack_bf16x2(o[e + 2], o[e + 3]);
+              v.z = ptx::pack_bf16x2(o[e + 4], o[e + 5]);
+              v.w = ptx::pack_bf16x2(o[e + 6], o[e + 7]);
+              *reinterpret_cast<uint4*>(orow + d) = v;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int d = 16 * c + e;
+            if (d < prm.dh) orow[d] = __float2bfloat16_rn(o[e]);
+          }
+        }
+      };
+      if (sg.n == B) {
+        const float inv_l = 1.0f / l_sum;
+#pragma unroll
+        for (int c = half; c < kChunks; c += 2) {
+          uint32_t r[16];
+          ptx::tmem_ld16(tmem_o + 16 * c, r);
+          ptx::tmem_wait_ld();
+          float o[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(r[j]) * inv_l;
+          store16(c, o);
+        }
+      } else if (rev && sg.b0 > 0) {
+        const int c0 = int(blockIdx.x);
+        const int wflag = (c0 - 1) * kAttnFlagsPerCta + idx;
+        if (lane == 0) {
+          while (ptx::ld_acquire_gpu(prm.flags + wflag) == 0) __nanosleep(32);
+          prm.flags[wflag] = 0;
+        }
+        __syncwarp();
+        const int prow = t * kAttnBM + trow;
+        const size_t sbase = size_t(2 * (c0 - 1) + 1);
+        const float m2 = prm.part_ml[(sbase * 2 + 0) * (NT * kAttnBM) + prow];
+        const float l2 = prm.part_ml[(sbase * 2 + 1) * (NT * kAttnBM) + prow];
+        const float mm = fmaxf(m_ref, m2);
+        const float w1 = ptx::ex2_approx(m_ref - mm), w2 = ptx::ex2_approx(m2 - mm);
+        const float inv_l = 1.0f / (w1 * l_sum + w2 * l2);
+        const float a1 = w1 * inv_l, a2 = w2 * inv_l;
+        const float* po = prm.part_o + sbase * DHP * (NT * kAttnBM) + prow;
+#pragma unroll
+        for (int c = half; c < kChunks; c += 2) {
+          uint32_t r[16];
+          ptx::tmem_ld16(tmem_o + 16 * c, r);
+          float pv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pv[j] = po[size_t(16 * c + j) * (NT * kAttnBM)];
+          ptx::tmem_wait_ld();
+          float o[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) o[j] = a1 * __uint_as_float(r[j]) + a2 * pv[j];
+          store16(c, o);
+        }
+      } else {
+        const int slot = 2 * int(blockIdx.x) + (sgi == 0 && !rev ? 0 : 1);
+        const int prow = t * kAttnBM + trow;
+        float* po = prm.part_o + size_t(slot) * DHP * (NT * kAttnBM) + prow;
+#pragma unroll
+        for (int c = half; c < kChunks; c += 2) {
+          uint32_t r[16];
+          ptx::tmem_ld16(tmem_o + 16 * c, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            po[size_t(16 * c + e) * (NT * kAttnBM)] = __uint_as_float(r[e]);
+        }
+        prm.part_ml[(size_t(slot) * 2 + 0) * (NT * kAttnBM) + prow] = m_ref;
+        prm.part_ml[(size_t(slot) * 2 + 1) * (NT * kAttnBM) + prow] = l_sum;
+        if (rev) pending_flag = prm.flags + int(blockIdx.x) * kAttnFlagsPerCta + idx;
+      }
+    }
+    if (pending_flag) {
+      __syncwarp();
+      if (lane == 0) ptx::st_release_gpu(pending_flag, 1);
     }
   } else {
     if constexpr (NT == 2) ptx::setmaxnreg_inc<224>();

@@ -945,35 +945,47 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.part_o = a.work;
     prm.part_ml = a.work + slots * DHP;
   }
-  auto go = [&](auto kern) {
-    cudaError_t e2 = ensure_smem_attr<decltype(kern)::value>(L::kTotal);
+  auto go = [&](auto kern, auto w) {
+    using LW = AttnSmem<DHP, NT, decltype(w)::value>;
+    cudaError_t e2 = ensure_smem_attr<decltype(kern)::value>(LW::kTotal);
     if (e2 != cudaSuccess) return e2;
-    return launch_pdl(decltype(kern)::value, dim3(prm.grid), dim3(L::kThreads), L::kTotal,
+    return launch_pdl(decltype(kern)::value, dim3(prm.grid), dim3(LW::kThreads), LW::kTotal,
                       stream, q, k, v, a.k2 ? *a.k2 : k, a.v2 ? *a.v2 : v, prm);
   };
+  using W1 = std::integral_constant<int, 1>;
+  using W2 = std::integral_constant<int, 2>;
   // Two softmax warpgroups exponentiate concurrently (no ping-pong) with 2 of
   // every 8 four-column groups on the FMA-pipe exp2: measured best of the
   // ping-pong / poly-ratio / f16x2-exp variants at C2 (119 vs 123.5 us).
   // With a row-sum column in V (padded head dims) the softmax skips its row
-  // sum. PF_ATTN_VAR (A/B runs, head dim 80 only): 1 ping-pong of the two
-  // softmax warpgroups' exp sections, 2 all-MUFU exp2, 3 ping-pong + all-MUFU.
+  // sum. PF_ATTN_VAR (A/B runs): 1 ping-pong of the two softmax warpgroups'
+  // exp sections, 2 all-MUFU exp2 (head dim 80 only); 4 two softmax warps
+  // per row quadrant (kW = 2), 5 / 6 the same with 50 % / 37.5 % FMA-pipe exp2.
   static const int var = [] {
     const char* e = std::getenv("PF_ATTN_VAR");
     return e ? std::atoi(e) : 0;
   }();
   auto pick = [&](auto sumcol) {
     constexpr bool SC = decltype(sumcol)::value;
+    if constexpr (SC) {  // two softmax warps per row quadrant (needs the sum column)
+      if (var == 4)
+        return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, SC, 2>),
+                                         &attn_fwd_kernel<DHP, NT, 0x88, false, SC, 2>>{}, W2{});
+      if (DHP == 80 && var == 5)
+        return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0xAA, false, SC, 2>),
+                                         &attn_fwd_kernel<DHP, NT, 0xAA, false, SC, 2>>{}, W2{});
+      if (DHP == 80 && var == 6)
+        return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x92, false, SC, 2>),
+                                         &attn_fwd_kernel<DHP, NT, 0x92, false, SC, 2>>{}, W2{});
+    }
     if (DHP == 80 && var == 1)
       return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, true, SC>),
-                                       &attn_fwd_kernel<DHP, NT, 0x88, true, SC>>{});
+                                       &attn_fwd_kernel<DHP, NT, 0x88, true, SC>>{}, W1{});
     if (DHP == 80 && var == 2)
       return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x00, false, SC>),
-                                       &attn_fwd_kernel<DHP, NT, 0x00, false, SC>>{});
-    if (DHP == 80 && var == 3)
-      return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x00, true, SC>),
-                                       &attn_fwd_kernel<DHP, NT, 0x00, true, SC>>{});
+                                       &attn_fwd_kernel<DHP, NT, 0x00, false, SC>>{}, W1{});
     return go(std::integral_constant<decltype(&attn_fwd_kernel<DHP, NT, 0x88, false, SC>),
-                                     &attn_fwd_kernel<DHP, NT, 0x88, false, SC>>{});
+                                     &attn_fwd_kernel<DHP, NT, 0x88, false, SC>>{}, W1{});
   };
   const cudaError_t e = (a.v_sum_col && a.dh < DHP) ? pick(std::true_type{})
                                                      : pick(std::false_type{});

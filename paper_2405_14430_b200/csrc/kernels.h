@@ -137,7 +137,7 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
 
 // Attention of query rows [row0, row0+rows) against all P kv rows.
 // stream-K attention: one merge flag per softmax warp of each CTA
-constexpr int kAttnFlagsPerCta = 8;
+constexpr int kAttnFlagsPerCta = 16;
 constexpr int kAttnPrefetchRegions = 4;
 
 struct AttnLaunch {
