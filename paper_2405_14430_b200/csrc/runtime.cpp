@@ -240,6 +240,9 @@ Engine::~Engine() {
     DeviceGuard g(stages_[0].device);
     if (send_stream_) cudaStreamSynchronize(send_stream_);
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (bf16* p : df_sk_) dfree(p);
+    for (bf16* p : df_sv_) dfree(p);
+    if (ev_replayed_) cudaEventDestroy(ev_replayed_);
     for (cudaEvent_t e : ev_sent_) cudaEventDestroy(e);
     if (ev_compute_) cudaEventDestroy(ev_compute_);
     for (cudaEvent_t e : ev_write_)
@@ -643,15 +646,27 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
     a.prefetch[3] = nx.wqkv;
     a.prefetch_bytes[3] = size_t(3) * m.hs * m.hs * 2;
   }
-  if (kv) {
+  if (kv && kv->sk) {
+    // merged K/V: the previous step's rows with this worker's fresh rows
+    const size_t pitch = size_t(m.P) * m.dhp * sizeof(bf16);
+    const size_t bytes = size_t(m.heads) * pitch;
+    const size_t off = size_t(row0) * m.dhp, width = size_t(rows) * m.dhp * sizeof(bf16);
+    PF_CUDA_CHECK(cudaMemcpyAsync(kv->sk, kv->prev_k, bytes, cudaMemcpyDeviceToDevice, s.stream));
+    PF_CUDA_CHECK(cudaMemcpyAsync(kv->sv, kv->prev_v, bytes, cudaMemcpyDeviceToDevice, s.stream));
+    PF_CUDA_CHECK(cudaMemcpy2DAsync(kv->sk + off, pitch, kv->k + off, pitch, width,
+                                    size_t(m.heads), cudaMemcpyDeviceToDevice, s.stream));
+    PF_CUDA_CHECK(cudaMemcpy2DAsync(kv->sv + off, pitch, kv->v + off, pitch, width,
+                                    size_t(m.heads), cudaMemcpyDeviceToDevice, s.stream));
+  } else if (kv) {
     a.k2 = kv->tm_k2;
     a.v2 = kv->tm_v2;
     a.fresh_lo = kv->fresh_lo;
     a.fresh_hi = kv->fresh_hi;
   }
   prof_begin(s, kAttention, 4 * r * P * hs, 0);
-  check(attention(s.tm_q, kv ? *kv->tm_k : L.tm_k, kv ? *kv->tm_v : L.tm_v, a, s.sm_count,
-                  s.stream), "attention");
+  const CUtensorMap& akm = kv ? (kv->sk ? *kv->tm_sk : *kv->tm_k) : L.tm_k;
+  const CUtensorMap& avm = kv ? (kv->sk ? *kv->tm_sv : *kv->tm_v) : L.tm_v;
+  check(attention(s.tm_q, akm, avm, a, s.sm_count, s.stream), "attention");
   prof_end(s);
   if (lane_rec_) PF_CUDA_CHECK(cudaEventRecord(lane_rec_, s.stream));
   EpiParams res;
@@ -1755,14 +1770,21 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
     throw ValidationError(os.str());
   }
   const int r = int(m.P / workers);
-  if (workers > 1 && r % 128 != 0) {
-    std::ostringstream os;
-    os << "CUDA DistriFusion needs seq_len / workers divisible by 128 (got " << r << ")";
-    throw ValidationError(os.str());
-  }
+  // shards off the attention's 128-row KV blocks: merged K/V copies per worker
+  const bool merge = workers > 1 && r % 128 != 0;
   Stage& s = stages_[0];
   DeviceGuard g(s.device);
   const size_t kvn = size_t(m.heads) * size_t(m.P) * size_t(m.dhp);
+  if (merge)
+    while (int(df_sk_.size()) < workers) {
+      PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
+      df_sk_.push_back(dalloc<bf16>(kvn));
+      df_sv_.push_back(dalloc<bf16>(kvn));
+      df_tm_sk_.push_back(tmap(df_sk_.back(), m.dhp, size_t(m.heads) * m.P,
+                               size_t(m.dhp) * 2, 16, 128, 32));
+      df_tm_sv_.push_back(tmap(df_sv_.back(), m.dhp, size_t(m.heads) * m.P,
+                               size_t(m.dhp) * 2, 16, 128, 32));
+    }
   for (StageLayer& L : s.layers)
     if (!L.k2) {
       PF_CUDA_CHECK(cudaStreamSynchronize(s.stream));
@@ -1848,6 +1870,15 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
           st.stale += workers - 1;
           codes_.emplace_back(t, l);
           KvView kv = view(s.layers[size_t(l)], row0, row0 + r);
+          if (merge) {
+            StageLayer& L = s.layers[size_t(l)];
+            kv.prev_k = prev ? L.k2 : L.k;
+            kv.prev_v = prev ? L.v2 : L.v;
+            kv.sk = df_sk_[size_t(i)];
+            kv.sv = df_sv_[size_t(i)];
+            kv.tm_sk = &df_tm_sk_[size_t(i)];
+            kv.tm_sv = &df_tm_sv_[size_t(i)];
+          }
           layer_forward(s, l, r, row0, int(codes_.size()) - 1, &kv);
         }
         st.fresh_fraction[size_t(i)].push_back(1.0 / double(workers));

@@ -394,7 +394,17 @@ class Engine {
     bf16 *k = nullptr, *v = nullptr;
     const CUtensorMap *tm_k = nullptr, *tm_v = nullptr, *tm_k2 = nullptr, *tm_v2 = nullptr;
     int fresh_lo = 0, fresh_hi = 0;
+    // fresh rows not on 128-row KV blocks: the attention reads a merged copy
+    // (previous step's buffers prev_k / prev_v with this worker's fresh rows
+    // from k / v) in the scratch sk / sv
+    const bf16 *prev_k = nullptr, *prev_v = nullptr;
+    bf16 *sk = nullptr, *sv = nullptr;
+    const CUtensorMap *tm_sk = nullptr, *tm_sv = nullptr;
   };
+  // DistriFusion merge scratch per worker (allocated when shards are not
+  // multiples of 128 rows)
+  std::vector<bf16*> df_sk_, df_sv_;
+  std::vector<CUtensorMap> df_tm_sk_, df_tm_sv_;
   void layer_forward(Stage& s, int lf, int rows, int row0, int code,
                      const KvView* kv = nullptr);
   void layer_forward_f32(Stage& s, int lf, int rows, int row0, int code);

@@ -12,7 +12,8 @@ shard's rows from the previous step.
   <= 1e-2 rel-L2 of the final latent vs the fp64 reference
   order   criterion 8 (acceptance.cpp:343-373): the pipeline tracks the serial
           result at least as closely as the shards, over ten seeds
-Shards are 128-row aligned here (the GPU path's constraint).
+Shards off the attention's 128-row KV blocks (e.g. the reference config:
+64 rows over 4 workers) attend over a merged copy of the K/V buffers.
 """
 import numpy as np
 import pytest
@@ -46,6 +47,21 @@ def test_distrifusion_matches_reference(ref, workers, S, W):
     assert rel(res.final_x, rx) <= TOL, rel(res.final_x, rx)
 
 
+@pytest.mark.parametrize("hs,heads,p,workers,S,W", [(32, 4, 64, 4, 20, 1), (128, 4, 384, 3, 4, 1),
+                                                     (64, 4, 256, 8, 3, 0)])
+def test_distrifusion_unaligned_shards(ref, hs, heads, p, workers, S, W):
+    """reference_execute.cfg's shape (16-row shards) and other shards that do
+    not fall on 128-row KV blocks."""
+    seed, L = 0, 4
+    x0 = ref.make_initial_latent(seed, p, hs)
+    rm = ref.build_toy_model(seed, L, hs, heads)
+    rx, (fresh, stale, ff) = ref.run_distrifusion(rm, x0, S, workers, W, 0.1, with_stats=True)
+    with ToyDiTCuda(seed, L, hs, heads, 4.0, p, 1) as m:
+        res = m.run_distrifusion(x0, S, workers, W, 0.1)
+    assert (res.stats.fresh_patch_reads, res.stats.stale_patch_reads) == (fresh, stale)
+    assert rel(res.final_x, rx) <= TOL, rel(res.final_x, rx)
+
+
 def test_full_warmup_and_single_worker_equal_serial_bitwise():
     # test_execute.cpp:99-125 and acceptance criterion 7
     seed, L, hs, heads, p = 0, 4, 128, 4, 512
@@ -61,12 +77,10 @@ def test_full_warmup_and_single_worker_equal_serial_bitwise():
     assert all(np.array_equal(a, again[0]) for a in again)
 
 
-def test_unaligned_shards_are_rejected():
+def test_indivisible_shards_are_rejected():
     with ToyDiTCuda(0, 2, 64, 4, 4.0, 256, 1) as m:
         with pytest.raises(ValidationError, match="divisible"):
             m.run_distrifusion(np.zeros((256, 64)), 2, 3, 0, 0.1)
-        with pytest.raises(ValidationError, match="128"):
-            m.run_distrifusion(np.zeros((256, 64)), 2, 4, 0, 0.1)
 
 
 def test_quality_ordering_proxy():
