@@ -29,6 +29,11 @@ int pf_debug_gemm(const void* A, const void* B, float* C, int rows, int row0,
 int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
                        int P, int rows, int row0, int heads, int hs,
                        void* stream);
+/* Same with the production V layout for padded head dims (dh < dhp): the
+ * row-sum column (V column dh = 1, AttnLaunch::v_sum_col) when v_sum_col. */
+int pf_debug_attention_ex(const void* q, const void* k, const void* v, void* out,
+                          int P, int rows, int row0, int heads, int hs, void* stream,
+                          int v_sum_col);
 
 /* Debug timeline: enable=1 allocates a device trace buffer that subsequent
  * pf_debug_attention launches fill with clock64 stamps of CTA (0,0,0);

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = [
     "pf_stage_first_layer", "pf_stage_layer_count", "pf_last_launch_count",
     "pf_version", "pf_make_initial_latent", "pf_set_graphs", "pf_set_profiling", "pf_kernel_profile",
     "pf_debug_gemm", "pf_debug_attention", "pf_debug_attention_trace", "pf_debug_gemm_trace",
+    "pf_debug_attention_ex",
     "pf_debug_attn_schedule", "pf_serial_reference_ex", "pf_auto_warmup", "pf_divergence",
     "pf_rank_reset", "pf_rank_broken", "pf_connect_world", "pf_device_count", "pf_debug_fail_at",
     "pf_debug_poison_layer", "pf_create_toy_ex", "pf_create_toy_rank_ex", "pf_precision_of",
@@ -185,6 +186,7 @@ def load_library(path: Optional[Path] = None) -> ctypes.CDLL:
     lib.pf_debug_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     lib.pf_debug_attention.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
     lib.pf_debug_attention_trace.argtypes = [i32, vp]
+    lib.pf_debug_attention_ex.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp, i32]
     lib.pf_debug_gemm_trace.argtypes = [i32, vp]
     lib.pf_debug_attn_schedule.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(ctypes.c_longlong)]
     if path is None:

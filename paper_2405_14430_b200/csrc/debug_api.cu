@@ -121,6 +121,12 @@ extern "C" int pf_debug_attention_trace(int enable, unsigned long long* host) {
 extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, void* out,
                                   int P, int rows, int row0, int heads, int hs,
                                   void* stream) {
+  return pf_debug_attention_ex(q, k, v, out, P, rows, row0, heads, hs, stream, 0);
+}
+
+extern "C" int pf_debug_attention_ex(const void* q, const void* k, const void* v, void* out,
+                                     int P, int rows, int row0, int heads, int hs,
+                                     void* stream, int v_sum_col) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = 0;
   cudaGetDevice(&dev);
@@ -146,6 +152,8 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
   ++pf::launch_counter();
   pack_heads_kernel<<<(total + 255) / 256, 256, 0, s>>>(static_cast<const pf::bf16*>(v), vp,
                                                          nullptr, P, hs, heads, dh, dhp);
+  const bool sumcol = v_sum_col && dh < dhp;
+  if (sumcol) pf::v_ones_col(vp, size_t(heads) * P, dhp, dh, s);
   CUtensorMap tq, tk, tv;
   bool ok = pf::encode_tmap_bf16_2d(&tq, qp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
                                     128, 32) &&
@@ -164,6 +172,7 @@ extern "C" int pf_debug_attention(const void* q, const void* k, const void* v, v
     cudaMallocAsync(reinterpret_cast<void**>(&flags), size_t(sms) * pf::kAttnFlagsPerCta * sizeof(int), s);
     cudaMemsetAsync(flags, 0, size_t(sms) * pf::kAttnFlagsPerCta * sizeof(int), s);
     a.flags = flags;
+    a.v_sum_col = sumcol;
     err = int(pf::attention(tq, tk, tv, a, sms, s));
   }
   cudaStreamSynchronize(s);

@@ -68,13 +68,13 @@ def test_gemm_a_multicast_matches_fp32(monkeypatch, total, rows, row0, N, K):
     test_gemm_matches_fp32(total, rows, row0, N, K)
 
 
-def _attn(q, k, v, heads, rows, row0):
+def _attn(q, k, v, heads, rows, row0, sumcol=False):
     lib = load_library()
     P, hs = q.shape
     out = torch.zeros(P, hs, dtype=torch.bfloat16, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
-    err = lib.pf_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                                 P, rows, row0, heads, hs, s)
+    err = lib.pf_debug_attention_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                    P, rows, row0, heads, hs, s, int(sumcol))
     torch.cuda.synchronize()
     assert err == 0, f"cuda error {err}"
     return out
@@ -105,11 +105,14 @@ def _attn_ref(q, k, v, heads, rows, row0):
     (5000, 16, 1152, 4600, 200, 2.0),  # stream-K in-kernel merge, ragged P and rows
     (3000, 12, 768, 3000, 0, 2.0),  # stream-K, separate merge kernel
 ])
-def test_attention_matches_fp32(P, heads, hs, rows, row0, scale):
+@pytest.mark.parametrize("sumcol", [False, True])
+def test_attention_matches_fp32(P, heads, hs, rows, row0, scale, sumcol):
+    # sumcol: the production V layout for padded head dims (row sum from the
+    # PV MMA through V's padding column dh; no-op when dh is a multiple of 16)
     g = torch.Generator(device="cuda").manual_seed(P + hs + rows)
     mk = lambda: ((torch.rand(P, hs, device="cuda", generator=g) * 2 - 1) * scale).to(torch.bfloat16)
     q, k, v = mk(), mk(), mk()
-    out = _attn(q, k, v, heads, rows, row0)[row0:row0 + rows].float()
+    out = _attn(q, k, v, heads, rows, row0, sumcol)[row0:row0 + rows].float()
     ref = _attn_ref(q, k, v, heads, rows, row0)
     err = (out - ref).abs().max().item()
     # outputs reach |x| ~ scale: the bf16 output ulp there is scale * 2^-7

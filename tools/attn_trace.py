@@ -18,8 +18,9 @@ mk = lambda: ((torch.rand(P, hs, device="cuda", generator=g) * 2 - 1) * 2).to(to
 q, k, v = mk(), mk(), mk()
 out = torch.zeros(P, hs, dtype=torch.bfloat16, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
-run = lambda: lib.pf_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                                     P, rows, row0, heads, hs, s)
+sumcol = int(__import__("os").environ.get("PF_DEBUG_SUMCOL", "1"))  # production V layout
+run = lambda: lib.pf_debug_attention_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                        out.data_ptr(), P, rows, row0, heads, hs, s, sumcol)
 for _ in range(3):
     run()
 torch.cuda.synchronize()

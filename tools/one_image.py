@@ -27,6 +27,12 @@ c = bench.CONFIGS[a.config]
 if c.get("block") == "pixart":
     m = pf.PixArtCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], a.stages,
                       [0] * a.stages)
+elif c.get("block") == "mmdit":
+    m = pf.MMDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], a.stages,
+                     [0] * a.stages, double_layers=c["D"], rope=c["rope"])
+elif c.get("block") == "joint":
+    m = pf.JointDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], c["T"], a.stages,
+                        [0] * a.stages, double_layers=c.get("D"))
 else:
     m = pf.ToyDiTCuda(0, c["L"], c["hs"], c["heads"], 4.0, c["p"], a.stages, [0] * a.stages)
 x0 = torch.from_numpy(pf.make_initial_latent(0, c["p"], c["hs"]).astype(np.float32)).cuda()
