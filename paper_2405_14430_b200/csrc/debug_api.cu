@@ -85,7 +85,7 @@ extern "C" int pf_debug_attn_schedule(int P, int rows, int heads, int dhp, int s
   static int dummy_flags = 0;
   pf::AttnLaunch a{dhp, P, rows, 0, heads, dhp, heads * dhp, 1.f, nullptr, nullptr, 0};
   a.flags = &dummy_flags;  // the runtime always provides merge flags
-  const pf::AttnSchedule sc = pf::attn_schedule(a, sm_count);
+  const pf::AttnSchedule sc = pf::attn_schedule(a, sm_count, pf::attn_block_rows(a));
   out[0] = sc.nq;
   out[1] = sc.blocks;
   out[2] = sc.units;
@@ -161,10 +161,20 @@ extern "C" int pf_debug_attention_ex(const void* q, const void* k, const void* v
                                     128, 32) &&
             pf::encode_tmap_bf16_2d(&tv, vp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
                                     128, 32);
+  CUtensorMap tk3, tv3;
+  const bool kv3 = dhp <= 80 &&
+                   pf::encode_tmap_bf16_2d(&tk3, kp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2,
+                                           16, 112, 32) &&
+                   pf::encode_tmap_bf16_2d(&tv3, vp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2,
+                                           16, 112, 32);
   int err = ok ? 0 : int(cudaErrorInvalidValue);
   if (ok) {
     pf::AttnLaunch a{dhp, P, rows, row0, heads, dh, hs, float(1.0 / std::sqrt(double(dh))),
                      static_cast<pf::bf16*>(out), nullptr, 0, g_attn_trace};
+    if (kv3) {
+      a.k3 = &tk3;
+      a.v3 = &tv3;
+    }
     const int sms = pf::device_sm_count(dev);
     a.work_floats = pf::attn_work_floats(dhp, sms);
     cudaMallocAsync(reinterpret_cast<void**>(&work), a.work_floats * 4, s);

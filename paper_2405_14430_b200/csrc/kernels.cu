@@ -7,6 +7,7 @@
 #include <mutex>
 
 #include "attn_sm100.cuh"
+#include "attn3_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "kernels.h"
 
@@ -844,16 +845,16 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
 // Persistent CTAs of the stream-K attention schedule (attn_sm100.cuh): one
 // per SM, or fewer so that every CTA owns at least two kv blocks.
 // PF_ATTN_ONE_ITEM_PER_CTA=1 restores one CTA per item (no cut items).
-int attn_grid(const AttnLaunch& a, int sm_count) {
+int attn_grid(const AttnLaunch& a, int sm_count, int bn) {
   static const bool per_item = [] {
     const char* e = std::getenv("PF_ATTN_ONE_ITEM_PER_CTA");
     return e && e[0] == '1';
   }();
   const int rows_per_item = attn_tiles_per_cta(a.dhp) * kAttnBM;
   const long long items = (long long)((a.rows + rows_per_item - 1) / rows_per_item) * a.heads;
-  const long long units = items * ((a.P + kAttnBN - 1) / kAttnBN);
+  const long long units = items * ((a.P + bn - 1) / bn);
   if (per_item) return int(items);
-  const long long blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  const long long blocks = (a.P + bn - 1) / bn;
   // A patch (fewer rows than the K/V buffer, M >= 2: patch lanes run other
   // patches concurrently) whose items fit in one wave: one CTA per item; the
   // stream-K cuts and their merges cost more than the SMs the other lanes
@@ -881,7 +882,7 @@ int attn_grid(const AttnLaunch& a, int sm_count) {
   return int(g);
 }
 
-AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count) {
+AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count, int bn) {
   static const bool no_fuse = [] {
     const char* e = std::getenv("PF_ATTN_SEPARATE_MERGE");
     return e && e[0] == '1';
@@ -889,9 +890,9 @@ AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count) {
   const int rows_per_item = attn_tiles_per_cta(a.dhp) * kAttnBM;
   AttnSchedule sc;
   sc.nq = (a.rows + rows_per_item - 1) / rows_per_item;
-  sc.blocks = (a.P + kAttnBN - 1) / kAttnBN;
+  sc.blocks = (a.P + bn - 1) / bn;
   sc.units = (long long)sc.nq * a.heads * sc.blocks;
-  sc.grid = attn_grid(a, sm_count);
+  sc.grid = attn_grid(a, sm_count, bn);
   sc.cut = sc.units % sc.grid != 0 || (sc.units / sc.grid) % sc.blocks != 0;
   // in-kernel merge when every item meets at most two CTAs, each holding a
   // head or a tail: ranges of at least one item, or exactly half an item
@@ -996,10 +997,88 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
 }
 }  // namespace
 
+namespace {
+bool attn3_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_ATTN3");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int DHP>
+cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count,
+                         cudaStream_t stream) {
+  constexpr int NT = 2;
+  using L = Attn3Smem<DHP>;
+  AttnParams prm;
+  prm.P = a.P;
+  prm.q_stride = a.q_stride > 0 ? a.q_stride : a.P;
+  prm.fresh_lo = prm.fresh_hi = 0;
+  prm.rows = a.rows;
+  prm.row0 = a.row0;
+  prm.heads = a.heads;
+  prm.dh = a.dh;
+  prm.hs = a.hs;
+  prm.scale_log2 = a.scale * 1.4426950408889634f;
+  const AttnSchedule sc = attn_schedule(a, sm_count, kAttn3BN);
+  prm.nq = sc.nq;
+  prm.blocks = sc.blocks;
+  prm.units = sc.units;
+  prm.grid = sc.grid;
+  prm.out = a.out;
+  prm.part_o = nullptr;
+  prm.part_ml = nullptr;
+  prm.trace = a.trace;
+  prm.flags = a.flags;
+  for (int i = 0; i < kAttnPrefetchRegions; ++i) {
+    prm.pf_ptr[i] = nullptr;
+    prm.pf_bytes[i] = 0;
+  }
+  prm.fused = sc.fused ? 1 : 0;
+  if (sc.cut) {
+    const size_t slots = size_t(2) * prm.grid * NT * kAttnBM;
+    if (!a.work || a.work_floats < slots * (DHP + 2)) return cudaErrorInvalidValue;
+    prm.part_o = a.work;
+    prm.part_ml = a.work + slots * DHP;
+  }
+  auto go = [&](auto kern) {
+    cudaError_t e2 = ensure_smem_attr<decltype(kern)::value>(L::kTotal);
+    if (e2 != cudaSuccess) return e2;
+    return launch_pdl(decltype(kern)::value, dim3(prm.grid), dim3(L::kThreads), L::kTotal,
+                      stream, q, *a.k3, *a.v3, prm);
+  };
+  const cudaError_t e =
+      (a.v_sum_col && a.dh < DHP)
+          ? go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, true>),
+                                      &attn3_fwd_kernel<DHP, 0x88, true>>{})
+          : go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, false>),
+                                      &attn3_fwd_kernel<DHP, 0x88, false>>{});
+  if (e != cudaSuccess || !sc.cut || prm.grid < 2 || prm.fused) return e;
+  const unsigned slices = unsigned((NT * kAttnBM * (DHP / 16) + 255) / 256);
+  return launch_pdl(attn_streamk_combine_kernel<DHP, NT>, dim3(prm.grid - 1, slices), dim3(256),
+                    0, stream, prm);
+}
+}  // namespace
+
+int attn_block_rows(const AttnLaunch& a) {
+  return (a.k3 && a.v3 && !a.k2 && a.dhp <= 80 && attn3_enabled()) ? kAttn3BN : kAttnBN;
+}
+
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
                       const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                       cudaStream_t stream) {
   if (a.rows <= 0) return cudaSuccess;
+  if (attn_block_rows(a) == kAttn3BN) {
+    switch (a.dhp) {
+      case 16: return launch_attn3<16>(q, a, sm_count, stream);
+      case 32: return launch_attn3<32>(q, a, sm_count, stream);
+      case 48: return launch_attn3<48>(q, a, sm_count, stream);
+      case 64: return launch_attn3<64>(q, a, sm_count, stream);
+      case 80: return launch_attn3<80>(q, a, sm_count, stream);
+      default: break;
+    }
+  }
   switch (a.dhp) {
     case 16: return launch_attn<16>(q, k, v, a, sm_count, stream);
     case 32: return launch_attn<32>(q, k, v, a, sm_count, stream);

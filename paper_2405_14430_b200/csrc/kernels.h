@@ -161,12 +161,19 @@ struct AttnLaunch {
   // (16-byte aligned regions; bytes 0 = unused)
   const void* prefetch[kAttnPrefetchRegions] = {};
   size_t prefetch_bytes[kAttnPrefetchRegions] = {};
+  // K / V tensor maps with 112-row boxes (dhp <= 80): the triple-buffered
+  // kernel (attn3_sm100.cuh) runs when present and no k2 / v2 is given
+  const CUtensorMap* k3 = nullptr;
+  const CUtensorMap* v3 = nullptr;
   // every V row (k/v, k2/v2) holds 1.0 in padding column dh (dh < dhp,
   // v_ones_col): the PV MMA then produces the softmax row sum in O column dh
   // and the softmax warps skip their per-element sum
   bool v_sum_col = false;
 };
-int attn_grid(const AttnLaunch& a, int sm_count);
+// KV rows per block of the kernel a launch uses (128, or 112 for the
+// triple-buffered kernel) and the schedule for a given block size
+int attn_block_rows(const AttnLaunch& a);
+int attn_grid(const AttnLaunch& a, int sm_count, int bn = 128);
 // The attention launch's schedule (host only): query-tile groups per head,
 // KV blocks per item, units, persistent CTAs, whether items are cut and
 // whether the cut items are merged in-kernel.
@@ -175,7 +182,7 @@ struct AttnSchedule {
   long long units = 0;
   bool cut = false, fused = false;
 };
-AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count);
+AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count, int bn = 128);
 // partial-result workspace the attention needs on a device with sm_count SMs
 size_t attn_work_floats(int dhp, int sm_count);
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,

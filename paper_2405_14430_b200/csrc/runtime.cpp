@@ -312,6 +312,11 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
       throw CudaError("cuTensorMapEncodeTiled failed for a weight matrix");
     L.tm_k = tmap(L.k, dhp, heads * P, dhp * 2, 16, 128, 32);
     L.tm_v = tmap(L.v, dhp, heads * P, dhp * 2, 16, 128, 32);
+    if (dhp <= 80) {
+      L.tm_k3 = tmap(L.k, dhp, heads * P, dhp * 2, 16, 112, 32);
+      L.tm_v3 = tmap(L.v, dhp, heads * P, dhp * 2, 16, 112, 32);
+      L.has_kv3 = true;
+    }
     check(v_ones_col(L.v, heads * P, int(dhp), m.dh, nullptr), "v_ones_col");
     if (m.precision == kPrecFp32) {
       L.w32 = dalloc<float>(4 * hs * hs + 2 * hs * mlp);
@@ -631,6 +636,10 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
                s.attn_work_floats};
   a.flags = s.attn_flags;
   a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
+  if (L.has_kv3) {
+    a.k3 = &L.tm_k3;
+    a.v3 = &L.tm_v3;
+  }
   // pull this layer's out-proj / MLP weights and the next layer's (or, after
   // the stage's last layer, the next patch's first layer's) QKV weights into
   // L2 while the attention runs: small patches otherwise stream them from HBM
@@ -664,6 +673,7 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
     a.fresh_hi = kv->fresh_hi;
   }
   prof_begin(s, kAttention, 4 * r * P * hs, 0);
+  if (kv) a.k3 = a.v3 = nullptr;  // DistriFusion buffers: the 128-row-block kernel
   const CUtensorMap& akm = kv ? (kv->sk ? *kv->tm_sk : *kv->tm_k) : L.tm_k;
   const CUtensorMap& avm = kv ? (kv->sk ? *kv->tm_sv : *kv->tm_v) : L.tm_v;
   check(attention(s.tm_q, akm, avm, a, s.sm_count, s.stream), "attention");
@@ -1638,6 +1648,10 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
                s.attn_work_floats};
   a.flags = s.attn_flags;
   a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
+  if (L.has_kv3) {
+    a.k3 = &L.tm_k3;
+    a.v3 = &L.tm_v3;
+  }
   prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (joint)");
   prof_end(s);
@@ -1715,6 +1729,10 @@ void Engine::layer_forward_single(Stage& s, int lf, int rows, int row0, int code
                s.attn_work_floats};
   a.flags = s.attn_flags;
   a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
+  if (L.has_kv3) {
+    a.k3 = &L.tm_k3;
+    a.v3 = &L.tm_v3;
+  }
   prof_begin(s, kAttention, 4 * r * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (single)");
   prof_end(s);
@@ -2713,6 +2731,10 @@ void Engine::layer_forward_px(Stage& s, int lf, int rows, int row0, int t, int c
                s.attn_work_floats};
   a.flags = s.attn_flags;
   a.v_sum_col = m.dh < m.dhp;  // V buffers carry the row-sum column
+  if (L.has_kv3) {
+    a.k3 = &L.tm_k3;
+    a.v3 = &L.tm_v3;
+  }
   prof_begin(s, kAttention, 4 * r * P * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention");
   prof_end(s);

@@ -110,6 +110,9 @@ struct StageLayer {
   bf16* v = nullptr;     // [heads][P][dhp]
   WeightMaps tm_wqkv, tm_wo, tm_win, tm_wout;
   CUtensorMap tm_k, tm_v;
+  // 112-row KV boxes for the triple-buffered attention (dhp <= 80)
+  CUtensorMap tm_k3, tm_v3;
+  bool has_kv3 = false;
   // DistriFusion: second K/V buffer (the two alternate as previous-step /
   // this-step per denoising step), allocated on first use
   bf16 *k2 = nullptr, *v2 = nullptr;

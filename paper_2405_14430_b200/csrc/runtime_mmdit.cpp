@@ -411,6 +411,10 @@ void Engine::layer_forward_mm(Stage& s, int lf, int rows, int row0, int t, int c
                s.attn, s.attn_work, s.attn_work_floats};
   a.flags = s.attn_flags;
   a.v_sum_col = m.dh < m.dhp;
+  if (L.has_kv3) {
+    a.k3 = &L.tm_k3;
+    a.v3 = &L.tm_v3;
+  }
   prof_begin(s, kAttention, 4.0 * rows * double(Pt) * dhs, 0);
   check(attention(s.tm_q, L.tm_k, L.tm_v, a, s.sm_count, s.stream), "attention (MMDiT)");
   prof_end(s);
