@@ -72,8 +72,13 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_full = k_empty + S;              // [S]
   uint64_t* v_empty = v_full + S;              // [S]
   uint64_t* s_full = v_empty + S;              // [3]   S buffer b written
-  uint64_t* p_full = s_full + kAttn3Buf;       // [NT]  P_t stored (softmax -> MMA)
-  uint64_t* pv_done = p_full + NT;             // [NT]  PV_t of a block complete
+  // [NT][2] P_t of a block stored (softmax -> MMA), by block parity: with the
+  // next block's scores already computed, a fast warp may finish block i + 1
+  // before a slow one finished block i, and its arrivals must not complete
+  // block i's phase (it cannot get two blocks ahead: S of block i + 2 is
+  // issued after PV of block i)
+  uint64_t* p_full = s_full + kAttn3Buf;
+  uint64_t* pv_done = p_full + 2 * NT;         // [NT]  PV_t of a block complete
   uint64_t* o_done = pv_done + NT;             // [NT]  last PV_t of a segment complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NT);
   int* nseg_slot = reinterpret_cast<int*>(tmem_slot + 1);
@@ -99,7 +104,8 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int b = 0; b < kAttn3Buf; ++b) ptx::mbar_init(&s_full[b], 1);
     for (int t = 0; t < NT; ++t) {
-      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&p_full[2 * t], 128);
+      ptx::mbar_init(&p_full[2 * t + 1], 128);
       ptx::mbar_init(&pv_done[t], 1);
       ptx::mbar_init(&o_done[t], 1);
     }
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(384, 1)
           if (t == 0) {
             ptx::mbar_wait(&v_full[vg % S], (vg / S) & 1);
           }
-          ptx::mbar_wait(&p_full[t], vg & 1);
+          ptx::mbar_wait(&p_full[2 * t + (vg & 1)], (vg >> 1) & 1);
           ptx::tc_fence_after();
           const uint32_t vb = v_base + (vg % S) * L::kKVAlloc;
           const uint32_t pt = tmem_base + uint32_t(((gn + n) % kAttn3Buf) * BN) + BN / 2;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_full[t]);
+        ptx::mbar_arrive(&p_full[2 * t + ((gb + i) & 1)]);
         if (pending_flag) {
           __syncwarp();
           if (lane == 0) ptx::st_release_gpu(pending_flag, 1);

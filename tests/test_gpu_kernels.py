@@ -157,3 +157,26 @@ def test_residual_split_k_opt_in(monkeypatch):
     assert np.array_equal(b[0], b[1])
     rel = float(np.linalg.norm(a[0] - b[0]) / np.linalg.norm(a[0]))
     assert rel <= 1e-3, rel
+
+
+@pytest.mark.parametrize("P,heads,hs,rows,row0", [
+    (4096, 16, 1152, 4096, 0),   # C2 full sequence (stream-K, in-kernel merge)
+    (4096, 16, 1152, 512, 2048),  # M = 8 patch
+    (2048, 16, 1024, 2048, 0),   # dh 64
+])
+@pytest.mark.parametrize("sumcol", [False, True])
+def test_attention_peaked_rows_rescale(P, heads, hs, rows, row0, sumcol):
+    """Each query row's largest score sits at its own KV row (q = k), so the
+    running max jumps mid-sequence and the lazy O rescale runs at a later
+    block (random data rarely reaches it)."""
+    g = torch.Generator(device="cuda").manual_seed(P + hs)
+    x = (torch.rand(P, hs, device="cuda", generator=g) * 2 - 1) * 3.0
+    ramp = torch.linspace(0.2, 1.6, P, device="cuda")[:, None]  # growing row norms
+    q = (x * ramp).to(torch.bfloat16)
+    k = q.clone()
+    v = ((torch.rand(P, hs, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
+    out = _attn(q, k, v, heads, rows, row0, sumcol)[row0:row0 + rows].float()
+    ref = _attn_ref(q, k, v, heads, rows, row0)
+    assert torch.isfinite(out).all()
+    rel = ((out - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
