@@ -666,14 +666,17 @@ void Engine::layer_forward(Stage& s, int lf, int rows, int row0, int code, const
                                     size_t(m.heads), cudaMemcpyDeviceToDevice, s.stream));
     PF_CUDA_CHECK(cudaMemcpy2DAsync(kv->sv + off, pitch, kv->v + off, pitch, width,
                                     size_t(m.heads), cudaMemcpyDeviceToDevice, s.stream));
-  } else if (kv) {
+  } else if (kv && kv->fresh_lo < kv->fresh_hi) {
     a.k2 = kv->tm_k2;
     a.v2 = kv->tm_v2;
     a.fresh_lo = kv->fresh_lo;
     a.fresh_hi = kv->fresh_hi;
   }
   prof_begin(s, kAttention, 4 * r * P * hs, 0);
-  if (kv) a.k3 = a.v3 = nullptr;  // DistriFusion buffers: the 128-row-block kernel
+  if (kv) {  // DistriFusion: the whole-buffer views run the serial path's kernel
+    a.k3 = kv->k3;
+    a.v3 = kv->v3;
+  }
   const CUtensorMap& akm = kv ? (kv->sk ? *kv->tm_sk : *kv->tm_k) : L.tm_k;
   const CUtensorMap& avm = kv ? (kv->sk ? *kv->tm_sv : *kv->tm_v) : L.tm_v;
   check(attention(s.tm_q, akm, avm, a, s.sm_count, s.stream), "attention");
@@ -1811,6 +1814,10 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
       check(v_ones_col(L.v2, kvn / size_t(m.dhp), m.dhp, m.dh, nullptr), "v_ones_col");
       L.tm_k2 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
       L.tm_v2 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
+      if (L.has_kv3) {
+        L.tm_k23 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 112, 32);
+        L.tm_v23 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 112, 32);
+      }
     }
   if (!ev_start_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
   RunStats local;
@@ -1846,6 +1853,15 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
     kv.tm_v2 = nxt ? &L.tm_v2 : &L.tm_v;
     kv.fresh_lo = fresh_lo;
     kv.fresh_hi = fresh_hi;
+    if (fresh_lo == 0 && fresh_hi == int(m.P)) {  // every row from this step's buffer
+      kv.tm_k = kv.tm_k2;
+      kv.tm_v = kv.tm_v2;
+      kv.fresh_lo = kv.fresh_hi = 0;
+      if (L.has_kv3) {
+        kv.k3 = nxt ? &L.tm_k23 : &L.tm_k3;
+        kv.v3 = nxt ? &L.tm_v23 : &L.tm_v3;
+      }
+    }
     return kv;
   };
   const size_t hs = size_t(m.hs);

@@ -112,6 +112,7 @@ struct StageLayer {
   CUtensorMap tm_k, tm_v;
   // 112-row KV boxes for the triple-buffered attention (dhp <= 80)
   CUtensorMap tm_k3, tm_v3;
+  CUtensorMap tm_k23, tm_v23;  // the same over k2 / v2 (DistriFusion)
   bool has_kv3 = false;
   // DistriFusion: second K/V buffer (the two alternate as previous-step /
   // this-step per denoising step), allocated on first use
@@ -403,6 +404,9 @@ class Engine {
     const bf16 *prev_k = nullptr, *prev_v = nullptr;
     bf16 *sk = nullptr, *sv = nullptr;
     const CUtensorMap *tm_sk = nullptr, *tm_sv = nullptr;
+    // whole-buffer attention (every row fresh): 112-row-box maps of that
+    // buffer, so the same kernel as the serial path runs (bitwise equality)
+    const CUtensorMap *k3 = nullptr, *v3 = nullptr;
   };
   // DistriFusion merge scratch per worker (allocated when shards are not
   // multiples of 128 rows)
