@@ -719,6 +719,10 @@ struct ResidTmaArgs {
   const float* colscale = nullptr;
   float2* stats = nullptr;
   int stats_ld = 0;
+  // rows at or past row_end belong to another stream / patch (a partial last
+  // tile: the output tensor maps end at row_end and clip the TMA stores);
+  // their statistics and finite checks are skipped. INT_MAX: whole tiles.
+  int row_end = 0x7fffffff;
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -773,6 +777,7 @@ __device__ __forceinline__ bool resid_chunk(uint8_t* sC, uint8_t* sD, int r, int
     uint2* pd = reinterpret_cast<uint2*>(drow + ((((byte >> 4) ^ sw) << 4) | (byte & 15)));
     *pd = make_uint2(ptx::pack_bf16x2(y.x, y.y), ptx::pack_bf16x2(y.z, y.w));
   }
+  if (grow >= args.row_end) return false;
   if constexpr (kMod) {
     if (args.stats) args.stats[size_t(col0 >> 5) * args.stats_ld + grow] = make_float2(s, ss);
   }
@@ -818,7 +823,7 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = ptx::lane_id();
-  const int m_tiles = rows / kGemmBM;
+  const int m_tiles = (rows + kGemmBM - 1) / kGemmBM;  // partial last tile: clipped maps
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int kblocks = (K + kGemmBK - 1) / kGemmBK;

@@ -807,14 +807,15 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
                             args);
     }
   }
-  if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % kGemmBM == 0 && N % 32 == 0 &&
-      gemm_bn_1sm(N) == 128 && !tune_flag("PF_NO_RESID_TMA")) {
+  if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && (rows % kGemmBM == 0 || ep.tma_clip) &&
+      N % 32 == 0 && gemm_bn_1sm(N) == 128 && !tune_flag("PF_NO_RESID_TMA")) {
     constexpr int kStages = 4;
     using L = GemmResSmem<kStages>;
-    const int tiles = (rows / kGemmBM) * ((N + L::BN - 1) / L::BN);
+    const int tiles = ((rows + kGemmBM - 1) / kGemmBM) * ((N + L::BN - 1) / L::BN);
     const int grid = tiles < sm_count ? tiles : sm_count;
-    const ResidTmaArgs args{ep.out_f32, ep.flag, ep.code, ep.bias, ep.gate, ep.colscale,
-                            ep.stats_out, ep.stats_ld};
+    ResidTmaArgs args{ep.out_f32, ep.flag, ep.code, ep.bias, ep.gate, ep.colscale,
+                      ep.stats_out, ep.stats_ld};
+    if (ep.tma_clip) args.row_end = row0 + rows;
     return ep.mod() ? launch_resid2<gemm_resid_tma_kernel<kStages, true>>(
                           grid, L::kTotal, stream, a, b.one_sm, ep, rows, row0, N, K, args)
                     : launch_resid2<gemm_resid_tma_kernel<kStages, false>>(
@@ -1048,12 +1049,30 @@ cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count
     return launch_pdl(decltype(kern)::value, dim3(prm.grid), dim3(L::kThreads), L::kTotal,
                       stream, q, *a.k3, *a.v3, prm);
   };
-  const cudaError_t e =
-      (a.v_sum_col && a.dh < DHP)
-          ? go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, true>),
-                                      &attn3_fwd_kernel<DHP, 0x88, true>>{})
-          : go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, false>),
-                                      &attn3_fwd_kernel<DHP, 0x88, false>>{});
+  // PF_ATTN3_POLY (A/B, head dim 80 with the row-sum column): share of
+  // FMA-pipe exp2 as a mask over 8 four-column groups
+  static const int poly = [] {
+    const char* e = std::getenv("PF_ATTN3_POLY");
+    return e ? int(std::strtol(e, nullptr, 16)) : 0x88;
+  }();
+  cudaError_t e;
+  if (a.v_sum_col && a.dh < DHP) {
+    if (DHP == 80 && poly == 0x92)
+      e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x92, true>),
+                                    &attn3_fwd_kernel<DHP, 0x92, true>>{});
+    else if (DHP == 80 && poly == 0xAA)
+      e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0xAA, true>),
+                                    &attn3_fwd_kernel<DHP, 0xAA, true>>{});
+    else if (DHP == 80 && poly == 0x80)
+      e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x80, true>),
+                                    &attn3_fwd_kernel<DHP, 0x80, true>>{});
+    else
+      e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, true>),
+                                    &attn3_fwd_kernel<DHP, 0x88, true>>{});
+  } else {
+    e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, false>),
+                                  &attn3_fwd_kernel<DHP, 0x88, false>>{});
+  }
   if (e != cudaSuccess || !sc.cut || prm.grid < 2 || prm.fused) return e;
   const unsigned slices = unsigned((NT * kAttnBM * (DHP / 16) + 255) / 256);
   return launch_pdl(attn_streamk_combine_kernel<DHP, NT>, dim3(prm.grid - 1, slices), dim3(256),

@@ -81,6 +81,9 @@ struct EpiParams {
   const CUtensorMap* a_half = nullptr;
   const CUtensorMap* tm_h32 = nullptr;
   const CUtensorMap* tm_hb = nullptr;
+  // tm_h32 / tm_hb (and the _dst maps) end at row row0 + rows: a partial last
+  // row tile may use the TMA epilogue (its stores are clipped by the maps)
+  bool tma_clip = false;
   // Residual: write the updated rows (fp32 and bf16 copy) to these buffers /
   // maps instead of out_f32 / out_bf16 (which are still read): a stage's last
   // layer storing its output directly into the next stage's landing buffers.

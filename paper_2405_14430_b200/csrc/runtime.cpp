@@ -294,6 +294,11 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
   s.tm_hb_half = tmap(s.hb, hs, P, hs * 2, 64, 64, 128);
   if (!encode_tmap_f32_2d(&s.tm_h32, s.h32, hs, P, hs * 4, 32, 128, 128))
     throw CudaError("cuTensorMapEncodeTiled failed for the residual stream");
+  if (m.joint_rows() && hs % 32 == 0) {
+    if (!encode_tmap_f32_2d(&s.tm_h32_txt, s.h32, hs, size_t(m.T), hs * 4, 32, 128, 128))
+      throw CudaError("cuTensorMapEncodeTiled failed for the text rows");
+    s.tm_hb_txt = tmap(s.hb, hs, size_t(m.T), hs * 2, 64, 128, 128);
+  }
   s.tm_attn = tmap(s.attn, hs, P, hs * 2, 64, 128, 128);
   s.tm_z = tmap(s.z, mlp, P, mlp * 2, 64, 128, 128);
   s.tm_q = tmap(s.q, dhp, heads * P, dhp * 2, 16, 128, 32);
@@ -1669,10 +1674,19 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
     res.tm_h32 = &s.tm_h32;
     res.tm_hb = &s.tm_hb;
   }
+  // text rows: TMA residual through maps that end at the last text row (clipped stores)
+  auto clip = [&](bool txt, EpiParams e) {
+    if (txt && !e.out_f32_dst && hs % 32 == 0) {
+      e.tm_h32 = &s.tm_h32_txt;
+      e.tm_hb = &s.tm_hb_txt;
+      e.tma_clip = true;
+    }
+    return e;
+  };
   both([&](bool txt, int r0, int n) {
     prof_begin(s, kGemmOut, 2.0 * n * dhs * dhs, 0);
-    check(gemm(s.tm_attn, txt ? L.tm_t_wo : L.tm_wo, n, r0, hs, hs, Epi::Residual, sk(s, res),
-               s.sm_count, s.stream), "gemm out-proj (joint)");
+    check(gemm(s.tm_attn, txt ? L.tm_t_wo : L.tm_wo, n, r0, hs, hs, Epi::Residual,
+               sk(s, clip(txt, res)), s.sm_count, s.stream), "gemm out-proj (joint)");
     prof_end(s);
   });
   EpiParams th;
@@ -1694,7 +1708,7 @@ void Engine::layer_forward_joint(Stage& s, int lf, int rows, int row0, int code)
   both([&](bool txt, int r0, int n) {
     prof_begin(s, kGemmMlpOut, 2.0 * n * dhs * mlp, 0);
     check(gemm(s.tm_z, txt ? L.tm_t_wout : L.tm_wout, n, r0, hs, m.mlp, Epi::Residual,
-               sk(s, res_out), s.sm_count, s.stream), "gemm mlp-out (joint)");
+               sk(s, clip(txt, res_out)), s.sm_count, s.stream), "gemm mlp-out (joint)");
     prof_end(s);
   });
 }

@@ -184,6 +184,9 @@ struct Stage {
   CUtensorMap tm_hb, tm_attn, tm_z, tm_q;
   CUtensorMap tm_hb_half;  // 64-row boxes over hb (A multicast across cluster pairs)
   CUtensorMap tm_h32;  // fp32 residual stream, box 32 x 128 (TMA epilogue)
+  // joint rows: maps over the T text rows only (clipped TMA residual stores of
+  // the text stream's partial last row tile)
+  CUtensorMap tm_h32_txt, tm_hb_txt;
   cudaEvent_t ev_fwd = nullptr;  // "rows sent to stage d+1"
   // Extra patch lanes (small patches): own stream and the per-launch scratch
   // concurrent patches must not share. The fields above always hold the

@@ -353,6 +353,15 @@ void Engine::layer_forward_mm(Stage& s, int lf, int rows, int row0, int t, int c
   auto wmap = [&](int st, const WeightMaps& a, const WeightMaps& b) -> const WeightMaps& {
     return st ? b : a;
   };
+  // text rows (a partial last row tile): residual epilogue through maps that
+  // end at the last text row, so the TMA stores clip there (not into the
+  // image rows that follow); a redirected store keeps the register path
+  auto text_maps = [&](int st, EpiParams& e) {
+    if (st != 1 || e.out_f32_dst) return;
+    e.tm_h32 = &s.tm_h32_txt;
+    e.tm_hb = &s.tm_hb_txt;
+    e.tma_clip = true;
+  };
 
   EpiParams res;
   res.out_f32 = s.h32;
@@ -436,6 +445,7 @@ void Engine::layer_forward_mm(Stage& s, int lf, int rows, int row0, int t, int c
       r1.gate = modv(lf, st) + 2 * hs;
       r1.colscale = modv(lf, st) + 4 * hs;
       r1.stats_out = px.stats;
+      text_maps(st, r1);
       prof_begin(s, kGemmOut, 2.0 * n * dhs * dhs, 0);
       check(gemm(s.tm_attn, wmap(st, L.tm_wo, L.tm_t_wo), n, r0, hs, hs, Epi::Residual,
                  sk(s, r1), s.sm_count, s.stream), "gemm out-proj (MMDiT)");
@@ -464,6 +474,7 @@ void Engine::layer_forward_mm(Stage& s, int lf, int rows, int row0, int t, int c
       r3.colscale = next_scale1(st);
       r3.stats_out = px.stats;
       redirect(r3);
+      text_maps(st, r3);
       prof_begin(s, kGemmMlpOut, 2.0 * n * dhs * mlp, 0);
       check(gemm(s.tm_z, wmap(st, L.tm_wout, L.tm_t_wout), n, r0, hs, m.mlp, Epi::Residual,
                  sk(s, r3), s.sm_count, s.stream), "gemm mlp-out (MMDiT)");
