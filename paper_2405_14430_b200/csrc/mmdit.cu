@@ -169,6 +169,80 @@ __global__ void mm_qk_norm_rope_kernel(bf16* __restrict__ q, bf16* __restrict__ 
   }
 }
 
+// Vectorised variant for dhp / 8 in {2, 4, 8, 16}: G = dhp / 8 lanes per
+// (row, head, q|k) item, 8 elements (one 16-byte vector) per lane, the RMS
+// reduction over the item's G lanes; 32 / G items per warp.
+template <int G>
+__global__ void mm_qk_norm_rope_vec_kernel(bf16* __restrict__ q, bf16* __restrict__ k, int heads,
+                                           int q_rows, int k_rows, int dhp, int dh, int row0,
+                                           int rows, int J, const float* __restrict__ gq_img,
+                                           const float* __restrict__ gk_img,
+                                           const float* __restrict__ gq_txt,
+                                           const float* __restrict__ gk_txt, int rope, int side) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t item = tid / G;
+  const int sub = int(tid % G);
+  const int64_t total = int64_t(rows) * heads * 2;
+  const bool live = item < total;
+  const int64_t it = live ? item : 0;
+  const int which = int(it & 1);
+  const int64_t rh = it >> 1;
+  const int head = int(rh % heads);
+  const int row = row0 + int(rh / heads);
+  const bool txt = row < J;
+  const float* g = which == 0 ? (txt ? gq_txt : gq_img) : (txt ? gk_txt : gk_img);
+  bf16* base = (which == 0 ? q + (size_t(head) * q_rows + row) * dhp
+                           : k + (size_t(head) * k_rows + row) * dhp) + 8 * sub;
+  float x[8];
+  uint4 raw = live ? *reinterpret_cast<const uint4*>(base) : make_uint4(0, 0, 0, 0);
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __bfloat1622float2(h2[j]);
+    x[2 * j] = f.x;
+    x[2 * j + 1] = f.y;
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ss += x[j] * x[j];  // padding columns are zero
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (!live) return;
+  const float inv = rsqrtf(ss / float(dh) + 1e-6f);
+  const int img = row - J;
+  const float pos1 = txt ? 0.f : float(img / side), pos2 = txt ? 0.f : float(img % side);
+  const int d0 = dh / 8, d1 = 7 * dh / 16;
+  uint4 outv;
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&outv);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int e = 8 * sub + 2 * j;
+    float y0 = 0.f, y1 = 0.f;
+    if (e < dh) {
+      y0 = x[2 * j] * inv * g[e];
+      y1 = x[2 * j + 1] * inv * g[e + 1];
+      if (rope) {
+        int off, d;
+        float pos;
+        if (e < d0) { off = 0; d = d0; pos = 0.f; }
+        else if (e < d0 + d1) { off = d0; d = d1; pos = pos1; }
+        else { off = d0 + d1; d = d1; pos = pos2; }
+        const int jj = (e - off) / 2;
+        const float w = expf(-9.210340371976184f * float(2 * jj) / float(d));
+        float sn, cs;
+        sincosf(pos * w, &sn, &cs);
+        const float z0 = cs * y0 - sn * y1, z1 = sn * y0 + cs * y1;
+        y0 = z0;
+        y1 = z1;
+      }
+    }
+    o2[j] = __floats2bfloat162_rn(y0, y1);
+  }
+  *reinterpret_cast<uint4*>(base) = outv;
+}
+
 int fill_grid(int64_t n) {
   const int64_t b = (n + 255) / 256;
   return int(b < 148 * 32 ? (b < 1 ? 1 : b) : 148 * 32);
@@ -200,6 +274,31 @@ cudaError_t mm_qk_norm_rope(bf16* q, bf16* k, int heads, int q_rows, int k_rows,
                             cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (dh > 128 || dh % 2 != 0) return cudaErrorInvalidValue;
+  const int G = dhp / 8;
+  if (G == 2 || G == 4 || G == 8 || G == 16) {
+    const int64_t threads = int64_t(rows) * heads * 2 * G;
+    const unsigned blocks = unsigned((threads + 255) / 256);
+    const int sd = side < 1 ? 1 : side;
+    const int rp = rope ? 1 : 0;
+    switch (G) {
+      case 2:
+        return launch_pdl(mm_qk_norm_rope_vec_kernel<2>, dim3(blocks), dim3(256), 0, stream, q,
+                          k, heads, q_rows, k_rows, dhp, dh, row0, rows, J, gq_img, gk_img,
+                          gq_txt, gk_txt, rp, sd);
+      case 4:
+        return launch_pdl(mm_qk_norm_rope_vec_kernel<4>, dim3(blocks), dim3(256), 0, stream, q,
+                          k, heads, q_rows, k_rows, dhp, dh, row0, rows, J, gq_img, gk_img,
+                          gq_txt, gk_txt, rp, sd);
+      case 8:
+        return launch_pdl(mm_qk_norm_rope_vec_kernel<8>, dim3(blocks), dim3(256), 0, stream, q,
+                          k, heads, q_rows, k_rows, dhp, dh, row0, rows, J, gq_img, gk_img,
+                          gq_txt, gk_txt, rp, sd);
+      default:
+        return launch_pdl(mm_qk_norm_rope_vec_kernel<16>, dim3(blocks), dim3(256), 0, stream, q,
+                          k, heads, q_rows, k_rows, dhp, dh, row0, rows, J, gq_img, gk_img,
+                          gq_txt, gk_txt, rp, sd);
+    }
+  }
   const int64_t warps = int64_t(rows) * heads * 2;
   const unsigned blocks = unsigned((warps * 32 + 255) / 256);
   return launch_pdl(mm_qk_norm_rope_kernel, dim3(blocks), dim3(256), 0, stream, q, k, heads,
