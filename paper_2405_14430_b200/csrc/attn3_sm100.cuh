@@ -20,15 +20,21 @@
 
 namespace pf {
 
-constexpr int kAttn3BN = 112;  // kv rows per block
 constexpr int kAttn3Buf = 3;   // S buffers
+// kv rows per block: the widest multiple of 16 with 3 S buffers + 2 O tiles
+// in the 512 TMEM columns (dhp <= 80: 112; dhp 96 / 112 / 128: 96 / 80 / 64)
+__host__ __device__ constexpr int attn3_bn(int dhp) {
+  return dhp <= 80 ? 112 : ((512 - 2 * dhp) / 3) / 16 * 16;
+}
+constexpr int kAttn3BN = 112;  // dhp <= 80
 
 template <int DHP>
 struct Attn3Smem {
+  static constexpr int BN = attn3_bn(DHP);
   static constexpr int NT = 2;
   static constexpr uint32_t kQBytes = kAttnBM * DHP * 2;
   static constexpr uint32_t kQAlloc = (kQBytes + 1023) & ~1023u;
-  static constexpr uint32_t kKVBytes = kAttn3BN * DHP * 2;
+  static constexpr uint32_t kKVBytes = BN * DHP * 2;
   static constexpr uint32_t kKVAlloc = (kKVBytes + 1023) & ~1023u;
   static constexpr uint32_t kBudget = 232448 - 1024 - 512 - 16 * kAttnMaxSegs;
   static constexpr int kStagesMax = int((kBudget - NT * kQAlloc) / (2 * kKVAlloc));
@@ -40,10 +46,11 @@ struct Attn3Smem {
   static constexpr uint32_t kSegOff = kBarOff + 512;
   static constexpr uint32_t kTotal = kSegOff + 16 * kAttnMaxSegs + 1024;
   static constexpr int kThreads = 128 + 128 * NT;
-  // TMEM columns: S buffer b at 112 b, O_t at kOCol + 80 t
-  static constexpr uint32_t kOCol = 352;
-  static_assert(DHP % 16 == 0 && DHP <= 80, "triple-buffered S needs DHP <= 80");
-  static_assert(kOCol + 2 * 80 <= 512 && kAttn3Buf * kAttn3BN <= kOCol, "TMEM budget");
+  // TMEM columns: S buffer b at BN b, O_t at kOCol + kOW t
+  static constexpr uint32_t kOW = DHP <= 80 ? 80 : DHP;
+  static constexpr uint32_t kOCol = 512 - 2 * kOW;
+  static_assert(DHP % 16 == 0 && DHP <= 128 && BN % 16 == 0 && BN >= 32, "attn3 shapes");
+  static_assert(kOCol + 2 * kOW <= 512 && kAttn3Buf * BN <= int(kOCol), "TMEM budget");
   static_assert(kStages >= 2, "attention smem budget");
   static_assert(kTotal <= 232448, "attention smem budget");
 };
@@ -56,7 +63,7 @@ __global__ void __launch_bounds__(384, 1)
   using L = Attn3Smem<DHP>;
   constexpr int NT = 2;
   constexpr int S = L::kStages;
-  constexpr int BN = kAttn3BN;
+  constexpr int BN = L::BN;
   constexpr int kChunks = DHP / 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(384, 1)
           ptx::tc_fence_after();
           const uint32_t vb = v_base + (vg % S) * L::kKVAlloc;
           const uint32_t pt = tmem_base + uint32_t(((gn + n) % kAttn3Buf) * BN) + BN / 2;
-          const uint32_t od = tmem_base + L::kOCol + 80u * uint32_t(t);
+          const uint32_t od = tmem_base + L::kOCol + L::kOW * uint32_t(t);
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
             ptx::umma_bf16_ts(od, pt + 8 * k,
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(384, 1)
     const int q = warp & 3;
     const int trow = 32 * q + int(lane);
     const uint32_t lane_off = uint32_t(32 * q) << 16;
-    const uint32_t tmem_o = tmem_base + L::kOCol + 80u * uint32_t(t) + lane_off;
+    const uint32_t tmem_o = tmem_base + L::kOCol + L::kOW * uint32_t(t) + lane_off;
     const float sc = prm.scale_log2;
     int gb = 0, gn = 0;
     int* pending_flag = nullptr;
@@ -264,10 +271,11 @@ __global__ void __launch_bounds__(384, 1)
         if (tr) attn_trace(prm, 2048 * t + 8 * (gb + i) + 1);
         ptx::tc_fence_after();
         uint32_t sr[BN];
-        ptx::tmem_ld32(tmem_s + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(tmem_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        ptx::tmem_ld32(tmem_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-        ptx::tmem_ld16(tmem_s + 96, *reinterpret_cast<uint32_t(*)[16]>(&sr[96]));
+#pragma unroll
+        for (int c = 0; c + 32 <= BN; c += 32)
+          ptx::tmem_ld32(tmem_s + c, *reinterpret_cast<uint32_t(*)[32]>(&sr[c]));
+        if constexpr (BN % 32 == 16)
+          ptx::tmem_ld16(tmem_s + (BN - 16), *reinterpret_cast<uint32_t(*)[16]>(&sr[BN - 16]));
         ptx::tmem_wait_ld();
         float* s = reinterpret_cast<float*>(sr);
         if (kv0 + BN > prm.P) {
@@ -276,14 +284,14 @@ __global__ void __launch_bounds__(384, 1)
           for (int e = 0; e < BN; ++e)
             if (e >= valid) s[e] = -INFINITY;
         }
-        // row max: 8 chains of 14 columns with FMNMX3
+        // row max: 8 chains of BN / 8 columns with FMNMX3
         float bm[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-          bm[a] = ptx::fmax3(s[a], s[a + 8], s[a + 16]);
+          bm[a] = s[a];
 #pragma unroll
-          for (int e = 24; e < 104; e += 16) bm[a] = ptx::fmax3(bm[a], s[e + a], s[e + 8 + a]);
-          bm[a] = fmaxf(bm[a], s[104 + a]);
+          for (int e = 8; e + 8 < BN; e += 16) bm[a] = ptx::fmax3(bm[a], s[e + a], s[e + 8 + a]);
+          if constexpr ((BN / 8) % 2 == 0) bm[a] = fmaxf(bm[a], s[BN - 8 + a]);
         }
         const float bmax = fmaxf(ptx::fmax3(bm[0], bm[1], bm[2]),
                                  ptx::fmax3(bm[3], ptx::fmax3(bm[4], bm[5], bm[6]), bm[7])) * sc;
@@ -310,13 +318,14 @@ __global__ void __launch_bounds__(384, 1)
         const float2 sc2 = make_float2(sc, sc);
         const float2 nm2 = make_float2(-m_new, -m_new);
         const uint32_t tmem_p = tmem_s + BN / 2;
+        constexpr int kParts = (BN + 31) / 32;  // 32 scores per part (the last may be 16)
 #pragma unroll
-        for (int part = 0; part < 4; ++part) {  // 32 + 32 + 32 + 16 scores
-          constexpr int kPartLen[4] = {32, 32, 32, 16};
+        for (int part = 0; part < kParts; ++part) {
+          const int plen = (32 * part + 32 <= BN) ? 32 : BN - 32 * part;
           uint32_t pk[16];
 #pragma unroll
           for (int gg = 0; gg < 8; ++gg) {
-            if (4 * gg >= kPartLen[part]) break;
+            if (4 * gg >= plen) break;
             const int e = 32 * part + 4 * gg;
             const int grp = (e / 4) & 7;
             const float2 x0 = ptx::ffma2(make_float2(s[e], s[e + 1]), sc2, nm2);
@@ -335,10 +344,10 @@ __global__ void __launch_bounds__(384, 1)
             pk[2 * gg] = ptx::pack_bf16x2(p0.x, p0.y);
             pk[2 * gg + 1] = ptx::pack_bf16x2(p1.x, p1.y);
           }
-          if (part < 3) {
+          if (plen == 32) {
             ptx::tmem_st16(tmem_p + 16 * part, pk);
           } else {
-            ptx::tmem_st8(tmem_p + 48, *reinterpret_cast<const uint32_t(*)[8]>(&pk[0]));
+            ptx::tmem_st8(tmem_p + 16 * part, *reinterpret_cast<const uint32_t(*)[8]>(&pk[0]));
           }
         }
         ptx::tmem_wait_st();

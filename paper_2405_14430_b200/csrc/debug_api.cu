@@ -162,11 +162,11 @@ extern "C" int pf_debug_attention_ex(const void* q, const void* k, const void* v
             pf::encode_tmap_bf16_2d(&tv, vp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2, 16,
                                     128, 32);
   CUtensorMap tk3, tv3;
-  const bool kv3 = dhp <= 80 &&
-                   pf::encode_tmap_bf16_2d(&tk3, kp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2,
-                                           16, 112, 32) &&
-                   pf::encode_tmap_bf16_2d(&tv3, vp, dhp, uint64_t(heads) * P, uint64_t(dhp) * 2,
-                                           16, 112, 32);
+  const uint32_t b3 = uint32_t(pf::attn3_kv_rows(dhp));
+  const bool kv3 = pf::encode_tmap_bf16_2d(&tk3, kp, dhp, uint64_t(heads) * P,
+                                           uint64_t(dhp) * 2, 16, b3, 32) &&
+                   pf::encode_tmap_bf16_2d(&tv3, vp, dhp, uint64_t(heads) * P,
+                                           uint64_t(dhp) * 2, 16, b3, 32);
   int err = ok ? 0 : int(cudaErrorInvalidValue);
   if (ok) {
     pf::AttnLaunch a{dhp, P, rows, row0, heads, dh, hs, float(1.0 / std::sqrt(double(dh))),

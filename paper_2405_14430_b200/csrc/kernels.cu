@@ -1022,7 +1022,7 @@ cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count
   prm.dh = a.dh;
   prm.hs = a.hs;
   prm.scale_log2 = a.scale * 1.4426950408889634f;
-  const AttnSchedule sc = attn_schedule(a, sm_count, kAttn3BN);
+  const AttnSchedule sc = attn_schedule(a, sm_count, attn3_bn(DHP));
   prm.nq = sc.nq;
   prm.blocks = sc.blocks;
   prm.units = sc.units;
@@ -1080,21 +1080,27 @@ cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count
 }
 }  // namespace
 
+int attn3_kv_rows(int dhp) { return attn3_bn(dhp); }
+
 int attn_block_rows(const AttnLaunch& a) {
-  return (a.k3 && a.v3 && !a.k2 && a.dhp <= 80 && attn3_enabled()) ? kAttn3BN : kAttnBN;
+  return (a.k3 && a.v3 && !a.k2 && a.dhp <= 128 && attn3_enabled()) ? attn3_bn(a.dhp)
+                                                                      : kAttnBN;
 }
 
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,
                       const CUtensorMap& v, const AttnLaunch& a, int sm_count,
                       cudaStream_t stream) {
   if (a.rows <= 0) return cudaSuccess;
-  if (attn_block_rows(a) == kAttn3BN) {
+  if (attn_block_rows(a) != kAttnBN) {
     switch (a.dhp) {
       case 16: return launch_attn3<16>(q, a, sm_count, stream);
       case 32: return launch_attn3<32>(q, a, sm_count, stream);
       case 48: return launch_attn3<48>(q, a, sm_count, stream);
       case 64: return launch_attn3<64>(q, a, sm_count, stream);
       case 80: return launch_attn3<80>(q, a, sm_count, stream);
+      case 96: return launch_attn3<96>(q, a, sm_count, stream);
+      case 112: return launch_attn3<112>(q, a, sm_count, stream);
+      case 128: return launch_attn3<128>(q, a, sm_count, stream);
       default: break;
     }
   }

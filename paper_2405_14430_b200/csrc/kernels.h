@@ -164,7 +164,7 @@ struct AttnLaunch {
   // (16-byte aligned regions; bytes 0 = unused)
   const void* prefetch[kAttnPrefetchRegions] = {};
   size_t prefetch_bytes[kAttnPrefetchRegions] = {};
-  // K / V tensor maps with 112-row boxes (dhp <= 80): the triple-buffered
+  // K / V tensor maps with attn3_kv_rows(dhp)-row boxes: the triple-buffered
   // kernel (attn3_sm100.cuh) runs when present and no k2 / v2 is given
   const CUtensorMap* k3 = nullptr;
   const CUtensorMap* v3 = nullptr;
@@ -176,6 +176,8 @@ struct AttnLaunch {
 // KV rows per block of the kernel a launch uses (128, or 112 for the
 // triple-buffered kernel) and the schedule for a given block size
 int attn_block_rows(const AttnLaunch& a);
+// KV rows per block (and K / V tensor-map box rows) of the triple-buffered kernel
+int attn3_kv_rows(int dhp);
 int attn_grid(const AttnLaunch& a, int sm_count, int bn = 128);
 // The attention launch's schedule (host only): query-tile groups per head,
 // KV blocks per item, units, persistent CTAs, whether items are cut and

@@ -317,9 +317,10 @@ void Engine::alloc_stage(Stage& s, int first, int count, bool is_first) {
       throw CudaError("cuTensorMapEncodeTiled failed for a weight matrix");
     L.tm_k = tmap(L.k, dhp, heads * P, dhp * 2, 16, 128, 32);
     L.tm_v = tmap(L.v, dhp, heads * P, dhp * 2, 16, 128, 32);
-    if (dhp <= 80) {
-      L.tm_k3 = tmap(L.k, dhp, heads * P, dhp * 2, 16, 112, 32);
-      L.tm_v3 = tmap(L.v, dhp, heads * P, dhp * 2, 16, 112, 32);
+    {
+      const uint32_t b3 = uint32_t(attn3_kv_rows(int(dhp)));
+      L.tm_k3 = tmap(L.k, dhp, heads * P, dhp * 2, 16, b3, 32);
+      L.tm_v3 = tmap(L.v, dhp, heads * P, dhp * 2, 16, b3, 32);
       L.has_kv3 = true;
     }
     check(v_ones_col(L.v, heads * P, int(dhp), m.dh, nullptr), "v_ones_col");
@@ -1829,8 +1830,9 @@ void Engine::enqueue_distrifusion(float* x_dev, int steps, int workers, int warm
       L.tm_k2 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
       L.tm_v2 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 128, 32);
       if (L.has_kv3) {
-        L.tm_k23 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 112, 32);
-        L.tm_v23 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, 112, 32);
+        const uint32_t b3 = uint32_t(attn3_kv_rows(m.dhp));
+        L.tm_k23 = tmap(L.k2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, b3, 32);
+        L.tm_v23 = tmap(L.v2, m.dhp, size_t(m.heads) * m.P, size_t(m.dhp) * 2, 16, b3, 32);
       }
     }
   if (!ev_start_) PF_CUDA_CHECK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));

@@ -110,7 +110,7 @@ struct StageLayer {
   bf16* v = nullptr;     // [heads][P][dhp]
   WeightMaps tm_wqkv, tm_wo, tm_win, tm_wout;
   CUtensorMap tm_k, tm_v;
-  // 112-row KV boxes for the triple-buffered attention (dhp <= 80)
+  // KV boxes of attn3_kv_rows(dhp) rows for the triple-buffered attention
   CUtensorMap tm_k3, tm_v3;
   CUtensorMap tm_k23, tm_v23;  // the same over k2 / v2 (DistriFusion)
   bool has_kv3 = false;
