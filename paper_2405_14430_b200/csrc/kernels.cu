@@ -1083,8 +1083,16 @@ cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count
 int attn3_kv_rows(int dhp) { return attn3_bn(dhp); }
 
 int attn_block_rows(const AttnLaunch& a) {
-  return (a.k3 && a.v3 && !a.k2 && a.dhp <= 128 && attn3_enabled()) ? attn3_bn(a.dhp)
-                                                                      : kAttnBN;
+  // dhp <= 80 (112-row blocks): measured faster (C2 105.9 vs 115.2 us, SD3 dh 64 178.5 vs
+  // 191.9 us); dhp 128 with 64-row blocks measured slower (Flux 4375 vs 4170 us), so the
+  // wider head dims keep the single-buffered kernel (PF_ATTN3=2 forces attn3 for them)
+  static const int mode = [] {
+    const char* e = std::getenv("PF_ATTN3");
+    return e ? std::atoi(e) : 1;
+  }();
+  const int max_dhp = mode >= 2 ? 128 : 80;
+  return (a.k3 && a.v3 && !a.k2 && a.dhp <= max_dhp && attn3_enabled()) ? attn3_bn(a.dhp)
+                                                                         : kAttnBN;
 }
 
 cudaError_t attention(const CUtensorMap& q, const CUtensorMap& k,

@@ -180,3 +180,32 @@ def test_attention_peaked_rows_rescale(P, heads, hs, rows, row0, sumcol):
     assert torch.isfinite(out).all()
     rel = ((out - ref).norm() / ref.norm()).item()
     assert rel < 1e-2, rel
+
+
+@pytest.mark.parametrize("P,heads,hs,rows,row0", [
+    (520, 2, 256, 136, 384),      # dh 128 (64-row blocks), ragged
+    (2048, 16, 2048, 2048, 0),    # dh 128, stream-K in-kernel merge
+    (1000, 8, 768, 1000, 0),      # dh 96 (96-row blocks)
+])
+def test_attention_triple_buffered_wide_heads(monkeypatch, P, heads, hs, rows, row0):
+    """The triple-buffered kernel at head dims above 80 (opt-in PF_ATTN3=2:
+    measured slower than the single-buffered kernel at dh 128)."""
+    monkeypatch.setenv("PF_ATTN3", "2")
+    import subprocess
+    import sys
+    code = f"""
+import torch, sys
+sys.path.insert(0, {str(__import__('pathlib').Path(__file__).resolve().parents[1])!r})
+from tests.test_gpu_kernels import _attn, _attn_ref
+g = torch.Generator(device="cuda").manual_seed(7)
+mk = lambda: ((torch.rand({P}, {hs}, device="cuda", generator=g) * 2 - 1) * 2).to(torch.bfloat16)
+q, k, v = mk(), mk(), mk()
+out = _attn(q, k, v, {heads}, {rows}, {row0})[{row0}:{row0} + {rows}].float()
+ref = _attn_ref(q, k, v, {heads}, {rows}, {row0})
+rel = ((out - ref).norm() / ref.norm()).item()
+assert rel < 1e-2, rel
+print("ok", rel)
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+

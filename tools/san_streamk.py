@@ -1,6 +1,9 @@
 """compute-sanitizer workload for the stream-K attention schedules (fused
-in-kernel merge, halves, one CTA per item, separate merge kernel), patch
-lanes and the opt-in residual split-K. Sanitizer input, not a test."""
+in-kernel merge, halves, one CTA per item, separate merge kernel) of both
+attention kernels (triple-buffered attn3 with the row-sum column, and the
+single-buffered one), patch lanes, the MMDiT blocks (QK-norm, RoPE, clipped
+text-row residual tiles) and the opt-in residual split-K. Sanitizer input,
+not a test."""
 import os
 import sys
 from pathlib import Path
@@ -17,9 +20,14 @@ for P, heads, hs, rows, row0 in [(4096, 16, 1152, 4096, 0), (4096, 16, 1152, 512
                                  (4096, 16, 1152, 2048, 0), (3000, 12, 768, 3000, 0)]:
     q, k, v = [(torch.rand(P, hs, device="cuda") - 0.5).to(torch.bfloat16) for _ in range(3)]
     out = torch.zeros(P, hs, dtype=torch.bfloat16, device="cuda")
-    assert lib.pf_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), P,
-                                  rows, row0, heads, hs, s) == 0
+    for sumcol in (0, 1):
+        assert lib.pf_debug_attention_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                         out.data_ptr(), P, rows, row0, heads, hs, s,
+                                         sumcol) == 0
     torch.cuda.synchronize()
+with pf.MMDiTCuda(1, 2, 128, 4, 4.0, 256, 20, 1, double_layers=1, rope=True) as mm:
+    c = mm.run_pipefusion(pf.make_initial_latent(0, 256, 128), 3, 2, 1, 0.1)
+assert np.isfinite(c.final_x).all()
 x0 = pf.make_initial_latent(0, 512, 128)
 with pf.ToyDiTCuda(0, 2, 128, 4, 4.0, 512, 1) as m:
     a = m.run_pipefusion(x0, 3, 4, 1, 0.1)
