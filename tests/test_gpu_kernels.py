@@ -196,7 +196,8 @@ def test_attention_triple_buffered_wide_heads(monkeypatch, P, heads, hs, rows, r
     code = f"""
 import torch, sys
 sys.path.insert(0, {str(__import__('pathlib').Path(__file__).resolve().parents[1])!r})
-from tests.test_gpu_kernels import _attn, _attn_ref
+sys.path.insert(0, {str(__import__('pathlib').Path(__file__).resolve().parent)!r})
+from test_gpu_kernels import _attn, _attn_ref
 g = torch.Generator(device="cuda").manual_seed(7)
 mk = lambda: ((torch.rand({P}, {hs}, device="cuda", generator=g) * 2 - 1) * 2).to(torch.bfloat16)
 q, k, v = mk(), mk(), mk()

@@ -30,16 +30,22 @@ def _single(seed, L, hs, heads, p, N, S, M, W, x0, text=0):
     return res
 
 
-def _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0, text=0, runs=1, joint=None):
+def _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0, text=0, runs=1, joint=None,
+                        mmdit=None, precision=0):
     import torch
-    if joint is not None:
+    if mmdit is not None:
+        D, rope = mmdit
+        ranks = [pf.MMDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, text, r, N, 0,
+                                         double_layers=D, rope=rope) for r in range(N)]
+    elif joint is not None:
         ranks = [pf.JointDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, text, r, N, 0,
                                             double_layers=joint) for r in range(N)]
     elif text:
         ranks = [pf.PixArtCuda.rank_stage(seed, L, hs, heads, 4.0, p, text, r, N, 0)
                  for r in range(N)]
     else:
-        ranks = [pf.ToyDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, r, N, 0) for r in range(N)]
+        ranks = [pf.ToyDiTCuda.rank_stage(seed, L, hs, heads, 4.0, p, r, N, 0,
+                                          precision=precision) for r in range(N)]
     pf.connect_ranks(ranks)
     outs, stats = [], []
     # one caller stream per rank: a shared caller stream would chain the ranks'
@@ -138,6 +144,36 @@ def test_process_per_rank_over_cuda_ipc():
     assert np.array_equal(got[0][0], ref.final_x)
     assert (sum(v[1] for v in got.values()), sum(v[2] for v in got.values())) == \
         (ref.stats.fresh_patch_reads, ref.stats.stale_patch_reads)
+
+
+@pytest.mark.parametrize("D,rope,N,M,W", [(4, False, 2, 4, 1), (2, True, 3, 2, 0),
+                                          (1, True, 4, 4, 1)])
+def test_same_process_ranks_mmdit(D, rope, N, M, W):
+    """MMDiT blocks in rank mode: the LayerNorm statistics travel with the rows
+    in the fused peer stores (text rows with patch 0); bitwise equal to the
+    single-context engine with the same stage count."""
+    seed, L, hs, heads, p, T, S = 4, 4, 128, 4, 256, 24, 4
+    x0 = pf.make_initial_latent(5, p, hs)
+    with pf.MMDiTCuda(seed, L, hs, heads, 4.0, p, T, N, double_layers=D, rope=rope) as m:
+        ref = m.run_pipefusion(x0, S, M, W, 0.1)
+    outs, stats = _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0, text=T,
+                                      mmdit=(D, rope))
+    assert np.array_equal(outs[0], ref.final_x)
+    assert stats[0] == (ref.stats.fresh_patch_reads, ref.stats.stale_patch_reads)
+
+
+def test_same_process_ranks_fp32_parity_mode():
+    """The fp32 parity mode in rank mode (fused sends write the fp32 rows)."""
+    seed, L, hs, heads, p, N, S, M, W = 0, 4, 128, 4, 256, 2, 4, 4, 1
+    x0 = pf.make_initial_latent(0, p, hs)
+    with pf.ToyDiTCuda(seed, L, hs, heads, 4.0, p, N, precision=pf.PRECISION_FP32) as m:
+        ref = m.run_pipefusion(x0, S, M, W, 0.1)
+    outs, _ = _same_process_ranks(seed, L, hs, heads, p, N, S, M, W, x0,
+                                  precision=pf.PRECISION_FP32)
+    assert np.array_equal(outs[0], ref.final_x)
+    o = loader.Restatement().build_toy_model(seed, L, hs, heads)
+    ora, _ = o.run_pipefusion(x0, S, N, M, W, 0.1)
+    assert np.linalg.norm(outs[0] - ora) / np.linalg.norm(ora) <= 1e-4
 
 
 @pytest.mark.parametrize("D,N", [(4, 2), (2, 3)])
