@@ -117,9 +117,12 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_init(&o_done[t], 1);
     }
     ptx::fence_barrier_init();
-    const long long u0 = attn_unit_start(prm, blockIdx.x);
-    const long long u1 = attn_unit_start(prm, blockIdx.x + 1);
+    const long long u0 = prm.strided ? 0 : attn_unit_start(prm, blockIdx.x);
+    const long long u1 = prm.strided ? 0 : attn_unit_start(prm, blockIdx.x + 1);
     int n = 0;
+    if (prm.strided)
+      for (long long x = blockIdx.x; x < prm.units / B && n < kAttnMaxSegs; x += prm.grid)
+        segs[n++] = make_int4(int(x), 0, B, 0);
     for (long long u = u0; u < u1 && n < kAttnMaxSegs; ++n) {
       const int x = int(u / B);
       const int b0 = int(u - (long long)x * B);
@@ -299,9 +302,11 @@ __global__ void __launch_bounds__(384, 1)
         const float m_new = need ? bmax : m_ref;
         const float alpha = need ? ptx::ex2_approx(m_ref - m_new) : 1.0f;
         if (tr) attn_trace(prm, 2048 * t + 8 * (gb + i) + 2);
+        // the previous block's PV has landed in O (needed before a rescale;
+        // waited every block so each pv_done phase is observed -- it is long
+        // complete by now: S load and row max take longer than one tile's PV)
+        if (gb + i > 0) ptx::mbar_wait(&pv_done[t], (gb + i - 1) & 1);
         if (i > 0 && __any_sync(0xffffffffu, need)) {
-          // the previous block's PV must have landed in O before rescaling it
-          ptx::mbar_wait(&pv_done[t], (gb + i - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll
           for (int c = 0; c < kChunks; ++c) {

@@ -121,6 +121,7 @@ struct AttnParams {
   int* flags;          // [grid][kAttnFlagsPerCta] head partial published, per softmax
                        // warp (fused merge; cleared by the reading warp)
   int fused;           // merge cut items in-kernel (every range >= one item)
+  int strided;         // whole items c, c + grid, ... per CTA (no cuts; AttnSchedule)
   // L2 prefetch of the weights the next kernels stream (the CTAs split every
   // region; issued by the otherwise idle warp 3 before the PDL wait)
   const char* pf_ptr[kAttnPrefetchRegions];
@@ -207,9 +208,12 @@ __global__ void __launch_bounds__(128 + 128 * NT * kW, 1)
     ptx::fence_barrier_init();
     // Segment table of this CTA's unit range [u0, u1): natural order, or
     // reversed when cut items are merged in-kernel (see header).
-    const long long u0 = attn_unit_start(prm, blockIdx.x);
-    const long long u1 = attn_unit_start(prm, blockIdx.x + 1);
+    const long long u0 = prm.strided ? 0 : attn_unit_start(prm, blockIdx.x);
+    const long long u1 = prm.strided ? 0 : attn_unit_start(prm, blockIdx.x + 1);
     int n = 0;
+    if (prm.strided)
+      for (long long x = blockIdx.x; x < prm.units / B && n < kAttnMaxSegs; x += prm.grid)
+        segs[n++] = make_int4(int(x), 0, B, 0);
     for (long long u = u0; u < u1 && n < kAttnMaxSegs; ++n) {
       const int x = int(u / B);
       const int b0 = int(u - (long long)x * B);

@@ -900,6 +900,21 @@ AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count, int bn) {
   const bool halves = sc.units % sc.grid == 0 && 2 * (sc.units / sc.grid) == sc.blocks;
   sc.fused = sc.cut && sc.grid >= 2 && a.flags && !no_fuse &&
              (sc.units / sc.grid >= sc.blocks || halves);
+  // K/V of all heads beyond ~3/4 of the 126 MB L2 and at least four items
+  // per SM: round-robin whole items (measured at Flux 2048 px, dh 128: the
+  // contiguous stream-K ranges re-read K/V from DRAM ~37x, 11.7 GB per launch)
+  static const bool no_strided = [] {
+    const char* e = std::getenv("PF_ATTN_STRIDED");
+    return e && e[0] == '0';
+  }();
+  const long long items = (long long)sc.nq * a.heads;
+  const double kv_bytes = 4.0 * a.heads * double(a.P) * a.dhp;
+  if (!no_strided && kv_bytes > 96e6 && items >= 4LL * sm_count) {
+    sc.strided = true;
+    sc.grid = sm_count;
+    sc.cut = false;
+    sc.fused = false;
+  }
   return sc;
 }
 
@@ -941,6 +956,7 @@ cudaError_t launch_attn(const CUtensorMap& q, const CUtensorMap& k,
     prm.pf_bytes[i] = a.prefetch[i] ? (a.prefetch_bytes[i] & ~size_t(15)) : 0;
   }
   prm.fused = sc.fused ? 1 : 0;
+  prm.strided = sc.strided ? 1 : 0;
   if (cut) {
     const size_t slots = size_t(2) * prm.grid * NT * kAttnBM;
     if (!a.work || a.work_floats < slots * (DHP + 2)) return cudaErrorInvalidValue;
@@ -1037,6 +1053,7 @@ cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count
     prm.pf_bytes[i] = 0;
   }
   prm.fused = sc.fused ? 1 : 0;
+  prm.strided = sc.strided ? 1 : 0;
   if (sc.cut) {
     const size_t slots = size_t(2) * prm.grid * NT * kAttnBM;
     if (!a.work || a.work_floats < slots * (DHP + 2)) return cudaErrorInvalidValue;

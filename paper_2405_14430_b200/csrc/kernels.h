@@ -186,6 +186,10 @@ struct AttnSchedule {
   int nq = 0, blocks = 0, grid = 0;
   long long units = 0;
   bool cut = false, fused = false;
+  // whole items dealt round-robin (CTA c: items c, c + grid, ...): the CTAs
+  // running at one time then share a few heads' K/V, for launches whose K/V
+  // exceed the L2 (stream-K's contiguous ranges would span every head at once)
+  bool strided = false;
 };
 AttnSchedule attn_schedule(const AttnLaunch& a, int sm_count, int bn = 128);
 // partial-result workspace the attention needs on a device with sm_count SMs

@@ -6,6 +6,8 @@ Inputs are bf16 (the kernels' operand type); the reference computation is
 fp32 on the same bf16 values, so the only differences are accumulation order
 (GEMM) and bf16 rounding of P plus exp2 approximation (attention).
 """
+import ctypes
+
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -210,3 +212,27 @@ print("ok", rel)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
+
+
+@pytest.mark.parametrize("P,heads,hs", [(16896, 24, 3072), (16384, 24, 1536)])
+def test_attention_strided_schedule_large_kv(P, heads, hs):
+    """K/V of all heads beyond the L2 (Flux 2048 px: 24 heads x 16896 rows x
+    dh 128): whole items dealt round-robin over the CTAs (AttnSchedule.strided).
+    Checked on a sample of query rows of every head."""
+    import numpy as np
+    lib = load_library()
+    g = torch.Generator(device="cuda").manual_seed(P + heads)
+    mk = lambda: ((torch.rand(P, hs, device="cuda", generator=g) * 2 - 1) * 2).to(torch.bfloat16)
+    q, k, v = mk(), mk(), mk()
+    out = _attn(q, k, v, heads, P, 0).float()
+    dh = hs // heads
+    rows = torch.cat([torch.arange(0, 200), torch.arange(P // 2, P // 2 + 100),
+                      torch.arange(P - 200, P)]).cuda()
+    errs = []
+    for h in range(heads):
+        c = slice(h * dh, (h + 1) * dh)
+        s = q[rows, c].float() @ k[:, c].float().T / dh ** 0.5
+        ref = torch.softmax(s, dim=-1) @ v[:, c].float()
+        got = out[rows, c]
+        errs.append(((got - ref).norm() / ref.norm()).item())
+    assert max(errs) < 1e-2, errs
