@@ -44,8 +44,9 @@ int pf_debug_attention_trace(int enable, unsigned long long* host);
 // kernel launches that follow; debug instrumentation, not part of the product.
 int pf_debug_gemm_trace(int enable, unsigned long long* host);
 // Host only (no GPU): the attention schedule the library picks for a launch of
-// `rows` query rows over `P` KV rows. out[6] = {query-tile groups per head, KV
-// blocks per item, units, persistent CTAs, items cut (0/1), merged in-kernel (0/1)}.
+// `rows` query rows over `P` KV rows (the 128-row-block kernel). out[7] =
+// {query-tile groups per head, KV blocks per item, units, persistent CTAs,
+// items cut (0/1), merged in-kernel (0/1), whole items round-robin (0/1)}.
 int pf_debug_attn_schedule(int P, int rows, int heads, int dhp, int sm_count, long long* out);
 
 /* Failure injection for the channel-close tests (rank mode): ctx's next runs

@@ -78,7 +78,7 @@ extern "C" int pf_debug_gemm_trace(int enable, unsigned long long* host) {
 }
 
 // Host-only: the stream-K attention schedule the library picks for a launch
-// (no GPU needed). out = {nq, blocks, units, grid, cut, fused}.
+// (no GPU needed). out = {nq, blocks, units, grid, cut, fused, strided}.
 extern "C" int pf_debug_attn_schedule(int P, int rows, int heads, int dhp, int sm_count,
                                       long long* out) {
   if (!out || P <= 0 || rows <= 0 || heads <= 0 || dhp <= 0 || sm_count <= 0) return 1;
@@ -92,6 +92,7 @@ extern "C" int pf_debug_attn_schedule(int P, int rows, int heads, int dhp, int s
   out[3] = sc.grid;
   out[4] = sc.cut ? 1 : 0;
   out[5] = sc.fused ? 1 : 0;
+  out[6] = sc.strided ? 1 : 0;
   return 0;
 }
 

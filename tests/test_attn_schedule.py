@@ -15,15 +15,18 @@ import pytest
 import paper_2405_14430_b200 as pf
 
 
-def schedule(P, rows, heads, dhp, sms=148):
-    out = (ctypes.c_longlong * 6)()
+def schedule(P, rows, heads, dhp, sms=148, with_strided=False):
+    out = (ctypes.c_longlong * 7)()
     assert pf.load_library().pf_debug_attn_schedule(P, rows, heads, dhp, sms, out) == 0
-    nq, blocks, units, grid, cut, fused = list(out)
-    return nq, blocks, units, grid, bool(cut), bool(fused)
+    nq, blocks, units, grid, cut, fused, strided = list(out)
+    res = (nq, blocks, units, grid, bool(cut), bool(fused))
+    return res + (bool(strided),) if with_strided else res
 
 
-def segments(units, grid, B):
+def segments(units, grid, B, strided=False):
     """Segments of each CTA in natural order: (item, b0, n)."""
+    if strided:  # whole items c, c + grid, ... (the kernel's segment table)
+        return [[(x, 0, B) for x in range(c, units // B, grid)] for c in range(grid)]
     out = []
     for c in range(grid):
         u, u1, segs = c * units // grid, (c + 1) * units // grid, []
@@ -46,10 +49,13 @@ SHAPES = [(P, rows, heads, dhp, sms)
 
 @pytest.mark.parametrize("P,rows,heads,dhp,sms", SHAPES)
 def test_schedule_invariants(P, rows, heads, dhp, sms):
-    nq, B, units, grid, cut, fused = schedule(P, rows, heads, dhp, sms)
+    nq, B, units, grid, cut, fused, strided = schedule(P, rows, heads, dhp, sms, True)
     assert nq == (rows + 255) // 256 and B == (P + 127) // 128 and units == nq * heads * B
     assert 1 <= grid
-    segs = segments(units, grid, B)
+    if strided:  # K/V beyond the L2: whole items, no cuts, at least four per CTA
+        assert not cut and not fused and 4 * heads * P * dhp > 96e6
+        assert nq * heads >= 4 * sms
+    segs = segments(units, grid, B, strided)
     owned = {}
     for c, ss in enumerate(segs):
         assert len(ss) <= 64
@@ -81,3 +87,11 @@ def test_c2_schedules():
     assert schedule(4096, 512, 16, 80)[3:] == (32, False, False)    # one CTA per item
     assert schedule(1024, 1024, 8, 64)[3:] == (64, True, True)     # full sequence, two CTAs per item
     assert schedule(4096, 2048, 16, 80)[3:] == (128, False, False)  # one CTA per item
+
+
+def test_flux_full_sequence_is_strided():
+    # Flux 2048 px, dh 128: 24 heads x 16896 KV rows exceed the L2
+    assert schedule(16896, 16896, 24, 128, with_strided=True)[3:] == (148, False, False, True)
+    # C3 (16 heads x 16384 x dh 80, 84 MB of K/V) keeps stream-K
+    assert schedule(16384, 16384, 16, 80, with_strided=True)[6] is False
+
