@@ -829,7 +829,11 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
   // otherwise the 1-SM tiling keeps more SMs busy (small patches).
   const int pair_tiles = ((rows + 2 * kGemmBM - 1) / (2 * kGemmBM)) *
                          ((N + gemm_bn_2sm(N) - 1) / gemm_bn_2sm(N));
-  if (rows >= 2 * kGemmBM && sm_count >= 2 && pair_tiles >= sm_count &&
+  // PF_GEMM_2SM_SMALL=1: CTA pairs for small patches too (A/B: under patch
+  // lanes the other lanes fill the SMs, and fatter tiles amortise each CTA's
+  // fixed prologue / TMA latency / epilogue cost better)
+  static const bool pairs_small = tune_flag("PF_GEMM_2SM_SMALL");
+  if (rows >= 2 * kGemmBM && sm_count >= 2 && (pair_tiles >= sm_count || pairs_small) &&
       (gemm_bn_2sm(N) == 256 || gemm_bn_2sm(N) == 192)) {
     switch (gemm_bn_2sm(N)) {
       case 256: return gemm_dispatch<true, 256, 6>(a, b.two_sm, rows, row0, N, K, kind, ep, sm_count, stream);
