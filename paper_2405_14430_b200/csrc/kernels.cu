@@ -757,8 +757,14 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
     return gemm_dispatch<false, 128, 6>(a, b.one_sm, rows, row0, N, K, kind, ep, sm_count,
                                         stream, sk);
   }
+  // CTA-pair residual GEMMs for every K (PF_RESID_2SM=0: long K only); measured
+  // at K = 1152 (out-proj) 0.5 % faster per image at M = 1 / 4 / 8
+  static const bool resid2_short = [] {
+    const char* e = std::getenv("PF_RESID_2SM");
+    return !(e && e[0] == '0');
+  }();
   if (kind == Epi::Residual && ep.tm_h32 && ep.tm_hb && rows % (2 * kGemmBM) == 0 &&
-      N % 32 == 0 && sm_count >= 2 && (K >= 2048 || tune_flag("PF_RESID_2SM"))) {
+      N % 32 == 0 && sm_count >= 2 && (K >= 2048 || resid2_short)) {
     // long-K residual GEMM (MLP-out): CTA pairs halve the per-SM smem
     // operand traffic of the main loop
     const ResidTmaArgs args{ep.out_f32, ep.flag, ep.code, ep.bias, ep.gate, ep.colscale,
@@ -829,10 +835,14 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
   // otherwise the 1-SM tiling keeps more SMs busy (small patches).
   const int pair_tiles = ((rows + 2 * kGemmBM - 1) / (2 * kGemmBM)) *
                          ((N + gemm_bn_2sm(N) - 1) / gemm_bn_2sm(N));
-  // PF_GEMM_2SM_SMALL=1: CTA pairs for small patches too (A/B: under patch
-  // lanes the other lanes fill the SMs, and fatter tiles amortise each CTA's
-  // fixed prologue / TMA latency / epilogue cost better)
-  static const bool pairs_small = tune_flag("PF_GEMM_2SM_SMALL");
+  // CTA pairs for small patches too (PF_GEMM_2SM_SMALL=0: only with enough pair
+  // tiles to fill the SMs twice): under patch lanes the other lanes fill the
+  // SMs, and fatter tiles amortise each CTA's fixed prologue / TMA latency /
+  // epilogue. Measured C2: M = 8 0.189 -> 0.180 s, M = 4 0.169 -> 0.165 s.
+  static const bool pairs_small = [] {
+    const char* e = std::getenv("PF_GEMM_2SM_SMALL");
+    return !(e && e[0] == '0');
+  }();
   if (rows >= 2 * kGemmBM && sm_count >= 2 && (pair_tiles >= sm_count || pairs_small) &&
       (gemm_bn_2sm(N) == 256 || gemm_bn_2sm(N) == 192)) {
     switch (gemm_bn_2sm(N)) {
