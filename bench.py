@@ -96,6 +96,16 @@ CONFIGS = {
 }
 
 
+def config_of(c, n, M):
+    """The `config` object of both arms (same keys and values)."""
+    return {"workload": c["name"], "layers": c["L"], "hidden_size": c["hs"],
+            "heads": c["heads"], "seq_len": c["p"], "diffusion_steps": c["S"],
+            "warmup_steps": c["W"], "patches": M, "stages": n,
+            "parallelism": f"pipefusion N={n} M={M}",
+            "l2": "working set > L2 (0.9 GB bf16 weights + 0.6 GB K/V per image pass at "
+                  "C2), no explicit flush"}
+
+
 def flops_per_image(c, mlp):
     """The reference's ComputeModel (simulate.cpp:30-44) for mlp_ratio 4:
     S * L * (24 p hs^2 + 4 p^2 hs); generalised to mlp = 4 hs."""
@@ -248,7 +258,7 @@ def cpu_port_baseline_mmdit(c, budget_s=20.0, sample_rows=32):
                        f"x{units:.0f} units/image")}
 
 
-def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
+def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32, run_shape=(1, 1)):
     """Time the reference's own toy_layer_forward (oracle/_ref, built from
     /root/reference) at the true shape on `sample_rows` query rows against a
     full p-row K/V buffer, one sample per host core in parallel, and
@@ -285,6 +295,19 @@ def cpu_reference_baseline(c, budget_s=20.0, sample_rows=32):
     wall = time.perf_counter() - t0
     per_sample = wall / done  # throughput-equivalent seconds per sample
     samples_per_image = c["S"] * c["L"] * (kvp / sample_rows)
+    if c.get("block") is None and per_sample * cores * samples_per_image < budget_s:
+        # small enough for the real thing: one full run_pipefusion image through the
+        # reference's own executor (Threads backend, the CLI default), timed
+        full = ref.build_toy_model(0, c["L"], c["hs"], c["heads"], 4.0)
+        x0 = ref.make_initial_latent(0, c["p"], c["hs"])
+        n, M = run_shape
+        t1 = time.perf_counter()
+        full.run_pipefusion(x0, c["S"], n, M, c["W"], 0.1)
+        dt = time.perf_counter() - t1
+        return {"value": dt, "unit": UNIT, "cores": n, "kind": "reference",
+                "sample": (f"one full image: the reference's run_pipefusion (toy_model.cpp / "
+                           f"execute.cpp, Threads backend, {n} worker threads, M={M}), timed "
+                           f"end to end")}
     return {
         "value": per_sample * samples_per_image, "unit": UNIT, "cores": cores,
         "kind": "reference",
@@ -487,12 +510,7 @@ def run_ours(args, c, world, rank):
                       else "one"),
         "dtype": "bf16", "data": "synthetic (reference RNG: build_toy_model seed 0, "
                                   "make_initial_latent seed 0)",
-        "config": {"workload": c["name"], "layers": c["L"], "hidden_size": c["hs"],
-                   "heads": c["heads"], "seq_len": c["p"], "diffusion_steps": c["S"],
-                   "warmup_steps": c["W"], "patches": M, "stages": n,
-                   "parallelism": f"pipefusion N={n} M={M}",
-                   "l2": "working set > L2 (0.9 GB bf16 weights + 0.6 GB K/V per image "
-                         "pass), no explicit flush"},
+        "config": config_of(c, n, M),
         "tc_frac_image": total_flops / sec_per_image / 1e12 / peak_tf,
         "block": c.get("block", "toy"),
         # the C ABI moves the fp64 host latent both ways (converted on the GPU)
@@ -635,12 +653,13 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            base = cpu_reference_baseline(c, budget_s=args.cpu_budget)
+            base = cpu_reference_baseline(c, budget_s=args.cpu_budget,
+                                          run_shape=(args.gpus, args.patches or args.gpus))
             line = {"metric": METRIC, "value": base["value"], "unit": UNIT,
                     "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                     "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
                     "dtype": "f64", "data": "synthetic", "impl": "reference",
-                    "config": {"workload": c["name"], "patches": args.patches or args.gpus},
+                    "config": config_of(c, args.gpus, args.patches or args.gpus),
                     "cpu_baseline": base,
                     "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                             "d2h_bytes_per_step": 0}}
@@ -655,7 +674,8 @@ def main():
     if rank == 0:
         if not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = cpu_reference_baseline(c, budget_s=args.cpu_budget)
+                line["cpu_baseline"] = cpu_reference_baseline(
+                    c, budget_s=args.cpu_budget, run_shape=(args.gpus, args.patches or args.gpus))
             except Exception as e:  # the checker must not sink the GPU number
                 line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
         print(json.dumps(line), flush=True)
