@@ -423,12 +423,19 @@ def run_ours(args, c, world, rank):
 
     sec_per_image = ms / 1e3 / args.steps
     # ---- e2e through the C ABI with host buffers (all ranks call it together)
+    # host buffers in pinned memory (the fp64 latent in, the fp64 result out),
+    # allocated once and reused across calls as a serving loop would
+    x_host = out_host = None
+    if holds_x:
+        x_host = torch.empty(x0.shape, dtype=torch.float64, pin_memory=True).numpy()
+        x_host[...] = x0
+        out_host = torch.empty(x0.shape, dtype=torch.float64, pin_memory=True).numpy()
     e2e_times = []
     out = None
     for i in range(max(2, args.steps) + 1):
         barrier(world)
         t0 = time.perf_counter()
-        out = model.run_pipefusion(x0 if holds_x else None, c["S"], M, c["W"], 0.1)
+        out = model.run_pipefusion(x_host, c["S"], M, c["W"], 0.1, out=out_host)
         dt = max_over_ranks(time.perf_counter() - t0, world)
         if i > 0:
             e2e_times.append(dt)
@@ -516,7 +523,8 @@ def run_ours(args, c, world, rank):
         # the C ABI moves the fp64 host latent both ways (converted on the GPU)
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": c["p"] * c["hs"] * 8,
                 "d2h_bytes_per_step": c["p"] * c["hs"] * 8,
-                "api": "pf_run_pipefusion (C ABI, fp64 host latent in/out)"},
+                "api": "pf_run_pipefusion (C ABI, fp64 host latent in/out, pinned host "
+                       "buffers reused across calls)"},
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved,
                      "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,
                      "traffic": traffic, "traffic_source": traffic_src,
