@@ -723,6 +723,56 @@ struct ResidTmaArgs {
   // tile: the output tensor maps end at row_end and clip the TMA stores);
   // their statistics and finite checks are skipped. INT_MAX: whole tiles.
   int row_end = 0x7fffffff;
+  // Stream-K schedule (gemm2sm_resid_tma_kernel only; null: tiles round-robin
+  // over the pairs). Pair c owns the (tile, K block) units [c U / P, (c+1) U / P);
+  // requires tiles >= pairs, so a tile spans at most two pairs. sk_ws holds one
+  // fp32 head partial [BN cols][128 rows] per CTA, sk_flags one flag per CTA
+  // (zero between launches: the reader clears it).
+  float* sk_ws = nullptr;
+  int* sk_flags = nullptr;
+};
+
+// Stream-K walk of a pair's unit range in REVERSE: the pair's last segment
+// (the head of a tile the next pair finishes) comes first, so its partial is
+// published long before the next pair needs it; the pair's first segment (the
+// tail of a tile whose head the previous pair computed) comes last.
+struct SkWalk {
+  int u, u0, kblocks;
+  __device__ __forceinline__ bool next(int& tile, int& kb0, int& kb1) {
+    if (u <= u0) return false;
+    tile = (u - 1) / kblocks;
+    const int ts = tile * kblocks;
+    const int s = ts > u0 ? ts : u0;
+    kb0 = s - ts;
+    kb1 = u - ts;
+    u = s;
+    return true;
+  }
+};
+
+// Segments of one CTA pair: the round-robin tile walk (every tile whole) or
+// the stream-K walk.
+struct ResidTiles {
+  bool sk;
+  int cluster, nclusters, num_tiles, kblocks;
+  int t;       // round-robin: next tile
+  SkWalk w;    // stream-K
+  __device__ __forceinline__ ResidTiles(bool sk_, int c, int nc, int nt, int kb)
+      : sk(sk_), cluster(c), nclusters(nc), num_tiles(nt), kblocks(kb), t(c) {
+    const long long units = (long long)nt * kb;
+    w.u0 = int(units * c / nc);
+    w.u = int(units * (c + 1) / nc);
+    w.kblocks = kb;
+  }
+  __device__ __forceinline__ bool next(int& tile, int& kb0, int& kb1) {
+    if (sk) return w.next(tile, kb0, kb1);
+    if (t >= num_tiles) return false;
+    tile = t;
+    kb0 = 0;
+    kb1 = kblocks;
+    t += nclusters;
+    return true;
+  }
 };
 
 __device__ __forceinline__ float4 ldg4(const float* p) {
@@ -1246,6 +1296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int n_tiles = (N + BN - 1) / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+  const bool sk = args.sk_ws != nullptr;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tma_a);
@@ -1278,11 +1329,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      ResidTiles it(sk, cluster, nclusters, num_tiles, kblocks);
+      for (int tile, kb0, kb1; it.next(tile, kb0, kb1);) {
         const int mt = tile % m_tiles;
         const int nt = tile / m_tiles;
         const int my_row = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
@@ -1301,7 +1353,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // residual parts, one ahead of the epilogue (double-buffered)
     if (lane == 0) {
       int g = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      ResidTiles it(sk, cluster, nclusters, num_tiles, kblocks);
+      for (int tile, kb0, kb1; it.next(tile, kb0, kb1);) {
+        if (kb1 < kblocks) continue;  // head partial: no residual
         const int mt = tile % m_tiles;
         const int nt = tile / m_tiles;
         const int my_row = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
@@ -1324,11 +1378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      ResidTiles it(sk, cluster, nclusters, num_tiles, kblocks);
+      for (int tile, kb0, kb1; it.next(tile, kb0, kb1);) {
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(smem + stage * L::kStageBytes);
@@ -1336,7 +1391,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k)
             ptx::umma2_bf16_ss(d_tmem, ptx::desc_kmajor_sw128(a_base + k * 32),
-                               ptx::desc_kmajor_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+                               ptx::desc_kmajor_sw128(b_base + k * 32), idesc,
+                               (kb != kb0) || (k != 0));
           ptx::umma2_commit_mc(&empty[stage], 0x3);
           if (++stage == STAGES) {
             stage = 0;
@@ -1356,12 +1412,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int g = 0;
-    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+    const int my_cta = int(blockIdx.x);
+    ResidTiles it(sk, cluster, nclusters, num_tiles, kblocks);
+    for (int tile, kb0, kb1; it.next(tile, kb0, kb1);) {
       const int mt = tile % m_tiles;
       const int nt = tile / m_tiles;
       const int gr = row0 + mt * 2 * kGemmBM + int(rank) * kGemmBM;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      if (kb1 < kblocks) {
+        // head of a tile the next pair finishes: publish the fp32 partial
+        // ([BN cols][128 rows] per CTA: coalesced over the rows of a warp)
+        float* ws = args.sk_ws + size_t(my_cta) * BN * kGemmBM + r;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 32 * c, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcg(ws + size_t(32 * c + j) * kGemmBM, __uint_as_float(v[j]));
+        }
+        ptx::tc_fence_before();
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (elect) {
+          ptx::mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          ptx::st_release_gpu(args.sk_flags + my_cta, 1);
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        continue;
+      }
+      const float* pws = nullptr;  // head partial of this tile (previous pair)
+      if (kb0 > 0) {
+        const int src = my_cta - 2;
+        if (elect) {
+          while (ptx::ld_acquire_gpu(args.sk_flags + src) == 0) __nanosleep(64);
+          args.sk_flags[src] = 0;
+        }
+        ptx::named_bar_sync(1, 128);
+        pws = args.sk_ws + size_t(src) * BN * kGemmBM + r;
+      }
       bool bad = false;
       for (int part = 0; part < kParts; ++part, ++g) {
         const int b = g & 1;
@@ -1371,6 +1462,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const uint32_t tcol = tmem_base + (uint32_t(32 * q) << 16) + acc * BN + 64 * part;
         ptx::tmem_ld32(tcol, v0);
         ptx::tmem_ld32(tcol + 32, v1);
+        if (pws) {
+          float p0[32], p1[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            p0[j] = __ldcg(pws + size_t(64 * part + j) * kGemmBM);
+            p1[j] = __ldcg(pws + size_t(64 * part + 32 + j) * kGemmBM);
+          }
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v0[j] = __float_as_uint(__uint_as_float(v0[j]) + p0[j]);
+            v1[j] = __float_as_uint(__uint_as_float(v1[j]) + p1[j]);
+          }
+        }
         ptx::mbar_wait(&c_full[b], (g >> 1) & 1);
         ptx::tmem_wait_ld();
         if (part == kParts - 1) {

@@ -794,6 +794,37 @@ cudaError_t gemm(const CUtensorMap& a, const WeightMaps& b, int rows, int row0,
         best = i;
       }
     }
+    // Stream-K over 256 x 192 pair tiles: equal (tile, K block) ranges per
+    // pair instead of whole tiles, so no partial last wave (N = 1152 at 4096
+    // rows: 96 tiles on 74 pairs); a tile cut between two pairs costs a
+    // 96 KB fp32 partial per CTA through L2 (~4 K blocks of operand traffic).
+    static const bool sk_on = [] {
+      const char* e = std::getenv("PF_RESID_SK");
+      return !(e && e[0] == '0');
+    }();
+    if (sk_on && N % 192 == 0 && ep.splitk_ws && ep.splitk_counters &&
+        ep.splitk_counter_cap >= 2048 + 2 * pairs &&
+        ep.splitk_ws_floats >= size_t(2 * pairs) * 192 * kGemmBM) {
+      const int kblocks = (K + kGemmBK - 1) / kGemmBK;
+      const int tiles = (rows / (2 * kGemmBM)) * (N / 192);
+      const long long units = (long long)tiles * kblocks;
+      const double cost_sk = double((units + pairs - 1) / pairs + 4) * 28.0;
+      // measured at C2: MLP-out (K = 4608) 56.8 -> 53.9 us; out-proj (K = 1152,
+      // 18 K blocks: the partial round trip is a large share) 26.8 -> 34.7 us
+      if (kblocks >= 36 && tiles >= pairs && units % pairs != 0 &&
+          cost_sk < best_cost * kblocks - 1e-9) {
+        ResidTmaArgs a2 = args;
+        a2.sk_ws = ep.splitk_ws;
+        a2.sk_flags = ep.splitk_counters + 2048;
+        using L = Gemm2SmResSmem<192, 4>;
+        return ep.mod() ? launch_resid2<gemm2sm_resid_tma_kernel<192, 4, true>>(
+                              2 * pairs, L::kTotal, stream, a, b.two_sm_res[1], ep, rows, row0,
+                              N, K, a2)
+                        : launch_resid2<gemm2sm_resid_tma_kernel<192, 4, false>>(
+                              2 * pairs, L::kTotal, stream, a, b.two_sm_res[1], ep, rows, row0,
+                              N, K, a2);
+      }
+    }
     if (best == 2)
       return run(std::integral_constant<int, 256>{}, std::integral_constant<int, 4>{},
                  b.two_sm_res[2]);
