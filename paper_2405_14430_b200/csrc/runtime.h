@@ -557,13 +557,14 @@ class Engine {
   // records lane_rec_ after its attention (see enqueue_run)
   cudaEvent_t lane_wait_ = nullptr;
   cudaEvent_t lane_rec_ = nullptr;
-  // lanes per stage for M >= 2 (PF_LANES=1..8, default 4 -- 6 and 8 measured no
-  // faster at C2 M = 8; PF_ONE_LANE=1 is PF_LANES=1)
+  // lanes per stage for M >= 2 (PF_LANES=1..8, default 8: with CTA-pair tiles
+  // for small patches, C2 M = 8 0.1738 / 0.1738 s vs 0.1797 / 0.1800 s with 4
+  // lanes in the same call; M = 4 unchanged; PF_ONE_LANE=1 is PF_LANES=1)
   int lanes_ = [] {
     const char* one = std::getenv("PF_ONE_LANE");
     if (one && one[0] == '1') return 1;
     const char* e = std::getenv("PF_LANES");
-    const int v = e ? std::atoi(e) : 4;
+    const int v = e ? std::atoi(e) : 8;
     return v < 1 ? 1 : (v > Stage::kMaxLanes ? Stage::kMaxLanes : v);
   }();
   void use_lane(Stage& s, int lane);

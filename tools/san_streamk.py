@@ -2,7 +2,8 @@
 in-kernel merge, halves, one CTA per item, separate merge kernel) of both
 attention kernels (triple-buffered attn3 with the row-sum column, and the
 single-buffered one), patch lanes, the MMDiT blocks (QK-norm, RoPE, clipped
-text-row residual tiles) and the opt-in residual split-K. Sanitizer input,
+text-row residual tiles), the opt-in residual split-K and the stream-K
+residual GEMM. Sanitizer input,
 not a test."""
 import os
 import sys
@@ -35,4 +36,10 @@ os.environ["PF_RESID_SPLITK"] = "1"
 os.environ["PF_LANES"] = "1"
 with pf.ToyDiTCuda(0, 1, 1152, 16, 4.0, 1024, 1) as m:
     b = m.run_pipefusion(pf.make_initial_latent(0, 1024, 1152), 2, 8, 1, 0.1)
-print("ok", np.isfinite(a.final_x).all(), np.isfinite(b.final_x).all())
+# stream-K residual GEMM (MLP-out of a 4096-row patch: 96 pair tiles of
+# 256 x 192 on 74 pairs, cut tiles' partials through the split-K workspace)
+rng = np.random.default_rng(3)
+h, kk, vv = [rng.uniform(-1, 1, (4096, 1152)) for _ in range(3)]
+with pf.ToyDiTCuda(0, 1, 1152, 16, 4.0, 4096, 1) as m:
+    g = m.layer_forward(0, h, kk, vv, 0)[0]
+print("ok", np.isfinite(a.final_x).all(), np.isfinite(b.final_x).all(), np.isfinite(g).all())
