@@ -253,14 +253,15 @@ struct EpiQKV {
   int hs, dh, dhp, P;
   __device__ void operator()(int row, int col0, const float (&acc)[32], int nvalid) const {
     if ((hs & 7) == 0 && (dh & 7) == 0) {
+      // (which, head, d) of the chunk's first column; an 8-column group never
+      // straddles a head (dh % 8 == 0), so later groups step d by 8 and wrap
+      // (no per-group integer divisions by the runtime hs / dh)
+      int which = col0 / hs;
+      int head = (col0 - which * hs) / dh;
+      int d = col0 - which * hs - head * dh;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         if (8 * g >= nvalid) break;
-        const int n = col0 + 8 * g;
-        const int which = n / hs;
-        const int nn = n - which * hs;
-        const int head = nn / dh;
-        const int d = nn - head * dh;
         bf16* base = which == 0 ? q : (which == 1 ? k : v);
         uint4 pk;
         pk.x = ptx::pack_bf16x2(acc[8 * g + 0], acc[8 * g + 1]);
@@ -268,6 +269,14 @@ struct EpiQKV {
         pk.z = ptx::pack_bf16x2(acc[8 * g + 4], acc[8 * g + 5]);
         pk.w = ptx::pack_bf16x2(acc[8 * g + 6], acc[8 * g + 7]);
         *reinterpret_cast<uint4*>(base + (size_t(head) * P + row) * dhp + d) = pk;
+        d += 8;
+        if (d == dh) {
+          d = 0;
+          if ((++head) * dh == hs) {
+            head = 0;
+            ++which;
+          }
+        }
       }
       return;
     }
@@ -1128,6 +1137,7 @@ cudaError_t launch_attn3(const CUtensorMap& q, const AttnLaunch& a, int sm_count
     else if (DHP == 80 && poly == 0x80)
       e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x80, true>),
                                     &attn3_fwd_kernel<DHP, 0x80, true>>{});
+
     else
       e = go(std::integral_constant<decltype(&attn3_fwd_kernel<DHP, 0x88, true>),
                                     &attn3_fwd_kernel<DHP, 0x88, true>>{});
